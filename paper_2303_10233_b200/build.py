@@ -1,0 +1,30 @@
+"""Build libetq.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+from __future__ import annotations
+
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SOURCES = ["assemble.cu", "ops.cu", "solvers.cu", "api.cu"]
+OUT = os.path.join(HERE, "libetq.so")
+
+
+def nvcc_cmd(out=OUT):
+    return ["nvcc", "-shared", "-Xcompiler", "-fPIC", "-gencode", "arch=compute_100a,code=sm_100a",
+            "-lineinfo", "-O3", "-std=c++17", "-o", out] + [os.path.join(HERE, "csrc", s) for s in SOURCES]
+
+
+def build(force: bool = False, verbose: bool = True) -> str:
+    srcs = [os.path.join(HERE, "csrc", s) for s in SOURCES] + \
+        [os.path.join(HERE, "csrc", "etq_internal.cuh"), os.path.join(os.path.dirname(HERE), "include", "etq.h")]
+    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(s) for s in srcs):
+        return OUT
+    cmd = nvcc_cmd()
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    return OUT
+
+
+if __name__ == "__main__":
+    build(force=True)

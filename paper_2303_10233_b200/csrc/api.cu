@@ -1,0 +1,480 @@
+// api.cu — the extern "C" boundary of libetq (declared and documented in include/etq.h).
+#include "etq_internal.cuh"
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+struct etq_problem { Problem P; };
+
+#include <atomic>
+static std::atomic<int64_t> g_launches{0};
+void etq_count_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+int64_t etq_launch_total() { return g_launches.load(std::memory_order_relaxed); }
+
+void etq_last_cuda_error(cudaError_t e, const char* file, int line) {
+  std::fprintf(stderr, "[etq] CUDA error %s (%d) at %s:%d\n", cudaGetErrorString(e), (int)e, file, line);
+}
+
+etq_status dev_alloc(void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes > 0 ? bytes : 8);
+  if (e != cudaSuccess) {
+    etq_last_cuda_error(e, __FILE__, __LINE__);
+    *p = nullptr;
+    return e == cudaErrorMemoryAllocation ? ETQ_ENOMEM : ETQ_ECUDA;
+  }
+  return ETQ_OK;
+}
+
+void sell_free(Sell& s) {
+  if (s.own_perm && s.perm) cudaFree(s.perm);
+  if (s.sptr) cudaFree(s.sptr);
+  if (s.slen) cudaFree(s.slen);
+  if (s.col) cudaFree(s.col);
+  if (s.val) cudaFree(s.val);
+  if (s.fval) cudaFree(s.fval);
+  s = Sell{};
+}
+
+namespace {
+// Order the library's work stream after the caller's stream and vice versa.
+struct StreamScope {
+  const Problem& P;
+  explicit StreamScope(const Problem& p) : P(p) {
+    cudaEventRecord(P.ev_in, P.ustream);
+    cudaStreamWaitEvent(P.stream, P.ev_in, 0);
+  }
+  ~StreamScope() {
+    cudaEventRecord(P.ev_out, P.stream);
+    cudaStreamWaitEvent(P.ustream, P.ev_out, 0);
+  }
+};
+
+etq_pc_params default_params(const Problem& P) {
+  etq_pc_params d;
+  std::memset(&d, 0, sizeof(d));
+  d.cheb_sgs_steps = 20;
+  d.cheb_sgs_lo = 0.0;
+  d.lanczos_steps = 60;
+  d.smooth_degree = 3;
+  d.smooth_hi = 1.6;
+  d.smooth_lo = 0.16;
+  d.coarse_n = P.oseen ? 32 : 2;
+  d.mass_cheb_steps = 10;
+  d.use_graphs = 1;
+  return d;
+}
+
+etq_pc_params merge_params(const Problem& P, const etq_pc_params* in) {
+  etq_pc_params d = default_params(P);
+  if (!in) return d;
+  if (in->cheb_sgs_steps > 0) d.cheb_sgs_steps = in->cheb_sgs_steps;
+  if (in->cheb_sgs_lo > 0) d.cheb_sgs_lo = in->cheb_sgs_lo;
+  if (in->lanczos_steps > 0) d.lanczos_steps = in->lanczos_steps;
+  if (in->smooth_degree > 0) d.smooth_degree = in->smooth_degree;
+  if (in->smooth_hi > 0) { d.smooth_hi = in->smooth_hi; d.smooth_lo = in->smooth_hi / 10.0; }
+  if (in->smooth_lo > 0) d.smooth_lo = in->smooth_lo;
+  if (in->coarse_n > 0) d.coarse_n = in->coarse_n;
+  if (in->mass_cheb_steps > 0) d.mass_cheb_steps = in->mass_cheb_steps;
+  d.use_graphs = in->use_graphs;
+  return d;
+}
+
+bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// deterministic start vector of the automatic Lanczos estimate (splitmix64 -> [-1, 1))
+void auto_start_vector(std::vector<double>& v) {
+  uint64_t s = 0x9E3779B97F4A7C15ull;
+  for (auto& x : v) {
+    s += 0x9E3779B97F4A7C15ull;
+    uint64_t z = s;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    x = 2.0 * ((double)(z >> 11) * (1.0 / 9007199254740992.0)) - 1.0;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* etq_status_string(etq_status s) {
+  switch (s) {
+    case ETQ_OK: return "ok";
+    case ETQ_NOT_CONVERGED: return "not converged (maxit reached)";
+    case ETQ_EINVAL: return "invalid argument";
+    case ETQ_ENOMEM: return "out of device memory";
+    case ETQ_ECUDA: return "CUDA error";
+    case ETQ_EINDEFINITE: return "indefinite preconditioner (<z,v> < 0)";
+    case ETQ_EBREAKDOWN: return "breakdown";
+    case ETQ_ENOTSETUP: return "preconditioner not set up";
+    case ETQ_ENAN: return "NaN/Inf in scalar recurrence";
+    default: return "unknown status";
+  }
+}
+
+etq_status etq_assemble(const etq_grid* grid, double viscosity, const etq_wind* wind, void* cuda_stream,
+                        etq_problem** out) {
+  if (!grid || !out) return ETQ_EINVAL;
+  if (grid->n < 2 || grid->n > 4096 || (grid->bc != 0 && grid->bc != 1)) return ETQ_EINVAL;
+  const bool oseen = wind && wind->kind != 0;
+  if (oseen && !(viscosity > 0.0)) return ETQ_EINVAL;
+  if (wind && (wind->kind < 0 || wind->kind > 1)) return ETQ_EINVAL;
+  etq_problem* h = new (std::nothrow) etq_problem();
+  if (!h) return ETQ_ENOMEM;
+  Problem& P = h->P;
+  P.g = make_geo(grid->n);
+  P.bc = grid->bc;
+  P.oseen = oseen;
+  P.wind = oseen ? wind->kind : 0;
+  P.nu = oseen ? viscosity : 1.0;
+  P.n_u = 2LL * P.g.nq;
+  P.n_p = (int64_t)P.g.nk + P.g.n0;
+  P.N = P.n_u + P.n_p;
+  P.ustream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  P.params = default_params(P);
+  auto fail = [&](etq_status s) { etq_destroy(h); return s; };
+#define A_CHECK(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) { etq_last_cuda_error(_e, __FILE__, __LINE__); return fail(ETQ_ECUDA); } } while (0)
+#define A_TRY(expr) do { etq_status _s = (expr); if (_s < 0) return fail(_s); } while (0)
+  A_CHECK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+  A_CHECK(cudaStreamCreateWithFlags(&P.aux, cudaStreamNonBlocking));
+  cudaEvent_t* evs[4] = {&P.ev_in, &P.ev_out, &P.ev_fork, &P.ev_join};
+  for (auto e : evs) A_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  A_CHECK(cudaEventCreate(&P.ev_t0));
+  A_CHECK(cudaEventCreate(&P.ev_t1));
+  A_CHECK(cudaEventRecord(P.ev_in, P.ustream));
+  A_CHECK(cudaStreamWaitEvent(P.stream, P.ev_in, 0));
+  int64_t nsl = 0;
+  A_TRY(build_node_perm(P.g, &P.node_perm, &nsl, P.stream));
+  A_TRY(assemble_velocity_op(P.g, P.oseen, P.nu, P.wind, P.node_perm, nsl, &P.Lv, P.stream));
+  A_TRY(assemble_bt(P.g, 0, 0, P.node_perm, nsl, &P.BxT1, P.stream));
+  A_TRY(assemble_bt(P.g, 1, 0, P.node_perm, nsl, &P.ByT1, P.stream));
+  A_TRY(assemble_bt(P.g, 0, 1, P.node_perm, nsl, &P.BxT0, P.stream));
+  A_TRY(assemble_bt(P.g, 1, 1, P.node_perm, nsl, &P.ByT0, P.stream));
+  A_TRY(assemble_b(P.g, &P.B, P.stream));
+  RedSite& rs = P.red[0];
+  rs.nslot = RED_SLOTS;
+  A_TRY(dalloc(&rs.partials, (size_t)RED_SLOTS * RED_MAXB));
+  A_TRY(dalloc(&rs.counter, RED_SLOTS));
+  A_CHECK(cudaMemsetAsync(rs.counter, 0, sizeof(unsigned) * RED_SLOTS, P.stream));
+  A_TRY(dalloc(&P.dscal, S_COUNT));
+  A_CHECK(cudaMemsetAsync(P.dscal, 0, sizeof(double) * S_COUNT, P.stream));
+  A_CHECK(cudaMallocHost(&P.hscal, sizeof(double) * S_COUNT));
+  A_CHECK(cudaStreamSynchronize(P.stream));
+#undef A_CHECK
+#undef A_TRY
+  *out = h;
+  return ETQ_OK;
+}
+
+etq_status etq_sizes(const etq_problem* h, int64_t* n_u, int64_t* n_k, int64_t* n_0) {
+  if (!h) return ETQ_EINVAL;
+  if (n_u) *n_u = h->P.n_u;
+  if (n_k) *n_k = h->P.g.nk;
+  if (n_0) *n_0 = h->P.g.n0;
+  return ETQ_OK;
+}
+
+etq_status etq_build_rhs(const etq_problem* h, const double* f_nodal, double* b) {
+  if (!h || !b) return ETQ_EINVAL;
+  StreamScope sc(h->P);
+  return build_rhs_dev(h->P, f_nodal, b);
+}
+
+etq_status etq_apply_saddle(const etq_problem* h, int32_t reduced, const double* x, double* y) {
+  if (!h || !x || !y || x == y) return ETQ_EINVAL;
+  const Problem& P = h->P;
+  StreamScope sc(P);
+  launch_saddle_ex(P, reduced != 0, x, y, nullptr, nullptr, 0, nullptr, nullptr, P.stream);
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
+etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_params* params) {
+  if (!h) return ETQ_EINVAL;
+  Problem& P = h->P;
+  StreamScope sc(P);
+  const etq_pc_params prm = merge_params(P, params);
+  P.params = prm;
+  if (kind == ETQ_PC_P1_EXACT) {
+    if (P.oseen || P.g.nq > 4225) return ETQ_EINVAL;   // dense exact solves: n <= 32
+    if (!P.p1.Ainv) {
+      ETQ_TRY(dalloc(&P.p1.Ainv, (size_t)P.g.nq * P.g.nq));
+      ETQ_TRY(dalloc(&P.p1.MQinv, (size_t)P.n_p * P.n_p));
+    }
+    ETQ_TRY(dense_from_sell(P.Lv, P.g.nq, P.p1.Ainv, P.stream));
+    ETQ_TRY(dense_inverse_spd(P.p1.Ainv, P.g.nq, P.stream));
+    ETQ_TRY(p1_build_mass_inverse(P.g, P.p1.MQinv, P.stream));
+    ETQ_CHECK(cudaStreamSynchronize(P.stream));
+    P.p1.ready = true;
+    return ETQ_OK;
+  }
+  if (kind == ETQ_PC_P2_GMG) {
+    if (P.oseen) return ETQ_EINVAL;
+    if (!is_pow2(P.g.n) || !is_pow2(prm.coarse_n) || prm.coarse_n > P.g.n) return ETQ_EINVAL;
+    if (P.mg.built) {
+      for (size_t l = 0; l < P.mg.lv.size(); ++l) {
+        Level& L = P.mg.lv[l];
+        if (l > 0) sell_free(L.A);
+        cudaFree(L.dinv); cudaFree(L.b); cudaFree(L.x); cudaFree(L.r); cudaFree(L.d0); cudaFree(L.d1);
+        cudaFree(L.coarse_inv);
+      }
+      P.mg = Hierarchy{};
+    }
+    ETQ_TRY(build_hierarchy(P, P.mg, prm.coarse_n, prm.smooth_lo, prm.smooth_hi, prm.smooth_degree));
+    ETQ_TRY(mass_pc_alloc(P));
+    P.pm.m = prm.cheb_sgs_steps;
+    double a = prm.cheb_sgs_lo;
+    if (!(a > 0.0)) {
+      std::vector<double> v0(P.n_p);
+      auto_start_vector(v0);
+      double* dv;
+      ETQ_TRY(dalloc(&dv, P.n_p));
+      ETQ_CHECK(cudaMemcpy(dv, v0.data(), sizeof(double) * P.n_p, cudaMemcpyHostToDevice));
+      double lam = 0.0;
+      ETQ_TRY(lanczos_sgs_lo(P, dv, std::min<int64_t>(prm.lanczos_steps, P.n_p / 2), &lam));
+      cudaFree(dv);
+      const double floor_ = 2.0 / ((double)P.pm.m * P.pm.m);   // reading R7: a = max(lam, 2/m^2)
+      a = lam > floor_ ? lam : floor_;
+    }
+    if (!(a > 0.0 && a < 1.0)) return ETQ_EINVAL;
+    P.pm.a = a;
+    P.pm.ready = true;
+    P.p2_ready = true;
+    for (int g = 0; g < 2; ++g)
+      if (P.minres_graph[g]) { cudaGraphExecDestroy(P.minres_graph[g]); P.minres_graph[g] = nullptr; }
+    ETQ_CHECK(cudaStreamSynchronize(P.stream));
+    return ETQ_OK;
+  }
+  return ETQ_EINVAL;
+}
+
+etq_status etq_apply_precond(const etq_problem* h, etq_pc_kind kind, const double* r, double* z) {
+  if (!h || !r || !z || r == z) return ETQ_EINVAL;
+  const Problem& P = h->P;
+  StreamScope sc(P);
+  return precond_apply_ex(P, kind, r, z, nullptr, nullptr, nullptr, nullptr, P.stream);
+}
+
+etq_status etq_apply_vcycle(const etq_problem* h, etq_pc_kind kind, const double* r_u, double* z_u) {
+  if (!h || !r_u || !z_u) return ETQ_EINVAL;
+  const Problem& P = h->P;
+  if (kind != ETQ_PC_P2_GMG || !P.mg.built) return ETQ_ENOTSETUP;
+  StreamScope sc(P);
+  return vcycle_apply_ex(P, P.mg, r_u, z_u, nullptr, 0, nullptr, nullptr, nullptr, P.stream);
+}
+
+etq_status etq_apply_mass_pc(const etq_problem* h, const double* r_p, double* z_p) {
+  if (!h || !r_p || !z_p) return ETQ_EINVAL;
+  const Problem& P = h->P;
+  if (!P.pm.ready) return ETQ_ENOTSETUP;
+  StreamScope sc(P);
+  return mass_pc_apply_ex(P, r_p, z_p, &P.red[0], 2, nullptr, nullptr, nullptr, P.stream);
+}
+
+etq_status etq_apply_mass(const etq_problem* h, const double* x_p, double* y_p) {
+  if (!h || !x_p || !y_p || x_p == y_p) return ETQ_EINVAL;
+  const Problem& P = h->P;
+  StreamScope sc(P);
+  mass_apply(P.g, x_p, y_p, P.stream);
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
+etq_status etq_sgs_sweep(const etq_problem* h, const double* r_p, const double* y_p, double* z_p) {
+  if (!h || !r_p || !z_p) return ETQ_EINVAL;
+  Problem& P = const_cast<Problem&>(h->P);
+  ETQ_TRY(mass_pc_alloc(P));
+  StreamScope sc(P);
+  sgs_sweep_dev(P.g, r_p, y_p, z_p, P.pm.t, P.stream);
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
+etq_status etq_estimate_sgs_lo(etq_problem* h, const double* v0, int32_t steps, double* lam) {
+  if (!h || !v0 || !lam || steps < 1) return ETQ_EINVAL;
+  StreamScope sc(h->P);
+  return lanczos_sgs_lo(h->P, v0, steps, lam);
+}
+
+etq_status etq_get_cheb_sgs_lo(const etq_problem* h, double* a) {
+  if (!h || !a) return ETQ_EINVAL;
+  if (!h->P.pm.ready) return ETQ_ENOTSETUP;
+  *a = h->P.pm.a;
+  return ETQ_OK;
+}
+
+etq_status etq_minres_solve(etq_problem* h, etq_pc_kind kind, const double* b, double* x, double rtol,
+                            int32_t maxit, etq_report* report) {
+  if (!h || !b || !x || !(rtol > 0.0) || maxit < 1) return ETQ_EINVAL;
+  if (kind != ETQ_PC_P1_EXACT && kind != ETQ_PC_P2_GMG) return ETQ_EINVAL;
+  Problem& P = h->P;
+  StreamScope sc(P);
+  return minres_run(P, kind, b, x, rtol, maxit, report);
+}
+
+etq_status etq_minres_solve_host(etq_problem* h, etq_pc_kind kind, const double* b_host, double* x_host,
+                                 double rtol, int32_t maxit, etq_report* report) {
+  if (!h || !b_host || !x_host) return ETQ_EINVAL;
+  Problem& P = h->P;
+  double *db, *dx;
+  ETQ_TRY(dalloc(&db, P.N));
+  ETQ_TRY(dalloc(&dx, P.N));
+  etq_status s;
+  {
+    StreamScope sc(P);
+    ETQ_CHECK(cudaMemcpyAsync(db, b_host, sizeof(double) * P.N, cudaMemcpyHostToDevice, P.stream));
+    ETQ_CHECK(cudaMemcpyAsync(dx, x_host, sizeof(double) * P.N, cudaMemcpyHostToDevice, P.stream));
+    s = minres_run(P, kind, db, dx, rtol, maxit, report);
+    if (s >= 0) {
+      ETQ_CHECK(cudaMemcpyAsync(x_host, dx, sizeof(double) * P.N, cudaMemcpyDeviceToHost, P.stream));
+      ETQ_CHECK(cudaStreamSynchronize(P.stream));
+    }
+  }
+  cudaFree(db); cudaFree(dx);
+  // the cached graphs referenced dx
+  for (int g = 0; g < 2; ++g)
+    if (P.minres_graph[g]) { cudaGraphExecDestroy(P.minres_graph[g]); P.minres_graph[g] = nullptr; }
+  return s;
+}
+
+etq_status etq_export_operator(const etq_problem* h, int32_t which, int32_t level, int64_t* nrows, int64_t* nnz,
+                               int64_t* rowptr, int32_t* col, double* val) {
+  if (!h || !nrows || !nnz) return ETQ_EINVAL;
+  const Problem& P = h->P;
+  std::vector<std::pair<const Sell*, std::pair<int64_t, int64_t>>> parts;   // (matrix, (row offset, col offset))
+  int64_t R = 0;
+  if (which == 0) {
+    if (level < 0) return ETQ_EINVAL;
+    if (level == 0) parts.push_back({&P.Lv, {0, 0}});
+    else {
+      if (!P.mg.built || level >= (int)P.mg.lv.size()) return ETQ_EINVAL;
+      parts.push_back({&P.mg.lv[level].A, {0, 0}});
+    }
+    R = parts[0].first->nrows;
+  } else if (which == 1) {
+    parts.push_back({&P.B, {0, 0}});
+    R = P.n_p;
+  } else if (which == 2) {
+    parts.push_back({&P.BxT1, {0, 0}});
+    parts.push_back({&P.BxT0, {0, P.g.nk}});
+    parts.push_back({&P.ByT1, {P.g.nq, 0}});
+    parts.push_back({&P.ByT0, {P.g.nq, P.g.nk}});
+    R = P.n_u;
+  } else {
+    return ETQ_EINVAL;
+  }
+  cudaStreamSynchronize(P.stream);
+  std::vector<std::vector<std::pair<int32_t, double>>> rows(R);
+  for (auto& pr : parts) {
+    const Sell& S = *pr.first;
+    std::vector<int64_t> sptr(S.nslices + 1);
+    std::vector<int> slen(S.nslices), perm(S.nslices * SELL_C), c(S.nnz_stored);
+    std::vector<double> v(S.nnz_stored);
+    ETQ_CHECK(cudaMemcpy(sptr.data(), S.sptr, sizeof(int64_t) * (S.nslices + 1), cudaMemcpyDeviceToHost));
+    ETQ_CHECK(cudaMemcpy(slen.data(), S.slen, sizeof(int) * S.nslices, cudaMemcpyDeviceToHost));
+    if (S.perm) ETQ_CHECK(cudaMemcpy(perm.data(), S.perm, sizeof(int) * S.nslices * SELL_C, cudaMemcpyDeviceToHost));
+    ETQ_CHECK(cudaMemcpy(c.data(), S.col, sizeof(int) * S.nnz_stored, cudaMemcpyDeviceToHost));
+    ETQ_CHECK(cudaMemcpy(v.data(), S.val, sizeof(double) * S.nnz_stored, cudaMemcpyDeviceToHost));
+    for (int64_t s = 0; s < S.nslices; ++s)
+      for (int l = 0; l < SELL_C; ++l) {
+        const int64_t t = s * SELL_C + l;
+        const int64_t row = S.perm ? perm[t] : (t < S.nrows ? t : -1);
+        if (row < 0) continue;
+        for (int k = 0; k < slen[s]; ++k) {
+          const int64_t e = sptr[s] + l + (int64_t)k * SELL_C;
+          if (v[e] != 0.0) rows[row + pr.second.first].push_back({(int32_t)(c[e] + pr.second.second), v[e]});
+        }
+      }
+  }
+  int64_t total = 0;
+  for (auto& r : rows) total += (int64_t)r.size();
+  *nrows = R; *nnz = total;
+  if (!rowptr) return ETQ_OK;
+  int64_t k = 0;
+  for (int64_t i = 0; i < R; ++i) {
+    rowptr[i] = k;
+    for (auto& e : rows[i]) { if (col) col[k] = e.first; if (val) val[k] = e.second; ++k; }
+  }
+  rowptr[R] = k;
+  return ETQ_OK;
+}
+
+etq_status etq_launch_count(int64_t* count) {
+  if (count) *count = etq_launch_total();
+  return ETQ_OK;
+}
+
+etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* ms, double* bytes) {
+  if (!h || reps < 1 || !ms || !bytes) return ETQ_EINVAL;
+  Problem& P = h->P;
+  if ((which >= 2) && !P.p2_ready) return ETQ_ENOTSETUP;
+  if (which < 0 || which > 4) return ETQ_EINVAL;
+  if (!P.tk) {
+    ETQ_TRY(dalloc(&P.tk, 3 * (size_t)P.N));
+    std::vector<double> v(P.N);
+    auto_start_vector(v);
+    for (int i = 0; i < 3; ++i)
+      ETQ_CHECK(cudaMemcpy(P.tk + (size_t)i * P.N, v.data(), sizeof(double) * P.N, cudaMemcpyHostToDevice));
+  }
+  if (which == 1 && !P.mg.built) return ETQ_ENOTSETUP;
+  StreamScope sc(P);
+  cudaStream_t st = P.stream;
+  double* a = P.tk; double* b = P.tk + P.N; double* c = P.tk + 2 * P.N;
+  auto one = [&](int k) -> etq_status {
+    switch (which) {
+      case 0: launch_saddle_ex(P, false, a, b, nullptr, nullptr, 0, nullptr, nullptr, st); break;
+      case 1: cheb_step_level0(P, (k & 1) ? b : a, (k & 1) ? a : b, st); break;
+      case 2: ETQ_TRY(vcycle_apply_ex(P, P.mg, a, b, nullptr, 0, nullptr, nullptr, nullptr, st)); break;
+      case 3: ETQ_TRY(mass_pc_apply_ex(P, a + P.n_u, b + P.n_u, &P.red[0], 2, nullptr, nullptr, nullptr, st)); break;
+      case 4: ETQ_TRY(precond_apply_ex(P, ETQ_PC_P2_GMG, a, c, nullptr, nullptr, nullptr, nullptr, st)); break;
+    }
+    return ETQ_OK;
+  };
+  ETQ_TRY(one(0));   // warm-up
+  ETQ_CHECK(cudaEventRecord(P.ev_t0, st));
+  for (int k = 0; k < reps; ++k) ETQ_TRY(one(k));
+  ETQ_CHECK(cudaEventRecord(P.ev_t1, st));
+  ETQ_CHECK(cudaEventSynchronize(P.ev_t1));
+  float t = 0.f;
+  ETQ_CHECK(cudaEventElapsedTime(&t, P.ev_t0, P.ev_t1));
+  *ms = (double)t / reps;
+  const double nnz_all = (double)(P.Lv.nnz + P.BxT1.nnz + P.ByT1.nnz + P.BxT0.nnz + P.ByT0.nnz + P.B.nnz);
+  switch (which) {
+    case 0: *bytes = 12.0 * nnz_all + 4.0 * P.Lv.nslices * SELL_C + 16.0 * P.N; break;
+    case 1: *bytes = cheb_step_bytes(P.mg.lv[0]); break;
+    case 2: case 4: *bytes = vcycle_bytes(P.mg); break;
+    default: *bytes = 0.0;
+  }
+  return ETQ_OK;
+}
+
+void etq_destroy(etq_problem* h) {
+  if (!h) return;
+  Problem& P = h->P;
+  if (P.stream) cudaStreamSynchronize(P.stream);
+  for (int g = 0; g < 2; ++g) if (P.minres_graph[g]) cudaGraphExecDestroy(P.minres_graph[g]);
+  for (size_t l = 0; l < P.mg.lv.size(); ++l) {
+    Level& L = P.mg.lv[l];
+    if (l > 0) sell_free(L.A);
+    cudaFree(L.dinv); cudaFree(L.b); cudaFree(L.x); cudaFree(L.r); cudaFree(L.d0); cudaFree(L.d1);
+    cudaFree(L.coarse_inv);
+  }
+  P.Lv.perm = nullptr; P.BxT1.perm = nullptr; P.ByT1.perm = nullptr; P.BxT0.perm = nullptr; P.ByT0.perm = nullptr;
+  sell_free(P.Lv); sell_free(P.BxT1); sell_free(P.ByT1); sell_free(P.BxT0); sell_free(P.ByT0); sell_free(P.B);
+  if (P.node_perm) cudaFree(P.node_perm);
+  cudaFree(P.p1.Ainv); cudaFree(P.p1.MQinv);
+  cudaFree(P.pm.t); cudaFree(P.pm.y0); cudaFree(P.pm.y1); cudaFree(P.pm.rr);
+  cudaFree(P.red[0].partials); cudaFree(P.red[0].counter);
+  cudaFree(P.dscal); cudaFree(P.dhist); cudaFree(P.tk);
+  if (P.hscal) cudaFreeHost(P.hscal);
+  for (int i = 0; i < P.nkv; ++i) cudaFree(P.kv[i]);
+  cudaEvent_t evs[6] = {P.ev_in, P.ev_out, P.ev_fork, P.ev_join, P.ev_t0, P.ev_t1};
+  for (auto e : evs) if (e) cudaEventDestroy(e);
+  if (P.aux) cudaStreamDestroy(P.aux);
+  if (P.stream) cudaStreamDestroy(P.stream);
+  delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,425 @@
+// assemble.cu — row-gather assembly of the Q2–Q1* blocks straight into SELL-32 slices.
+//
+// On the uniform grid every block is a sum of tensor products of 1D "global" matrices, so a
+// thread computes its row from closed-form 1D element tables (no element loop, no atomics):
+//   L   = M1 (x) K1 + K1 (x) M1                 a(u,v) = int grad u : grad v
+//   B1x = -H1 (x) G1, B1y = -G1 (x) H1          b(u,p) = -int p div u
+//   B0x = -W1 (x) E1, B0y = -E1 (x) W1          P0 rows, -int_T d_x phi
+//   M_v = M1 (x) M1                              Galerkin load (reading R10)
+//   N   = A1 (x) T2 - T2 (x) A1                  int (w . grad phi_j) phi_i for the separable
+//                                                cavity wind w = (2y(1-x^2), -2x(1-y^2))
+// (first factor acts on y / the slow index, second on x.)  The 1D tables are the exact
+// integrals of the quadratic (Q2) and linear (Q1) Lagrange bases on one interval; A1 and T2
+// use 3-point Gauss per interval, exact for their degree-5 integrands.
+// Dirichlet handling (reading R2): boundary velocity rows are identity rows, boundary columns
+// are dropped from L, F and B, and their contribution is lifted into the right-hand side.
+#include "etq_internal.cuh"
+#include <cstdio>
+
+namespace {
+
+// ---------------------------------------------------------------- 1D element tables
+__device__ __constant__ double cK2[3][3] = {{7.0 / 3, -8.0 / 3, 1.0 / 3},
+                                           {-8.0 / 3, 16.0 / 3, -8.0 / 3},
+                                           {1.0 / 3, -8.0 / 3, 7.0 / 3}};          // x 1/h
+__device__ __constant__ double cM2[3][3] = {{4.0 / 30, 2.0 / 30, -1.0 / 30},
+                                           {2.0 / 30, 16.0 / 30, 2.0 / 30},
+                                           {-1.0 / 30, 2.0 / 30, 4.0 / 30}};       // x h
+__device__ __constant__ double cG[2][3] = {{-5.0 / 6, 4.0 / 6, 1.0 / 6},
+                                          {-1.0 / 6, -4.0 / 6, 5.0 / 6}};          // int N_a L_b'
+__device__ __constant__ double cH[2][3] = {{1.0 / 6, 2.0 / 6, 0.0},
+                                          {0.0, 2.0 / 6, 1.0 / 6}};                // x h
+__device__ __constant__ double cE[3] = {-1.0, 0.0, 1.0};                          // int L_b'
+__device__ __constant__ double cW[3] = {1.0 / 6, 4.0 / 6, 1.0 / 6};               // x h
+
+__device__ __forceinline__ double lag2(int a, double x) {
+  return a == 0 ? 2.0 * (x - 0.5) * (x - 1.0) : (a == 1 ? 4.0 * x * (1.0 - x) : 2.0 * x * (x - 0.5));
+}
+__device__ __forceinline__ double dlag2(int a, double x) {
+  return a == 0 ? 4.0 * x - 3.0 : (a == 1 ? 4.0 - 8.0 * x : 4.0 * x - 1.0);
+}
+
+// Oseen 1D tables on element e: A1loc[a][b] = int (1-x^2) L_b' L_a dx, T2loc[a][b] = int 2x L_b L_a dx
+__device__ double oseen_tab(int which, int n, double h, int e, int a, int b) {
+  const double gx[3] = {0.5 - 0.5 * 0.7745966692414834, 0.5, 0.5 + 0.5 * 0.7745966692414834};
+  const double gw[3] = {5.0 / 18, 8.0 / 18, 5.0 / 18};
+  double s = 0.0;
+  for (int q = 0; q < 3; ++q) {
+    double x = -1.0 + (e + gx[q]) * h;
+    if (which == 0) s += gw[q] * (1.0 - x * x) * dlag2(b, gx[q]) * lag2(a, gx[q]);
+    else s += gw[q] * h * 2.0 * x * lag2(b, gx[q]) * lag2(a, gx[q]);
+  }
+  return s;
+}
+
+// 1D global Q2-Q2 entries: sum over the (<= 2) intervals containing both nodes
+__device__ double k1(int n, double h, int i, int ip) {
+  int lo = min(i, ip), hi = max(i, ip);
+  if (hi - lo > 2) return 0.0;
+  double s = 0.0;
+  for (int e = lo / 2 - 1; e <= lo / 2; ++e)
+    if (e >= 0 && e < n && 2 * e <= lo && hi <= 2 * e + 2) s += cK2[i - 2 * e][ip - 2 * e];
+  return s / h;
+}
+__device__ double m1(int n, double h, int i, int ip) {
+  int lo = min(i, ip), hi = max(i, ip);
+  if (hi - lo > 2) return 0.0;
+  double s = 0.0;
+  for (int e = lo / 2 - 1; e <= lo / 2; ++e)
+    if (e >= 0 && e < n && 2 * e <= lo && hi <= 2 * e + 2) s += cM2[i - 2 * e][ip - 2 * e];
+  return s * h;
+}
+__device__ double osn1(int which, int n, double h, int i, int ip) {
+  int lo = min(i, ip), hi = max(i, ip);
+  if (hi - lo > 2) return 0.0;
+  double s = 0.0;
+  for (int e = lo / 2 - 1; e <= lo / 2; ++e)
+    if (e >= 0 && e < n && 2 * e <= lo && hi <= 2 * e + 2)
+      s += oseen_tab(which, n, h, e, i - 2 * e, ip - 2 * e);
+  return s;
+}
+// Q1 (row a) x Q2 (column i)
+__device__ double g1(int n, int a, int i) {
+  double s = 0.0;
+  for (int e = a - 1; e <= a; ++e)
+    if (e >= 0 && e < n && i >= 2 * e && i <= 2 * e + 2) s += cG[a - e][i - 2 * e];
+  return s;
+}
+__device__ double h1(int n, double h, int a, int i) {
+  double s = 0.0;
+  for (int e = a - 1; e <= a; ++e)
+    if (e >= 0 && e < n && i >= 2 * e && i <= 2 * e + 2) s += cH[a - e][i - 2 * e];
+  return s * h;
+}
+// P0 (element e) x Q2 (column i)
+__device__ double e1(int e, int i) { return (i >= 2 * e && i <= 2 * e + 2) ? cE[i - 2 * e] : 0.0; }
+__device__ double w1(double h, int e, int i) {
+  return (i >= 2 * e && i <= 2 * e + 2) ? cW[i - 2 * e] * h : 0.0;
+}
+
+struct VelParams { Geo g; int oseen; double nu; };
+
+// entry of the scalar velocity operator between nodes (i,j) and (ii,jj), no Dirichlet masking
+__device__ double vel_entry(const VelParams& P, int i, int j, int ii, int jj) {
+  const int n = P.g.n; const double h = P.g.h;
+  double v = m1(n, h, j, jj) * k1(n, h, i, ii) + k1(n, h, j, jj) * m1(n, h, i, ii);
+  if (P.oseen) {
+    v = P.nu * v + osn1(0, n, h, i, ii) * osn1(1, n, h, j, jj) - osn1(1, n, h, i, ii) * osn1(0, n, h, j, jj);
+  }
+  return v;
+}
+
+__device__ __forceinline__ bool on_boundary(int i, int j, int m) {
+  return i == 0 || j == 0 || i == m - 1 || j == m - 1;
+}
+
+// Enumerate row `node` of the Dirichlet-modified scalar operator.  Stokes drops the entries
+// that cancel exactly in M1(x)K1 + K1(x)M1 (vertex-vertex distance 2 along a midpoint line).
+template <class Emit>
+__device__ int vel_row(const VelParams& P, int node, Emit& emit) {
+  const int m = P.g.m;
+  const int i = node % m, j = node / m;
+  if (on_boundary(i, j, m)) { emit(node, 1.0); return 1; }
+  const int rx = (i & 1) ? 1 : 2, ry = (j & 1) ? 1 : 2;
+  int cnt = 0;
+  for (int dj = -ry; dj <= ry; ++dj) {
+    const int jj = j + dj;
+    if (jj <= 0 || jj >= m - 1) continue;
+    for (int di = -rx; di <= rx; ++di) {
+      const int ii = i + di;
+      if (ii <= 0 || ii >= m - 1) continue;
+      if (!P.oseen) {
+        if ((di == 2 || di == -2) && dj == 0 && (j & 1)) continue;
+        if ((dj == 2 || dj == -2) && di == 0 && (i & 1)) continue;
+      }
+      emit(ii + m * jj, vel_entry(P, i, j, ii, jj));
+      ++cnt;
+    }
+  }
+  return cnt;
+}
+
+// B^T row (velocity node -> pressure columns): comp 0 = x, 1 = y; part 0 = Q1, 1 = P0
+struct BtParams { Geo g; int comp; int part; };
+template <class Emit>
+__device__ int bt_row(const BtParams& P, int node, Emit& emit) {
+  const int m = P.g.m, n = P.g.n; const double h = P.g.h;
+  const int i = node % m, j = node / m;
+  if (on_boundary(i, j, m)) return 0;
+  int cnt = 0;
+  if (P.part == 0) {
+    for (int c = max(0, j / 2 - 1); c <= min(n, j / 2 + 1); ++c)
+      for (int a = max(0, i / 2 - 1); a <= min(n, i / 2 + 1); ++a) {
+        double v = P.comp == 0 ? -g1(n, a, i) * h1(n, h, c, j) : -h1(n, h, a, i) * g1(n, c, j);
+        if (v != 0.0) { emit(a + (n + 1) * c, v); ++cnt; }
+      }
+  } else {
+    for (int f = max(0, j / 2 - 1); f <= min(n - 1, j / 2); ++f)
+      for (int e = max(0, i / 2 - 1); e <= min(n - 1, i / 2); ++e) {
+        double v = P.comp == 0 ? -e1(e, i) * w1(h, f, j) : -w1(h, e, i) * e1(f, j);
+        if (v != 0.0) { emit(e + n * f, v); ++cnt; }
+      }
+  }
+  return cnt;
+}
+
+// B row: pressure dof (Q1 vertex rows first, then P0 rows) -> columns in [u_x; u_y]
+struct BParams { Geo g; };
+template <class Emit>
+__device__ int b_row(const BParams& P, int row, Emit& emit) {
+  const int m = P.g.m, n = P.g.n, nq = P.g.nq; const double h = P.g.h;
+  int cnt = 0;
+  if (row < P.g.nk) {
+    const int a = row % (n + 1), c = row / (n + 1);
+    for (int j = max(1, 2 * c - 2); j <= min(m - 2, 2 * c + 2); ++j) {
+      const double hc = h1(n, h, c, j), gc = g1(n, c, j);
+      for (int i = max(1, 2 * a - 2); i <= min(m - 2, 2 * a + 2); ++i) {
+        const double vx = -g1(n, a, i) * hc, vy = -h1(n, h, a, i) * gc;
+        if (vx != 0.0) { emit(i + m * j, vx); ++cnt; }
+        if (vy != 0.0) { emit(nq + i + m * j, vy); ++cnt; }
+      }
+    }
+  } else {
+    const int t = row - P.g.nk;
+    const int e = t % n, f = t / n;
+    for (int j = max(1, 2 * f); j <= min(m - 2, 2 * f + 2); ++j)
+      for (int i = max(1, 2 * e); i <= min(m - 2, 2 * e + 2); ++i) {
+        const double vx = -e1(e, i) * w1(h, f, j), vy = -w1(h, e, i) * e1(f, j);
+        if (vx != 0.0) { emit(i + m * j, vx); ++cnt; }
+        if (vy != 0.0) { emit(nq + i + m * j, vy); ++cnt; }
+      }
+  }
+  return cnt;
+}
+
+struct CountEmit { __device__ void operator()(int, double) {} };
+struct FillEmit {
+  int* col; double* val; int64_t base; int k;
+  __device__ void operator()(int c, double v) {
+    col[base + (int64_t)k * SELL_C] = c; val[base + (int64_t)k * SELL_C] = v; ++k;
+  }
+};
+
+struct VelFn { VelParams p; template <class E> __device__ int operator()(int r, E& e) const { return vel_row(p, r, e); } };
+struct BtFn { BtParams p; template <class E> __device__ int operator()(int r, E& e) const { return bt_row(p, r, e); } };
+struct BFn { BParams p; template <class E> __device__ int operator()(int r, E& e) const { return b_row(p, r, e); } };
+
+template <class Fn>
+__global__ void k_sell_count(Fn fn, const int* perm, int64_t nrows, int64_t nslices, int* slen,
+                             unsigned long long* nnz) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t s = t / SELL_C;
+  if (s >= nslices) return;
+  const int row = perm ? perm[t] : (t < nrows ? (int)t : -1);
+  CountEmit ce;
+  int len = row >= 0 ? fn(row, ce) : 0;
+  int mx = len;
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int tot = len;
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  if ((threadIdx.x & 31) == 0) { slen[s] = mx; atomicAdd(nnz, (unsigned long long)tot); }
+}
+
+template <class Fn>
+__global__ void k_sell_fill(Fn fn, const int* perm, int64_t nrows, int64_t nslices, const int64_t* sptr,
+                            const int* slen, int* col, double* val) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t s = t / SELL_C;
+  if (s >= nslices) return;
+  const int lane = (int)(t % SELL_C);
+  const int row = perm ? perm[t] : (t < nrows ? (int)t : -1);
+  FillEmit fe{col, val, sptr[s] + lane, 0};
+  if (row >= 0) fn(row, fe);
+  for (int k = fe.k; k < slen[s]; ++k) {
+    col[sptr[s] + lane + (int64_t)k * SELL_C] = 0;
+    val[sptr[s] + lane + (int64_t)k * SELL_C] = 0.0;
+  }
+}
+
+// exclusive scan of 32 * slen into sptr (single block; setup only)
+__global__ void k_scan_slices(const int* slen, int64_t nslices, int64_t* sptr) {
+  __shared__ int64_t part[1024];
+  const int tid = threadIdx.x;
+  const int64_t chunk = (nslices + 1023) / 1024;
+  const int64_t b = tid * chunk, e = min(nslices, b + chunk);
+  int64_t s = 0;
+  for (int64_t i = b; i < e; ++i) s += (int64_t)slen[i] * SELL_C;
+  part[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    int64_t acc = 0;
+    for (int k = 0; k < 1024; ++k) { int64_t v = part[k]; part[k] = acc; acc += v; }
+    sptr[nslices] = acc;
+  }
+  __syncthreads();
+  int64_t acc = part[tid];
+  for (int64_t i = b; i < e; ++i) { sptr[i] = acc; acc += (int64_t)slen[i] * SELL_C; }
+}
+
+__global__ void k_node_perm(int n, int64_t total, int* perm) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  const int m = 2 * n + 1;
+  const int64_t nq = (int64_t)m * m;
+  if (t >= nq) { perm[t] = -1; return; }
+  // classes: (i even, j even), (i odd, j even), (i even, j odd), (i odd, j odd)
+  const int64_t cnt[4] = {(int64_t)(n + 1) * (n + 1), (int64_t)n * (n + 1), (int64_t)(n + 1) * n,
+                          (int64_t)n * n};
+  int c = 0; int64_t idx = t;
+  while (idx >= cnt[c]) { idx -= cnt[c]; ++c; }
+  const int px = c & 1, py = c >> 1;
+  const int cx = px ? n : n + 1;
+  const int ix = (int)(idx % cx), iy = (int)(idx / cx);
+  const int i = 2 * ix + px, j = 2 * iy + py;
+  perm[t] = i + m * j;
+}
+
+template <class Fn>
+etq_status build_sell(Fn fn, int* perm, int64_t nrows, int64_t nslices, Sell* out, cudaStream_t st) {
+  Sell& S = *out;
+  S.nrows = nrows; S.nslices = nslices; S.perm = perm;
+  ETQ_TRY(dalloc(&S.slen, nslices));
+  ETQ_TRY(dalloc(&S.sptr, nslices + 1));
+  unsigned long long* dnnz;
+  ETQ_TRY(dalloc(&dnnz, 1));
+  ETQ_CHECK(cudaMemsetAsync(dnnz, 0, sizeof(unsigned long long), st));
+  const int64_t threads = nslices * SELL_C;
+  const int bs = 256;
+  const int64_t grid = (threads + bs - 1) / bs;
+  k_sell_count<<<(unsigned)grid, bs, 0, st>>>(fn, perm, nrows, nslices, S.slen, dnnz); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  k_scan_slices<<<1, 1024, 0, st>>>(S.slen, nslices, S.sptr); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  int64_t total = 0; unsigned long long nnz = 0;
+  ETQ_CHECK(cudaMemcpyAsync(&total, S.sptr + nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  ETQ_CHECK(cudaMemcpyAsync(&nnz, dnnz, sizeof(nnz), cudaMemcpyDeviceToHost, st));
+  ETQ_CHECK(cudaStreamSynchronize(st));
+  cudaFree(dnnz);
+  S.nnz_stored = total; S.nnz = (int64_t)nnz;
+  ETQ_TRY(dalloc(&S.col, total > 0 ? total : 1));
+  ETQ_TRY(dalloc(&S.val, total > 0 ? total : 1));
+  k_sell_fill<<<(unsigned)grid, bs, 0, st>>>(fn, perm, nrows, nslices, S.sptr, S.slen, S.col, S.val); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
+// ---------------------------------------------------------------- diagonal and RHS
+__global__ void k_vel_dinv(VelParams P, double* dinv) {
+  const int node = blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= P.g.nq) return;
+  const int m = P.g.m, i = node % m, j = node / m;
+  dinv[node] = on_boundary(i, j, m) ? 1.0 : 1.0 / vel_entry(P, i, j, i, j);
+}
+
+__device__ __forceinline__ double lid_ux(const Geo& g, int bc, int i, int j) {
+  if (bc != 0 || j != g.m - 1) return 0.0;
+  const double x = -1.0 + i * (g.h * 0.5);
+  return 1.0 - x * x * x * x;   // reading R1: tangential lid velocity u_x = 1 - x^4
+}
+
+// f rows: boundary -> Dirichlet value; interior -> Galerkin load minus lifting (reading R2, R10)
+__global__ void k_rhs_velocity(VelParams P, int bc, const double* f_nodal, double* b) {
+  const int node = blockIdx.x * blockDim.x + threadIdx.x;
+  const Geo& g = P.g;
+  if (node >= g.nq) return;
+  const int m = g.m, n = g.n; const double h = g.h;
+  const int i = node % m, j = node / m;
+  if (on_boundary(i, j, m)) {
+    b[node] = lid_ux(g, bc, i, j);
+    b[g.nq + node] = 0.0;
+    return;
+  }
+  const int rx = (i & 1) ? 1 : 2, ry = (j & 1) ? 1 : 2;
+  double fx = 0.0, fy = 0.0, lift = 0.0;
+  for (int dj = -ry; dj <= ry; ++dj) {
+    const int jj = j + dj;
+    for (int di = -rx; di <= rx; ++di) {
+      const int ii = i + di;
+      const int col = ii + m * jj;
+      if (f_nodal) {
+        const double mv = m1(n, h, j, jj) * m1(n, h, i, ii);
+        fx += mv * f_nodal[col];
+        fy += mv * f_nodal[g.nq + col];
+      }
+      if (on_boundary(ii, jj, m)) {
+        const double u = lid_ux(g, bc, ii, jj);
+        if (u != 0.0) lift += vel_entry(P, i, j, ii, jj) * u;
+      }
+    }
+  }
+  b[node] = fx - lift;
+  b[g.nq + node] = fy;
+}
+
+// g rows: -B[:, boundary] u_boundary (only the lid's u_x is non-zero)
+__global__ void k_rhs_pressure(Geo g, int bc, double* bp) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= g.nk + g.n0) return;
+  const int m = g.m, n = g.n; const double h = g.h;
+  double s = 0.0;
+  if (bc == 0) {
+    const int j = m - 1;
+    if (row < g.nk) {
+      const int a = row % (n + 1), c = row / (n + 1);
+      const double hc = h1(n, h, c, j);
+      if (hc != 0.0)
+        for (int i = max(0, 2 * a - 2); i <= min(m - 1, 2 * a + 2); ++i) {
+          const double u = lid_ux(g, bc, i, j);
+          s += -g1(n, a, i) * hc * u;
+        }
+    } else {
+      const int t = row - g.nk, e = t % n, f = t / n;
+      const double wf = w1(h, f, j);
+      if (wf != 0.0)
+        for (int i = 2 * e; i <= 2 * e + 2; ++i) s += -e1(e, i) * wf * lid_ux(g, bc, i, j);
+    }
+  }
+  bp[row] = -s;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host entry points
+etq_status build_node_perm(const Geo& g, int** perm, int64_t* nslices, cudaStream_t st) {
+  const int64_t ns = ((int64_t)g.nq + SELL_C - 1) / SELL_C;
+  ETQ_TRY(dalloc(perm, ns * SELL_C));
+  const int64_t tot = ns * SELL_C;
+  k_node_perm<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g.n, tot, *perm); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  *nslices = ns;
+  return ETQ_OK;
+}
+
+etq_status assemble_velocity_op(const Geo& g, bool oseen, double nu, int wind, int* perm,
+                                int64_t nslices, Sell* out, cudaStream_t st) {
+  VelFn fn{VelParams{g, (oseen && wind == 1) ? 1 : 0, oseen ? nu : 1.0}};
+  return build_sell(fn, perm, g.nq, nslices, out, st);
+}
+
+etq_status assemble_bt(const Geo& g, int comp, int part, int* perm, int64_t nslices, Sell* out,
+                       cudaStream_t st) {
+  BtFn fn{BtParams{g, comp, part}};
+  return build_sell(fn, perm, g.nq, nslices, out, st);
+}
+
+etq_status assemble_b(const Geo& g, Sell* out, cudaStream_t st) {
+  BFn fn{BParams{g}};
+  const int64_t nrows = (int64_t)g.nk + g.n0;
+  return build_sell(fn, nullptr, nrows, (nrows + SELL_C - 1) / SELL_C, out, st);
+}
+
+etq_status velocity_dinv_dev(const Geo& g, bool oseen, double nu, int wind, double* dinv, cudaStream_t st) {
+  VelParams P{g, (oseen && wind == 1) ? 1 : 0, oseen ? nu : 1.0};
+  k_vel_dinv<<<(g.nq + 255) / 256, 256, 0, st>>>(P, dinv); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
+etq_status build_rhs_dev(const Problem& P, const double* f_nodal, double* b) {
+  VelParams vp{P.g, (P.oseen && P.wind == 1) ? 1 : 0, P.oseen ? P.nu : 1.0};
+  k_rhs_velocity<<<(P.g.nq + 255) / 256, 256, 0, P.stream>>>(vp, P.bc, f_nodal, b); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  k_rhs_pressure<<<(unsigned)((P.n_p + 255) / 256), 256, 0, P.stream>>>(P.g, P.bc, b + P.n_u); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}

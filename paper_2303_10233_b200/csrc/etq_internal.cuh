@@ -1,0 +1,211 @@
+// etq_internal.cuh — internal data structures and device helpers of libetq (sm_100a).
+//
+// Layout in HBM:
+//   * SELL-32 sliced ELLPACK: rows are processed by one thread each, 32 rows (one warp) per
+//     slice; entry k of lane l of slice s lives at sptr[s] + 32 k + l, so a warp reads 256 B of
+//     values and 128 B of column indices per k, fully coalesced.  Row order inside the slices is
+//     a permutation `perm` grouping Q2 nodes by class (i mod 2, j mod 2), so all rows of a slice
+//     have the same stencil width (25 / 15 / 15 / 9 for the Laplacian) and padding is confined
+//     to slices that touch the boundary.
+//   * The scalar velocity operator (L or F_s) is stored ONCE and applied to both components.
+//   * B^T is stored as four SELL blocks over the velocity-node permutation (x/y component times
+//     Q1/P0 pressure part) so the reduced Taylor-Hood operator can skip the P0 part.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <vector>
+#include <string>
+#include "../../include/etq.h"
+
+#define ETQ_CHECK(call)                                                        \
+  do {                                                                         \
+    cudaError_t _e = (call);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      etq_last_cuda_error(_e, __FILE__, __LINE__);                             \
+      return (_e == cudaErrorMemoryAllocation) ? ETQ_ENOMEM : ETQ_ECUDA;       \
+    }                                                                          \
+  } while (0)
+
+#define ETQ_TRY(expr)                                                          \
+  do {                                                                         \
+    etq_status _s = (expr);                                                    \
+    if (_s < 0) return _s;                                                     \
+  } while (0)
+
+void etq_last_cuda_error(cudaError_t e, const char* file, int line);
+void etq_count_launch(int64_t k = 1);   // host-side launch counter (etq_launch_count)
+
+constexpr int SELL_C = 32;           // slice height = warp size
+constexpr int RED_BLOCKS = 592;      // 4 x 148 SMs: grid of plain reduction kernels
+constexpr int RED_MAXB = 2368;       // max blocks of any reducing kernel (16 x 148)
+constexpr int RED_SLOTS = 16;        // reduction slots per site (see solvers.cu for the map)
+
+// ---------------------------------------------------------------- SELL-32
+struct Sell {
+  int64_t nrows = 0;       // logical rows
+  int64_t nslices = 0;
+  int64_t nnz_stored = 0;  // padded entries
+  int64_t nnz = 0;         // true entries
+  int* perm = nullptr;     // [nslices*32] row id or -1 (may be shared, not owned)
+  bool own_perm = false;
+  int64_t* sptr = nullptr; // [nslices+1]
+  int* slen = nullptr;     // [nslices]
+  int* col = nullptr;      // [nnz_stored]
+  double* val = nullptr;   // [nnz_stored]
+  float* fval = nullptr;   // optional fp32 copy of val (c5 sweep)
+};
+
+// ---------------------------------------------------------------- grid geometry
+struct Geo {
+  int n;        // elements per side
+  int m;        // 2n+1 Q2 nodes per side
+  int nq;       // m*m
+  int nk;       // (n+1)^2
+  int n0;       // n^2
+  double h;     // 2/n
+};
+
+inline Geo make_geo(int n) {
+  Geo g; g.n = n; g.m = 2 * n + 1; g.nq = g.m * g.m; g.nk = (n + 1) * (n + 1); g.n0 = n * n;
+  g.h = 2.0 / n; return g;
+}
+
+// ---------------------------------------------------------------- deterministic reductions
+// A reduction "site" owns RED_BLOCKS partial sums per slot and a completion counter; the last
+// block to finish sums the partials in fixed order (no fp64 atomics on result paths).
+struct RedSite {
+  double* partials = nullptr;   // [nslot * RED_BLOCKS]
+  unsigned* counter = nullptr;  // [1]
+  int nslot = 0;
+};
+
+// ---------------------------------------------------------------- MG level
+struct Level {
+  Geo g;
+  Sell A;                     // scalar operator with identity Dirichlet rows
+  double* dinv = nullptr;     // [nq]
+  // two-component work vectors, each [2*nq]
+  double *b = nullptr, *x = nullptr, *r = nullptr, *d0 = nullptr, *d1 = nullptr;
+  double* coarse_inv = nullptr;   // dense inverse (coarsest level only), nq x nq row-major
+};
+
+struct Hierarchy {
+  std::vector<Level> lv;
+  double lo = 0.16, hi = 1.6;
+  int degree = 3;
+  bool built = false;
+};
+
+// ---------------------------------------------------------------- device scalars (MINRES / GMRES)
+enum ScalarIdx {
+  S_GAMMA = 0, S_GAMMA_PREV, S_DELTA, S_ETA, S_C, S_C_PREV, S_S, S_S_PREV, S_GAMMA1,
+  S_A2, S_A3, S_A1, S_CNEW_ETA, S_DONE, S_STATUS, S_IT, S_RTOL, S_MAXIT,
+  S_DOT0, S_DOT1, S_DOT2, S_DOT3, S_DOT4, S_DOT5, S_KR, S_KY, S_INV_GAMMA, S_TMP0, S_TMP1,
+  S_COUNT = 64
+};
+
+struct PcP1 {
+  bool ready = false;
+  double* Ainv = nullptr;     // nq x nq inverse of the scalar velocity block (Dirichlet rows)
+  double* MQinv = nullptr;    // n_p x n_p inverse of (M_Q + k k^T)
+};
+
+struct PcMass {               // Chebyshev-SGS on M_Q (P2 / M1 pressure block)
+  bool ready = false;
+  double a = 0.0;             // lower end of the SGS-preconditioned spectrum
+  int m = 20;
+  double *t = nullptr, *y0 = nullptr, *y1 = nullptr, *rr = nullptr;   // n_p work vectors
+};
+
+struct Problem {
+  Geo g;
+  int bc = 0;
+  int wind = 0;
+  double nu = 1.0;
+  bool oseen = false;
+  int64_t n_u = 0, n_p = 0, N = 0;
+  cudaStream_t stream = nullptr;              // library work stream (capturable)
+  cudaStream_t ustream = nullptr;             // caller's stream (may be the legacy stream)
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaStream_t aux = nullptr;                 // pressure branch of the block preconditioner
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+
+  Sell Lv;                                    // scalar velocity operator, level-0 rows, node perm
+  Sell BxT1, ByT1, BxT0, ByT0;                // B^T split by component and pressure part
+  Sell B;                                     // pressure rows (Q1 then P0) over [u_x; u_y]
+  int* node_perm = nullptr;                   // shared by Lv and the B^T blocks
+
+  Hierarchy mg;                               // velocity-block V-cycle
+  PcP1 p1;
+  PcMass pm;
+  etq_pc_params params{};
+  bool p2_ready = false;
+
+  // reductions and device scalars
+  RedSite red[1];                             // RED_SLOTS slots (map in solvers.cu)
+  double* dscal = nullptr;                    // [S_COUNT]
+  double* hscal = nullptr;                    // pinned host mirror
+  double* dhist = nullptr;                    // [4 * hist_cap]: |eta|, delta, gamma
+  int hist_cap = 0;
+
+  // Krylov workspace (length N each)
+  double* kv[10] = {nullptr};
+  int nkv = 0;
+  cudaGraphExec_t minres_graph[2] = {nullptr, nullptr};
+  int minres_graph_kind = -1;
+  const double* minres_graph_x = nullptr;     // graphs bake in the caller's x pointer
+  int64_t minres_graph_nodes[2] = {0, 0};     // kernel launches per graph launch
+  double* tk = nullptr;                       // scratch for etq_time_kernel (3 x N)
+};
+
+// ---------------------------------------------------------------- helpers (host)
+etq_status dev_alloc(void** p, size_t bytes);
+template <class T> inline etq_status dalloc(T** p, size_t count) {
+  return dev_alloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+void sell_free(Sell& s);
+
+// assemble.cu
+etq_status build_node_perm(const Geo& g, int** perm, int64_t* nslices, cudaStream_t st);
+etq_status assemble_velocity_op(const Geo& g, bool oseen, double nu, int wind, int* perm,
+                                int64_t nslices, Sell* out, cudaStream_t st);
+etq_status assemble_bt(const Geo& g, int comp, int part, int* perm, int64_t nslices, Sell* out,
+                       cudaStream_t st);
+etq_status assemble_b(const Geo& g, Sell* out, cudaStream_t st);
+etq_status velocity_dinv_dev(const Geo& g, bool oseen, double nu, int wind, double* dinv, cudaStream_t st);
+etq_status build_rhs_dev(const Problem& P, const double* f_nodal, double* b);
+
+// ops.cu
+void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y, const double* inv_scale,
+                      const RedSite* site, int slot, double* dot_out, const double* done, cudaStream_t st);
+void launch_vel_spmv(const Sell& A, const double* x, double* y, int nq, cudaStream_t st);
+void launch_dot(const double* a, const double* b, int64_t n, RedSite* site, int slot, double* out,
+                const double* done, cudaStream_t st);
+etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, double hi, int degree);
+etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r_u, double* z_u,
+                           const RedSite* site, int slot, double* dot_out, const double* dot_with,
+                           const double* done, cudaStream_t st);
+void mass_apply(const Geo& g, const double* x, double* y, cudaStream_t st);
+void sgs_sweep_dev(const Geo& g, const double* r, const double* y, double* z, double* t, cudaStream_t st);
+etq_status mass_pc_alloc(Problem& P);
+etq_status mass_pc_apply_ex(const Problem& P, const double* r_p, double* z_p, const RedSite* site, int slot,
+                            double* dot_out, const double* dot_with, const double* done, cudaStream_t st);
+etq_status dense_inverse_spd(double* A, int m, cudaStream_t st);
+etq_status dense_from_sell(const Sell& A, int m, double* D, cudaStream_t st);
+etq_status p1_build_mass_inverse(const Geo& g, double* W, cudaStream_t st);
+void dense_gemv(const double* A, int m, int ncomp, const double* x, int64_t xstride, double* y,
+                int64_t ystride, const double* done, cudaStream_t st);
+etq_status lanczos_sgs_lo(Problem& P, const double* v0, int steps, double* lam);
+int64_t etq_launch_total();
+void cheb_step_level0(const Problem& P, const double* d_in, double* d_out, cudaStream_t st);
+double vcycle_bytes(const Hierarchy& H);
+double cheb_step_bytes(const Level& L);
+
+// solvers.cu
+void vec_scale_copy(double* y, const double* x, double a, int64_t n, cudaStream_t st);
+void vec_lincomb3(double* w, const double* a, double ca, const double* b, double cb, const double* c,
+                  double cc, int64_t n, cudaStream_t st);
+etq_status precond_apply_ex(const Problem& P, etq_pc_kind kind, const double* r, double* z, const double* w,
+                            double* out_u, double* out_p, const double* done, cudaStream_t st);
+etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, double rtol,
+                      int maxit, etq_report* rep);

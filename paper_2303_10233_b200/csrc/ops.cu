@@ -1,0 +1,989 @@
+// ops.cu — hot-path kernels of libetq (sm_100a, fp64):
+//   * fused block SpMV  y = [A B^T; B 0] x  (Oseen P:756-773) with the optional
+//     MINRES dot delta = <K z, z> fused into the same pass (Algorithm 1 line 7);
+//   * Q2 geometric-multigrid V-cycle: Chebyshev-3 smoothing fused with the SpMV, matrix-free
+//     nested-Q2 restriction/prolongation, dense coarse solve (reading R9);
+//   * matrix-free 5-colour symmetric Gauss-Seidel on the singular M_Q = [[Qk, R^T],[R, Q0]]
+//     and its Chebyshev semi-iteration with the symmetric k-projection Pi C Pi
+//     (readings R6/R7);
+//   * deterministic reductions (block partials + last-block fixed-order sum), dense
+//     Gauss-Jordan inverse and GEMV for the exact (P1) and coarse solves.
+#include "etq_internal.cuh"
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+// ================================================================ launch helpers
+namespace {
+constexpr int BS = 256;
+constexpr int MAXB = RED_MAXB;
+
+inline int grid_for(int64_t work_items, int per_block, int cap = MAXB) {
+  int64_t g = (work_items + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+__device__ __forceinline__ bool is_done(const double* done) { return done && *done != 0.0; }
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block sum; the result is valid in thread 0.  Safe to call repeatedly in one kernel.
+__device__ double block_sum(double v) {
+  __shared__ double sh[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  v = (threadIdx.x < nw) ? sh[threadIdx.x] : 0.0;
+  if (wid == 0) v = warp_sum(v);
+  return v;
+}
+
+// Store this block's partial of NV sums into `site` and, in the last block to finish, sum the
+// gridDim.x partials in a fixed order into out[0..NV).  Deterministic for a fixed grid.
+template <int NV>
+__device__ void reduce_finish(const double (&v)[NV], RedSite site, int slot, double* out) {
+  __shared__ bool last;
+  double tot[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) tot[k] = block_sum(v[k]);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) site.partials[(int64_t)(slot + k) * MAXB + blockIdx.x] = tot[k];
+    __threadfence();
+    unsigned t = atomicAdd(site.counter + slot, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = 0.0;
+      for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+        s += __ldcg(site.partials + (int64_t)(slot + k) * MAXB + i);
+      s = block_sum(s);
+      if (threadIdx.x == 0) out[k] = s;
+    }
+    if (threadIdx.x == 0) site.counter[slot] = 0u;
+  }
+}
+
+// ---------------------------------------------------------------- SELL row products
+__device__ __forceinline__ double sell_row1(const Sell& A, int64_t s, int lane, const double* __restrict__ x) {
+  const int64_t base = A.sptr[s] + lane;
+  const int len = A.slen[s];
+  const int* __restrict__ cp = A.col + base;
+  const double* __restrict__ vp = A.val + base;
+  double acc = 0.0;
+  int k = 0;
+  for (; k + 4 <= len; k += 4) {
+    int c[4]; double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { c[u] = __ldg(cp + (k + u) * SELL_C); v[u] = __ldg(vp + (k + u) * SELL_C); }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc = fma(v[u], __ldg(x + c[u]), acc);
+  }
+  for (; k < len; ++k) acc = fma(__ldg(vp + k * SELL_C), __ldg(x + __ldg(cp + k * SELL_C)), acc);
+  return acc;
+}
+
+__device__ __forceinline__ void sell_row2(const Sell& A, int64_t s, int lane, const double* __restrict__ x0,
+                                          const double* __restrict__ x1, double& a0, double& a1) {
+  const int64_t base = A.sptr[s] + lane;
+  const int len = A.slen[s];
+  const int* __restrict__ cp = A.col + base;
+  const double* __restrict__ vp = A.val + base;
+  int k = 0;
+  for (; k + 4 <= len; k += 4) {
+    int c[4]; double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { c[u] = __ldg(cp + (k + u) * SELL_C); v[u] = __ldg(vp + (k + u) * SELL_C); }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { a0 = fma(v[u], __ldg(x0 + c[u]), a0); a1 = fma(v[u], __ldg(x1 + c[u]), a1); }
+  }
+  for (; k < len; ++k) {
+    const int c = __ldg(cp + k * SELL_C); const double v = __ldg(vp + k * SELL_C);
+    a0 = fma(v, __ldg(x0 + c), a0); a1 = fma(v, __ldg(x1 + c), a1);
+  }
+}
+
+// ================================================================ fused saddle SpMV
+struct SaddleArgs {
+  Sell L, BxT1, ByT1, BxT0, ByT0, B;
+  int nq, nk;
+  int64_t n_u, n_p;
+  int reduced;
+  const double* x;
+  double* y;
+  const double* inv_scale;   // optional device scalar s: y = K (s x)
+  RedSite site; int slot; double* dot_out;   // optional: dot_out = <y, s x>
+  const double* done;
+};
+
+__global__ void __launch_bounds__(BS) k_saddle(SaddleArgs a) {
+  if (is_done(a.done)) return;
+  const double sc = a.inv_scale ? *a.inv_scale : 1.0;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nsv = a.L.nslices, nsp = a.B.nslices;
+  const double* xu = a.x;
+  const double* xv = a.x + a.nq;
+  const double* p1 = a.x + a.n_u;
+  const double* p0 = p1 + a.nk;
+  double dot = 0.0;
+  for (int64_t s = gw; s < nsv + nsp; s += nw) {
+    if (s < nsv) {
+      const int row = a.L.perm[s * SELL_C + lane];
+      double ax = 0.0, ay = 0.0;
+      sell_row2(a.L, s, lane, xu, xv, ax, ay);
+      ax += sell_row1(a.BxT1, s, lane, p1);
+      ay += sell_row1(a.ByT1, s, lane, p1);
+      if (!a.reduced) {
+        ax += sell_row1(a.BxT0, s, lane, p0);
+        ay += sell_row1(a.ByT0, s, lane, p0);
+      }
+      if (row >= 0) {
+        ax *= sc; ay *= sc;
+        a.y[row] = ax; a.y[a.nq + row] = ay;
+        if (a.dot_out) dot += ax * (sc * xu[row]) + ay * (sc * xv[row]);
+      }
+    } else {
+      const int64_t sp = s - nsv;
+      const int64_t row = sp * SELL_C + lane;
+      double acc = sell_row1(a.B, sp, lane, xu);
+      if (row < a.n_p) {
+        acc *= sc;
+        if (a.reduced && row >= a.nk) acc = 0.0;
+        a.y[a.n_u + row] = acc;
+        if (a.dot_out) dot += acc * (sc * p1[row]);
+      }
+    }
+  }
+  if (a.dot_out) {
+    double v[1] = {dot};
+    reduce_finish<1>(v, a.site, a.slot, a.dot_out);
+  }
+}
+
+// scalar operator on two components: y_c = A x_c
+__global__ void __launch_bounds__(BS) k_vel_spmv2(Sell A, int nq, const double* x, double* y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = gw; s < A.nslices; s += nw) {
+    const int row = A.perm[s * SELL_C + lane];
+    double a0 = 0.0, a1 = 0.0;
+    sell_row2(A, s, lane, x, x + nq, a0, a1);
+    if (row >= 0) { y[row] = a0; y[nq + row] = a1; }
+  }
+}
+
+// ================================================================ V-cycle kernels
+// One Chebyshev step fused with the SpMV (Saad Alg. 12.1, reading R9), both components:
+//   x_out = x_in + d_in ; r_out = r_in - A d_in ; d_out = c1 d_in + c2 D^{-1} r_out
+struct ChebArgs {
+  Sell A; const double* dinv; int nq;
+  const double* d_in; const double* r_in; const double* x_in;
+  double* x_out; double* r_out; double* d_out;
+  double c1, c2;
+  const double* done;
+};
+__global__ void __launch_bounds__(BS) k_cheb_step(ChebArgs a) {
+  if (is_done(a.done)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = gw; s < a.A.nslices; s += nw) {
+    const int row = a.A.perm[s * SELL_C + lane];
+    double q0 = 0.0, q1 = 0.0;
+    sell_row2(a.A, s, lane, a.d_in, a.d_in + a.nq, q0, q1);
+    if (row < 0) continue;
+    const double di = a.dinv[row];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int64_t idx = (int64_t)c * a.nq + row;
+      const double dd = a.d_in[idx];
+      const double ro = a.r_in[idx] - (c == 0 ? q0 : q1);
+      a.x_out[idx] = (a.x_in ? a.x_in[idx] : 0.0) + dd;
+      if (a.r_out) a.r_out[idx] = ro;
+      if (a.d_out) a.d_out[idx] = a.c1 * dd + a.c2 * (di * ro);
+    }
+  }
+}
+
+// r = b - A x ; d = D^{-1} r / theta  (start of post-smoothing)
+__global__ void __launch_bounds__(BS) k_post_residual(Sell A, const double* dinv, int nq, const double* b,
+                                                      const double* x, double* r, double* d, double theta,
+                                                      const double* done) {
+  if (is_done(done)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = gw; s < A.nslices; s += nw) {
+    const int row = A.perm[s * SELL_C + lane];
+    double q0 = 0.0, q1 = 0.0;
+    sell_row2(A, s, lane, x, x + nq, q0, q1);
+    if (row < 0) continue;
+    const double di = dinv[row];
+    const double r0 = b[row] - q0, r1 = b[nq + row] - q1;
+    r[row] = r0; r[nq + row] = r1;
+    d[row] = di * r0 / theta; d[nq + row] = di * r1 / theta;
+  }
+}
+
+// d = D^{-1} b / theta (start of pre-smoothing from x = 0)
+__global__ void k_cheb_init(const double* dinv, int nq, const double* b, double* d, double theta,
+                            const double* done) {
+  if (is_done(done)) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * (int64_t)nq;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(i % nq);
+    d[i] = dinv[row] * b[i] / theta;
+  }
+}
+
+// 1D nested-Q2 transfer weights: coarse node I gathers fine nodes 2I + off
+__device__ __forceinline__ int restrict_taps(int I, int* off, double* w) {
+  if ((I & 1) == 0) {
+    off[0] = -3; w[0] = -0.125; off[1] = -1; w[1] = 0.375; off[2] = 0; w[2] = 1.0;
+    off[3] = 1; w[3] = 0.375; off[4] = 3; w[4] = -0.125;
+    return 5;
+  }
+  off[0] = -1; w[0] = 0.75; off[1] = 0; w[1] = 1.0; off[2] = 1; w[2] = 0.75;
+  return 3;
+}
+
+// b_c = Z_c P^T r_f (both components) and d0_c = D_c^{-1} b_c / theta
+__global__ void k_restrict(int mf, int mc, int nqf, int nqc, const double* rf, double* bc, double* d0c,
+                           const double* dinvc, double theta, const double* done) {
+  if (is_done(done)) return;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)nqc;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int I = (int)(t % mc), J = (int)(t / mc);
+    if (I == 0 || J == 0 || I == mc - 1 || J == mc - 1) {
+      bc[t] = 0.0; bc[nqc + t] = 0.0; d0c[t] = 0.0; d0c[nqc + t] = 0.0;
+      continue;
+    }
+    int ox[5], oy[5]; double wx[5], wy[5];
+    const int nx = restrict_taps(I, ox, wx), ny = restrict_taps(J, oy, wy);
+    double s0 = 0.0, s1 = 0.0;
+    for (int q = 0; q < ny; ++q) {
+      const int64_t rowf = (int64_t)(2 * J + oy[q]) * mf;
+      double t0 = 0.0, t1 = 0.0;
+      for (int p = 0; p < nx; ++p) {
+        const int64_t f = rowf + 2 * I + ox[p];
+        t0 = fma(wx[p], rf[f], t0);
+        t1 = fma(wx[p], rf[nqf + f], t1);
+      }
+      s0 = fma(wy[q], t0, s0);
+      s1 = fma(wy[q], t1, s1);
+    }
+    bc[t] = s0; bc[nqc + t] = s1;
+    const double di = dinvc[t];
+    d0c[t] = di * s0 / theta; d0c[nqc + t] = di * s1 / theta;
+  }
+}
+
+// fine node k interpolates coarse nodes: k even -> k/2 (weight 1); k = 4e+1 -> (3/8, 3/4, -1/8)
+// on 2e..2e+2; k = 4e+3 -> (-1/8, 3/4, 3/8)
+__device__ __forceinline__ int prolong_taps(int k, int* idx, double* w) {
+  if ((k & 1) == 0) { idx[0] = k >> 1; w[0] = 1.0; return 1; }
+  const int e = k >> 2;
+  idx[0] = 2 * e; idx[1] = 2 * e + 1; idx[2] = 2 * e + 2;
+  if ((k & 3) == 1) { w[0] = 0.375; w[1] = 0.75; w[2] = -0.125; }
+  else { w[0] = -0.125; w[1] = 0.75; w[2] = 0.375; }
+  return 3;
+}
+
+// x_f += Z_f P (x_c + d_c)
+__global__ void k_prolong(int mf, int mc, int nqf, int nqc, const double* xc, const double* dc, double* xf,
+                          const double* done) {
+  if (is_done(done)) return;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)nqf;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(t % mf), l = (int)(t / mf);
+    if (k == 0 || l == 0 || k == mf - 1 || l == mf - 1) continue;
+    int ix[3], iy[3]; double wx[3], wy[3];
+    const int nx = prolong_taps(k, ix, wx), ny = prolong_taps(l, iy, wy);
+    double s0 = 0.0, s1 = 0.0;
+    for (int q = 0; q < ny; ++q) {
+      double t0 = 0.0, t1 = 0.0;
+      for (int p = 0; p < nx; ++p) {
+        const int64_t c = (int64_t)iy[q] * mc + ix[p];
+        const double v0 = dc ? xc[c] + dc[c] : xc[c];
+        const double v1 = dc ? xc[nqc + c] + dc[nqc + c] : xc[nqc + c];
+        t0 = fma(wx[p], v0, t0);
+        t1 = fma(wx[p], v1, t1);
+      }
+      s0 = fma(wy[q], t0, s0);
+      s1 = fma(wy[q], t1, s1);
+    }
+    xf[t] += s0; xf[nqf + t] += s1;
+  }
+}
+
+// z = x + d (d nullable), optional dot partial <z, w>
+__global__ void __launch_bounds__(BS) k_final_add(const double* x, const double* d, double* z, int64_t n,
+                                                  const double* dw, RedSite site, int slot, double* out,
+                                                  const double* done) {
+  if (is_done(done)) return;
+  double dot = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = d ? x[i] + d[i] : x[i];
+    z[i] = v;
+    if (dw) dot += v * dw[i];
+  }
+  if (out) { double a[1] = {dot}; reduce_finish<1>(a, site, slot, out); }
+}
+
+// ================================================================ dense helpers
+// in-place Gauss-Jordan inverse without pivoting (SPD input), step p, part 1: save column, scale row
+__global__ void k_gj_row(double* A, int m, int p, double* colp) {
+  const double piv = A[(int64_t)p * m + p];
+  const double pinv = 1.0 / piv;
+  for (int i = threadIdx.x + blockIdx.x * blockDim.x; i < m; i += blockDim.x * gridDim.x)
+    colp[i] = A[(int64_t)i * m + p];
+  __syncthreads();   // single block launch: column saved before the row changes
+  for (int j = threadIdx.x; j < m; j += blockDim.x)
+    A[(int64_t)p * m + j] = (j == p ? 1.0 : A[(int64_t)p * m + j]) * pinv;
+}
+__global__ void k_gj_update(double* A, int m, int p, const double* colp) {
+  const int64_t total = (int64_t)m * m;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t / m), j = (int)(t % m);
+    if (i == p) continue;
+    const double f = colp[i];
+    A[t] = (j == p ? 0.0 : A[t]) - f * A[(int64_t)p * m + j];
+  }
+}
+
+// y_c = A x_c for ncomp components (A dense m x m row-major), warp per row
+__global__ void k_gemv(const double* A, int m, int ncomp, const double* x, int64_t xs, double* y, int64_t ys,
+                       const double* done) {
+  if (is_done(done)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = gw; r < m; r += nw) {
+    for (int c = 0; c < ncomp; ++c) {
+      double s = 0.0;
+      for (int j = lane; j < m; j += 32) s = fma(A[r * m + j], x[c * xs + j], s);
+      s = warp_sum(s);
+      if (lane == 0) y[c * ys + r] = s;
+    }
+  }
+}
+
+// ================================================================ pressure mass (matrix-free)
+// 1D Q1 mass entries (h/6)[[2,1],[1,2]] assembled: diag 4h/6 inside, 2h/6 at the ends, off h/6.
+__device__ __forceinline__ double ml1(int n, double h, int a, int ap) {
+  const int d = a - ap;
+  if (d == 0) return (a == 0 || a == n) ? (2.0 * h / 6.0) : (4.0 * h / 6.0);
+  return (d == 1 || d == -1) ? (h / 6.0) : 0.0;
+}
+
+struct MassGeo { int n; int nk; int n0; double h; };
+
+// y = M_Q x  (Prop 2.1 matrix; R_{T,p} = h^2/4, Q0 = h^2)
+__global__ void k_mass_apply(MassGeo g, const double* x, double* y) {
+  const int n = g.n, n1 = n + 1; const double h = g.h, r = 0.25 * h * h, q0 = h * h;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)g.nk + g.n0;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < g.nk) {
+      const int a = (int)(t % n1), c = (int)(t / n1);
+      double s = 0.0;
+      for (int cc = max(0, c - 1); cc <= min(n, c + 1); ++cc) {
+        const double mc = ml1(n, h, c, cc);
+        for (int aa = max(0, a - 1); aa <= min(n, a + 1); ++aa) s += mc * ml1(n, h, a, aa) * x[aa + n1 * cc];
+      }
+      double s0 = 0.0;
+      for (int f = max(0, c - 1); f <= min(n - 1, c); ++f)
+        for (int e = max(0, a - 1); e <= min(n - 1, a); ++e) s0 += x[g.nk + e + n * f];
+      y[t] = s + r * s0;
+    } else {
+      const int te = (int)(t - g.nk), e = te % n, f = te / n;
+      const double s1 = x[e + n1 * f] + x[e + 1 + n1 * f] + x[e + n1 * (f + 1)] + x[e + 1 + n1 * (f + 1)];
+      y[t] = r * s1 + q0 * x[t];
+    }
+  }
+}
+
+// Gauss-Seidel value of Q1 vertex (a,c): (r' - sum_{q != p} M_pq z_q) / M_pp, r' = r - alpha k
+__device__ __forceinline__ double gs_vertex(const MassGeo& g, int a, int c, double rp, const double* z) {
+  const int n = g.n, n1 = n + 1; const double h = g.h, r = 0.25 * h * h;
+  double s = rp;
+  for (int cc = max(0, c - 1); cc <= min(n, c + 1); ++cc) {
+    const double mc = ml1(n, h, c, cc);
+    for (int aa = max(0, a - 1); aa <= min(n, a + 1); ++aa)
+      if (aa != a || cc != c) s -= mc * ml1(n, h, a, aa) * z[aa + n1 * cc];
+  }
+  for (int f = max(0, c - 1); f <= min(n - 1, c); ++f)
+    for (int e = max(0, a - 1); e <= min(n - 1, a); ++e) s -= r * z[g.nk + e + n * f];
+  return s / (ml1(n, h, a, a) * ml1(n, h, c, c));
+}
+__device__ __forceinline__ double gs_cell(const MassGeo& g, int e, int f, double rt, const double* z) {
+  const int n1 = g.n + 1; const double h = g.h, r = 0.25 * h * h;
+  const double s1 = z[e + n1 * f] + z[e + 1 + n1 * f] + z[e + n1 * (f + 1)] + z[e + 1 + n1 * (f + 1)];
+  return (rt - r * s1) / (h * h);
+}
+
+struct SgsArgs {
+  MassGeo g;
+  const double* r;          // right-hand side (n_p)
+  const double* kproj;      // optional device scalar: r' = r - (kproj / kk) k
+  double inv_kk;
+  const double* done;
+};
+__device__ __forceinline__ double rhs_at(const SgsArgs& a, int64_t i) {
+  double v = a.r[i];
+  if (a.kproj) v -= (*a.kproj * a.inv_kk) * (i < a.g.nk ? 1.0 : -1.0);
+  return v;
+}
+
+// in-place update of one vertex colour (0..3) or of all cells (colour 4) of t
+__global__ void k_sgs_colour(SgsArgs a, int colour, double* t) {
+  if (is_done(a.done)) return;
+  const MassGeo& g = a.g;
+  const int n = g.n, n1 = n + 1;
+  if (colour < 4) {
+    const int px = colour & 1, py = colour >> 1;
+    const int cx = (n - px) / 2 + 1, cy = (n - py) / 2 + 1;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < (int64_t)cx * cy;
+         q += (int64_t)gridDim.x * blockDim.x) {
+      const int a_ = 2 * (int)(q % cx) + px, c_ = 2 * (int)(q / cx) + py;
+      const int64_t p = a_ + (int64_t)n1 * c_;
+      t[p] = gs_vertex(g, a_, c_, rhs_at(a, p), t);
+    }
+  } else {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < g.n0; q += (int64_t)gridDim.x * blockDim.x) {
+      const int e = (int)(q % n), f = (int)(q / n);
+      t[g.nk + q] = gs_cell(g, e, f, rhs_at(a, g.nk + q), t);
+    }
+  }
+}
+
+// first kernel of a sweep: t = y (y nullable -> 0) with colour 0 updated from y
+__global__ void k_sgs_first(SgsArgs a, const double* y, double* t) {
+  if (is_done(a.done)) return;
+  const MassGeo& g = a.g;
+  const int n1 = g.n + 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)g.nk + g.n0;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = y ? y[i] : 0.0;
+    if (i < g.nk) {
+      const int a_ = (int)(i % n1), c_ = (int)(i / n1);
+      if (((a_ & 1) | ((c_ & 1) << 1)) == 0) {
+        if (y) v = gs_vertex(g, a_, c_, rhs_at(a, i), y);
+        else {   // neighbours are zero
+          const double h = g.h;
+          v = rhs_at(a, i) / (ml1(g.n, h, a_, a_) * ml1(g.n, h, c_, c_));
+        }
+      }
+    }
+    t[i] = v;
+  }
+}
+
+// last kernel of a sweep: t_fin = t with colour 0 updated from t; then
+//   mode 0: out = t_fin
+//   mode 1: out = omega (gam (t_fin - y) + y - yp) + yp   (Chebyshev semi-iteration step)
+// optional partial sum of k^T out into (site, slot) -> kout
+struct SgsLastArgs {
+  SgsArgs s; const double* t; const double* y; const double* yp; double* out; int mode;
+  double omega, gam;
+  RedSite site; int slot; double* kout;
+};
+__global__ void __launch_bounds__(BS) k_sgs_last(SgsLastArgs a) {
+  if (is_done(a.s.done)) return;
+  const MassGeo& g = a.s.g;
+  const int n1 = g.n + 1;
+  double kd = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)g.nk + g.n0;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = a.t[i];
+    if (i < g.nk) {
+      const int a_ = (int)(i % n1), c_ = (int)(i / n1);
+      if (((a_ & 1) | ((c_ & 1) << 1)) == 0) v = gs_vertex(g, a_, c_, rhs_at(a.s, i), a.t);
+    }
+    double o;
+    if (a.mode == 0) o = v;
+    else {
+      const double y = a.y ? a.y[i] : 0.0, yp = a.yp ? a.yp[i] : 0.0;
+      o = a.omega * (a.gam * (v - y) + y - yp) + yp;
+    }
+    a.out[i] = o;
+    kd += (i < g.nk) ? o : -o;
+  }
+  if (a.kout) { double v[1] = {kd}; reduce_finish<1>(v, a.site, a.slot, a.kout); }
+}
+
+// k^T x
+__global__ void __launch_bounds__(BS) k_kdot(int nk, int64_t np, const double* x, RedSite site, int slot,
+                                             double* out, const double* done) {
+  if (is_done(done)) return;
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x)
+    s += (i < nk) ? x[i] : -x[i];
+  double v[1] = {s};
+  reduce_finish<1>(v, site, slot, out);
+}
+
+// z = y - (ky / kk) k, optional partial <z, w>
+__global__ void __launch_bounds__(BS) k_kproject_out(int nk, int64_t np, const double* y, const double* ky,
+                                                     double inv_kk, double* z, const double* w, RedSite site,
+                                                     int slot, double* out, const double* done) {
+  if (is_done(done)) return;
+  const double beta = *ky * inv_kk;
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = y[i] - beta * ((i < nk) ? 1.0 : -1.0);
+    z[i] = v;
+    if (w) s += v * w[i];
+  }
+  if (out) { double v[1] = {s}; reduce_finish<1>(v, site, slot, out); }
+}
+
+// generic dot product
+__global__ void __launch_bounds__(BS) k_dot(const double* a, const double* b, int64_t n, RedSite site, int slot,
+                                            double* out, const double* done) {
+  if (is_done(done)) return;
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s = fma(a[i], b[i], s);
+  double v[1] = {s};
+  reduce_finish<1>(v, site, slot, out);
+}
+
+// dense (M_Q + k k^T) for the P1 exact solve (small n only)
+__global__ void k_dense_mq_kk(MassGeo g, double* D) {
+  const int64_t np = (int64_t)g.nk + g.n0;
+  const int n = g.n, n1 = n + 1; const double h = g.h;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < np * np; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / np, j = t % np;
+    double v = 0.0;
+    if (i < g.nk && j < g.nk) {
+      const int a = (int)(i % n1), c = (int)(i / n1), aa = (int)(j % n1), cc = (int)(j / n1);
+      v = ml1(n, h, a, aa) * ml1(n, h, c, cc);
+    } else if (i >= g.nk && j >= g.nk) {
+      v = (i == j) ? h * h : 0.0;
+    } else {
+      const int64_t p = i < g.nk ? i : j, T = (i < g.nk ? j : i) - g.nk;
+      const int a = (int)(p % n1), c = (int)(p / n1), e = (int)(T % n), f = (int)(T / n);
+      if ((a == e || a == e + 1) && (c == f || c == f + 1)) v = 0.25 * h * h;
+    }
+    const double ki = (i < g.nk) ? 1.0 : -1.0, kj = (j < g.nk) ? 1.0 : -1.0;
+    D[t] = v + ki * kj;
+  }
+}
+// W = Minv - k k^T / (k^T k)^2
+__global__ void k_dense_fix_k(double* W, int nk, int64_t np) {
+  const double kk = (double)np;
+  const double f = 1.0 / (kk * kk);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < np * np; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / np, j = t % np;
+    const double ki = (i < nk) ? 1.0 : -1.0, kj = (j < nk) ? 1.0 : -1.0;
+    W[t] -= f * ki * kj;
+  }
+}
+// dense copy of a scalar SELL operator (coarse level)
+__global__ void k_sell_to_dense(Sell A, int m, double* D) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t s = t / SELL_C;
+  if (s >= A.nslices) return;
+  const int lane = (int)(t % SELL_C);
+  const int row = A.perm ? A.perm[t] : (t < A.nrows ? (int)t : -1);
+  if (row < 0) return;
+  for (int k = 0; k < A.slen[s]; ++k) {
+    const int64_t e = A.sptr[s] + lane + (int64_t)k * SELL_C;
+    D[(int64_t)row * m + A.col[e]] += A.val[e];
+  }
+}
+
+}  // namespace
+
+// ================================================================ host side
+
+static MassGeo mass_geo(const Geo& g) { MassGeo m{g.n, g.nk, g.n0, g.h}; return m; }
+
+void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y, const double* inv_scale,
+                      const RedSite* site, int slot, double* dot_out, const double* done, cudaStream_t st) {
+  SaddleArgs a;
+  a.L = P.Lv; a.BxT1 = P.BxT1; a.ByT1 = P.ByT1; a.BxT0 = P.BxT0; a.ByT0 = P.ByT0; a.B = P.B;
+  a.nq = P.g.nq; a.nk = P.g.nk; a.n_u = P.n_u; a.n_p = P.n_p; a.reduced = reduced ? 1 : 0;
+  a.x = x; a.y = y; a.inv_scale = inv_scale;
+  a.site = site ? *site : RedSite{}; a.slot = slot; a.dot_out = dot_out; a.done = done;
+  const int64_t warps = P.Lv.nslices + P.B.nslices;
+  const int grid = grid_for(warps * 32, BS);
+  k_saddle<<<grid, BS, 0, st>>>(a); etq_count_launch();
+}
+
+void launch_vel_spmv(const Sell& A, const double* x, double* y, int nq, cudaStream_t st) {
+  k_vel_spmv2<<<grid_for(A.nslices * 32, BS), BS, 0, st>>>(A, nq, x, y); etq_count_launch();
+}
+
+void launch_dot(const double* a, const double* b, int64_t n, RedSite* site, int slot, double* out,
+                const double* done, cudaStream_t st) {
+  k_dot<<<grid_for(n, BS, RED_BLOCKS), BS, 0, st>>>(a, b, n, *site, slot, out, done); etq_count_launch();
+}
+
+// ---------------------------------------------------------------- dense inverse (setup)
+etq_status dense_inverse_spd(double* A, int m, cudaStream_t st) {
+  double* colp;
+  ETQ_TRY(dalloc(&colp, m));
+  const int64_t tot = (int64_t)m * m;
+  const int g2 = grid_for(tot, BS, 4096);
+  for (int p = 0; p < m; ++p) {
+    k_gj_row<<<1, 1024, 0, st>>>(A, m, p, colp); etq_count_launch();
+    k_gj_update<<<g2, BS, 0, st>>>(A, m, p, colp); etq_count_launch();
+  }
+  ETQ_CHECK(cudaGetLastError());
+  ETQ_CHECK(cudaStreamSynchronize(st));
+  cudaFree(colp);
+  return ETQ_OK;
+}
+
+void dense_gemv(const double* A, int m, int ncomp, const double* x, int64_t xstride, double* y, int64_t ystride,
+                const double* done, cudaStream_t st) {
+  k_gemv<<<grid_for((int64_t)m * 32, BS, 4096), BS, 0, st>>>(A, m, ncomp, x, xstride, y, ystride, done); etq_count_launch();
+}
+
+etq_status dense_from_sell(const Sell& A, int m, double* D, cudaStream_t st) {
+  ETQ_CHECK(cudaMemsetAsync(D, 0, sizeof(double) * (size_t)m * m, st));
+  k_sell_to_dense<<<(unsigned)((A.nslices * 32 + 255) / 256), 256, 0, st>>>(A, m, D); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
+etq_status p1_build_mass_inverse(const Geo& g, double* W, cudaStream_t st) {
+  const int64_t np = (int64_t)g.nk + g.n0;
+  MassGeo mg = mass_geo(g);
+  k_dense_mq_kk<<<grid_for(np * np, BS, 4096), BS, 0, st>>>(mg, W); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  ETQ_TRY(dense_inverse_spd(W, (int)np, st));
+  k_dense_fix_k<<<grid_for(np * np, BS, 4096), BS, 0, st>>>(W, g.nk, np); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
+// ---------------------------------------------------------------- hierarchy
+
+etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, double hi, int degree) {
+  if (coarse_n < 1) return ETQ_EINVAL;
+  int m = P.g.n;
+  std::vector<int> ns;
+  while (true) {
+    ns.push_back(m);
+    if (m <= coarse_n) break;
+    if (m % 2) return ETQ_EINVAL;
+    m /= 2;
+  }
+  if (ns.back() != coarse_n && ns.size() > 1) return ETQ_EINVAL;
+  H.lv.resize(ns.size());
+  for (size_t l = 0; l < ns.size(); ++l) {
+    Level& L = H.lv[l];
+    L.g = make_geo(ns[l]);
+    if (l == 0) {
+      L.A = P.Lv;   // shallow: owned by the problem
+    } else {
+      int* perm; int64_t nsl;
+      ETQ_TRY(build_node_perm(L.g, &perm, &nsl, P.stream));
+      ETQ_TRY(assemble_velocity_op(L.g, P.oseen, P.nu, P.wind, perm, nsl, &L.A, P.stream));
+      L.A.own_perm = true;
+    }
+    ETQ_TRY(dalloc(&L.dinv, L.g.nq));
+    ETQ_TRY(velocity_dinv_dev(L.g, P.oseen, P.nu, P.wind, L.dinv, P.stream));
+    const size_t nv = 2 * (size_t)L.g.nq;
+    if (l > 0) ETQ_TRY(dalloc(&L.b, nv));
+    ETQ_TRY(dalloc(&L.x, nv));
+    ETQ_TRY(dalloc(&L.r, nv));
+    ETQ_TRY(dalloc(&L.d0, nv));
+    ETQ_TRY(dalloc(&L.d1, nv));
+  }
+  Level& C = H.lv.back();
+  ETQ_TRY(dalloc(&C.coarse_inv, (size_t)C.g.nq * C.g.nq));
+  ETQ_TRY(dense_from_sell(C.A, C.g.nq, C.coarse_inv, P.stream));
+  ETQ_TRY(dense_inverse_spd(C.coarse_inv, C.g.nq, P.stream));
+  H.lo = lo; H.hi = hi; H.degree = degree; H.built = true;
+  ETQ_CHECK(cudaStreamSynchronize(P.stream));
+  return ETQ_OK;
+}
+
+// One V-cycle on both velocity components (reading R9).  z_u = V(r_u); optional partial
+// <z_u, dot_with> into (site, slot) -> dot_out.
+etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r_u, double* z_u,
+                           const RedSite* site, int slot, double* dot_out, const double* dot_with,
+                           const double* done, cudaStream_t st) {
+  const int L = (int)H.lv.size();
+  const double theta = 0.5 * (H.hi + H.lo), delta = 0.5 * (H.hi - H.lo), sigma = theta / delta;
+  std::vector<double> c1(H.degree), c2(H.degree);
+  {
+    double rho = 1.0 / sigma;
+    for (int k = 0; k < H.degree; ++k) {
+      const double rn = 1.0 / (2.0 * sigma - rho);
+      c1[k] = rn * rho; c2[k] = 2.0 * rn / delta;
+      rho = rn;
+    }
+  }
+  RedSite dummy{};
+  if (L == 1) {   // coarse solve only
+    const Level& C = H.lv[0];
+    dense_gemv(C.coarse_inv, C.g.nq, 2, r_u, C.g.nq, z_u, C.g.nq, done, st);
+    if (dot_out && site)
+      k_final_add<<<grid_for(2LL * C.g.nq, BS, RED_BLOCKS), BS, 0, st>>>(z_u, nullptr, z_u, 2LL * C.g.nq, dot_with,
+                                                                       *site, slot, dot_out, done); etq_count_launch();
+    return ETQ_OK;
+  }
+  std::vector<const double*> bvec(L);
+  std::vector<const double*> pend(L, nullptr);
+  // ---- down
+  for (int l = 0; l < L - 1; ++l) {
+    const Level& lv = H.lv[l];
+    const int nq = lv.g.nq;
+    const double* b = (l == 0) ? r_u : lv.b;
+    bvec[l] = b;
+    if (l == 0)
+      k_cheb_init<<<grid_for(2LL * nq, BS, 4096), BS, 0, st>>>(lv.dinv, nq, b, lv.d0, theta, done); etq_count_launch();
+    const int gs = grid_for(lv.A.nslices * 32, BS, 4096);
+    double* din = lv.d0; double* dout = lv.d1;
+    for (int k = 0; k < H.degree; ++k) {
+      ChebArgs a;
+      a.A = lv.A; a.dinv = lv.dinv; a.nq = nq;
+      a.d_in = din; a.r_in = (k == 0) ? b : lv.r; a.x_in = (k == 0) ? nullptr : lv.x;
+      a.x_out = lv.x; a.r_out = lv.r; a.d_out = (k == H.degree - 1) ? nullptr : dout;
+      a.c1 = c1[k]; a.c2 = c2[k]; a.done = done;
+      k_cheb_step<<<gs, BS, 0, st>>>(a); etq_count_launch();
+      std::swap(din, dout);
+    }
+    const Level& cv = H.lv[l + 1];
+    k_restrict<<<grid_for(cv.g.nq, BS, 4096), BS, 0, st>>>(lv.g.m, cv.g.m, nq, cv.g.nq, lv.r, cv.b, cv.d0,
+                                                          cv.dinv, theta, done); etq_count_launch();
+  }
+  // ---- coarse
+  {
+    const Level& C = H.lv[L - 1];
+    dense_gemv(C.coarse_inv, C.g.nq, 2, C.b, C.g.nq, C.x, C.g.nq, done, st);
+    pend[L - 1] = nullptr;
+  }
+  // ---- up
+  for (int l = L - 2; l >= 0; --l) {
+    const Level& lv = H.lv[l];
+    const Level& cv = H.lv[l + 1];
+    const int nq = lv.g.nq;
+    k_prolong<<<grid_for(nq, BS, 4096), BS, 0, st>>>(lv.g.m, cv.g.m, nq, cv.g.nq, cv.x, pend[l + 1], lv.x, done); etq_count_launch();
+    const int gs = grid_for(lv.A.nslices * 32, BS, 4096);
+    k_post_residual<<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, theta, done); etq_count_launch();
+    double* din = lv.d0; double* dout = lv.d1;
+    for (int k = 0; k < H.degree - 1; ++k) {
+      ChebArgs a;
+      a.A = lv.A; a.dinv = lv.dinv; a.nq = nq;
+      a.d_in = din; a.r_in = lv.r; a.x_in = lv.x;
+      a.x_out = lv.x; a.r_out = (k == H.degree - 2) ? nullptr : lv.r; a.d_out = dout;
+      a.c1 = c1[k]; a.c2 = c2[k]; a.done = done;
+      k_cheb_step<<<gs, BS, 0, st>>>(a); etq_count_launch();
+      std::swap(din, dout);
+    }
+    pend[l] = din;   // last correction deferred to the consumer
+  }
+  const Level& F = H.lv[0];
+  const int64_t nv = 2LL * F.g.nq;
+  k_final_add<<<grid_for(nv, BS, RED_BLOCKS), BS, 0, st>>>(F.x, pend[0], z_u, nv, dot_with,
+                                                          site ? *site : dummy, slot, dot_out, done); etq_count_launch();
+  return ETQ_OK;
+}
+
+// ---------------------------------------------------------------- mass / SGS
+void mass_apply(const Geo& g, const double* x, double* y, cudaStream_t st) {
+  k_mass_apply<<<grid_for((int64_t)g.nk + g.n0, BS, 4096), BS, 0, st>>>(mass_geo(g), x, y); etq_count_launch();
+}
+
+// S(y) sweep sequence: [first: colour 0 from y] 1 2 3 P0 3 2 1 [last: colour 0]
+static void sgs_inner(const SgsArgs& a, double* t, cudaStream_t st) {
+  const Geo dummy{};
+  (void)dummy;
+  const int n = a.g.n;
+  const int64_t nv = ((int64_t)(n / 2 + 1)) * (n / 2 + 1);
+  const int gv = grid_for(nv, BS, 4096), gc = grid_for(a.g.n0, BS, 4096);
+  const int seq[7] = {1, 2, 3, 4, 3, 2, 1};
+  for (int q = 0; q < 7; ++q) {
+    k_sgs_colour<<<seq[q] == 4 ? gc : gv, BS, 0, st>>>(a, seq[q], t);
+    etq_count_launch();
+  }
+}
+
+void sgs_sweep_dev(const Geo& g, const double* r, const double* y, double* z, double* t, cudaStream_t st) {
+  SgsArgs a{mass_geo(g), r, nullptr, 0.0, nullptr};
+  const int64_t np = (int64_t)g.nk + g.n0;
+  const int gf = grid_for(np, BS, RED_BLOCKS);
+  k_sgs_first<<<gf, BS, 0, st>>>(a, y, t); etq_count_launch();
+  sgs_inner(a, t, st);
+  SgsLastArgs la;
+  la.s = a; la.t = t; la.y = nullptr; la.yp = nullptr; la.out = z; la.mode = 0; la.omega = 1; la.gam = 1;
+  la.site = RedSite{}; la.slot = 0; la.kout = nullptr;
+  k_sgs_last<<<gf, BS, 0, st>>>(la); etq_count_launch();
+}
+
+// z_p = Pi C Pi r_p (reading R6) with C = m-step Chebyshev semi-iteration on SGS (reading R7)
+etq_status mass_pc_apply_ex(const Problem& P, const double* r_p, double* z_p, const RedSite* site, int slot,
+                            double* dot_out, const double* dot_with, const double* done, cudaStream_t st) {
+  const PcMass& M = P.pm;
+  if (!M.ready) return ETQ_ENOTSETUP;
+  const Geo& g = P.g;
+  const int64_t np = (int64_t)g.nk + g.n0;
+  const double inv_kk = 1.0 / (double)np;
+  const int gf = grid_for(np, BS, RED_BLOCKS);
+  RedSite rs = *site;
+  // k^T r
+  k_kdot<<<gf, BS, 0, st>>>(g.nk, np, r_p, rs, 3, P.dscal + S_KR, done); etq_count_launch();
+  SgsArgs a{mass_geo(g), r_p, P.dscal + S_KR, inv_kk, done};
+  const double rho = 1.0 - M.a;
+  const double gam = 2.0 / (2.0 - rho), rh = rho / (2.0 - rho);
+  double omega = 1.0;
+  const double* cur = nullptr; const double* prev = nullptr;
+  double* bufs[2] = {M.y0, M.y1};
+  int nb = 0;
+  for (int k = 0; k < M.m; ++k) {
+    if (k == 1) omega = 1.0 / (1.0 - 0.5 * rh * rh);
+    else if (k > 1) omega = 1.0 / (1.0 - 0.25 * rh * rh * omega);
+    k_sgs_first<<<gf, BS, 0, st>>>(a, cur, M.t); etq_count_launch();
+    sgs_inner(a, M.t, st);
+    double* out = bufs[nb]; nb ^= 1;
+    SgsLastArgs la;
+    la.s = a; la.t = M.t; la.y = cur; la.yp = prev; la.out = out; la.mode = 1;
+    la.omega = (k == 0) ? 1.0 : omega; la.gam = gam;
+    la.site = rs; la.slot = 4; la.kout = (k == M.m - 1) ? P.dscal + S_KY : nullptr;
+    k_sgs_last<<<gf, BS, 0, st>>>(la); etq_count_launch();
+    prev = cur; cur = out;
+  }
+  k_kproject_out<<<gf, BS, 0, st>>>(g.nk, np, cur, P.dscal + S_KY, inv_kk, z_p, dot_with, rs, slot, dot_out, done); etq_count_launch();
+  return ETQ_OK;
+}
+
+etq_status mass_pc_alloc(Problem& P) {
+  const int64_t np = P.n_p;
+  PcMass& M = P.pm;
+  if (!M.t) {
+    ETQ_TRY(dalloc(&M.t, np)); ETQ_TRY(dalloc(&M.y0, np)); ETQ_TRY(dalloc(&M.y1, np)); ETQ_TRY(dalloc(&M.rr, np));
+  }
+  return ETQ_OK;
+}
+
+// Lanczos for the pencil (M_Q, C_sgs), start p_1 = M_Q v0 (reading R7); smallest Ritz value.
+etq_status lanczos_sgs_lo(Problem& P, const double* v0, int steps, double* lam) {
+  ETQ_TRY(mass_pc_alloc(P));
+  const Geo& g = P.g;
+  const int64_t np = P.n_p;
+  cudaStream_t st = P.stream;
+  double *p, *pp, *q, *w, *z;
+  ETQ_TRY(dalloc(&p, np)); ETQ_TRY(dalloc(&pp, np)); ETQ_TRY(dalloc(&q, np)); ETQ_TRY(dalloc(&w, np));
+  ETQ_TRY(dalloc(&z, np));
+  RedSite rs = P.red[0];
+  double* d0 = P.dscal + S_TMP0 + 8;
+  auto dot = [&](const double* a, const double* b) -> double {
+    launch_dot(a, b, np, &rs, 5, d0, nullptr, st);
+    double h = 0;
+    cudaMemcpyAsync(&h, d0, sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    return h;
+  };
+  mass_apply(g, v0, p, st);
+  sgs_sweep_dev(g, p, nullptr, q, P.pm.t, st);
+  const double b0 = std::sqrt(dot(q, p));
+  std::vector<double> al, be;
+  // scale p, q by 1/b0 ; pp = 0
+  vec_scale_copy(p, p, 1.0 / b0, np, st);
+  vec_scale_copy(q, q, 1.0 / b0, np, st);
+  ETQ_CHECK(cudaMemsetAsync(pp, 0, np * 8, st));
+  double beta_prev = 0.0;
+  for (int j = 0; j < steps; ++j) {
+    mass_apply(g, q, w, st);
+    const double alpha = dot(q, w);
+    vec_lincomb3(w, w, 1.0, p, -alpha, pp, -beta_prev, np, st);
+    al.push_back(alpha);
+    if (j == steps - 1) break;
+    sgs_sweep_dev(g, w, nullptr, z, P.pm.t, st);
+    const double zw = dot(z, w);
+    if (!(zw > 0.0)) break;
+    const double beta = std::sqrt(zw);
+    be.push_back(beta);
+    std::swap(pp, p);
+    vec_scale_copy(p, w, 1.0 / beta, np, st);
+    vec_scale_copy(q, z, 1.0 / beta, np, st);
+    beta_prev = beta;
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(p); cudaFree(pp); cudaFree(q); cudaFree(w); cudaFree(z);
+  // smallest eigenvalue of the tridiagonal by Sturm bisection
+  const int k = (int)al.size();
+  double lo = 1e300, hi = -1e300;
+  for (int i = 0; i < k; ++i) {
+    const double r = (i > 0 ? std::fabs(be[i - 1]) : 0.0) + (i < k - 1 ? std::fabs(be[i]) : 0.0);
+    lo = std::fmin(lo, al[i] - r); hi = std::fmax(hi, al[i] + r);
+  }
+  auto count_below = [&](double x) {
+    int c = 0; double d = 1.0;
+    for (int i = 0; i < k; ++i) {
+      d = al[i] - x - (i > 0 ? be[i - 1] * be[i - 1] / d : 0.0);
+      if (d == 0.0) d = -1e-300;
+      if (d < 0) ++c;
+    }
+    return c;
+  };
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (count_below(mid) >= 1) hi = mid; else lo = mid;
+  }
+  *lam = 0.5 * (lo + hi);
+  return ETQ_OK;
+}
+
+// ---------------------------------------------------------------- bench helpers
+// middle Chebyshev step of the finest level (x, r in place; d_in -> d_out)
+void cheb_step_level0(const Problem& P, const double* d_in, double* d_out, cudaStream_t st) {
+  const Level& lv = P.mg.lv[0];
+  ChebArgs a;
+  a.A = lv.A; a.dinv = lv.dinv; a.nq = lv.g.nq;
+  a.d_in = d_in; a.r_in = lv.r; a.x_in = lv.x; a.x_out = lv.x; a.r_out = lv.r; a.d_out = d_out;
+  a.c1 = 0.5; a.c2 = 0.1; a.done = nullptr;
+  k_cheb_step<<<grid_for(lv.A.nslices * 32, BS, 4096), BS, 0, st>>>(a); etq_count_launch();
+}
+
+// Algorithmic bytes: every stored value/index once (12 B per true nnz), the
+// row permutation (4 B per slot), every vector element the kernel must read or write once.
+double cheb_step_bytes(const Level& L) {
+  const double nq = L.g.nq;
+  return 12.0 * L.A.nnz + 4.0 * L.A.nslices * SELL_C + 8.0 * nq /*dinv*/ + 8.0 * 2 * nq * 6 /*d,r,x in; x,r,d out*/;
+}
+
+double vcycle_bytes(const Hierarchy& H) {
+  double b = 0.0;
+  const int L = (int)H.lv.size();
+  const int deg = H.degree;
+  for (int l = 0; l < L - 1; ++l) {
+    const Level& lv = H.lv[l];
+    const double nq = lv.g.nq, mat = 12.0 * lv.A.nnz + 4.0 * lv.A.nslices * SELL_C + 8.0 * nq;
+    const double v = 8.0 * 2 * nq;   // one two-component vector
+    if (l == 0) b += 8.0 * nq + 2 * v;                       // init: dinv, b -> d
+    for (int k = 0; k < deg; ++k)                            // pre-smoothing steps
+      b += mat + v * ((k == 0 ? 2 : 3) + (k == deg - 1 ? 2 : 3));
+    const double nqc = H.lv[l + 1].g.nq, vc = 8.0 * 2 * nqc;
+    b += v + 2 * vc + 8.0 * nqc;                             // restriction: r -> b_c, d0_c
+    b += 2 * vc + 2 * v;                                     // prolongation: x_c + d_c -> x += P e
+    b += mat + 2 * v + 2 * v;                                // post residual: b, x -> r, d
+    for (int k = 0; k < deg - 1; ++k)                        // post steps
+      b += mat + v * (3 + (k == deg - 2 ? 2 : 3));
+    if (l == 0) b += 2 * v + v;                              // final: x + d -> z
+  }
+  const Level& C = H.lv[L - 1];
+  b += 8.0 * (double)C.g.nq * C.g.nq + 4.0 * 8.0 * C.g.nq;  // dense coarse solve
+  return b;
+}

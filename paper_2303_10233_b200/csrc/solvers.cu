@@ -1,0 +1,282 @@
+// solvers.cu — block preconditioner composition and preconditioned MINRES (Algorithm 1).
+//
+// MINRES keeps every scalar of Algorithm 1 in device memory: one single-thread
+// kernel evaluates lines 10-18 (gamma_{j+1}, alpha_0..3, c, s, eta) from the two fused dot
+// products, so an iteration is a fixed kernel sequence with no host round trip inside it.
+// One iteration is captured in a CUDA graph (two graphs: the v/z/w buffers alternate with
+// period 2); the host only reads a done flag after each graph launch.
+#include "etq_internal.cuh"
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+namespace {
+constexpr int BS = 256;
+inline int grid_for(int64_t n, int cap = 4096) {
+  int64_t g = (n + BS - 1) / BS;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+__global__ void k_scale_copy(double* y, const double* x, double a, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = a * x[i];
+}
+__global__ void k_lincomb3(double* w, const double* a, double ca, const double* b, double cb, const double* c,
+                           double cc, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    w[i] = ca * a[i] + cb * b[i] + cc * c[i];
+}
+__global__ void k_sub(double* y, const double* a, const double* b, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = a[i] - b[i];
+}
+
+// MINRES line 8: v_new = q - (delta/gamma) v - (gamma/gamma_prev) v_prev   (in place on v_prev)
+__global__ void k_minres_v(const double* q, const double* v, double* vp, const double* sc, int64_t n) {
+  if (sc[S_DONE] != 0.0) return;
+  const double g = sc[S_GAMMA], gp = sc[S_GAMMA_PREV], d = sc[S_DELTA];
+  const double a = d / g;
+  const double b = (gp != 0.0) ? g / gp : 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    vp[i] = (b != 0.0) ? (q[i] - a * v[i] - b * vp[i]) : (q[i] - a * v[i]);
+}
+
+// MINRES lines 10-19 on one thread
+__global__ void k_minres_scalars(double* sc, double* hist, int hist_cap) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  sc[S_TMP0] = sc[S_DONE];            // done flag seen by this iteration's w/x update
+  if (sc[S_DONE] != 0.0) return;
+  const double zv = sc[S_DOT0] + sc[S_DOT1];
+  if (!(zv >= 0.0)) {
+    sc[S_STATUS] = (zv != zv) ? (double)ETQ_ENAN : (double)ETQ_EINDEFINITE;
+    sc[S_DONE] = 1.0; sc[S_TMP0] = 1.0;
+    return;
+  }
+  const double gamma = sc[S_GAMMA], delta = sc[S_DELTA];
+  const double c = sc[S_C], cp = sc[S_C_PREV], s = sc[S_S], sp = sc[S_S_PREV];
+  const double eta = sc[S_ETA];
+  const double gn = sqrt(zv);                                    // line 10
+  const double a0 = c * delta - cp * s * gamma;                  // line 11
+  const double a1 = sqrt(a0 * a0 + gn * gn);                     // line 12
+  const double a2 = s * delta + cp * c * gamma;                  // line 13
+  const double a3 = sp * gamma;                                  // line 14
+  if (a1 == 0.0 || a1 != a1) {
+    sc[S_STATUS] = (a1 != a1) ? (double)ETQ_ENAN : (double)ETQ_EBREAKDOWN;
+    sc[S_DONE] = 1.0; sc[S_TMP0] = 1.0;
+    return;
+  }
+  const double cn = a0 / a1, sn = gn / a1;                       // line 15
+  sc[S_A1] = a1; sc[S_A2] = a2; sc[S_A3] = a3;
+  sc[S_CNEW_ETA] = cn * eta;                                     // line 17 coefficient
+  sc[S_TMP1] = 1.0 / gamma;                                      // z^{(j)} / gamma_j in line 16
+  const double etan = -sn * eta;                                 // line 18
+  sc[S_ETA] = etan;
+  sc[S_C_PREV] = c; sc[S_C] = cn; sc[S_S_PREV] = s; sc[S_S] = sn;
+  sc[S_GAMMA_PREV] = gamma; sc[S_GAMMA] = gn;
+  sc[S_INV_GAMMA] = gn > 0.0 ? 1.0 / gn : 0.0;
+  const int it = (int)sc[S_IT];
+  if (it < hist_cap) {
+    hist[it] = fabs(etan);
+    hist[hist_cap + it] = delta;
+    hist[2 * hist_cap + it] = gn;
+  }
+  sc[S_IT] = it + 1;
+  if (fabs(etan) / sc[S_GAMMA1] < sc[S_RTOL]) sc[S_DONE] = 1.0;   // line 19
+  else if (it + 1 >= (int)sc[S_MAXIT]) sc[S_DONE] = 1.0;
+}
+
+// line 16-17: w_new = (z/gamma - a3 w_prev - a2 w)/a1 (in place on w_prev); x += c eta w_new
+__global__ void k_minres_wx(const double* z, const double* w, double* wp, double* x, const double* sc, int64_t n) {
+  if (sc[S_TMP0] != 0.0) return;
+  const double ig = sc[S_TMP1], a1 = sc[S_A1], a2 = sc[S_A2], a3 = sc[S_A3], ce = sc[S_CNEW_ETA];
+  const double inv_a1 = 1.0 / a1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double wn = (z[i] * ig - a3 * wp[i] - a2 * w[i]) * inv_a1;
+    wp[i] = wn;
+    x[i] += ce * wn;
+  }
+}
+
+__global__ void k_minres_init(double* sc) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double zv = sc[S_DOT0] + sc[S_DOT1];
+  if (!(zv >= 0.0)) {
+    sc[S_STATUS] = (zv != zv) ? (double)ETQ_ENAN : (double)ETQ_EINDEFINITE;
+    sc[S_DONE] = 1.0;
+    return;
+  }
+  const double g = sqrt(zv);                                     // line 3
+  sc[S_GAMMA] = g; sc[S_GAMMA1] = g; sc[S_ETA] = g;              // line 4
+  sc[S_GAMMA_PREV] = 0.0;
+  sc[S_C] = 1.0; sc[S_C_PREV] = 1.0; sc[S_S] = 0.0; sc[S_S_PREV] = 0.0;
+  sc[S_INV_GAMMA] = g > 0.0 ? 1.0 / g : 0.0;
+  sc[S_IT] = 0.0;
+  sc[S_DONE] = (g == 0.0) ? 1.0 : 0.0;
+  sc[S_STATUS] = 0.0;
+}
+}  // namespace
+
+void vec_scale_copy(double* y, const double* x, double a, int64_t n, cudaStream_t st) {
+  k_scale_copy<<<grid_for(n), BS, 0, st>>>(y, x, a, n); etq_count_launch();
+}
+void vec_lincomb3(double* w, const double* a, double ca, const double* b, double cb, const double* c, double cc,
+                  int64_t n, cudaStream_t st) {
+  k_lincomb3<<<grid_for(n), BS, 0, st>>>(w, a, ca, b, cb, c, cc, n); etq_count_launch();
+}
+
+// z = P^{-1} r for the block-diagonal Stokes preconditioners; optional dot partials
+// <z_u, w_u> -> out_u and <z_p, w_p> -> out_p.
+etq_status precond_apply_ex(const Problem& P, etq_pc_kind kind, const double* r, double* z, const double* w,
+                            double* out_u, double* out_p, const double* done, cudaStream_t st) {
+  const RedSite* site = &P.red[0];
+  const int64_t nu = P.n_u, np = P.n_p;
+  if (kind == ETQ_PC_P1_EXACT) {
+    if (!P.p1.ready) return ETQ_ENOTSETUP;
+    dense_gemv(P.p1.Ainv, P.g.nq, 2, r, P.g.nq, z, P.g.nq, done, st);
+    dense_gemv(P.p1.MQinv, (int)np, 1, r + nu, np, z + nu, np, done, st);
+    if (out_u) launch_dot(z, w, nu, const_cast<RedSite*>(site), 1, out_u, done, st);
+    if (out_p) launch_dot(z + nu, w + nu, np, const_cast<RedSite*>(site), 2, out_p, done, st);
+    return ETQ_OK;
+  }
+  if (kind == ETQ_PC_P2_GMG) {
+    if (!P.p2_ready) return ETQ_ENOTSETUP;
+    // pressure branch on the aux stream, velocity V-cycle on the main stream
+    ETQ_CHECK(cudaEventRecord(P.ev_fork, st));
+    ETQ_CHECK(cudaStreamWaitEvent(P.aux, P.ev_fork, 0));
+    ETQ_TRY(mass_pc_apply_ex(P, r + nu, z + nu, site, 2, out_p, w ? w + nu : nullptr, done, P.aux));
+    ETQ_TRY(vcycle_apply_ex(P, P.mg, r, z, site, 1, out_u, w, done, st));
+    ETQ_CHECK(cudaEventRecord(P.ev_join, P.aux));
+    ETQ_CHECK(cudaStreamWaitEvent(st, P.ev_join, 0));
+    return ETQ_OK;
+  }
+  return ETQ_ENOTSETUP;
+}
+
+static etq_status minres_alloc(Problem& P) {
+  if (P.nkv >= 7) return ETQ_OK;
+  for (int i = P.nkv; i < 7; ++i) ETQ_TRY(dalloc(&P.kv[i], P.N));
+  P.nkv = 7;
+  return ETQ_OK;
+}
+
+static etq_status minres_iteration(Problem& P, etq_pc_kind kind, int cur, double* x, cudaStream_t st) {
+  double* V[2] = {P.kv[0], P.kv[1]};
+  double* Z[2] = {P.kv[2], P.kv[3]};
+  double* W[2] = {P.kv[4], P.kv[5]};
+  double* Q = P.kv[6];
+  double* sc = P.dscal;
+  const int64_t N = P.N;
+  const double* done = sc + S_DONE;
+  // line 6-7: q = K (z / gamma), delta = <q, z / gamma>
+  launch_saddle_ex(P, false, Z[cur], Q, sc + S_INV_GAMMA, &P.red[0], 0, sc + S_DELTA, done, st);
+  // line 8
+  k_minres_v<<<grid_for(N), BS, 0, st>>>(Q, V[cur], V[1 - cur], sc, N); etq_count_launch();
+  // line 9-10 (dot products fused into the preconditioner's last kernels)
+  ETQ_TRY(precond_apply_ex(P, kind, V[1 - cur], Z[1 - cur], V[1 - cur], sc + S_DOT0, sc + S_DOT1, done, st));
+  // lines 10-19
+  k_minres_scalars<<<1, 32, 0, st>>>(sc, P.dhist, P.hist_cap); etq_count_launch();
+  // lines 16-17
+  k_minres_wx<<<grid_for(N), BS, 0, st>>>(Z[cur], W[cur], W[1 - cur], x, sc, N); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
+etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, double rtol, int maxit,
+                      etq_report* rep) {
+  if (maxit < 1) return ETQ_EINVAL;
+  ETQ_TRY(minres_alloc(P));
+  cudaStream_t st = P.stream;
+  const int64_t N = P.N;
+  double* V[2] = {P.kv[0], P.kv[1]};
+  double* Z[2] = {P.kv[2], P.kv[3]};
+  double* W[2] = {P.kv[4], P.kv[5]};
+  double* Q = P.kv[6];
+  double* sc = P.dscal;
+  if (P.hist_cap < maxit + 1) {
+    if (P.dhist) cudaFree(P.dhist);
+    P.hist_cap = maxit + 1;
+    ETQ_TRY(dalloc(&P.dhist, 3 * (size_t)P.hist_cap));
+  }
+  ETQ_CHECK(cudaEventRecord(P.ev_t0, st));
+  // scalars
+  std::vector<double> h(S_COUNT, 0.0);
+  h[S_RTOL] = rtol; h[S_MAXIT] = maxit;
+  ETQ_CHECK(cudaMemcpyAsync(sc, h.data(), sizeof(double) * S_COUNT, cudaMemcpyHostToDevice, st));
+  // line 1-2: v^(0) = 0, w^(0) = w^(1) = 0, v^(1) = b - K x0
+  ETQ_CHECK(cudaMemsetAsync(V[0], 0, N * sizeof(double), st));
+  ETQ_CHECK(cudaMemsetAsync(W[0], 0, N * sizeof(double), st));
+  ETQ_CHECK(cudaMemsetAsync(W[1], 0, N * sizeof(double), st));
+  launch_saddle_ex(P, false, x, Q, nullptr, nullptr, 0, nullptr, nullptr, st);
+  k_sub<<<grid_for(N), BS, 0, st>>>(V[1], b, Q, N); etq_count_launch();
+  // line 3
+  ETQ_TRY(precond_apply_ex(P, kind, V[1], Z[1], V[1], sc + S_DOT0, sc + S_DOT1, nullptr, st));
+  k_minres_init<<<1, 32, 0, st>>>(sc); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+
+  const bool graphs = P.params.use_graphs != 0;
+  if (graphs && (P.minres_graph_kind != (int)kind || P.minres_graph_x != x || !P.minres_graph[0])) {
+    for (int g = 0; g < 2; ++g) {
+      if (P.minres_graph[g]) { cudaGraphExecDestroy(P.minres_graph[g]); P.minres_graph[g] = nullptr; }
+    }
+    for (int g = 0; g < 2; ++g) {
+      cudaGraph_t graph;
+      const int64_t before = etq_launch_total();
+      ETQ_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      etq_status s = minres_iteration(P, kind, g, x, st);
+      cudaError_t e = cudaStreamEndCapture(st, &graph);
+      P.minres_graph_nodes[g] = etq_launch_total() - before;
+      etq_count_launch(-P.minres_graph_nodes[g]);   // captured, not launched
+      if (s < 0) return s;
+      ETQ_CHECK(e);
+      ETQ_CHECK(cudaGraphInstantiate(&P.minres_graph[g], graph, 0));
+      cudaGraphDestroy(graph);
+    }
+    P.minres_graph_kind = (int)kind;
+    P.minres_graph_x = x;
+  }
+  int cur = 1;
+  int it = 0;
+  for (;;) {
+    ETQ_CHECK(cudaMemcpyAsync(P.hscal, sc, sizeof(double) * 20, cudaMemcpyDeviceToHost, st));
+    ETQ_CHECK(cudaStreamSynchronize(st));
+    if (P.hscal[S_DONE] != 0.0) break;
+    if (graphs) {
+      ETQ_CHECK(cudaGraphLaunch(P.minres_graph[cur], st));
+      etq_count_launch(P.minres_graph_nodes[cur]);
+    }
+    else ETQ_TRY(minres_iteration(P, kind, cur, x, st));
+    cur = 1 - cur;
+    if (++it > maxit + 2) break;   // safety net; the device flag ends the loop
+  }
+  ETQ_CHECK(cudaEventRecord(P.ev_t1, st));
+  ETQ_CHECK(cudaMemcpyAsync(P.hscal, sc, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost, st));
+  ETQ_CHECK(cudaStreamSynchronize(st));
+  const int iters = (int)P.hscal[S_IT];
+  const int status = (int)P.hscal[S_STATUS];
+  const double g1 = P.hscal[S_GAMMA1];
+  const double eta = std::fabs(P.hscal[S_ETA]);
+  const bool conv = status == 0 && (g1 == 0.0 || eta / g1 < rtol);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1);
+  if (rep) {
+    rep->iterations = iters; rep->converged = conv ? 1 : 0; rep->restarts = 0; rep->status = status;
+    rep->abs_res = eta; rep->rel_res = g1 > 0 ? eta / g1 : 0.0; rep->ms_total = ms;
+    const int nh = std::min(iters, P.hist_cap);
+    if (rep->history && rep->history_cap > 0) {
+      const int k = std::min(nh, rep->history_cap);
+      ETQ_CHECK(cudaMemcpy(rep->history, P.dhist, sizeof(double) * k, cudaMemcpyDeviceToHost));
+    }
+    if (rep->lanczos_delta && rep->lanczos_cap > 0) {
+      const int k = std::min(nh, rep->lanczos_cap);
+      ETQ_CHECK(cudaMemcpy(rep->lanczos_delta, P.dhist + P.hist_cap, sizeof(double) * k, cudaMemcpyDeviceToHost));
+    }
+    if (rep->lanczos_gamma && rep->lanczos_cap > 0) {
+      const int k = std::min(nh, rep->lanczos_cap);
+      ETQ_CHECK(cudaMemcpy(rep->lanczos_gamma, P.dhist + 2 * P.hist_cap, sizeof(double) * k, cudaMemcpyDeviceToHost));
+    }
+  }
+  if (status < 0) return status;
+  return conv ? ETQ_OK : ETQ_NOT_CONVERGED;
+}

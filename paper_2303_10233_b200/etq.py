@@ -1,0 +1,260 @@
+"""Thin ctypes binding of libetq (include/etq.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of libetq.so; this module only turns
+torch tensors into device pointers, passes torch's current CUDA stream, and raises on a
+negative etq_status.  There is no CPU fallback: if libetq.so is missing the import fails.
+Function names mirror the C ABI (etq_<name> -> <name>).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libetq.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "etq.h")
+
+ETQ_OK, ETQ_NOT_CONVERGED = 0, 1
+PC_P1_EXACT, PC_P2_GMG, PC_OSEEN_M1, PC_OSEEN_PCD1 = 0, 1, 2, 3
+
+
+class EtqError(RuntimeError):
+    def __init__(self, status, what):
+        super().__init__(f"{what}: etq status {status} ({status_string(status)})")
+        self.status = status
+
+
+class Grid(C.Structure):
+    _fields_ = [("n", C.c_int32), ("bc", C.c_int32)]
+
+
+class Wind(C.Structure):
+    _fields_ = [("kind", C.c_int32)]
+
+
+class PcParams(C.Structure):
+    _fields_ = [("cheb_sgs_steps", C.c_int32), ("cheb_sgs_lo", C.c_double), ("lanczos_steps", C.c_int32),
+                ("smooth_degree", C.c_int32), ("smooth_hi", C.c_double), ("smooth_lo", C.c_double),
+                ("coarse_n", C.c_int32), ("mass_cheb_steps", C.c_int32), ("use_graphs", C.c_int32)]
+
+
+class Report(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("restarts", C.c_int32),
+                ("status", C.c_int32), ("rel_res", C.c_double), ("abs_res", C.c_double),
+                ("ms_total", C.c_double), ("history", C.POINTER(C.c_double)), ("history_cap", C.c_int32),
+                ("lanczos_delta", C.POINTER(C.c_double)), ("lanczos_gamma", C.POINTER(C.c_double)),
+                ("lanczos_cap", C.c_int32)]
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"libetq.so not built at {path}; run __graft_entry__.build()")
+    lib = C.CDLL(path)
+    P, I32, I64, D, VP = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_void_p
+    sig = {
+        "etq_assemble": ([C.POINTER(Grid), D, C.POINTER(Wind), VP, C.POINTER(P)], I32),
+        "etq_sizes": ([P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)], I32),
+        "etq_build_rhs": ([P, VP, VP], I32),
+        "etq_apply_saddle": ([P, I32, VP, VP], I32),
+        "etq_precond_setup": ([P, I32, C.POINTER(PcParams)], I32),
+        "etq_apply_precond": ([P, I32, VP, VP], I32),
+        "etq_apply_vcycle": ([P, I32, VP, VP], I32),
+        "etq_apply_mass_pc": ([P, VP, VP], I32),
+        "etq_apply_mass": ([P, VP, VP], I32),
+        "etq_sgs_sweep": ([P, VP, VP, VP], I32),
+        "etq_estimate_sgs_lo": ([P, VP, I32, C.POINTER(D)], I32),
+        "etq_get_cheb_sgs_lo": ([P, C.POINTER(D)], I32),
+        "etq_minres_solve": ([P, I32, VP, VP, D, I32, C.POINTER(Report)], I32),
+        "etq_minres_solve_host": ([P, I32, VP, VP, D, I32, C.POINTER(Report)], I32),
+        "etq_export_operator": ([P, I32, I32, C.POINTER(I64), C.POINTER(I64), VP, VP, VP], I32),
+        "etq_launch_count": ([C.POINTER(I64)], I32),
+        "etq_time_kernel": ([P, I32, I32, C.POINTER(D), C.POINTER(D)], I32),
+        "etq_status_string": ([I32], C.c_char_p),
+        "etq_destroy": ([P], None),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    return lib
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        _lib = load_library()
+    return _lib
+
+
+def header_functions(path: str = HEADER):
+    """Names of the functions declared in include/etq.h."""
+    txt = open(path).read()
+    return sorted(set(re.findall(r"^\s*(?:[\w\*]+\s+)+\**(etq_\w+)\s*\(", txt, flags=re.M)))
+
+
+def launch_count() -> int:
+    """libetq kernel launches so far in this process (graph kernel nodes included)."""
+    c = C.c_int64()
+    lib().etq_launch_count(C.byref(c))
+    return c.value
+
+
+def status_string(s: int) -> str:
+    return lib().etq_status_string(int(s)).decode()
+
+
+def _check(s, what):
+    if s < 0:
+        raise EtqError(s, what)
+    return s
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    import torch
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError("expected a contiguous float64 CUDA tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def make_params(**kw) -> PcParams:
+    p = PcParams()
+    p.use_graphs = 1
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+class Problem:
+    """Owns an etq_problem (device matrices and workspaces)."""
+
+    def __init__(self, n: int, bc: int = 0, viscosity: float = 1.0, wind: int = 0):
+        h = C.c_void_p()
+        g = Grid(n, bc)
+        w = Wind(wind)
+        _check(lib().etq_assemble(C.byref(g), viscosity, C.byref(w), _stream(), C.byref(h)), "etq_assemble")
+        self.h = h
+        self.n = n
+        n_u, n_k, n_0 = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().etq_sizes(h, C.byref(n_u), C.byref(n_k), C.byref(n_0)), "etq_sizes")
+        self.n_u, self.n_k, self.n_0 = n_u.value, n_k.value, n_0.value
+        self.n_p = self.n_k + self.n_0
+        self.N = self.n_u + self.n_p
+        self.nq = self.n_u // 2
+
+    def close(self):
+        if self.h:
+            lib().etq_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- C-ABI mirrors
+    def build_rhs(self, b, f_nodal=None):
+        _check(lib().etq_build_rhs(self.h, _ptr(f_nodal), _ptr(b)), "etq_build_rhs")
+        return b
+
+    def apply_saddle(self, x, y, reduced=False):
+        _check(lib().etq_apply_saddle(self.h, int(reduced), _ptr(x), _ptr(y)), "etq_apply_saddle")
+        return y
+
+    def precond_setup(self, kind, params: PcParams | None = None):
+        _check(lib().etq_precond_setup(self.h, kind, C.byref(params) if params is not None else None),
+               "etq_precond_setup")
+
+    def apply_precond(self, kind, r, z):
+        _check(lib().etq_apply_precond(self.h, kind, _ptr(r), _ptr(z)), "etq_apply_precond")
+        return z
+
+    def apply_vcycle(self, kind, r_u, z_u):
+        _check(lib().etq_apply_vcycle(self.h, kind, _ptr(r_u), _ptr(z_u)), "etq_apply_vcycle")
+        return z_u
+
+    def apply_mass_pc(self, r_p, z_p):
+        _check(lib().etq_apply_mass_pc(self.h, _ptr(r_p), _ptr(z_p)), "etq_apply_mass_pc")
+        return z_p
+
+    def apply_mass(self, x_p, y_p):
+        _check(lib().etq_apply_mass(self.h, _ptr(x_p), _ptr(y_p)), "etq_apply_mass")
+        return y_p
+
+    def sgs_sweep(self, r_p, y_p, z_p):
+        _check(lib().etq_sgs_sweep(self.h, _ptr(r_p), _ptr(y_p), _ptr(z_p)), "etq_sgs_sweep")
+        return z_p
+
+    def estimate_sgs_lo(self, v0, steps):
+        lam = C.c_double()
+        _check(lib().etq_estimate_sgs_lo(self.h, _ptr(v0), steps, C.byref(lam)), "etq_estimate_sgs_lo")
+        return lam.value
+
+    def get_cheb_sgs_lo(self):
+        a = C.c_double()
+        _check(lib().etq_get_cheb_sgs_lo(self.h, C.byref(a)), "etq_get_cheb_sgs_lo")
+        return a.value
+
+    def time_kernel(self, which, reps=20):
+        """(ms per launch, algorithmic bytes per launch) of hot kernel `which` (etq_time_kernel)."""
+        ms, by = C.c_double(), C.c_double()
+        _check(lib().etq_time_kernel(self.h, which, reps, C.byref(ms), C.byref(by)), "etq_time_kernel")
+        return ms.value, by.value
+
+    def _report(self, cap):
+        import numpy as np
+        rep = Report()
+        hist = np.zeros(cap); dl = np.zeros(cap); gm = np.zeros(cap)
+        rep.history = hist.ctypes.data_as(C.POINTER(C.c_double)); rep.history_cap = cap
+        rep.lanczos_delta = dl.ctypes.data_as(C.POINTER(C.c_double))
+        rep.lanczos_gamma = gm.ctypes.data_as(C.POINTER(C.c_double)); rep.lanczos_cap = cap
+        return rep, hist, dl, gm
+
+    @staticmethod
+    def _report_dict(rep, hist, dl, gm, status):
+        k = rep.iterations
+        return {"status": status, "iterations": k, "converged": bool(rep.converged), "rel_res": rep.rel_res,
+                "abs_res": rep.abs_res, "ms_total": rep.ms_total, "history": hist[:k].copy(),
+                "delta": dl[:k].copy(), "gamma": gm[:k].copy()}
+
+    def minres_solve(self, kind, b, x, rtol=1e-8, maxit=1000):
+        rep, hist, dl, gm = self._report(maxit + 1)
+        s = _check(lib().etq_minres_solve(self.h, kind, _ptr(b), _ptr(x), rtol, maxit, C.byref(rep)),
+                   "etq_minres_solve")
+        return self._report_dict(rep, hist, dl, gm, s)
+
+    def minres_solve_host(self, kind, b_host, x_host, rtol=1e-8, maxit=1000):
+        """b_host, x_host: contiguous float64 CPU tensors or numpy arrays (x in/out)."""
+        rep, hist, dl, gm = self._report(maxit + 1)
+        pb = C.c_void_p(b_host.data_ptr() if hasattr(b_host, "data_ptr") else b_host.ctypes.data)
+        px = C.c_void_p(x_host.data_ptr() if hasattr(x_host, "data_ptr") else x_host.ctypes.data)
+        s = _check(lib().etq_minres_solve_host(self.h, kind, pb, px, rtol, maxit, C.byref(rep)),
+                   "etq_minres_solve_host")
+        return self._report_dict(rep, hist, dl, gm, s)
+
+    def export_operator(self, which, level=0):
+        """Assembled operator as a scipy CSR matrix (host copy; tests only)."""
+        import numpy as np
+        import scipy.sparse as sp
+        nr, nz = C.c_int64(), C.c_int64()
+        _check(lib().etq_export_operator(self.h, which, level, C.byref(nr), C.byref(nz), None, None, None),
+               "etq_export_operator")
+        rp = np.zeros(nr.value + 1, dtype=np.int64)
+        col = np.zeros(max(nz.value, 1), dtype=np.int32)
+        val = np.zeros(max(nz.value, 1))
+        _check(lib().etq_export_operator(self.h, which, level, C.byref(nr), C.byref(nz),
+                                         C.c_void_p(rp.ctypes.data), C.c_void_p(col.ctypes.data),
+                                         C.c_void_p(val.ctypes.data)), "etq_export_operator")
+        ncol = {0: nr.value, 1: self.n_u, 2: self.n_p}[which]
+        return sp.csr_matrix((val[:nz.value], col[:nz.value], rp), shape=(nr.value, ncol))
