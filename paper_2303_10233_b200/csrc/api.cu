@@ -138,7 +138,13 @@ etq_status etq_assemble(const etq_grid* grid, double viscosity, const etq_wind* 
 #define A_CHECK(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) { etq_last_cuda_error(_e, __FILE__, __LINE__); return fail(ETQ_ECUDA); } } while (0)
 #define A_TRY(expr) do { etq_status _s = (expr); if (_s < 0) return fail(_s); } while (0)
   A_CHECK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
-  A_CHECK(cudaStreamCreateWithFlags(&P.aux, cudaStreamNonBlocking));
+  {
+    // the latency-bound pressure branch gets the higher stream priority so its blocks are
+    // scheduled between the bandwidth-bound V-cycle blocks
+    int lo_prio = 0, hi_prio = 0;
+    A_CHECK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    A_CHECK(cudaStreamCreateWithPriority(&P.aux, cudaStreamNonBlocking, hi_prio));
+  }
   cudaEvent_t* evs[4] = {&P.ev_in, &P.ev_out, &P.ev_fork, &P.ev_join};
   for (auto e : evs) A_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   A_CHECK(cudaEventCreate(&P.ev_t0));

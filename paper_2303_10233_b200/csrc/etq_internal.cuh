@@ -37,7 +37,7 @@ void etq_count_launch(int64_t k = 1);   // host-side launch counter (etq_launch_
 
 constexpr int SELL_C = 32;           // slice height = warp size
 constexpr int RED_BLOCKS = 592;      // 4 x 148 SMs: grid of plain reduction kernels
-constexpr int RED_MAXB = 2368;       // max blocks of any reducing kernel (16 x 148)
+constexpr int RED_MAXB = 8192;       // max blocks of any reducing kernel
 constexpr int RED_SLOTS = 16;        // reduction slots per site (see solvers.cu for the map)
 
 // ---------------------------------------------------------------- SELL-32

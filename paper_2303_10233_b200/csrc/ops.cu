@@ -33,16 +33,21 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Linear thread index / block size (kernels may use 2D blocks).
+__device__ __forceinline__ int lin_tid() { return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z); }
+__device__ __forceinline__ int lin_bs() { return blockDim.x * blockDim.y * blockDim.z; }
+
 // Block sum; the result is valid in thread 0.  Safe to call repeatedly in one kernel.
 __device__ double block_sum(double v) {
   __shared__ double sh[32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int t = lin_tid();
+  const int lane = t & 31, wid = t >> 5;
   v = warp_sum(v);
   __syncthreads();
   if (lane == 0) sh[wid] = v;
   __syncthreads();
-  const int nw = (blockDim.x + 31) >> 5;
-  v = (threadIdx.x < nw) ? sh[threadIdx.x] : 0.0;
+  const int nw = (lin_bs() + 31) >> 5;
+  v = (t < nw) ? sh[t] : 0.0;
   if (wid == 0) v = warp_sum(v);
   return v;
 }
@@ -52,15 +57,16 @@ __device__ double block_sum(double v) {
 template <int NV>
 __device__ void reduce_finish(const double (&v)[NV], RedSite site, int slot, double* out) {
   __shared__ bool last;
+  const int t = lin_tid(), bs = lin_bs();
   double tot[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) tot[k] = block_sum(v[k]);
-  if (threadIdx.x == 0) {
+  if (t == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) site.partials[(int64_t)(slot + k) * MAXB + blockIdx.x] = tot[k];
     __threadfence();
-    unsigned t = atomicAdd(site.counter + slot, 1u);
-    last = (t == gridDim.x - 1);
+    unsigned c = atomicAdd(site.counter + slot, 1u);
+    last = (c == gridDim.x - 1);
   }
   __syncthreads();
   if (last) {
@@ -68,12 +74,12 @@ __device__ void reduce_finish(const double (&v)[NV], RedSite site, int slot, dou
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       double s = 0.0;
-      for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+      for (int i = t; i < (int)gridDim.x; i += bs)
         s += __ldcg(site.partials + (int64_t)(slot + k) * MAXB + i);
       s = block_sum(s);
-      if (threadIdx.x == 0) out[k] = s;
+      if (t == 0) out[k] = s;
     }
-    if (threadIdx.x == 0) site.counter[slot] = 0u;
+    if (t == 0) site.counter[slot] = 0u;
   }
 }
 
@@ -418,111 +424,186 @@ __global__ void k_mass_apply(MassGeo g, const double* x, double* y) {
   }
 }
 
-// Gauss-Seidel value of Q1 vertex (a,c): (r' - sum_{q != p} M_pq z_q) / M_pp, r' = r - alpha k
-__device__ __forceinline__ double gs_vertex(const MassGeo& g, int a, int c, double rp, const double* z) {
-  const int n = g.n, n1 = n + 1; const double h = g.h, r = 0.25 * h * h;
-  double s = rp;
-  for (int cc = max(0, c - 1); cc <= min(n, c + 1); ++cc) {
-    const double mc = ml1(n, h, c, cc);
-    for (int aa = max(0, a - 1); aa <= min(n, a + 1); ++aa)
-      if (aa != a || cc != c) s -= mc * ml1(n, h, a, aa) * z[aa + n1 * cc];
-  }
-  for (int f = max(0, c - 1); f <= min(n - 1, c); ++f)
-    for (int e = max(0, a - 1); e <= min(n - 1, a); ++e) s -= r * z[g.nk + e + n * f];
-  return s / (ml1(n, h, a, a) * ml1(n, h, c, c));
-}
-__device__ __forceinline__ double gs_cell(const MassGeo& g, int e, int f, double rt, const double* z) {
-  const int n1 = g.n + 1; const double h = g.h, r = 0.25 * h * h;
-  const double s1 = z[e + n1 * f] + z[e + 1 + n1 * f] + z[e + n1 * (f + 1)] + z[e + 1 + n1 * (f + 1)];
-  return (rt - r * s1) / (h * h);
-}
+// ---------------------------------------------------------------- temporally blocked SGS
+// One launch = one symmetric Gauss-Seidel sweep S(y) on M_Q z = r' (r' = r - alpha k, reading R6)
+// in the colour order 0,1,2,3,P0 | P0,3,2,1,0 (reading R7; the repeated P0 update is idempotent
+// and done once), fused with the Chebyshev semi-iteration update of P:455 (mode 1):
+//     out = omega (gam (S(y) - y) + y - yp) + yp          (mode 0: out = S(y)).
+// Each CTA owns a T x T tile of Q1 vertices (and the P0 cells whose lower-left vertex is in the
+// tile), loads it with a halo of SGS_H = 9 (the dependency radius of the 9 colour steps) into
+// shared memory, runs all colour steps there and writes only its tile: the 16.8 MB pressure
+// vectors are read once per Chebyshev step instead of once per colour step.
+constexpr int SGS_H = 10;             // halo >= 9 (dependency radius of the 9 colour steps); even
+constexpr int SGS_W = 64;              // loaded window
+constexpr int SGS_T = SGS_W - 2 * SGS_H;   // 44: tile origin A0 = 44 t - 10 is even
+constexpr int SGS_P = SGS_W / 2;       // colour-plane side (32)
+constexpr int SGS_TX = 32, SGS_TY = 16;
+constexpr int SGS_SMEM = (4 * SGS_P * SGS_P + SGS_W * SGS_W) * (int)sizeof(double);
 
-struct SgsArgs {
+struct SgsTileArgs {
   MassGeo g;
   const double* r;          // right-hand side (n_p)
-  const double* kproj;      // optional device scalar: r' = r - (kproj / kk) k
+  const double* kproj;      // optional device scalar k^T r: r' = r - (kproj / k^T k) k
   double inv_kk;
+  const double* y;          // current iterate (nullable = 0)
+  const double* yp;         // previous iterate (nullable = 0)
+  double* out;
+  int mode;                 // 0: out = S(y); 1: Chebyshev combination
+  double omega, gam;
+  int tiles_x;
+  RedSite site; int slot; double* kout;   // optional k^T out
   const double* done;
 };
-__device__ __forceinline__ double rhs_at(const SgsArgs& a, int64_t i) {
-  double v = a.r[i];
-  if (a.kproj) v -= (*a.kproj * a.inv_kk) * (i < a.g.nk ? 1.0 : -1.0);
-  return v;
-}
 
-// in-place update of one vertex colour (0..3) or of all cells (colour 4) of t
-__global__ void k_sgs_colour(SgsArgs a, int colour, double* t) {
-  if (is_done(a.done)) return;
-  const MassGeo& g = a.g;
-  const int n = g.n, n1 = n + 1;
-  if (colour < 4) {
-    const int px = colour & 1, py = colour >> 1;
-    const int cx = (n - px) / 2 + 1, cy = (n - py) / 2 + 1;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < (int64_t)cx * cy;
-         q += (int64_t)gridDim.x * blockDim.x) {
-      const int a_ = 2 * (int)(q % cx) + px, c_ = 2 * (int)(q / cx) + py;
-      const int64_t p = a_ + (int64_t)n1 * c_;
-      t[p] = gs_vertex(g, a_, c_, rhs_at(a, p), t);
-    }
-  } else {
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < g.n0; q += (int64_t)gridDim.x * blockDim.x) {
-      const int e = (int)(q % n), f = (int)(q / n);
-      t[g.nk + q] = gs_cell(g, e, f, rhs_at(a, g.nk + q), t);
-    }
+// Shared-memory layout: the 64 x 64 window of Q1 vertices is stored as four 32 x 32 colour
+// planes V[c][j][i] <-> local vertex (2i + px, 2j + py), c = px + 2 py, so a warp updating one
+// colour touches consecutive words; cells are one 64 x 64 plane C[lc][la] (lower-left vertex).
+struct SgsSmem {
+  double* V;   // [4][32][32]
+  double* C;   // [64][64]
+  __device__ __forceinline__ double& v(int c, int i, int j) const { return V[(c * SGS_P + j) * SGS_P + i]; }
+  __device__ __forceinline__ double& vl(int la, int lc) const {   // by local vertex coordinates
+    return V[((((la & 1) + 2 * (lc & 1)) * SGS_P) + (lc >> 1)) * SGS_P + (la >> 1)];
   }
-}
+  __device__ __forceinline__ double& cl(int la, int lc) const { return C[lc * SGS_W + la]; }
+};
 
-// first kernel of a sweep: t = y (y nullable -> 0) with colour 0 updated from y
-__global__ void k_sgs_first(SgsArgs a, const double* y, double* t) {
-  if (is_done(a.done)) return;
-  const MassGeo& g = a.g;
-  const int n1 = g.n + 1;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)g.nk + g.n0;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double v = y ? y[i] : 0.0;
-    if (i < g.nk) {
-      const int a_ = (int)(i % n1), c_ = (int)(i / n1);
-      if (((a_ & 1) | ((c_ & 1) << 1)) == 0) {
-        if (y) v = gs_vertex(g, a_, c_, rhs_at(a, i), y);
-        else {   // neighbours are zero
-          const double h = g.h;
-          v = rhs_at(a, i) / (ml1(g.n, h, a_, a_) * ml1(g.n, h, c_, c_));
+// update of colour (PX, PY) vertices owned by this thread: plane column i = tx, rows j = ty, ty + 16
+template <int PX, int PY>
+__device__ __forceinline__ void sgs_colour(const SgsSmem& S, const double (&rr)[2], int A0, int C0, int n,
+                                           double w_in, double w_bd, double w_off, double rq, double c_dd,
+                                           double c_ed, double inv_in2) {
+  constexpr int c = PX + 2 * PY, cx = (1 - PX) + 2 * PY, cy = PX + 2 * (1 - PY), cxy = (1 - PX) + 2 * (1 - PY);
+  const int i = threadIdx.x;
+  const int la = 2 * i + PX, ga = A0 + la;
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    const int j = threadIdx.y + SGS_TY * m;
+    const int lc = 2 * j + PY, gc = C0 + lc;
+    if (la == 0 || la == SGS_W - 1 || lc == 0 || lc == SGS_W - 1) continue;   // window edge: garbage halo
+    if (ga < 0 || ga > n || gc < 0 || gc > n) continue;
+    const int iw = i - 1 + PX, ie = i + PX, js = j - 1 + PY, jn = j + PY;
+    if (ga > 0 && ga < n && gc > 0 && gc < n) {
+      const double sd = S.v(cxy, iw, js) + S.v(cxy, ie, js) + S.v(cxy, iw, jn) + S.v(cxy, ie, jn);
+      const double se = S.v(cx, iw, j) + S.v(cx, ie, j) + S.v(cy, i, js) + S.v(cy, i, jn);
+      const double sc = S.cl(la - 1, lc - 1) + S.cl(la, lc - 1) + S.cl(la - 1, lc) + S.cl(la, lc);
+      S.v(c, i, j) = (rr[m] - c_dd * sd - c_ed * se - rq * sc) * inv_in2;
+    } else {   // domain-boundary vertex: 1D mass diagonal 2h/6, neighbours only inside [0, n]
+      const double da0 = (ga == 0 || ga == n) ? w_bd : w_in;
+      const double dc0 = (gc == 0 || gc == n) ? w_bd : w_in;
+      double s = rr[m];
+      for (int dc = -1; dc <= 1; ++dc) {
+        if (gc + dc < 0 || gc + dc > n) continue;
+        const double wc = dc == 0 ? dc0 : w_off;
+        for (int da = -1; da <= 1; ++da) {
+          if ((da == 0 && dc == 0) || ga + da < 0 || ga + da > n) continue;
+          s -= wc * (da == 0 ? da0 : w_off) * S.vl(la + da, lc + dc);
         }
       }
+      for (int df = -1; df <= 0; ++df) {
+        if (gc + df < 0 || gc + df >= n) continue;
+        for (int de = -1; de <= 0; ++de) {
+          if (ga + de < 0 || ga + de >= n) continue;
+          s -= rq * S.cl(la + de, lc + df);
+        }
+      }
+      S.v(c, i, j) = s / (da0 * dc0);
     }
-    t[i] = v;
   }
 }
 
-// last kernel of a sweep: t_fin = t with colour 0 updated from t; then
-//   mode 0: out = t_fin
-//   mode 1: out = omega (gam (t_fin - y) + y - yp) + yp   (Chebyshev semi-iteration step)
-// optional partial sum of k^T out into (site, slot) -> kout
-struct SgsLastArgs {
-  SgsArgs s; const double* t; const double* y; const double* yp; double* out; int mode;
-  double omega, gam;
-  RedSite site; int slot; double* kout;
-};
-__global__ void __launch_bounds__(BS) k_sgs_last(SgsLastArgs a) {
-  if (is_done(a.s.done)) return;
-  const MassGeo& g = a.s.g;
-  const int n1 = g.n + 1;
+__global__ void __launch_bounds__(SGS_TX * SGS_TY, 2) k_sgs_tile(SgsTileArgs a) {
+  if (is_done(a.done)) return;
+  constexpr int W = SGS_W, T = SGS_T, H = SGS_H;
+  extern __shared__ double sm[];
+  SgsSmem S{sm, sm + 4 * SGS_P * SGS_P};
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int n = a.g.n, n1 = n + 1, nk = a.g.nk;
+  const int A0 = (blockIdx.x % a.tiles_x) * T - H, C0 = (blockIdx.x / a.tiles_x) * T - H;
+  const double alpha = a.kproj ? (*a.kproj * a.inv_kk) : 0.0;
+  // ---- load y (planes, cells) and this thread's right-hand sides into registers
+  double rv[4][2], rc[2][4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int ga = A0 + 2 * tx + (c & 1);
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int gc = C0 + 2 * (ty + SGS_TY * m) + (c >> 1);
+      const bool in = ga >= 0 && ga <= n && gc >= 0 && gc <= n;
+      const int idx = ga + n1 * gc;
+      S.v(c, tx, ty + SGS_TY * m) = (in && a.y) ? a.y[idx] : 0.0;
+      rv[c][m] = in ? __ldg(a.r + idx) - alpha : 0.0;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int la = tx + 32 * u, ga = A0 + la;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int lc = ty + SGS_TY * v, gc = C0 + lc;
+      const bool in = ga >= 0 && ga < n && gc >= 0 && gc < n;
+      const int idx = nk + ga + n * gc;
+      S.cl(la, lc) = (in && a.y) ? a.y[idx] : 0.0;
+      rc[u][v] = in ? __ldg(a.r + idx) + alpha : 0.0;
+    }
+  }
+  __syncthreads();
+  const double h = a.g.h;
+  const double w_in = 4.0 * h / 6.0, w_bd = 2.0 * h / 6.0, w_off = h / 6.0, rq = 0.25 * h * h;
+  const double c_dd = w_off * w_off, c_ed = w_off * w_in, inv_in2 = 1.0 / (w_in * w_in), inv_q0 = 1.0 / (h * h);
+#define SGS_V(PX, PY) do { sgs_colour<PX, PY>(S, rv[PX + 2 * PY], A0, C0, n, w_in, w_bd, w_off, rq, c_dd, c_ed, inv_in2); __syncthreads(); } while (0)
+  SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
+  // P0 cells (once: the backward sweep's P0 update would repeat it exactly)
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int la = tx + 32 * u, ga = A0 + la;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int lc = ty + SGS_TY * v, gc = C0 + lc;
+      if (la == W - 1 || lc == W - 1 || ga < 0 || ga >= n || gc < 0 || gc >= n) continue;
+      S.cl(la, lc) = (rc[u][v] - rq * (S.vl(la, lc) + S.vl(la + 1, lc) + S.vl(la, lc + 1) + S.vl(la + 1, lc + 1))) * inv_q0;
+    }
+  }
+  __syncthreads();
+  SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
+#undef SGS_V
+  // ---- write the tile with the semi-iteration update
   double kd = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)g.nk + g.n0;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double v = a.t[i];
-    if (i < g.nk) {
-      const int a_ = (int)(i % n1), c_ = (int)(i / n1);
-      if (((a_ & 1) | ((c_ & 1) << 1)) == 0) v = gs_vertex(g, a_, c_, rhs_at(a.s, i), a.t);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int la = 2 * tx + (c & 1), ga = A0 + la;
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int lc = 2 * (ty + SGS_TY * m) + (c >> 1), gc = C0 + lc;
+      if (la < H || la >= H + T || lc < H || lc >= H + T || ga > n || gc > n) continue;
+      const int idx = ga + n1 * gc;
+      const double v = S.v(c, tx, ty + SGS_TY * m);
+      double o = v;
+      if (a.mode) {
+        const double y = a.y ? a.y[idx] : 0.0, yp = a.yp ? a.yp[idx] : 0.0;
+        o = a.omega * (a.gam * (v - y) + y - yp) + yp;
+      }
+      a.out[idx] = o;
+      kd += o;
     }
-    double o;
-    if (a.mode == 0) o = v;
-    else {
-      const double y = a.y ? a.y[i] : 0.0, yp = a.yp ? a.yp[i] : 0.0;
-      o = a.omega * (a.gam * (v - y) + y - yp) + yp;
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int la = tx + 32 * u, ga = A0 + la;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int lc = ty + SGS_TY * v, gc = C0 + lc;
+      if (la < H || la >= H + T || lc < H || lc >= H + T || ga >= n || gc >= n) continue;
+      const int idx = nk + ga + n * gc;
+      const double val = S.cl(la, lc);
+      double o = val;
+      if (a.mode) {
+        const double y = a.y ? a.y[idx] : 0.0, yp = a.yp ? a.yp[idx] : 0.0;
+        o = a.omega * (a.gam * (val - y) + y - yp) + yp;
+      }
+      a.out[idx] = o;
+      kd -= o;
     }
-    a.out[i] = o;
-    kd += (i < g.nk) ? o : -o;
   }
   if (a.kout) { double v[1] = {kd}; reduce_finish<1>(v, a.site, a.slot, a.kout); }
 }
@@ -806,30 +887,32 @@ void mass_apply(const Geo& g, const double* x, double* y, cudaStream_t st) {
   k_mass_apply<<<grid_for((int64_t)g.nk + g.n0, BS, 4096), BS, 0, st>>>(mass_geo(g), x, y); etq_count_launch();
 }
 
-// S(y) sweep sequence: [first: colour 0 from y] 1 2 3 P0 3 2 1 [last: colour 0]
-static void sgs_inner(const SgsArgs& a, double* t, cudaStream_t st) {
-  const Geo dummy{};
-  (void)dummy;
-  const int n = a.g.n;
-  const int64_t nv = ((int64_t)(n / 2 + 1)) * (n / 2 + 1);
-  const int gv = grid_for(nv, BS, 4096), gc = grid_for(a.g.n0, BS, 4096);
-  const int seq[7] = {1, 2, 3, 4, 3, 2, 1};
-  for (int q = 0; q < 7; ++q) {
-    k_sgs_colour<<<seq[q] == 4 ? gc : gv, BS, 0, st>>>(a, seq[q], t);
-    etq_count_launch();
+static void launch_sgs_tile(SgsTileArgs a, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sgs_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, SGS_SMEM);
+    attr = true;
   }
+  a.tiles_x = (a.g.n + 1 + SGS_T - 1) / SGS_T;
+  const int tiles = a.tiles_x * a.tiles_x;
+  k_sgs_tile<<<tiles, dim3(SGS_TX, SGS_TY), SGS_SMEM, st>>>(a); etq_count_launch();
 }
 
+// z = S(y) (one symmetric sweep from y; y nullable = 0); t is scratch for the in-place case
 void sgs_sweep_dev(const Geo& g, const double* r, const double* y, double* z, double* t, cudaStream_t st) {
-  SgsArgs a{mass_geo(g), r, nullptr, 0.0, nullptr};
+  SgsTileArgs a{};
+  a.g = mass_geo(g); a.r = r; a.kproj = nullptr; a.inv_kk = 0.0;
+  a.y = y; a.yp = nullptr; a.mode = 0; a.omega = 1.0; a.gam = 1.0;
+  a.site = RedSite{}; a.slot = 0; a.kout = nullptr; a.done = nullptr;
   const int64_t np = (int64_t)g.nk + g.n0;
-  const int gf = grid_for(np, BS, RED_BLOCKS);
-  k_sgs_first<<<gf, BS, 0, st>>>(a, y, t); etq_count_launch();
-  sgs_inner(a, t, st);
-  SgsLastArgs la;
-  la.s = a; la.t = t; la.y = nullptr; la.yp = nullptr; la.out = z; la.mode = 0; la.omega = 1; la.gam = 1;
-  la.site = RedSite{}; la.slot = 0; la.kout = nullptr;
-  k_sgs_last<<<gf, BS, 0, st>>>(la); etq_count_launch();
+  if (y == z) {
+    a.out = t;
+    launch_sgs_tile(a, st);
+    cudaMemcpyAsync(z, t, sizeof(double) * np, cudaMemcpyDeviceToDevice, st);
+  } else {
+    a.out = z;
+    launch_sgs_tile(a, st);
+  }
 }
 
 // z_p = Pi C Pi r_p (reading R6) with C = m-step Chebyshev semi-iteration on SGS (reading R7)
@@ -842,9 +925,8 @@ etq_status mass_pc_apply_ex(const Problem& P, const double* r_p, double* z_p, co
   const double inv_kk = 1.0 / (double)np;
   const int gf = grid_for(np, BS, RED_BLOCKS);
   RedSite rs = *site;
-  // k^T r
+  // k^T r (Pi applied on the fly inside the sweeps)
   k_kdot<<<gf, BS, 0, st>>>(g.nk, np, r_p, rs, 3, P.dscal + S_KR, done); etq_count_launch();
-  SgsArgs a{mass_geo(g), r_p, P.dscal + S_KR, inv_kk, done};
   const double rho = 1.0 - M.a;
   const double gam = 2.0 / (2.0 - rho), rh = rho / (2.0 - rho);
   double omega = 1.0;
@@ -854,14 +936,13 @@ etq_status mass_pc_apply_ex(const Problem& P, const double* r_p, double* z_p, co
   for (int k = 0; k < M.m; ++k) {
     if (k == 1) omega = 1.0 / (1.0 - 0.5 * rh * rh);
     else if (k > 1) omega = 1.0 / (1.0 - 0.25 * rh * rh * omega);
-    k_sgs_first<<<gf, BS, 0, st>>>(a, cur, M.t); etq_count_launch();
-    sgs_inner(a, M.t, st);
     double* out = bufs[nb]; nb ^= 1;
-    SgsLastArgs la;
-    la.s = a; la.t = M.t; la.y = cur; la.yp = prev; la.out = out; la.mode = 1;
-    la.omega = (k == 0) ? 1.0 : omega; la.gam = gam;
-    la.site = rs; la.slot = 4; la.kout = (k == M.m - 1) ? P.dscal + S_KY : nullptr;
-    k_sgs_last<<<gf, BS, 0, st>>>(la); etq_count_launch();
+    SgsTileArgs a{};
+    a.g = mass_geo(g); a.r = r_p; a.kproj = P.dscal + S_KR; a.inv_kk = inv_kk;
+    a.y = cur; a.yp = prev; a.out = out; a.mode = 1;
+    a.omega = (k == 0) ? 1.0 : omega; a.gam = gam;
+    a.site = rs; a.slot = 4; a.kout = (k == M.m - 1) ? P.dscal + S_KY : nullptr; a.done = done;
+    launch_sgs_tile(a, st);
     prev = cur; cur = out;
   }
   k_kproject_out<<<gf, BS, 0, st>>>(g.nk, np, cur, P.dscal + S_KY, inv_kk, z_p, dot_with, rs, slot, dot_out, done); etq_count_launch();
