@@ -89,12 +89,55 @@ def chebyshev_smooth(A, dinv, b, x0, lo, hi, degree):
     return x, r
 
 
+def chebyshev_smooth_ellipse(A, dinv, b, x0, lo, hi, bim, degree):
+    """Chebyshev iteration in D^{-1}A for a spectrum enclosed by the ellipse with centre
+    theta = (hi+lo)/2, real semi-axis a = (hi-lo)/2 and imaginary semi-axis bim (Manteuffel's
+    Chebyshev iteration for nonsymmetric matrices; reading R9' for the convection-diffusion
+    block).  Same recurrence as chebyshev_smooth with delta = sqrt(a^2 - bim^2), which is
+    imaginary when bim > a; the coefficients rho_{k+1} rho_k and 2 rho_{k+1}/delta stay real.
+    bim = 0 reduces to chebyshev_smooth."""
+    if bim == 0.0:
+        return chebyshev_smooth(A, dinv, b, x0, lo, hi, degree)
+    theta = 0.5 * (hi + lo)
+    a = 0.5 * (hi - lo)
+    delta = np.sqrt(complex(a * a - bim * bim))
+    sigma = theta / delta
+    rho = 1.0 / sigma
+    if x0 is None:
+        x = np.zeros_like(b)
+        r = b.copy()
+    else:
+        x = x0.copy()
+        r = b - A @ x
+    d = dinv * r / theta
+    for _ in range(degree):
+        x = x + d
+        r = r - A @ d
+        rho_new = 1.0 / (2.0 * sigma - rho)
+        c1 = (rho_new * rho).real
+        c2 = (2.0 * rho_new / delta).real
+        d = c1 * d + c2 * (dinv * r)
+        rho = rho_new
+    return x, r
+
+
+def gershgorin_offdiag(N, A):
+    """max_i sum_{j != i} |N_ij| / |A_ii|: the imaginary semi-axis used for D^{-1}F (reading R9')."""
+    N = N.tocsr().copy()
+    N.setdiag(0.0)
+    N.eliminate_zeros()
+    rs = np.asarray(abs(N).sum(axis=1)).ravel()
+    return float(np.max(rs / np.abs(A.diagonal())))
+
+
 class Hierarchy:
     """Level operators A_l (rediscretised at n/2^l), prolongations and coarse factor."""
 
     def __init__(self, n: int, n_coarse: int = 2, lo: float = 0.16, hi: float = 1.6,
-                 degree: int = 3, operator=None):
-        """operator(g) -> scalar CSR matrix before Dirichlet rows (default: Laplacian)."""
+                 degree: int = 3, operator=None, skew=None):
+        """operator(g) -> scalar CSR matrix before Dirichlet rows (default: Laplacian).
+        skew(g) -> the convection part N of the operator: if given, each level smooths on the
+        ellipse with imaginary semi-axis gershgorin_offdiag(N_l, A_l) (reading R9')."""
         if operator is None:
             operator = fem.laplacian
         self.levels = []
@@ -102,7 +145,10 @@ class Hierarchy:
         while True:
             g = fem.Grid(m)
             A = dirichlet_scalar(operator(g), g)
-            self.levels.append({"n": m, "A": A, "dinv": 1.0 / A.diagonal()})
+            bim = 0.0
+            if skew is not None:
+                bim = gershgorin_offdiag(dirichlet_scalar(skew(g), g), A)
+            self.levels.append({"n": m, "A": A, "dinv": 1.0 / A.diagonal(), "bim": bim})
             if m <= n_coarse:
                 break
             if m % 2:
@@ -111,18 +157,21 @@ class Hierarchy:
         for l in range(len(self.levels) - 1):
             self.levels[l]["P"] = prolongation(self.levels[l + 1]["n"])
         self.coarse_dense = self.levels[-1]["A"].toarray()
+        import scipy.linalg as sla
+        self.coarse_lu = sla.lu_factor(self.coarse_dense)   # LAPACK getrf, as np.linalg.solve
         self.lo, self.hi, self.degree = lo, hi, degree
 
     def vcycle(self, b, l: int = 0):
         """One V-cycle applied to a scalar right-hand side b on level l (reading R9)."""
         lev = self.levels[l]
         if l == len(self.levels) - 1:
-            return np.linalg.solve(self.coarse_dense, b)
-        A, dinv, P = lev["A"], lev["dinv"], lev["P"]
-        x, r = chebyshev_smooth(A, dinv, b, None, self.lo, self.hi, self.degree)
+            import scipy.linalg as sla
+            return sla.lu_solve(self.coarse_lu, b)              # exact coarse solve (LU)
+        A, dinv, P, bim = lev["A"], lev["dinv"], lev["P"], lev["bim"]
+        x, r = chebyshev_smooth_ellipse(A, dinv, b, None, self.lo, self.hi, bim, self.degree)
         ec = self.vcycle(P.T @ r, l + 1)
         x = x + P @ ec
-        x, _ = chebyshev_smooth(A, dinv, b, x, self.lo, self.hi, self.degree)
+        x, _ = chebyshev_smooth_ellipse(A, dinv, b, x, self.lo, self.hi, bim, self.degree)
         return x
 
     def apply_velocity(self, r_u):

@@ -161,3 +161,30 @@ def test_sgs_spectrum_top_is_one_and_lanczos_brackets():
     assert abs(ev[0]) < 1e-12
     est = mass.estimate_cheb_lo(s.MQ, synth.lanczos_start(s.g.n_p), 10, col)
     assert lam_min * (1 - 1e-10) <= est <= 1.0
+
+
+def test_ellipse_chebyshev_closed_form():
+    """Chebyshev iteration on an ellipse (reading R9'): with D = I and a normal matrix whose
+    eigenvalues are mu +- i nu, x = (1 - p(lam))/lam b, p(lam) = T_k((theta-lam)/delta)/T_k(theta/delta),
+    delta = sqrt(a^2 - b^2) possibly imaginary (textbook complex Chebyshev polynomials)."""
+    rng = np.random.default_rng(9)
+    mus = rng.uniform(0.2, 1.5, 6); nus = rng.uniform(0.0, 1.2, 6)
+    blocks = [np.array([[m, -v], [v, m]]) for m, v in zip(mus, nus)]
+    A = sp.csr_matrix(sp.block_diag(blocks))
+    b = rng.standard_normal(12)
+    lo, hi, bim = 0.16, 1.6, 1.3
+    theta, a = 0.5 * (hi + lo), 0.5 * (hi - lo)
+    delta = np.sqrt(complex(a * a - bim * bim))
+    Ad = A.toarray()
+    w, V = np.linalg.eig(Ad)
+    for deg in (1, 2, 3, 4):
+        T = np.polynomial.chebyshev.Chebyshev.basis(deg)
+        p = T((theta - w) / delta) / T(theta / delta)
+        ref = (V @ np.diag((1 - p) / w) @ np.linalg.inv(V) @ b).real
+        x, r = mg.chebyshev_smooth_ellipse(A, np.ones(12), b, None, lo, hi, bim, deg)
+        np.testing.assert_allclose(x, ref, rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(r, b - A @ x, atol=1e-12)
+    # bim = 0 is the real Chebyshev iteration
+    x0, _ = mg.chebyshev_smooth_ellipse(A, np.ones(12), b, None, lo, hi, 0.0, 3)
+    x1, _ = mg.chebyshev_smooth(A, np.ones(12), b, None, lo, hi, 3)
+    np.testing.assert_array_equal(x0, x1)
