@@ -141,11 +141,35 @@ etq_status etq_minres_solve_host(etq_problem* p, etq_pc_kind kind, const double*
 
 /* Export an assembled operator to caller-owned HOST CSR buffers (tests).  which:
  *   0 = scalar velocity operator with Dirichlet rows (L or F_s) of MG level `level`,
- *   1 = B (n_p x n_u), 2 = B^T (n_u x n_p).
+ *   1 = B (n_p x n_u), 2 = B^T (n_u x n_p), 3 = Ap of Q1 level `level` (PCD set up),
+ *   4 = F1 (PCD set up).
  * Call with rowptr == NULL to query *nrows and *nnz. */
 etq_status etq_export_operator(const etq_problem* p, int32_t which, int32_t level,
                                int64_t* nrows, int64_t* nnz,
                                int64_t* rowptr, int32_t* col, double* val);
+
+/* Right-preconditioned restarted GMRES(m) with classical Gram-Schmidt applied twice (
+ * readings R14, R18) on the Oseen system [F B^T; B 0] (reduced = 0, kind = ETQ_PC_OSEEN_M1) or the
+ * reduced Taylor-Hood system [F B1^T; B1 0] (reduced = 1, kind = ETQ_PC_OSEEN_PCD1; the p_0 block of
+ * b is ignored and x's p_0 block is left unchanged).  Stops when the residual estimate
+ * |g_{j+1}| <= rtol * ||b||_2 (Euclidean residual); report.abs_res is the true
+ * ||b - K x||_2 after the last restart, report.history the estimates (entry 0 = ||r_0||).
+ * x is the initial guess on input (device).  Returns ETQ_OK, ETQ_NOT_CONVERGED or an error. */
+etq_status etq_gmres_solve(etq_problem* p, int32_t reduced, etq_pc_kind kind, const double* b, double* x,
+                           double rtol, int32_t restart, int32_t maxit, etq_report* report);
+
+/* Two-stage PCD strategy: Step I = GMRES on the reduced system with the PCD
+ * preconditioner from x = 0, stopped at ||r|| <= c eta ||b_red||; Step II = GMRES on the full
+ * system with M1 from [u1*; q1*; 0], stopped at ||r|| <= eta ||b||.  Both kinds must be set up.
+ * bound_out[0] = ||z*|| (full-system residual at the transition), bound_out[1] = the Prop 3.3 bound
+ * sqrt(c^2 eta^2 ||b_red||^2 + ||g0 - B0 u1*||^2) (reading R16).  x: device output. */
+etq_status etq_two_stage_solve(etq_problem* p, const double* b, double* x, double eta, double c,
+                               int32_t restart, int32_t maxit, etq_report* st1, etq_report* st2,
+                               double bound_out[2]);
+
+/* z_p1 = M_S1^{-1} r_p1 = Ap^{-1} F1 Mp^{-1} r_p1 on the Q1 pressure block (length n_k; PCD set up;
+ * paper order of Eq. (discrete-commutator1x), reading R11).  Test hook of the Step-I Schur apply. */
+etq_status etq_apply_pcd_schur(const etq_problem* p, const double* r_p1, double* z_p1);
 
 /* Number of libetq kernel launches issued so far in this process: direct launches plus the
  * kernel nodes of every graph launch (launches recorded during graph capture are excluded).

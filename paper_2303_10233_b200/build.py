@@ -5,7 +5,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["assemble.cu", "ops.cu", "solvers.cu", "api.cu"]
+SOURCES = ["assemble.cu", "ops.cu", "solvers.cu", "oseen.cu", "api.cu"]
 OUT = os.path.join(HERE, "libetq.so")
 
 
@@ -16,7 +16,7 @@ def nvcc_cmd(out=OUT):
 
 def build(force: bool = False, verbose: bool = True) -> str:
     srcs = [os.path.join(HERE, "csrc", s) for s in SOURCES] + \
-        [os.path.join(HERE, "csrc", "etq_internal.cuh"), os.path.join(os.path.dirname(HERE), "include", "etq.h")]
+        [os.path.join(HERE, "csrc", "etq_internal.cuh"), os.path.join(HERE, "csrc", "device_common.cuh"), os.path.join(os.path.dirname(HERE), "include", "etq.h")]
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(s) for s in srcs):
         return OUT
     cmd = nvcc_cmd()

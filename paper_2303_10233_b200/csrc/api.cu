@@ -219,15 +219,7 @@ etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_para
   if (kind == ETQ_PC_P2_GMG) {
     if (P.oseen) return ETQ_EINVAL;
     if (!is_pow2(P.g.n) || !is_pow2(prm.coarse_n) || prm.coarse_n > P.g.n) return ETQ_EINVAL;
-    if (P.mg.built) {
-      for (size_t l = 0; l < P.mg.lv.size(); ++l) {
-        Level& L = P.mg.lv[l];
-        if (l > 0) sell_free(L.A);
-        cudaFree(L.dinv); cudaFree(L.b); cudaFree(L.x); cudaFree(L.r); cudaFree(L.d0); cudaFree(L.d1);
-        cudaFree(L.coarse_inv);
-      }
-      P.mg = Hierarchy{};
-    }
+    if (P.mg.built) free_hierarchy(P.mg);
     ETQ_TRY(build_hierarchy(P, P.mg, prm.coarse_n, prm.smooth_lo, prm.smooth_hi, prm.smooth_degree));
     ETQ_TRY(mass_pc_alloc(P));
     P.pm.m = prm.cheb_sgs_steps;
@@ -253,6 +245,22 @@ etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_para
     ETQ_CHECK(cudaStreamSynchronize(P.stream));
     return ETQ_OK;
   }
+  if (kind == ETQ_PC_OSEEN_M1 || kind == ETQ_PC_OSEEN_PCD1) {
+    if (!P.oseen) return ETQ_EINVAL;
+    if (!is_pow2(P.g.n)) return ETQ_EINVAL;
+    if (kind == ETQ_PC_OSEEN_M1) {   // Chebyshev-SGS for the -(1/nu) M_Q~ block
+      ETQ_TRY(mass_pc_alloc(P));
+      P.pm.m = prm.cheb_sgs_steps;
+      double a = prm.cheb_sgs_lo;
+      if (!(a > 0.0)) a = 2.0 / ((double)P.pm.m * P.pm.m);
+      P.pm.a = a;
+      P.pm.ready = true;
+    }
+    ETQ_TRY(oseen_setup(P, kind));
+    if (P.gmres_graph) { cudaGraphExecDestroy(P.gmres_graph); P.gmres_graph = nullptr; }
+    ETQ_CHECK(cudaStreamSynchronize(P.stream));
+    return ETQ_OK;
+  }
   return ETQ_EINVAL;
 }
 
@@ -266,7 +274,7 @@ etq_status etq_apply_precond(const etq_problem* h, etq_pc_kind kind, const doubl
 etq_status etq_apply_vcycle(const etq_problem* h, etq_pc_kind kind, const double* r_u, double* z_u) {
   if (!h || !r_u || !z_u) return ETQ_EINVAL;
   const Problem& P = h->P;
-  if (kind != ETQ_PC_P2_GMG || !P.mg.built) return ETQ_ENOTSETUP;
+  if (kind == ETQ_PC_P1_EXACT || !P.mg.built) return ETQ_ENOTSETUP;
   StreamScope sc(P);
   return vcycle_apply_ex(P, P.mg, r_u, z_u, nullptr, 0, nullptr, nullptr, nullptr, P.stream);
 }
@@ -345,6 +353,39 @@ etq_status etq_minres_solve_host(etq_problem* h, etq_pc_kind kind, const double*
   return s;
 }
 
+etq_status etq_apply_pcd_schur(const etq_problem* h, const double* r_p1, double* z_p1) {
+  if (!h || !r_p1 || !z_p1) return ETQ_EINVAL;
+  const Problem& P = h->P;
+  StreamScope sc(P);
+  return pcd_schur_apply(P, r_p1, z_p1, P.stream);
+}
+
+etq_status etq_gmres_solve(etq_problem* h, int32_t reduced, etq_pc_kind kind, const double* b, double* x,
+                           double rtol, int32_t restart, int32_t maxit, etq_report* report) {
+  if (!h || !b || !x || !(rtol > 0.0) || restart < 1 || maxit < 1) return ETQ_EINVAL;
+  if (kind != ETQ_PC_OSEEN_M1 && kind != ETQ_PC_OSEEN_PCD1) return ETQ_EINVAL;
+  if (kind == ETQ_PC_OSEEN_PCD1 && !reduced) return ETQ_EINVAL;   // PCD1 preconditions the reduced system
+  Problem& P = h->P;
+  StreamScope sc(P);
+  const double* bb = b;
+  if (reduced) {
+    double* bred;
+    ETQ_TRY(make_reduced_rhs(P, b, &bred));
+    bb = bred;
+  }
+  // tolerance relative to ||b|| (reading R14): computed on the device inside gmres_run
+  const double nb = host_norm(P, bb, P.N);
+  return gmres_run(P, reduced != 0, kind, bb, x, rtol * nb, restart, maxit, report, nullptr);
+}
+
+etq_status etq_two_stage_solve(etq_problem* h, const double* b, double* x, double eta, double c, int32_t restart,
+                               int32_t maxit, etq_report* st1, etq_report* st2, double bound_out[2]) {
+  if (!h || !b || !x || !(eta > 0.0) || !(c > 0.0) || restart < 1 || maxit < 1) return ETQ_EINVAL;
+  Problem& P = h->P;
+  StreamScope sc(P);
+  return two_stage_run(P, b, x, eta, c, restart, maxit, st1, st2, bound_out);
+}
+
 etq_status etq_export_operator(const etq_problem* h, int32_t which, int32_t level, int64_t* nrows, int64_t* nnz,
                                int64_t* rowptr, int32_t* col, double* val) {
   if (!h || !nrows || !nnz) return ETQ_EINVAL;
@@ -362,6 +403,14 @@ etq_status etq_export_operator(const etq_problem* h, int32_t which, int32_t leve
   } else if (which == 1) {
     parts.push_back({&P.B, {0, 0}});
     R = P.n_p;
+  } else if (which == 3) {
+    if (!P.apH.built || level < 0 || level >= (int)P.apH.lv.size()) return ETQ_EINVAL;
+    parts.push_back({&P.apH.lv[level].A, {0, 0}});
+    R = P.apH.lv[level].A.nrows;
+  } else if (which == 4) {
+    if (!P.pcd_ready) return ETQ_EINVAL;
+    parts.push_back({&P.F1, {0, 0}});
+    R = P.F1.nrows;
   } else if (which == 2) {
     parts.push_back({&P.BxT1, {0, 0}});
     parts.push_back({&P.BxT0, {0, P.g.nk}});
@@ -461,12 +510,8 @@ void etq_destroy(etq_problem* h) {
   Problem& P = h->P;
   if (P.stream) cudaStreamSynchronize(P.stream);
   for (int g = 0; g < 2; ++g) if (P.minres_graph[g]) cudaGraphExecDestroy(P.minres_graph[g]);
-  for (size_t l = 0; l < P.mg.lv.size(); ++l) {
-    Level& L = P.mg.lv[l];
-    if (l > 0) sell_free(L.A);
-    cudaFree(L.dinv); cudaFree(L.b); cudaFree(L.x); cudaFree(L.r); cudaFree(L.d0); cudaFree(L.d1);
-    cudaFree(L.coarse_inv);
-  }
+  free_hierarchy(P.mg);
+  oseen_free(P);
   P.Lv.perm = nullptr; P.BxT1.perm = nullptr; P.ByT1.perm = nullptr; P.BxT0.perm = nullptr; P.ByT0.perm = nullptr;
   sell_free(P.Lv); sell_free(P.BxT1); sell_free(P.ByT1); sell_free(P.BxT0); sell_free(P.ByT0); sell_free(P.B);
   if (P.node_perm) cudaFree(P.node_perm);

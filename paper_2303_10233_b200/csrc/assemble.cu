@@ -15,6 +15,7 @@
 // are dropped from L, F and B, and their contribution is lifted into the right-hand side.
 #include "etq_internal.cuh"
 #include <cstdio>
+#include <cstring>
 
 namespace {
 
@@ -192,6 +193,83 @@ __device__ int b_row(const BParams& P, int row, Emit& emit) {
   return cnt;
 }
 
+// Ap = B1 Mdiag^{-1} B1^T on Q1 vertices (reading R12/R13): row p gathers over the
+// interior velocity nodes of its B1 support and accumulates into a 5 x 5 vertex window.
+struct ApParams { Geo g; };
+template <class Emit>
+__device__ int ap_row(const ApParams& P, int row, Emit& emit) {
+  const int m = P.g.m, n = P.g.n; const double h = P.g.h;
+  const int a = row % (n + 1), c = row / (n + 1);
+  double acc[25];
+#pragma unroll
+  for (int k = 0; k < 25; ++k) acc[k] = 0.0;
+  for (int jj = max(1, 2 * c - 2); jj <= min(m - 2, 2 * c + 2); ++jj) {
+    for (int ii = max(1, 2 * a - 2); ii <= min(m - 2, 2 * a + 2); ++ii) {
+      const double bx = -g1(n, a, ii) * h1(n, h, c, jj), by = -h1(n, h, a, ii) * g1(n, c, jj);
+      if (bx == 0.0 && by == 0.0) continue;
+      const double md = m1(n, h, ii, ii) * m1(n, h, jj, jj);   // diagonal of the Q2 mass
+      const double wx = bx / md, wy = by / md;
+      for (int cc = max(0, jj / 2 - 1); cc <= min(n, jj / 2 + 1); ++cc) {
+        if (cc - c > 2 || c - cc > 2) continue;
+        for (int aa = max(0, ii / 2 - 1); aa <= min(n, ii / 2 + 1); ++aa) {
+          if (aa - a > 2 || a - aa > 2) continue;
+          const double qx = -g1(n, aa, ii) * h1(n, h, cc, jj), qy = -h1(n, h, aa, ii) * g1(n, cc, jj);
+          acc[(cc - c + 2) * 5 + (aa - a + 2)] += wx * qx + wy * qy;
+        }
+      }
+    }
+  }
+  int cnt = 0;
+  for (int dc = -2; dc <= 2; ++dc)
+    for (int da = -2; da <= 2; ++da) {
+      const double v = acc[(dc + 2) * 5 + (da + 2)];
+      if (v != 0.0) { emit((a + da) + (n + 1) * (c + dc), v); ++cnt; }
+    }
+  return cnt;
+}
+
+// F1 = nu int grad psi_j . grad psi_i + int (w . grad psi_j) psi_i on Q1, natural
+// boundary (reading R13); for the separable cavity wind the convection part is
+// Aq (x) Tq - Tq (x) Aq with Aq = int (1-x^2) N_b' N_a, Tq = int 2x N_b N_a (3-point Gauss, exact).
+__device__ double q1tab(int which, double h, int e, int a, int b) {
+  const double gx[3] = {0.5 - 0.5 * 0.7745966692414834, 0.5, 0.5 + 0.5 * 0.7745966692414834};
+  const double gw[3] = {5.0 / 18, 8.0 / 18, 5.0 / 18};
+  double s = 0.0;
+  for (int q = 0; q < 3; ++q) {
+    const double xi = gx[q], x = -1.0 + (e + xi) * h;
+    const double Na = a == 0 ? 1.0 - xi : xi, Nb = b == 0 ? 1.0 - xi : xi, dNb = b == 0 ? -1.0 : 1.0;
+    if (which == 0) s += gw[q] * (1.0 - x * x) * dNb * Na;
+    else s += gw[q] * h * 2.0 * x * Nb * Na;
+  }
+  return s;
+}
+__device__ double q1glob(int which, int n, double h, int a, int ap) {   // 0: Aq, 1: Tq, 2: K, 3: M
+  double s = 0.0;
+  for (int e = max(a, ap) - 1; e <= min(a, ap); ++e) {
+    if (e < 0 || e >= n) continue;
+    const int la = a - e, lb = ap - e;
+    if (which <= 1) s += q1tab(which, h, e, la, lb);
+    else if (which == 2) s += (la == lb ? 1.0 : -1.0) / h;
+    else s += (la == lb ? 2.0 : 1.0) * h / 6.0;
+  }
+  return s;
+}
+struct F1Params { Geo g; double nu; int wind; };
+template <class Emit>
+__device__ int f1_row(const F1Params& P, int row, Emit& emit) {
+  const int n = P.g.n; const double h = P.g.h;
+  const int a = row % (n + 1), c = row / (n + 1);
+  int cnt = 0;
+  for (int cc = max(0, c - 1); cc <= min(n, c + 1); ++cc)
+    for (int aa = max(0, a - 1); aa <= min(n, a + 1); ++aa) {
+      double v = P.nu * (q1glob(2, n, h, a, aa) * q1glob(3, n, h, c, cc) + q1glob(3, n, h, a, aa) * q1glob(2, n, h, c, cc));
+      if (P.wind == 1)
+        v += q1glob(0, n, h, a, aa) * q1glob(1, n, h, c, cc) - q1glob(1, n, h, a, aa) * q1glob(0, n, h, c, cc);
+      emit(aa + (n + 1) * cc, v); ++cnt;
+    }
+  return cnt;
+}
+
 struct CountEmit { __device__ void operator()(int, double) {} };
 struct FillEmit {
   int* col; double* val; int64_t base; int k;
@@ -203,6 +281,8 @@ struct FillEmit {
 struct VelFn { VelParams p; template <class E> __device__ int operator()(int r, E& e) const { return vel_row(p, r, e); } };
 struct BtFn { BtParams p; template <class E> __device__ int operator()(int r, E& e) const { return bt_row(p, r, e); } };
 struct BFn { BParams p; template <class E> __device__ int operator()(int r, E& e) const { return b_row(p, r, e); } };
+struct ApFn { ApParams p; template <class E> __device__ int operator()(int r, E& e) const { return ap_row(p, r, e); } };
+struct F1Fn { F1Params p; template <class E> __device__ int operator()(int r, E& e) const { return f1_row(p, r, e); } };
 
 template <class Fn>
 __global__ void k_sell_count(Fn fn, const int* perm, int64_t nrows, int64_t nslices, int* slen,
@@ -377,6 +457,43 @@ __global__ void k_rhs_pressure(Geo g, int bc, double* bp) {
   bp[row] = -s;
 }
 
+
+// max over interior rows of sum_{j != i} |N_ij| / |F_ii| (reading R9': imaginary semi-axis)
+__global__ void k_gershgorin_n(VelParams P, unsigned long long* out) {
+  const int node = blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= P.g.nq) return;
+  const int m = P.g.m, n = P.g.n; const double h = P.g.h;
+  const int i = node % m, j = node / m;
+  if (on_boundary(i, j, m)) return;
+  const int rx = (i & 1) ? 1 : 2, ry = (j & 1) ? 1 : 2;
+  double s = 0.0;
+  for (int dj = -ry; dj <= ry; ++dj) {
+    const int jj = j + dj;
+    if (jj <= 0 || jj >= m - 1) continue;
+    for (int di = -rx; di <= rx; ++di) {
+      const int ii = i + di;
+      if (ii <= 0 || ii >= m - 1 || (di == 0 && dj == 0)) continue;
+      s += fabs(osn1(0, n, h, i, ii) * osn1(1, n, h, j, jj) - osn1(1, n, h, i, ii) * osn1(0, n, h, j, jj));
+    }
+  }
+  const double v = s / fabs(vel_entry(P, i, j, i, j));
+  atomicMax(out, (unsigned long long)__double_as_longlong(v));
+}
+
+__global__ void k_sell_diag_inv(Sell A, double* dinv) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t s = t / SELL_C;
+  if (s >= A.nslices) return;
+  const int lane = (int)(t % SELL_C);
+  const int row = A.perm ? A.perm[t] : (t < A.nrows ? (int)t : -1);
+  if (row < 0) return;
+  double d = 0.0;
+  for (int k = 0; k < A.slen[s]; ++k) {
+    const int64_t e = A.sptr[s] + lane + (int64_t)k * SELL_C;
+    if (A.col[e] == row && A.val[e] != 0.0) d = A.val[e];
+  }
+  dinv[row] = 1.0 / d;
+}
 }  // namespace
 
 // ---------------------------------------------------------------- host entry points
@@ -420,6 +537,38 @@ etq_status build_rhs_dev(const Problem& P, const double* f_nodal, double* b) {
   k_rhs_velocity<<<(P.g.nq + 255) / 256, 256, 0, P.stream>>>(vp, P.bc, f_nodal, b); etq_count_launch();
   ETQ_CHECK(cudaGetLastError());
   k_rhs_pressure<<<(unsigned)((P.n_p + 255) / 256), 256, 0, P.stream>>>(P.g, P.bc, b + P.n_u); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
+etq_status oseen_gershgorin(const Geo& g, double nu, int wind, double* bim, cudaStream_t st) {
+  VelParams P{g, wind == 1 ? 1 : 0, nu};
+  unsigned long long* d;
+  ETQ_TRY(dalloc(&d, 1));
+  ETQ_CHECK(cudaMemsetAsync(d, 0, sizeof(unsigned long long), st));
+  k_gershgorin_n<<<(g.nq + 255) / 256, 256, 0, st>>>(P, d); etq_count_launch();
+  unsigned long long hv = 0;
+  ETQ_CHECK(cudaMemcpyAsync(&hv, d, sizeof(hv), cudaMemcpyDeviceToHost, st));
+  ETQ_CHECK(cudaStreamSynchronize(st));
+  cudaFree(d);
+  double v;
+  std::memcpy(&v, &hv, sizeof(v));
+  *bim = v;
+  return ETQ_OK;
+}
+
+etq_status assemble_ap(const Geo& g, Sell* out, cudaStream_t st) {
+  ApFn fn{ApParams{g}};
+  return build_sell(fn, nullptr, g.nk, ((int64_t)g.nk + SELL_C - 1) / SELL_C, out, st);
+}
+
+etq_status assemble_f1(const Geo& g, double nu, int wind, Sell* out, cudaStream_t st) {
+  F1Fn fn{F1Params{g, nu, wind}};
+  return build_sell(fn, nullptr, g.nk, ((int64_t)g.nk + SELL_C - 1) / SELL_C, out, st);
+}
+
+etq_status sell_diag_inv(const Sell& A, double* dinv, cudaStream_t st) {
+  k_sell_diag_inv<<<(unsigned)((A.nslices * SELL_C + 255) / 256), 256, 0, st>>>(A, dinv); etq_count_launch();
   ETQ_CHECK(cudaGetLastError());
   return ETQ_OK;
 }

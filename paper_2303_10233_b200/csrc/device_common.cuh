@@ -1,0 +1,115 @@
+// device_common.cuh — device helpers shared by the kernel files of libetq: launch sizing,
+// deterministic block/grid reductions, SELL-32 row products.
+#pragma once
+#include "etq_internal.cuh"
+
+// ================================================================ launch helpers
+namespace etqd {
+constexpr int BS = 256;
+constexpr int MAXB = RED_MAXB;
+
+inline int grid_for(int64_t work_items, int per_block, int cap = MAXB) {
+  int64_t g = (work_items + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+__device__ __forceinline__ bool is_done(const double* done) { return done && *done != 0.0; }
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Linear thread index / block size (kernels may use 2D blocks).
+__device__ __forceinline__ int lin_tid() { return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z); }
+__device__ __forceinline__ int lin_bs() { return blockDim.x * blockDim.y * blockDim.z; }
+
+// Block sum; the result is valid in thread 0.  Safe to call repeatedly in one kernel.
+static __device__ double block_sum(double v) {
+  __shared__ double sh[32];
+  const int t = lin_tid();
+  const int lane = t & 31, wid = t >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  const int nw = (lin_bs() + 31) >> 5;
+  v = (t < nw) ? sh[t] : 0.0;
+  if (wid == 0) v = warp_sum(v);
+  return v;
+}
+
+// Store this block's partial of NV sums into `site` and, in the last block to finish, sum the
+// gridDim.x partials in a fixed order into out[0..NV).  Deterministic for a fixed grid.
+template <int NV>
+__device__ void reduce_finish(const double (&v)[NV], RedSite site, int slot, double* out) {
+  __shared__ bool last;
+  const int t = lin_tid(), bs = lin_bs();
+  double tot[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) tot[k] = block_sum(v[k]);
+  if (t == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) site.partials[(int64_t)(slot + k) * MAXB + blockIdx.x] = tot[k];
+    __threadfence();
+    unsigned c = atomicAdd(site.counter + slot, 1u);
+    last = (c == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = 0.0;
+      for (int i = t; i < (int)gridDim.x; i += bs)
+        s += __ldcg(site.partials + (int64_t)(slot + k) * MAXB + i);
+      s = block_sum(s);
+      if (t == 0) out[k] = s;
+    }
+    if (t == 0) site.counter[slot] = 0u;
+  }
+}
+
+// ---------------------------------------------------------------- SELL row products
+__device__ __forceinline__ double sell_row1(const Sell& A, int64_t s, int lane, const double* __restrict__ x) {
+  const int64_t base = A.sptr[s] + lane;
+  const int len = A.slen[s];
+  const int* __restrict__ cp = A.col + base;
+  const double* __restrict__ vp = A.val + base;
+  double acc = 0.0;
+  int k = 0;
+  for (; k + 4 <= len; k += 4) {
+    int c[4]; double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { c[u] = __ldg(cp + (k + u) * SELL_C); v[u] = __ldg(vp + (k + u) * SELL_C); }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc = fma(v[u], __ldg(x + c[u]), acc);
+  }
+  for (; k < len; ++k) acc = fma(__ldg(vp + k * SELL_C), __ldg(x + __ldg(cp + k * SELL_C)), acc);
+  return acc;
+}
+
+__device__ __forceinline__ void sell_row2(const Sell& A, int64_t s, int lane, const double* __restrict__ x0,
+                                          const double* __restrict__ x1, double& a0, double& a1) {
+  const int64_t base = A.sptr[s] + lane;
+  const int len = A.slen[s];
+  const int* __restrict__ cp = A.col + base;
+  const double* __restrict__ vp = A.val + base;
+  int k = 0;
+  for (; k + 4 <= len; k += 4) {
+    int c[4]; double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { c[u] = __ldg(cp + (k + u) * SELL_C); v[u] = __ldg(vp + (k + u) * SELL_C); }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { a0 = fma(v[u], __ldg(x0 + c[u]), a0); a1 = fma(v[u], __ldg(x1 + c[u]), a1); }
+  }
+  for (; k < len; ++k) {
+    const int c = __ldg(cp + k * SELL_C); const double v = __ldg(vp + k * SELL_C);
+    a0 = fma(v, __ldg(x0 + c), a0); a1 = fma(v, __ldg(x1 + c), a1);
+  }
+}
+
+}  // namespace etqd

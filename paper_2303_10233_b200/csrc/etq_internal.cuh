@@ -82,8 +82,10 @@ struct RedSite {
 // ---------------------------------------------------------------- MG level
 struct Level {
   Geo g;
-  Sell A;                     // scalar operator with identity Dirichlet rows
-  double* dinv = nullptr;     // [nq]
+  Sell A;                     // scalar operator (Q2: identity Dirichlet rows; Q1: Ap)
+  double* dinv = nullptr;     // [nrows]
+  int nrows = 0;              // nq (Q2 velocity) or nk (Q1 pressure)
+  double bim = 0.0;           // imaginary semi-axis of the smoother ellipse (0: real interval)
   // two-component work vectors, each [2*nq]
   double *b = nullptr, *x = nullptr, *r = nullptr, *d0 = nullptr, *d1 = nullptr;
   double* coarse_inv = nullptr;   // dense inverse (coarsest level only), nq x nq row-major
@@ -93,6 +95,8 @@ struct Hierarchy {
   std::vector<Level> lv;
   double lo = 0.16, hi = 1.6;
   int degree = 3;
+  int kind = 0;               // 0: Q2 velocity (2 components, Dirichlet rows); 1: Q1 pressure (Ap)
+  int ncomp = 2;
   bool built = false;
 };
 
@@ -101,6 +105,9 @@ enum ScalarIdx {
   S_GAMMA = 0, S_GAMMA_PREV, S_DELTA, S_ETA, S_C, S_C_PREV, S_S, S_S_PREV, S_GAMMA1,
   S_A2, S_A3, S_A1, S_CNEW_ETA, S_DONE, S_STATUS, S_IT, S_RTOL, S_MAXIT,
   S_DOT0, S_DOT1, S_DOT2, S_DOT3, S_DOT4, S_DOT5, S_KR, S_KY, S_INV_GAMMA, S_TMP0, S_TMP1,
+  S_APSUM,
+  // GMRES (solvers in oseen.cu)
+  G_J = 32, G_JW, G_HN, G_RES, G_TOL, G_DONE, G_BREAK, G_TOT, G_BETA, G_MAXIT, G_NRM_P0, G_CAP,
   S_COUNT = 64
 };
 
@@ -148,6 +155,22 @@ struct Problem {
   double* dhist = nullptr;                    // [4 * hist_cap]: |eta|, delta, gamma
   int hist_cap = 0;
 
+  // Oseen preconditioners (oseen.cu)
+  Hierarchy apH;                              // Q1 hierarchy for Ap (PCD)
+  Sell F1;                                    // PCD convection-diffusion on Q1
+  bool pcd_ready = false, m1_ready = false;
+  double* pw[3] = {nullptr, nullptr, nullptr};   // n_k work vectors of the PCD chain
+  double* tu = nullptr;                       // [n_u] r_u - B^T z_p
+  // GMRES workspace
+  double* gV = nullptr; int gm = 0;           // (m+1) x N Arnoldi basis
+  double* gH = nullptr;                       // (m+1) x m Hessenberg (column-major)
+  double* gsm = nullptr;                      // cs[m], sn[m], g[m+1], y[m], hh[m+1]
+  double* gW = nullptr; double* gZ = nullptr; double* gT = nullptr; double* gU = nullptr;
+  double* ghist = nullptr; int ghist_cap = 0;
+  RedSite gred{};                             // 64 slots for the CGS2 multi-dots
+  cudaGraphExec_t gmres_graph = nullptr; int gmres_graph_key = -1;
+  int64_t gmres_graph_nodes = 0;
+
   // Krylov workspace (length N each)
   double* kv[10] = {nullptr};
   int nkv = 0;
@@ -173,6 +196,10 @@ etq_status assemble_bt(const Geo& g, int comp, int part, int* perm, int64_t nsli
                        cudaStream_t st);
 etq_status assemble_b(const Geo& g, Sell* out, cudaStream_t st);
 etq_status velocity_dinv_dev(const Geo& g, bool oseen, double nu, int wind, double* dinv, cudaStream_t st);
+etq_status oseen_gershgorin(const Geo& g, double nu, int wind, double* bim, cudaStream_t st);
+etq_status assemble_ap(const Geo& g, Sell* out, cudaStream_t st);
+etq_status assemble_f1(const Geo& g, double nu, int wind, Sell* out, cudaStream_t st);
+etq_status sell_diag_inv(const Sell& A, double* dinv, cudaStream_t st);
 etq_status build_rhs_dev(const Problem& P, const double* f_nodal, double* b);
 
 // ops.cu
@@ -182,6 +209,9 @@ void launch_vel_spmv(const Sell& A, const double* x, double* y, int nq, cudaStre
 void launch_dot(const double* a, const double* b, int64_t n, RedSite* site, int slot, double* out,
                 const double* done, cudaStream_t st);
 etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, double hi, int degree);
+etq_status build_ap_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, double hi, int degree);
+void free_hierarchy(Hierarchy& H);
+etq_status dense_inverse_pivot(double* A, int m, cudaStream_t st);
 etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r_u, double* z_u,
                            const RedSite* site, int slot, double* dot_out, const double* dot_with,
                            const double* done, cudaStream_t st);
@@ -189,7 +219,8 @@ void mass_apply(const Geo& g, const double* x, double* y, cudaStream_t st);
 void sgs_sweep_dev(const Geo& g, const double* r, const double* y, double* z, double* t, cudaStream_t st);
 etq_status mass_pc_alloc(Problem& P);
 etq_status mass_pc_apply_ex(const Problem& P, const double* r_p, double* z_p, const RedSite* site, int slot,
-                            double* dot_out, const double* dot_with, const double* done, cudaStream_t st);
+                            double* dot_out, const double* dot_with, const double* done, cudaStream_t st,
+                            double scale = 1.0);
 etq_status dense_inverse_spd(double* A, int m, cudaStream_t st);
 etq_status dense_from_sell(const Sell& A, int m, double* D, cudaStream_t st);
 etq_status p1_build_mass_inverse(const Geo& g, double* W, cudaStream_t st);
@@ -200,6 +231,20 @@ int64_t etq_launch_total();
 void cheb_step_level0(const Problem& P, const double* d_in, double* d_out, cudaStream_t st);
 double vcycle_bytes(const Hierarchy& H);
 double cheb_step_bytes(const Level& L);
+
+// oseen.cu
+etq_status oseen_setup(Problem& P, etq_pc_kind kind);
+etq_status oseen_precond_apply(const Problem& P, etq_pc_kind kind, const double* r, double* z, cudaStream_t st);
+etq_status gmres_run(Problem& P, bool reduced, etq_pc_kind kind, const double* b, double* x, double tol_abs,
+                     int restart, int maxit, etq_report* rep, double* p0_res_norm);
+void oseen_free(Problem& P);
+etq_status pcd_schur_apply(const Problem& P, const double* r, double* z, cudaStream_t st);
+etq_status make_reduced_rhs(Problem& P, const double* b, double** bred);
+double host_norm(Problem& P, const double* v, int64_t n);
+etq_status two_stage_run(Problem& P, const double* b, double* x, double eta, double c, int restart, int maxit,
+                         etq_report* r1, etq_report* r2, double* bound);
+etq_status ap_solve(const Problem& P, const Hierarchy& H, const double* r, double* z, double* sum_slot,
+                    const double* done, cudaStream_t st);
 
 // solvers.cu
 void vec_scale_copy(double* y, const double* x, double a, int64_t n, cudaStream_t st);

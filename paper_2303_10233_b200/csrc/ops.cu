@@ -12,116 +12,12 @@
 #include <cmath>
 #include <cstdio>
 #include <vector>
+#include <complex>
 
-// ================================================================ launch helpers
+#include "device_common.cuh"
+using namespace etqd;
+
 namespace {
-constexpr int BS = 256;
-constexpr int MAXB = RED_MAXB;
-
-inline int grid_for(int64_t work_items, int per_block, int cap = MAXB) {
-  int64_t g = (work_items + per_block - 1) / per_block;
-  if (g < 1) g = 1;
-  if (g > cap) g = cap;
-  return (int)g;
-}
-
-__device__ __forceinline__ bool is_done(const double* done) { return done && *done != 0.0; }
-
-// ---------------------------------------------------------------- reductions
-__device__ __forceinline__ double warp_sum(double v) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Linear thread index / block size (kernels may use 2D blocks).
-__device__ __forceinline__ int lin_tid() { return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z); }
-__device__ __forceinline__ int lin_bs() { return blockDim.x * blockDim.y * blockDim.z; }
-
-// Block sum; the result is valid in thread 0.  Safe to call repeatedly in one kernel.
-__device__ double block_sum(double v) {
-  __shared__ double sh[32];
-  const int t = lin_tid();
-  const int lane = t & 31, wid = t >> 5;
-  v = warp_sum(v);
-  __syncthreads();
-  if (lane == 0) sh[wid] = v;
-  __syncthreads();
-  const int nw = (lin_bs() + 31) >> 5;
-  v = (t < nw) ? sh[t] : 0.0;
-  if (wid == 0) v = warp_sum(v);
-  return v;
-}
-
-// Store this block's partial of NV sums into `site` and, in the last block to finish, sum the
-// gridDim.x partials in a fixed order into out[0..NV).  Deterministic for a fixed grid.
-template <int NV>
-__device__ void reduce_finish(const double (&v)[NV], RedSite site, int slot, double* out) {
-  __shared__ bool last;
-  const int t = lin_tid(), bs = lin_bs();
-  double tot[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) tot[k] = block_sum(v[k]);
-  if (t == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) site.partials[(int64_t)(slot + k) * MAXB + blockIdx.x] = tot[k];
-    __threadfence();
-    unsigned c = atomicAdd(site.counter + slot, 1u);
-    last = (c == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (last) {
-    __threadfence();
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      double s = 0.0;
-      for (int i = t; i < (int)gridDim.x; i += bs)
-        s += __ldcg(site.partials + (int64_t)(slot + k) * MAXB + i);
-      s = block_sum(s);
-      if (t == 0) out[k] = s;
-    }
-    if (t == 0) site.counter[slot] = 0u;
-  }
-}
-
-// ---------------------------------------------------------------- SELL row products
-__device__ __forceinline__ double sell_row1(const Sell& A, int64_t s, int lane, const double* __restrict__ x) {
-  const int64_t base = A.sptr[s] + lane;
-  const int len = A.slen[s];
-  const int* __restrict__ cp = A.col + base;
-  const double* __restrict__ vp = A.val + base;
-  double acc = 0.0;
-  int k = 0;
-  for (; k + 4 <= len; k += 4) {
-    int c[4]; double v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { c[u] = __ldg(cp + (k + u) * SELL_C); v[u] = __ldg(vp + (k + u) * SELL_C); }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) acc = fma(v[u], __ldg(x + c[u]), acc);
-  }
-  for (; k < len; ++k) acc = fma(__ldg(vp + k * SELL_C), __ldg(x + __ldg(cp + k * SELL_C)), acc);
-  return acc;
-}
-
-__device__ __forceinline__ void sell_row2(const Sell& A, int64_t s, int lane, const double* __restrict__ x0,
-                                          const double* __restrict__ x1, double& a0, double& a1) {
-  const int64_t base = A.sptr[s] + lane;
-  const int len = A.slen[s];
-  const int* __restrict__ cp = A.col + base;
-  const double* __restrict__ vp = A.val + base;
-  int k = 0;
-  for (; k + 4 <= len; k += 4) {
-    int c[4]; double v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { c[u] = __ldg(cp + (k + u) * SELL_C); v[u] = __ldg(vp + (k + u) * SELL_C); }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { a0 = fma(v[u], __ldg(x0 + c[u]), a0); a1 = fma(v[u], __ldg(x1 + c[u]), a1); }
-  }
-  for (; k < len; ++k) {
-    const int c = __ldg(cp + k * SELL_C); const double v = __ldg(vp + k * SELL_C);
-    a0 = fma(v, __ldg(x0 + c), a0); a1 = fma(v, __ldg(x1 + c), a1);
-  }
-}
-
 // ================================================================ fused saddle SpMV
 struct SaddleArgs {
   Sell L, BxT1, ByT1, BxT0, ByT0, B;
@@ -195,7 +91,13 @@ __global__ void __launch_bounds__(BS) k_vel_spmv2(Sell A, int nq, const double* 
 }
 
 // ================================================================ V-cycle kernels
-// One Chebyshev step fused with the SpMV (Saad Alg. 12.1, reading R9), both components:
+__device__ __forceinline__ int sell_row_id(const Sell& A, int64_t s, int lane) {
+  const int64_t t = s * SELL_C + lane;
+  return A.perm ? A.perm[t] : (t < A.nrows ? (int)t : -1);
+}
+
+// One Chebyshev step fused with the level SpMV (Saad Alg. 12.1; readings R9/R9'), NC components
+// (2: both velocity components share the scalar operator; 1: the Q1 pressure operator Ap):
 //   x_out = x_in + d_in ; r_out = r_in - A d_in ; d_out = c1 d_in + c2 D^{-1} r_out
 struct ChebArgs {
   Sell A; const double* dinv; int nq;
@@ -204,22 +106,24 @@ struct ChebArgs {
   double c1, c2;
   const double* done;
 };
+template <int NC>
 __global__ void __launch_bounds__(BS) k_cheb_step(ChebArgs a) {
   if (is_done(a.done)) return;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t s = gw; s < a.A.nslices; s += nw) {
-    const int row = a.A.perm[s * SELL_C + lane];
-    double q0 = 0.0, q1 = 0.0;
-    sell_row2(a.A, s, lane, a.d_in, a.d_in + a.nq, q0, q1);
+    const int row = sell_row_id(a.A, s, lane);
+    double q[2] = {0.0, 0.0};
+    if (NC == 2) sell_row2(a.A, s, lane, a.d_in, a.d_in + a.nq, q[0], q[1]);
+    else q[0] = sell_row1(a.A, s, lane, a.d_in);
     if (row < 0) continue;
     const double di = a.dinv[row];
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < NC; ++c) {
       const int64_t idx = (int64_t)c * a.nq + row;
       const double dd = a.d_in[idx];
-      const double ro = a.r_in[idx] - (c == 0 ? q0 : q1);
+      const double ro = a.r_in[idx] - q[c];
       a.x_out[idx] = (a.x_in ? a.x_in[idx] : 0.0) + dd;
       if (a.r_out) a.r_out[idx] = ro;
       if (a.d_out) a.d_out[idx] = a.c1 * dd + a.c2 * (di * ro);
@@ -227,7 +131,8 @@ __global__ void __launch_bounds__(BS) k_cheb_step(ChebArgs a) {
   }
 }
 
-// r = b - A x ; d = D^{-1} r / theta  (start of post-smoothing)
+// r = b - A x ; d = D^{-1} r / theta  (start of post-smoothing), NC components
+template <int NC>
 __global__ void __launch_bounds__(BS) k_post_residual(Sell A, const double* dinv, int nq, const double* b,
                                                       const double* x, double* r, double* d, double theta,
                                                       const double* done) {
@@ -236,26 +141,85 @@ __global__ void __launch_bounds__(BS) k_post_residual(Sell A, const double* dinv
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t s = gw; s < A.nslices; s += nw) {
-    const int row = A.perm[s * SELL_C + lane];
-    double q0 = 0.0, q1 = 0.0;
-    sell_row2(A, s, lane, x, x + nq, q0, q1);
+    const int row = sell_row_id(A, s, lane);
+    double q[2] = {0.0, 0.0};
+    if (NC == 2) sell_row2(A, s, lane, x, x + nq, q[0], q[1]);
+    else q[0] = sell_row1(A, s, lane, x);
     if (row < 0) continue;
     const double di = dinv[row];
-    const double r0 = b[row] - q0, r1 = b[nq + row] - q1;
-    r[row] = r0; r[nq + row] = r1;
-    d[row] = di * r0 / theta; d[nq + row] = di * r1 / theta;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int64_t idx = (int64_t)c * nq + row;
+      const double rr = b[idx] - q[c];
+      r[idx] = rr;
+      d[idx] = di * rr / theta;
+    }
   }
 }
 
-// d = D^{-1} b / theta (start of pre-smoothing from x = 0)
-__global__ void k_cheb_init(const double* dinv, int nq, const double* b, double* d, double theta,
+// d = D^{-1} b / theta (start of pre-smoothing from x = 0), NC components
+__global__ void k_cheb_init(const double* dinv, int nq, int nc, const double* b, double* d, double theta,
                             const double* done) {
   if (is_done(done)) return;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * (int64_t)nq;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)nc * nq;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int row = (int)(i % nq);
     d[i] = dinv[row] * b[i] / theta;
   }
+}
+
+// Q1 (pressure) transfers: nested bilinear interpolation, no boundary rows (no pressure BC)
+// b_c = P^T r_f and d0_c = D_c^{-1} b_c / theta
+__global__ void k_restrict_q1(int mf, int mc, const double* rf, double* bc, double* d0c, const double* dinvc,
+                              double theta, const double* done) {
+  if (is_done(done)) return;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)mc * mc;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int I = (int)(t % mc), J = (int)(t / mc);
+    double s = 0.0;
+    for (int dl = -1; dl <= 1; ++dl) {
+      const int l = 2 * J + dl;
+      if (l < 0 || l >= mf) continue;
+      const double wy = dl == 0 ? 1.0 : 0.5;
+      double tt = 0.0;
+      for (int dk = -1; dk <= 1; ++dk) {
+        const int k = 2 * I + dk;
+        if (k < 0 || k >= mf) continue;
+        tt = fma(dk == 0 ? 1.0 : 0.5, rf[(int64_t)l * mf + k], tt);
+      }
+      s = fma(wy, tt, s);
+    }
+    bc[t] = s;
+    d0c[t] = dinvc[t] * s / theta;
+  }
+}
+// x_f += P (x_c + d_c)
+__global__ void k_prolong_q1(int mf, int mc, const double* xc, const double* dc, double* xf, const double* done) {
+  if (is_done(done)) return;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)mf * mf;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(t % mf), l = (int)(t / mf);
+    const int nx = (k & 1) ? 2 : 1, ny = (l & 1) ? 2 : 1;
+    double s = 0.0;
+    for (int q = 0; q < ny; ++q) {
+      const int J = (l >> 1) + q;
+      double tt = 0.0;
+      for (int p = 0; p < nx; ++p) {
+        const int I = (k >> 1) + p;
+        const int64_t c = (int64_t)J * mc + I;
+        tt = fma(nx == 2 ? 0.5 : 1.0, dc ? xc[c] + dc[c] : xc[c], tt);
+      }
+      s = fma(ny == 2 ? 0.5 : 1.0, tt, s);
+    }
+    xf[t] += s;
+  }
+}
+// z -= (sum / n) 1 (mean-zero projection after the Ap V-cycle, reading R13)
+__global__ void k_sub_mean(double* z, int64_t n, const double* sum, const double* done) {
+  if (is_done(done)) return;
+  const double m = *sum / (double)n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    z[i] -= m;
 }
 
 // 1D nested-Q2 transfer weights: coarse node I gathers fine nodes 2I + off
@@ -347,7 +311,7 @@ __global__ void __launch_bounds__(BS) k_final_add(const double* x, const double*
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double v = d ? x[i] + d[i] : x[i];
     z[i] = v;
-    if (dw) dot += v * dw[i];
+    dot += dw ? v * dw[i] : v;     // dw == nullptr: plain sum (mean projection)
   }
   if (out) { double a[1] = {dot}; reduce_finish<1>(a, site, slot, out); }
 }
@@ -621,13 +585,14 @@ __global__ void __launch_bounds__(BS) k_kdot(int nk, int64_t np, const double* x
 
 // z = y - (ky / kk) k, optional partial <z, w>
 __global__ void __launch_bounds__(BS) k_kproject_out(int nk, int64_t np, const double* y, const double* ky,
-                                                     double inv_kk, double* z, const double* w, RedSite site,
-                                                     int slot, double* out, const double* done) {
+                                                     double inv_kk, double scale, double* z, const double* w,
+                                                     RedSite site, int slot, double* out, const double* done) {
   if (is_done(done)) return;
   const double beta = *ky * inv_kk;
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = y[i] - beta * ((i < nk) ? 1.0 : -1.0);
+    double v = y[i] - beta * ((i < nk) ? 1.0 : -1.0);
+    if (scale != 1.0) v *= scale;
     z[i] = v;
     if (w) s += v * w[i];
   }
@@ -733,9 +698,88 @@ etq_status dense_inverse_spd(double* A, int m, cudaStream_t st) {
   return ETQ_OK;
 }
 
+// Gauss-Jordan with partial pivoting on the augmented [A | I] (m x 2m), for the nonsymmetric
+// coarse F of the Oseen V-cycle.  Deterministic (ties -> smallest row index).
+__global__ void k_piv_find(const double* Aug, int m, int p, int* piv) {
+  __shared__ double bv[1024];
+  __shared__ int bi[1024];
+  double best = -1.0; int bidx = p;
+  for (int i = p + threadIdx.x; i < m; i += blockDim.x) {
+    const double v = fabs(Aug[(int64_t)i * 2 * m + p]);
+    if (v > best) { best = v; bidx = i; }
+  }
+  bv[threadIdx.x] = best; bi[threadIdx.x] = bidx;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double o = bv[threadIdx.x + s]; const int oi = bi[threadIdx.x + s];
+      if (o > bv[threadIdx.x] || (o == bv[threadIdx.x] && oi < bi[threadIdx.x])) { bv[threadIdx.x] = o; bi[threadIdx.x] = oi; }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *piv = bi[0];
+}
+__global__ void k_piv_swap_scale(double* Aug, int m, int p, const int* piv, double* colp) {
+  const int q = *piv;
+  const int64_t w = 2LL * m;
+  if (q != p)
+    for (int j = threadIdx.x; j < 2 * m; j += blockDim.x) {
+      const double t = Aug[(int64_t)p * w + j];
+      Aug[(int64_t)p * w + j] = Aug[(int64_t)q * w + j];
+      Aug[(int64_t)q * w + j] = t;
+    }
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) colp[i] = Aug[(int64_t)i * w + p];
+  __syncthreads();
+  const double pinv = 1.0 / colp[p];
+  for (int j = threadIdx.x; j < 2 * m; j += blockDim.x) Aug[(int64_t)p * w + j] *= pinv;
+}
+__global__ void k_piv_update(double* Aug, int m, int p, const double* colp) {
+  const int64_t w = 2LL * m;
+  const int64_t ncol = w - p;
+  const int64_t total = (int64_t)m * ncol;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t / ncol);
+    if (i == p) continue;
+    const int64_t j = p + t % ncol;
+    Aug[i * w + j] -= colp[i] * Aug[(int64_t)p * w + j];
+  }
+}
+__global__ void k_aug_init(const double* A, double* Aug, int m) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2LL * m * m; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / (2 * m), j = t % (2 * m);
+    Aug[t] = j < m ? A[i * m + j] : (j - m == i ? 1.0 : 0.0);
+  }
+}
+__global__ void k_aug_extract(const double* Aug, double* A, int m) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)m * m; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / m, j = t % m;
+    A[t] = Aug[i * 2 * m + m + j];
+  }
+}
+
 void dense_gemv(const double* A, int m, int ncomp, const double* x, int64_t xstride, double* y, int64_t ystride,
                 const double* done, cudaStream_t st) {
   k_gemv<<<grid_for((int64_t)m * 32, BS, 4096), BS, 0, st>>>(A, m, ncomp, x, xstride, y, ystride, done); etq_count_launch();
+}
+
+etq_status dense_inverse_pivot(double* A, int m, cudaStream_t st) {
+  double *Aug, *colp; int* piv;
+  ETQ_TRY(dalloc(&Aug, 2 * (size_t)m * m));
+  ETQ_TRY(dalloc(&colp, m));
+  ETQ_TRY(dalloc(&piv, 1));
+  k_aug_init<<<grid_for(2LL * m * m, BS, 8192), BS, 0, st>>>(A, Aug, m); etq_count_launch();
+  for (int p = 0; p < m; ++p) {
+    k_piv_find<<<1, 1024, 0, st>>>(Aug, m, p, piv);
+    k_piv_swap_scale<<<1, 1024, 0, st>>>(Aug, m, p, piv, colp);
+    k_piv_update<<<grid_for((int64_t)m * (2 * m - p), BS, 8192), BS, 0, st>>>(Aug, m, p, colp);
+    etq_count_launch(3);
+  }
+  k_aug_extract<<<grid_for((int64_t)m * m, BS, 8192), BS, 0, st>>>(Aug, A, m); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  ETQ_CHECK(cudaStreamSynchronize(st));
+  cudaFree(Aug); cudaFree(colp); cudaFree(piv);
+  return ETQ_OK;
 }
 
 etq_status dense_from_sell(const Sell& A, int m, double* D, cudaStream_t st) {
@@ -757,22 +801,40 @@ etq_status p1_build_mass_inverse(const Geo& g, double* W, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------- hierarchy
+static etq_status alloc_level_vectors(Level& L, int nc, bool need_b) {
+  const size_t nv = (size_t)nc * L.nrows;
+  if (need_b) ETQ_TRY(dalloc(&L.b, nv));
+  ETQ_TRY(dalloc(&L.x, nv));
+  ETQ_TRY(dalloc(&L.r, nv));
+  ETQ_TRY(dalloc(&L.d0, nv));
+  ETQ_TRY(dalloc(&L.d1, nv));
+  return ETQ_OK;
+}
 
-etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, double hi, int degree) {
+static etq_status level_sizes(int n, int coarse_n, std::vector<int>& ns) {
   if (coarse_n < 1) return ETQ_EINVAL;
-  int m = P.g.n;
-  std::vector<int> ns;
+  int m = n;
   while (true) {
     ns.push_back(m);
     if (m <= coarse_n) break;
     if (m % 2) return ETQ_EINVAL;
     m /= 2;
   }
-  if (ns.back() != coarse_n && ns.size() > 1) return ETQ_EINVAL;
+  return ETQ_OK;
+}
+
+// Velocity-block hierarchy (reading R9/R9'): rediscretised scalar operator L or F_s per level,
+// Dirichlet identity rows, smoother ellipse per level (Oseen: imaginary semi-axis = Gershgorin
+// radius of D^{-1}N), dense coarse inverse (Gauss-Jordan; pivoted for the nonsymmetric F).
+etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, double hi, int degree) {
+  std::vector<int> ns;
+  ETQ_TRY(level_sizes(P.g.n, coarse_n, ns));
+  H.kind = 0; H.ncomp = 2;
   H.lv.resize(ns.size());
   for (size_t l = 0; l < ns.size(); ++l) {
     Level& L = H.lv[l];
     L.g = make_geo(ns[l]);
+    L.nrows = L.g.nq;
     if (l == 0) {
       L.A = P.Lv;   // shallow: owned by the problem
     } else {
@@ -783,57 +845,121 @@ etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, do
     }
     ETQ_TRY(dalloc(&L.dinv, L.g.nq));
     ETQ_TRY(velocity_dinv_dev(L.g, P.oseen, P.nu, P.wind, L.dinv, P.stream));
-    const size_t nv = 2 * (size_t)L.g.nq;
-    if (l > 0) ETQ_TRY(dalloc(&L.b, nv));
-    ETQ_TRY(dalloc(&L.x, nv));
-    ETQ_TRY(dalloc(&L.r, nv));
-    ETQ_TRY(dalloc(&L.d0, nv));
-    ETQ_TRY(dalloc(&L.d1, nv));
+    L.bim = 0.0;
+    if (P.oseen && l + 1 < ns.size()) ETQ_TRY(oseen_gershgorin(L.g, P.nu, P.wind, &L.bim, P.stream));
+    ETQ_TRY(alloc_level_vectors(L, 2, l > 0));
   }
   Level& C = H.lv.back();
   ETQ_TRY(dalloc(&C.coarse_inv, (size_t)C.g.nq * C.g.nq));
   ETQ_TRY(dense_from_sell(C.A, C.g.nq, C.coarse_inv, P.stream));
-  ETQ_TRY(dense_inverse_spd(C.coarse_inv, C.g.nq, P.stream));
+  if (P.oseen) ETQ_TRY(dense_inverse_pivot(C.coarse_inv, C.g.nq, P.stream));
+  else ETQ_TRY(dense_inverse_spd(C.coarse_inv, C.g.nq, P.stream));
   H.lo = lo; H.hi = hi; H.degree = degree; H.built = true;
   ETQ_CHECK(cudaStreamSynchronize(P.stream));
   return ETQ_OK;
 }
 
-// One V-cycle on both velocity components (reading R9).  z_u = V(r_u); optional partial
-// <z_u, dot_with> into (site, slot) -> dot_out.
-etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r_u, double* z_u,
-                           const RedSite* site, int slot, double* dot_out, const double* dot_with,
-                           const double* done, cudaStream_t st) {
-  const int L = (int)H.lv.size();
-  const double theta = 0.5 * (H.hi + H.lo), delta = 0.5 * (H.hi - H.lo), sigma = theta / delta;
-  std::vector<double> c1(H.degree), c2(H.degree);
-  {
+// W = (A + 1 1^T)^{-1} - 1 1^T / m^2 = A^+ for a symmetric A with null space span{1}
+__global__ void k_add_ones(double* A, int m, double v) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)m * m; t += (int64_t)gridDim.x * blockDim.x)
+    A[t] += v;
+}
+
+// Pressure hierarchy for Ap = B1 Mdiag^{-1} B1^T (reading R13): Q1 levels n ... coarse_n,
+// nested bilinear transfers, real Chebyshev smoother, coarse pseudo-inverse.
+etq_status build_ap_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, double hi, int degree) {
+  std::vector<int> ns;
+  ETQ_TRY(level_sizes(P.g.n, coarse_n, ns));
+  H.kind = 1; H.ncomp = 1;
+  H.lv.resize(ns.size());
+  for (size_t l = 0; l < ns.size(); ++l) {
+    Level& L = H.lv[l];
+    L.g = make_geo(ns[l]);
+    L.nrows = L.g.nk;
+    ETQ_TRY(assemble_ap(L.g, &L.A, P.stream));
+    ETQ_TRY(dalloc(&L.dinv, L.g.nk));
+    ETQ_TRY(sell_diag_inv(L.A, L.dinv, P.stream));
+    L.bim = 0.0;
+    ETQ_TRY(alloc_level_vectors(L, 1, true));
+  }
+  Level& C = H.lv.back();
+  const int m = C.g.nk;
+  ETQ_TRY(dalloc(&C.coarse_inv, (size_t)m * m));
+  ETQ_TRY(dense_from_sell(C.A, m, C.coarse_inv, P.stream));
+  k_add_ones<<<grid_for((int64_t)m * m, BS, 4096), BS, 0, P.stream>>>(C.coarse_inv, m, 1.0); etq_count_launch();
+  ETQ_TRY(dense_inverse_spd(C.coarse_inv, m, P.stream));
+  k_add_ones<<<grid_for((int64_t)m * m, BS, 4096), BS, 0, P.stream>>>(C.coarse_inv, m, -1.0 / ((double)m * m)); etq_count_launch();
+  H.lo = lo; H.hi = hi; H.degree = degree; H.built = true;
+  ETQ_CHECK(cudaStreamSynchronize(P.stream));
+  return ETQ_OK;
+}
+
+void free_hierarchy(Hierarchy& H) {
+  for (size_t l = 0; l < H.lv.size(); ++l) {
+    Level& L = H.lv[l];
+    if (H.kind == 1 || l > 0) sell_free(L.A);
+    cudaFree(L.dinv); cudaFree(L.b); cudaFree(L.x); cudaFree(L.r); cudaFree(L.d0); cudaFree(L.d1);
+    cudaFree(L.coarse_inv);
+  }
+  H = Hierarchy{};
+}
+
+// Chebyshev coefficients c1_k = rho_{k+1} rho_k, c2_k = 2 rho_{k+1} / delta on the ellipse with
+// centre theta, real semi-axis a and imaginary semi-axis bim (real interval when bim = 0).
+static void cheb_coeffs(double lo, double hi, double bim, int degree, std::vector<double>& c1, std::vector<double>& c2) {
+  c1.resize(degree); c2.resize(degree);
+  const double theta = 0.5 * (hi + lo), a = 0.5 * (hi - lo);
+  if (bim == 0.0) {
+    const double delta = a, sigma = theta / delta;
     double rho = 1.0 / sigma;
-    for (int k = 0; k < H.degree; ++k) {
+    for (int k = 0; k < degree; ++k) {
       const double rn = 1.0 / (2.0 * sigma - rho);
       c1[k] = rn * rho; c2[k] = 2.0 * rn / delta;
       rho = rn;
     }
+    return;
   }
+  const std::complex<double> delta = std::sqrt(std::complex<double>(a * a - bim * bim, 0.0));
+  const std::complex<double> sigma = theta / delta;
+  std::complex<double> rho = 1.0 / sigma;
+  for (int k = 0; k < degree; ++k) {
+    const std::complex<double> rn = 1.0 / (2.0 * sigma - rho);
+    c1[k] = (rn * rho).real(); c2[k] = (2.0 * rn / delta).real();
+    rho = rn;
+  }
+}
+
+// One V-cycle (readings R9/R9'/R13) on H.ncomp components: z = V(r); optional partial
+// <z, dot_with> into (site, slot) -> dot_out.
+etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r_u, double* z_u,
+                           const RedSite* site, int slot, double* dot_out, const double* dot_with,
+                           const double* done, cudaStream_t st) {
+  const int L = (int)H.lv.size();
+  const int nc = H.ncomp;
+  const double theta = 0.5 * (H.hi + H.lo);
   RedSite dummy{};
   if (L == 1) {   // coarse solve only
     const Level& C = H.lv[0];
-    dense_gemv(C.coarse_inv, C.g.nq, 2, r_u, C.g.nq, z_u, C.g.nq, done, st);
-    if (dot_out && site)
-      k_final_add<<<grid_for(2LL * C.g.nq, BS, RED_BLOCKS), BS, 0, st>>>(z_u, nullptr, z_u, 2LL * C.g.nq, dot_with,
-                                                                       *site, slot, dot_out, done); etq_count_launch();
+    dense_gemv(C.coarse_inv, C.nrows, nc, r_u, C.nrows, z_u, C.nrows, done, st);
+    if (dot_out && site) {
+      k_final_add<<<grid_for((int64_t)nc * C.nrows, BS, RED_BLOCKS), BS, 0, st>>>(
+          z_u, nullptr, z_u, (int64_t)nc * C.nrows, dot_with, *site, slot, dot_out, done); etq_count_launch();
+    }
     return ETQ_OK;
   }
   std::vector<const double*> bvec(L);
   std::vector<const double*> pend(L, nullptr);
+  std::vector<double> c1, c2;
   // ---- down
   for (int l = 0; l < L - 1; ++l) {
     const Level& lv = H.lv[l];
-    const int nq = lv.g.nq;
+    const int nq = lv.nrows;
+    cheb_coeffs(H.lo, H.hi, lv.bim, H.degree, c1, c2);
     const double* b = (l == 0) ? r_u : lv.b;
     bvec[l] = b;
-    if (l == 0)
-      k_cheb_init<<<grid_for(2LL * nq, BS, 4096), BS, 0, st>>>(lv.dinv, nq, b, lv.d0, theta, done); etq_count_launch();
+    if (l == 0) {
+      k_cheb_init<<<grid_for((int64_t)nc * nq, BS, 4096), BS, 0, st>>>(lv.dinv, nq, nc, b, lv.d0, theta, done); etq_count_launch();
+    }
     const int gs = grid_for(lv.A.nslices * 32, BS, 4096);
     double* din = lv.d0; double* dout = lv.d1;
     for (int k = 0; k < H.degree; ++k) {
@@ -842,27 +968,43 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       a.d_in = din; a.r_in = (k == 0) ? b : lv.r; a.x_in = (k == 0) ? nullptr : lv.x;
       a.x_out = lv.x; a.r_out = lv.r; a.d_out = (k == H.degree - 1) ? nullptr : dout;
       a.c1 = c1[k]; a.c2 = c2[k]; a.done = done;
-      k_cheb_step<<<gs, BS, 0, st>>>(a); etq_count_launch();
+      if (nc == 2) k_cheb_step<2><<<gs, BS, 0, st>>>(a);
+      else k_cheb_step<1><<<gs, BS, 0, st>>>(a);
+      etq_count_launch();
       std::swap(din, dout);
     }
     const Level& cv = H.lv[l + 1];
-    k_restrict<<<grid_for(cv.g.nq, BS, 4096), BS, 0, st>>>(lv.g.m, cv.g.m, nq, cv.g.nq, lv.r, cv.b, cv.d0,
-                                                          cv.dinv, theta, done); etq_count_launch();
+    if (H.kind == 0) {
+      k_restrict<<<grid_for(cv.g.nq, BS, 4096), BS, 0, st>>>(lv.g.m, cv.g.m, nq, cv.g.nq, lv.r, cv.b, cv.d0,
+                                                            cv.dinv, theta, done);
+    } else {
+      k_restrict_q1<<<grid_for(cv.g.nk, BS, 4096), BS, 0, st>>>(lv.g.n + 1, cv.g.n + 1, lv.r, cv.b, cv.d0,
+                                                               cv.dinv, theta, done);
+    }
+    etq_count_launch();
   }
   // ---- coarse
   {
     const Level& C = H.lv[L - 1];
-    dense_gemv(C.coarse_inv, C.g.nq, 2, C.b, C.g.nq, C.x, C.g.nq, done, st);
+    dense_gemv(C.coarse_inv, C.nrows, nc, C.b, C.nrows, C.x, C.nrows, done, st);
     pend[L - 1] = nullptr;
   }
   // ---- up
   for (int l = L - 2; l >= 0; --l) {
     const Level& lv = H.lv[l];
     const Level& cv = H.lv[l + 1];
-    const int nq = lv.g.nq;
-    k_prolong<<<grid_for(nq, BS, 4096), BS, 0, st>>>(lv.g.m, cv.g.m, nq, cv.g.nq, cv.x, pend[l + 1], lv.x, done); etq_count_launch();
+    const int nq = lv.nrows;
+    cheb_coeffs(H.lo, H.hi, lv.bim, H.degree, c1, c2);
+    if (H.kind == 0) {
+      k_prolong<<<grid_for(nq, BS, 4096), BS, 0, st>>>(lv.g.m, cv.g.m, nq, cv.g.nq, cv.x, pend[l + 1], lv.x, done);
+    } else {
+      k_prolong_q1<<<grid_for(nq, BS, 4096), BS, 0, st>>>(lv.g.n + 1, cv.g.n + 1, cv.x, pend[l + 1], lv.x, done);
+    }
+    etq_count_launch();
     const int gs = grid_for(lv.A.nslices * 32, BS, 4096);
-    k_post_residual<<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, theta, done); etq_count_launch();
+    if (nc == 2) k_post_residual<2><<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, theta, done);
+    else k_post_residual<1><<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, theta, done);
+    etq_count_launch();
     double* din = lv.d0; double* dout = lv.d1;
     for (int k = 0; k < H.degree - 1; ++k) {
       ChebArgs a;
@@ -870,15 +1012,28 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       a.d_in = din; a.r_in = lv.r; a.x_in = lv.x;
       a.x_out = lv.x; a.r_out = (k == H.degree - 2) ? nullptr : lv.r; a.d_out = dout;
       a.c1 = c1[k]; a.c2 = c2[k]; a.done = done;
-      k_cheb_step<<<gs, BS, 0, st>>>(a); etq_count_launch();
+      if (nc == 2) k_cheb_step<2><<<gs, BS, 0, st>>>(a);
+      else k_cheb_step<1><<<gs, BS, 0, st>>>(a);
+      etq_count_launch();
       std::swap(din, dout);
     }
     pend[l] = din;   // last correction deferred to the consumer
   }
   const Level& F = H.lv[0];
-  const int64_t nv = 2LL * F.g.nq;
+  const int64_t nv = (int64_t)nc * F.nrows;
   k_final_add<<<grid_for(nv, BS, RED_BLOCKS), BS, 0, st>>>(F.x, pend[0], z_u, nv, dot_with,
                                                           site ? *site : dummy, slot, dot_out, done); etq_count_launch();
+  return ETQ_OK;
+}
+
+// Ap^{-1} r ~ one Q1 V-cycle, then the mean-zero projection (reading R13)
+etq_status ap_solve(const Problem& P, const Hierarchy& H, const double* r, double* z, double* sum_slot,
+                    const double* done, cudaStream_t st) {
+  ETQ_TRY(vcycle_apply_ex(P, H, r, z, nullptr, 0, nullptr, nullptr, done, st));
+  const int64_t nk = H.lv[0].nrows;
+  k_final_add<<<grid_for(nk, BS, RED_BLOCKS), BS, 0, st>>>(z, nullptr, z, nk, nullptr, P.red[0], 6, sum_slot, done);
+  etq_count_launch();
+  k_sub_mean<<<grid_for(nk, BS, 4096), BS, 0, st>>>(z, nk, sum_slot, done); etq_count_launch();
   return ETQ_OK;
 }
 
@@ -917,7 +1072,8 @@ void sgs_sweep_dev(const Geo& g, const double* r, const double* y, double* z, do
 
 // z_p = Pi C Pi r_p (reading R6) with C = m-step Chebyshev semi-iteration on SGS (reading R7)
 etq_status mass_pc_apply_ex(const Problem& P, const double* r_p, double* z_p, const RedSite* site, int slot,
-                            double* dot_out, const double* dot_with, const double* done, cudaStream_t st) {
+                            double* dot_out, const double* dot_with, const double* done, cudaStream_t st,
+                            double scale) {
   const PcMass& M = P.pm;
   if (!M.ready) return ETQ_ENOTSETUP;
   const Geo& g = P.g;
@@ -945,7 +1101,8 @@ etq_status mass_pc_apply_ex(const Problem& P, const double* r_p, double* z_p, co
     launch_sgs_tile(a, st);
     prev = cur; cur = out;
   }
-  k_kproject_out<<<gf, BS, 0, st>>>(g.nk, np, cur, P.dscal + S_KY, inv_kk, z_p, dot_with, rs, slot, dot_out, done); etq_count_launch();
+  k_kproject_out<<<gf, BS, 0, st>>>(g.nk, np, cur, P.dscal + S_KY, inv_kk, scale, z_p, dot_with, rs, slot, dot_out,
+                                    done); etq_count_launch();
   return ETQ_OK;
 }
 
@@ -1035,13 +1192,13 @@ void cheb_step_level0(const Problem& P, const double* d_in, double* d_out, cudaS
   a.A = lv.A; a.dinv = lv.dinv; a.nq = lv.g.nq;
   a.d_in = d_in; a.r_in = lv.r; a.x_in = lv.x; a.x_out = lv.x; a.r_out = lv.r; a.d_out = d_out;
   a.c1 = 0.5; a.c2 = 0.1; a.done = nullptr;
-  k_cheb_step<<<grid_for(lv.A.nslices * 32, BS, 4096), BS, 0, st>>>(a); etq_count_launch();
+  k_cheb_step<2><<<grid_for(lv.A.nslices * 32, BS, 4096), BS, 0, st>>>(a); etq_count_launch();
 }
 
 // Algorithmic bytes: every stored value/index once (12 B per true nnz), the
 // row permutation (4 B per slot), every vector element the kernel must read or write once.
 double cheb_step_bytes(const Level& L) {
-  const double nq = L.g.nq;
+  const double nq = L.nrows;
   return 12.0 * L.A.nnz + 4.0 * L.A.nslices * SELL_C + 8.0 * nq /*dinv*/ + 8.0 * 2 * nq * 6 /*d,r,x in; x,r,d out*/;
 }
 

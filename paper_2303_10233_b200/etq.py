@@ -69,6 +69,10 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "etq_minres_solve_host": ([P, I32, VP, VP, D, I32, C.POINTER(Report)], I32),
         "etq_export_operator": ([P, I32, I32, C.POINTER(I64), C.POINTER(I64), VP, VP, VP], I32),
         "etq_launch_count": ([C.POINTER(I64)], I32),
+        "etq_gmres_solve": ([P, I32, I32, VP, VP, D, I32, I32, C.POINTER(Report)], I32),
+        "etq_two_stage_solve": ([P, VP, VP, D, D, I32, I32, C.POINTER(Report), C.POINTER(Report),
+                                 C.POINTER(D)], I32),
+        "etq_apply_pcd_schur": ([P, VP, VP], I32),
         "etq_time_kernel": ([P, I32, I32, C.POINTER(D), C.POINTER(D)], I32),
         "etq_status_string": ([I32], C.c_char_p),
         "etq_destroy": ([P], None),
@@ -243,6 +247,29 @@ class Problem:
                    "etq_minres_solve_host")
         return self._report_dict(rep, hist, dl, gm, s)
 
+    def apply_pcd_schur(self, r_p1, z_p1):
+        _check(lib().etq_apply_pcd_schur(self.h, _ptr(r_p1), _ptr(z_p1)), "etq_apply_pcd_schur")
+        return z_p1
+
+    def gmres_solve(self, kind, b, x, rtol=1e-6, restart=50, maxit=1000, reduced=False):
+        rep, hist, dl, gm = self._report(maxit + 2)
+        s = _check(lib().etq_gmres_solve(self.h, int(reduced), kind, _ptr(b), _ptr(x), rtol, restart, maxit,
+                                         C.byref(rep)), "etq_gmres_solve")
+        d = self._report_dict(rep, hist, dl, gm, s)
+        d["history"] = hist[:rep.iterations + 1].copy()
+        d["restarts"] = rep.restarts
+        return d
+
+    def two_stage_solve(self, b, x, eta=1e-6, c=10.0, restart=50, maxit=2000):
+        r1, h1, d1, g1 = self._report(maxit + 2)
+        r2, h2, d2, g2 = self._report(maxit + 2)
+        bound = (C.c_double * 2)()
+        s = _check(lib().etq_two_stage_solve(self.h, _ptr(b), _ptr(x), eta, c, restart, maxit, C.byref(r1),
+                                             C.byref(r2), bound), "etq_two_stage_solve")
+        st1 = self._report_dict(r1, h1, d1, g1, s); st1["history"] = h1[:r1.iterations + 1].copy()
+        st2 = self._report_dict(r2, h2, d2, g2, s); st2["history"] = h2[:r2.iterations + 1].copy()
+        return {"status": s, "step1": st1, "step2": st2, "zstar": bound[0], "bound": bound[1]}
+
     def export_operator(self, which, level=0):
         """Assembled operator as a scipy CSR matrix (host copy; tests only)."""
         import numpy as np
@@ -256,5 +283,5 @@ class Problem:
         _check(lib().etq_export_operator(self.h, which, level, C.byref(nr), C.byref(nz),
                                          C.c_void_p(rp.ctypes.data), C.c_void_p(col.ctypes.data),
                                          C.c_void_p(val.ctypes.data)), "etq_export_operator")
-        ncol = {0: nr.value, 1: self.n_u, 2: self.n_p}[which]
+        ncol = {0: nr.value, 1: self.n_u, 2: self.n_p, 3: nr.value, 4: nr.value}[which]
         return sp.csr_matrix((val[:nz.value], col[:nz.value], rp), shape=(nr.value, ncol))
