@@ -46,6 +46,7 @@ def parse():
                     help="oracle MINRES iterations timed for cpu_baseline (0 = skip)")
     ap.add_argument("--kernel-reps", type=int, default=20)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--clock-ms", type=int, default=1000, help="nvidia-smi sampling period during the timed region")
     return ap.parse_args()
 
 
@@ -70,15 +71,16 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index):
+    def __init__(self, gpu_index, period_ms=1000):
         self.idx = gpu_index
+        self.period = max(int(period_ms), 100)
         self.proc = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", str(self.period)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
 
@@ -215,7 +217,7 @@ def run_ours(args):
         x.zero_()
         P.minres_solve(etq.PC_P2_GMG, b, x, rtol=args.rtol, maxit=args.maxit)
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local, args.clock_ms)
     clocks.start()
     time.sleep(0.3)
     L0 = etq.launch_count()

@@ -336,21 +336,45 @@ __global__ void k_scan_slices(const int* slen, int64_t nslices, int64_t* sptr) {
   for (int64_t i = b; i < e; ++i) { sptr[i] = acc; acc += (int64_t)slen[i] * SELL_C; }
 }
 
-__global__ void k_node_perm(int n, int64_t total, int* perm) {
+// Row order of the velocity node slices: the grid is swept ONCE in bands of two node rows
+// (j = 2b, 2b+1); inside a band the four node classes (i mod 2, j mod 2) form separate row
+// segments, each padded to a multiple of 32, so every slice holds nodes of one class and one row
+// (uniform stencil width) and the gathered x rows stay L2-resident while the band advances.
+// Row order of the velocity node slices.  Class-major: the four node classes (i mod 2, j mod 2)
+// one after the other, lexicographic inside a class, so every slice holds rows of one stencil
+// width (25 / 15 / 15 / 9).  Band: the grid is swept once in bands of two node rows with the
+// four class segments of the band padded to multiples of 32, so the gathered rows stay in L2
+// while the band advances.  Measured (variants A/B, n = 1024 / 2048): class-major is faster
+// while a two-component vector fits in the L2, band order beyond (etq_band_order).
+__host__ __device__ inline int64_t pad32(int64_t v) { return (v + 31) / 32 * 32; }
+__global__ void k_node_perm_class(int n, int64_t total, int* perm) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= total) return;
   const int m = 2 * n + 1;
   const int64_t nq = (int64_t)m * m;
   if (t >= nq) { perm[t] = -1; return; }
-  // classes: (i even, j even), (i odd, j even), (i even, j odd), (i odd, j odd)
-  const int64_t cnt[4] = {(int64_t)(n + 1) * (n + 1), (int64_t)n * (n + 1), (int64_t)(n + 1) * n,
-                          (int64_t)n * n};
+  const int64_t cnt[4] = {(int64_t)(n + 1) * (n + 1), (int64_t)n * (n + 1), (int64_t)(n + 1) * n, (int64_t)n * n};
   int c = 0; int64_t idx = t;
   while (idx >= cnt[c]) { idx -= cnt[c]; ++c; }
   const int px = c & 1, py = c >> 1;
   const int cx = px ? n : n + 1;
   const int ix = (int)(idx % cx), iy = (int)(idx / cx);
-  const int i = 2 * ix + px, j = 2 * iy + py;
+  perm[t] = (2 * ix + px) + m * (2 * iy + py);
+}
+__global__ void k_node_perm_band(int n, int64_t total, int* perm) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  const int m = 2 * n + 1;
+  const int64_t pe = pad32(n + 1), po = pad32(n);        // even-i / odd-i segment sizes
+  const int64_t band = 2 * (pe + po);
+  const int64_t b = t / band;
+  int64_t r = t % band;
+  int j, i;
+  if (r < pe) { j = 2 * (int)b; i = 2 * (int)r; if (r > n) { perm[t] = -1; return; } }
+  else if ((r -= pe) < po) { j = 2 * (int)b; i = 2 * (int)r + 1; if (r >= n) { perm[t] = -1; return; } }
+  else if ((r -= po) < pe) { j = 2 * (int)b + 1; i = 2 * (int)r; if (r > n) { perm[t] = -1; return; } }
+  else { r -= pe; j = 2 * (int)b + 1; i = 2 * (int)r + 1; if (r >= n) { perm[t] = -1; return; } }
+  if (j >= m) { perm[t] = -1; return; }
   perm[t] = i + m * j;
 }
 
@@ -497,11 +521,19 @@ __global__ void k_sell_diag_inv(Sell A, double* dinv) {
 }  // namespace
 
 // ---------------------------------------------------------------- host entry points
+bool etq_band_order(const Geo& g) {
+  return 2.0 * 8.0 * (double)g.nq > 126.0e6;   // two-component vector larger than the 126 MB L2
+}
+
 etq_status build_node_perm(const Geo& g, int** perm, int64_t* nslices, cudaStream_t st) {
-  const int64_t ns = ((int64_t)g.nq + SELL_C - 1) / SELL_C;
+  const bool band = etq_band_order(g);
+  const int64_t ns = band ? (2 * (pad32(g.n + 1) + pad32(g.n)) * (g.n + 1)) / SELL_C   // last odd row: padding
+                          : ((int64_t)g.nq + SELL_C - 1) / SELL_C;
   ETQ_TRY(dalloc(perm, ns * SELL_C));
   const int64_t tot = ns * SELL_C;
-  k_node_perm<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g.n, tot, *perm); etq_count_launch();
+  if (band) k_node_perm_band<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g.n, tot, *perm);
+  else k_node_perm_class<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g.n, tot, *perm);
+  etq_count_launch();
   ETQ_CHECK(cudaGetLastError());
   *nslices = ns;
   return ETQ_OK;

@@ -74,21 +74,58 @@ __device__ void reduce_finish(const double (&v)[NV], RedSite site, int slot, dou
 }
 
 // ---------------------------------------------------------------- SELL row products
+// One thread per row; entry k of the row at base + 32 k.  The matrix is streamed once per apply,
+// so its values and indices are loaded with the evict-first hint (__ldcs) to keep the gathered
+// vectors in L1/L2; SELL_U entries are loaded before their gathers to keep SELL_U x 12 B of
+// matrix data plus SELL_U gathers in flight per thread.
+#ifndef SELL_U
+#define SELL_U 4
+#endif
+#ifndef SELL_STREAM
+#define SELL_STREAM 0
+#endif
+template <class T>
+__device__ __forceinline__ T ld_mat(const T* p) {
+#if SELL_STREAM
+  return __ldcs(p);
+#else
+  return __ldg(p);
+#endif
+}
+#ifndef SELL_PRED
+#define SELL_PRED 0
+#endif
+// all rows of a slice have the same length, so chunk predicates are warp-uniform
 __device__ __forceinline__ double sell_row1(const Sell& A, int64_t s, int lane, const double* __restrict__ x) {
   const int64_t base = A.sptr[s] + lane;
   const int len = A.slen[s];
   const int* __restrict__ cp = A.col + base;
   const double* __restrict__ vp = A.val + base;
   double acc = 0.0;
-  int k = 0;
-  for (; k + 4 <= len; k += 4) {
-    int c[4]; double v[4];
+#if SELL_PRED
+  for (int k = 0; k < len; k += SELL_U) {
+    int c[SELL_U]; double v[SELL_U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { c[u] = __ldg(cp + (k + u) * SELL_C); v[u] = __ldg(vp + (k + u) * SELL_C); }
+    for (int u = 0; u < SELL_U; ++u) {
+      const bool ok = k + u < len;
+      c[u] = ok ? ld_mat(cp + (k + u) * SELL_C) : 0;
+      v[u] = ok ? ld_mat(vp + (k + u) * SELL_C) : 0.0;
+    }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc = fma(v[u], __ldg(x + c[u]), acc);
+    for (int u = 0; u < SELL_U; ++u)
+      if (k + u < len) acc = fma(v[u], __ldg(x + c[u]), acc);
   }
-  for (; k < len; ++k) acc = fma(__ldg(vp + k * SELL_C), __ldg(x + __ldg(cp + k * SELL_C)), acc);
+#else
+  int k = 0;
+  for (; k + SELL_U <= len; k += SELL_U) {
+    int c[SELL_U]; double v[SELL_U];
+#pragma unroll
+    for (int u = 0; u < SELL_U; ++u) { c[u] = ld_mat(cp + (k + u) * SELL_C); v[u] = ld_mat(vp + (k + u) * SELL_C); }
+#pragma unroll
+    for (int u = 0; u < SELL_U; ++u) acc = fma(v[u], __ldg(x + c[u]), acc);
+  }
+  for (; k < len; ++k) acc = fma(ld_mat(vp + k * SELL_C), __ldg(x + ld_mat(cp + k * SELL_C)), acc);
+#endif
   return acc;
 }
 
@@ -98,18 +135,32 @@ __device__ __forceinline__ void sell_row2(const Sell& A, int64_t s, int lane, co
   const int len = A.slen[s];
   const int* __restrict__ cp = A.col + base;
   const double* __restrict__ vp = A.val + base;
+#if SELL_PRED
+  for (int k = 0; k < len; k += SELL_U) {
+    int c[SELL_U]; double v[SELL_U];
+#pragma unroll
+    for (int u = 0; u < SELL_U; ++u) {
+      const bool ok = k + u < len;
+      c[u] = ok ? ld_mat(cp + (k + u) * SELL_C) : 0;
+      v[u] = ok ? ld_mat(vp + (k + u) * SELL_C) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < SELL_U; ++u)
+      if (k + u < len) { a0 = fma(v[u], __ldg(x0 + c[u]), a0); a1 = fma(v[u], __ldg(x1 + c[u]), a1); }
+  }
+#else
   int k = 0;
-  for (; k + 4 <= len; k += 4) {
-    int c[4]; double v[4];
+  for (; k + SELL_U <= len; k += SELL_U) {
+    int c[SELL_U]; double v[SELL_U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { c[u] = __ldg(cp + (k + u) * SELL_C); v[u] = __ldg(vp + (k + u) * SELL_C); }
+    for (int u = 0; u < SELL_U; ++u) { c[u] = ld_mat(cp + (k + u) * SELL_C); v[u] = ld_mat(vp + (k + u) * SELL_C); }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { a0 = fma(v[u], __ldg(x0 + c[u]), a0); a1 = fma(v[u], __ldg(x1 + c[u]), a1); }
+    for (int u = 0; u < SELL_U; ++u) { a0 = fma(v[u], __ldg(x0 + c[u]), a0); a1 = fma(v[u], __ldg(x1 + c[u]), a1); }
   }
   for (; k < len; ++k) {
-    const int c = __ldg(cp + k * SELL_C); const double v = __ldg(vp + k * SELL_C);
+    const int c = ld_mat(cp + k * SELL_C); const double v = ld_mat(vp + k * SELL_C);
     a0 = fma(v, __ldg(x0 + c), a0); a1 = fma(v, __ldg(x1 + c), a1);
   }
+#endif
 }
-
 }  // namespace etqd

@@ -12,7 +12,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libetq.so")
+LIB_PATH = os.environ.get("ETQ_LIB", os.path.join(_HERE, "libetq.so"))
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "etq.h")
 
 ETQ_OK, ETQ_NOT_CONVERGED = 0, 1
