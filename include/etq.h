@@ -171,6 +171,20 @@ etq_status etq_two_stage_solve(etq_problem* p, const double* b, double* x, doubl
  * paper order of Eq. (discrete-commutator1x), reading R11).  Test hook of the Step-I Schur apply. */
 etq_status etq_apply_pcd_schur(const etq_problem* p, const double* r_p1, double* z_p1);
 
+/* fp32-value variants for the kernel sweep (BASELINE.json configs[4]): y = K x with fp32 matrix
+ * values, fp32 vectors and fp32 accumulation (device float arrays, same layout), and one Stokes
+ * V-cycle (P2 set up) in fp32.  The solvers always run in fp64. */
+etq_status etq_apply_saddle_f32(etq_problem* p, int32_t reduced, const float* x, float* y);
+etq_status etq_apply_vcycle_f32(etq_problem* p, const float* r_u, float* z_u);
+
+/* EST-MINRES estimate of the discrete inf-sup constant gamma^2 (NEXT-1 of SURVEY
+ * §8(f)) from the Lanczos scalars of a MINRES solve: the tridiagonal T_k with diagonal
+ * delta[0..k) and off-diagonal gamma[0..k-1) (report.lanczos_delta / report.lanczos_gamma, i.e.
+ * delta_1..delta_k and gamma_2..gamma_k of Algorithm 1).  With lam (lam - 1) = sigma for the
+ * eigenvalues sigma of M_S^{-1} B A^{-1} B^T, the negative Ritz value mu closest to 0 gives
+ * *gamma2 = mu (mu - 1).  Host arrays; *gamma2 = NaN when T_k has no negative Ritz value. */
+etq_status etq_est_minres(const double* delta, const double* gamma, int32_t k, double* gamma2);
+
 /* Number of libetq kernel launches issued so far in this process: direct launches plus the
  * kernel nodes of every graph launch (launches recorded during graph capture are excluded).
  * Host output; never fails. */
@@ -182,7 +196,8 @@ etq_status etq_launch_count(int64_t* count);
  *        1 = finest-level fused Chebyshev step of the V-cycle (SpMV + update, both components);
  *        2 = one V-cycle on both velocity components (P2 set up);
  *        3 = one Pi C Pi pressure apply (P2 set up; L2-resident, bytes reported as 0);
- *        4 = one P2 preconditioner apply (velocity and pressure branches concurrently).
+ *        4 = one P2 preconditioner apply (velocity and pressure branches concurrently);
+ *        5 = fp32 fused saddle SpMV; 6 = fp32 V-cycle (P2 set up).
  * Host outputs: *ms = average device time per launch, *bytes = algorithmic bytes per launch. */
 etq_status etq_time_kernel(etq_problem* p, int32_t which, int32_t reps, double* ms, double* bytes);
 

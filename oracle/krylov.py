@@ -152,3 +152,25 @@ def gmres(Kop, b, Minv, tol_abs, restart=50, maxit=1000, x0=None):
     true_res = np.linalg.norm(b - Kop(x))
     return x, Report(iterations=total, converged=bool(converged), history=np.array(hist),
                      restarts=restarts, true_residual=true_res)
+
+
+def est_minres_gamma2(delta, gamma):
+    """EST-MINRES inf-sup estimate (reading of S:439/S:461).
+
+    The MINRES recurrences of Algorithm 1 are the Lanczos process for P^{-1} K with the
+    tridiagonal T_k = tridiag(gamma_{j+1}; delta_j; gamma_{j+1}) (delta_1..delta_k on the diagonal,
+    gamma_2..gamma_k off the diagonal).  With the exact velocity block, eigenvalues lam of P^{-1} K
+    satisfy lam (lam - 1) = sigma, sigma an eigenvalue of M_S^{-1} B A^{-1} B^T (Eq. (7)), so the
+    negative Ritz value mu closest to 0 gives gamma^2 ~ mu (mu - 1).  Returns nan if T_k has no
+    negative Ritz value yet.  gamma: [gamma_1, gamma_2, ...] as recorded by minres()."""
+    k = len(delta)
+    if k == 0:
+        return float("nan")
+    off = np.asarray(gamma[1:k], dtype=np.float64)
+    T = np.diag(np.asarray(delta[:k], dtype=np.float64)) + np.diag(off, 1) + np.diag(off, -1)
+    mu = np.linalg.eigvalsh(T)
+    neg = mu[mu < 0]
+    if neg.size == 0:
+        return float("nan")
+    m = neg.max()
+    return float(m * (m - 1.0))

@@ -353,6 +353,25 @@ etq_status etq_minres_solve_host(etq_problem* h, etq_pc_kind kind, const double*
   return s;
 }
 
+etq_status etq_apply_saddle_f32(etq_problem* h, int32_t reduced, const float* x, float* y) {
+  if (!h || !x || !y || (const void*)x == (const void*)y) return ETQ_EINVAL;
+  Problem& P = h->P;
+  ETQ_TRY(ensure_f32(P));
+  StreamScope sc(P);
+  launch_saddle_f32(P, reduced != 0, x, y, P.stream);
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
+etq_status etq_apply_vcycle_f32(etq_problem* h, const float* r_u, float* z_u) {
+  if (!h || !r_u || !z_u) return ETQ_EINVAL;
+  Problem& P = h->P;
+  if (!P.mg.built || P.mg.kind != 0 || P.oseen) return ETQ_ENOTSETUP;
+  ETQ_TRY(ensure_f32(P));
+  StreamScope sc(P);
+  return vcycle_f32(P, r_u, z_u, P.stream);
+}
+
 etq_status etq_apply_pcd_schur(const etq_problem* h, const double* r_p1, double* z_p1) {
   if (!h || !r_p1 || !z_p1) return ETQ_EINVAL;
   const Problem& P = h->P;
@@ -456,6 +475,37 @@ etq_status etq_export_operator(const etq_problem* h, int32_t which, int32_t leve
   return ETQ_OK;
 }
 
+etq_status etq_est_minres(const double* delta, const double* gamma, int32_t k, double* gamma2) {
+  if (!delta || !gamma2 || k < 0 || (k > 1 && !gamma)) return ETQ_EINVAL;
+  *gamma2 = std::nan("");
+  if (k == 0) return ETQ_OK;
+  auto off = [&](int i) { return gamma[i]; };   // between rows i and i+1
+  auto count_below = [&](double x) {             // Sturm count of eigenvalues < x
+    int c = 0; double d = 1.0;
+    for (int i = 0; i < k; ++i) {
+      d = delta[i] - x - (i > 0 ? off(i - 1) * off(i - 1) / d : 0.0);
+      if (d == 0.0) d = -1e-300;
+      if (d < 0) ++c;
+    }
+    return c;
+  };
+  const int nneg = count_below(0.0);
+  if (nneg == 0) return ETQ_OK;
+  double lo = 0.0;
+  for (int i = 0; i < k; ++i) {
+    const double r = (i > 0 ? std::fabs(off(i - 1)) : 0.0) + (i < k - 1 ? std::fabs(off(i)) : 0.0);
+    lo = std::fmin(lo, delta[i] - r);
+  }
+  double hi = 0.0;
+  for (int it = 0; it < 200; ++it) {   // the nneg-th smallest eigenvalue = largest negative one
+    const double mid = 0.5 * (lo + hi);
+    if (count_below(mid) >= nneg) hi = mid; else lo = mid;
+  }
+  const double mu = 0.5 * (lo + hi);
+  *gamma2 = mu * (mu - 1.0);
+  return ETQ_OK;
+}
+
 etq_status etq_launch_count(int64_t* count) {
   if (count) *count = etq_launch_total();
   return ETQ_OK;
@@ -464,8 +514,15 @@ etq_status etq_launch_count(int64_t* count) {
 etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* ms, double* bytes) {
   if (!h || reps < 1 || !ms || !bytes) return ETQ_EINVAL;
   Problem& P = h->P;
-  if ((which >= 2) && !P.p2_ready) return ETQ_ENOTSETUP;
-  if (which < 0 || which > 4) return ETQ_EINVAL;
+  if ((which >= 2 && which != 5) && !P.p2_ready) return ETQ_ENOTSETUP;
+  if (which < 0 || which > 6) return ETQ_EINVAL;
+  if (which >= 5) {
+    ETQ_TRY(ensure_f32(P));
+    if (!P.tkf) {
+      ETQ_TRY(dalloc(&P.tkf, 2 * (size_t)P.N));
+      ETQ_CHECK(cudaMemset(P.tkf, 0, sizeof(float) * 2 * (size_t)P.N));
+    }
+  }
   if (!P.tk) {
     ETQ_TRY(dalloc(&P.tk, 3 * (size_t)P.N));
     std::vector<double> v(P.N);
@@ -484,6 +541,8 @@ etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* 
       case 2: ETQ_TRY(vcycle_apply_ex(P, P.mg, a, b, nullptr, 0, nullptr, nullptr, nullptr, st)); break;
       case 3: ETQ_TRY(mass_pc_apply_ex(P, a + P.n_u, b + P.n_u, &P.red[0], 2, nullptr, nullptr, nullptr, st)); break;
       case 4: ETQ_TRY(precond_apply_ex(P, ETQ_PC_P2_GMG, a, c, nullptr, nullptr, nullptr, nullptr, st)); break;
+      case 5: launch_saddle_f32(P, false, P.tkf, P.tkf + P.N, st); break;
+      case 6: ETQ_TRY(vcycle_f32(P, P.tkf, P.tkf + P.N, st)); break;
     }
     return ETQ_OK;
   };
@@ -500,6 +559,8 @@ etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* 
     case 0: *bytes = 12.0 * nnz_all + 4.0 * P.Lv.nslices * SELL_C + 16.0 * P.N; break;
     case 1: *bytes = cheb_step_bytes(P.mg.lv[0]); break;
     case 2: case 4: *bytes = vcycle_bytes(P.mg); break;
+    case 5: *bytes = 8.0 * nnz_all + 4.0 * P.Lv.nslices * SELL_C + 8.0 * P.N; break;
+    case 6: *bytes = vcycle_bytes_f32(P.mg); break;
     default: *bytes = 0.0;
   }
   return ETQ_OK;
@@ -518,7 +579,7 @@ void etq_destroy(etq_problem* h) {
   cudaFree(P.p1.Ainv); cudaFree(P.p1.MQinv);
   cudaFree(P.pm.t); cudaFree(P.pm.y0); cudaFree(P.pm.y1); cudaFree(P.pm.rr);
   cudaFree(P.red[0].partials); cudaFree(P.red[0].counter);
-  cudaFree(P.dscal); cudaFree(P.dhist); cudaFree(P.tk);
+  cudaFree(P.dscal); cudaFree(P.dhist); cudaFree(P.tk); cudaFree(P.tkf);
   if (P.hscal) cudaFreeHost(P.hscal);
   for (int i = 0; i < P.nkv; ++i) cudaFree(P.kv[i]);
   cudaEvent_t evs[6] = {P.ev_in, P.ev_out, P.ev_fork, P.ev_join, P.ev_t0, P.ev_t1};

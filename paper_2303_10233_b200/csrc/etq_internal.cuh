@@ -89,6 +89,9 @@ struct Level {
   // two-component work vectors, each [2*nq]
   double *b = nullptr, *x = nullptr, *r = nullptr, *d0 = nullptr, *d1 = nullptr;
   double* coarse_inv = nullptr;   // dense inverse (coarsest level only), nq x nq row-major
+  // fp32 copies for the c5 sweep (sweep32.cu)
+  float *f_dinv = nullptr, *f_b = nullptr, *f_x = nullptr, *f_r = nullptr, *f_d0 = nullptr, *f_d1 = nullptr;
+  float* f_coarse = nullptr;
 };
 
 struct Hierarchy {
@@ -98,6 +101,7 @@ struct Hierarchy {
   int kind = 0;               // 0: Q2 velocity (2 components, Dirichlet rows); 1: Q1 pressure (Ap)
   int ncomp = 2;
   bool built = false;
+  bool f32 = false;           // fp32 copies present
 };
 
 // ---------------------------------------------------------------- device scalars (MINRES / GMRES)
@@ -179,6 +183,7 @@ struct Problem {
   const double* minres_graph_x = nullptr;     // graphs bake in the caller's x pointer
   int64_t minres_graph_nodes[2] = {0, 0};     // kernel launches per graph launch
   double* tk = nullptr;                       // scratch for etq_time_kernel (3 x N)
+  float* tkf = nullptr;                       // fp32 scratch (2 x N)
 };
 
 // ---------------------------------------------------------------- helpers (host)
@@ -245,6 +250,12 @@ etq_status two_stage_run(Problem& P, const double* b, double* x, double eta, dou
                          etq_report* r1, etq_report* r2, double* bound);
 etq_status ap_solve(const Problem& P, const Hierarchy& H, const double* r, double* z, double* sum_slot,
                     const double* done, cudaStream_t st);
+
+// sweep32.cu
+etq_status ensure_f32(Problem& P);
+void launch_saddle_f32(const Problem& P, bool reduced, const float* x, float* y, cudaStream_t st);
+etq_status vcycle_f32(const Problem& P, const float* r_u, float* z_u, cudaStream_t st);
+double vcycle_bytes_f32(const Hierarchy& H);
 
 // solvers.cu
 void vec_scale_copy(double* y, const double* x, double a, int64_t n, cudaStream_t st);

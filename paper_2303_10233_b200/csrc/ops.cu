@@ -897,6 +897,9 @@ etq_status build_ap_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo,
 void free_hierarchy(Hierarchy& H) {
   for (size_t l = 0; l < H.lv.size(); ++l) {
     Level& L = H.lv[l];
+    if (l == 0 && H.kind == 0) L.A.fval = nullptr;   // owned by the problem's Lv
+    cudaFree(L.f_dinv); cudaFree(L.f_b); cudaFree(L.f_x); cudaFree(L.f_r); cudaFree(L.f_d0); cudaFree(L.f_d1);
+    cudaFree(L.f_coarse);
     if (H.kind == 1 || l > 0) sell_free(L.A);
     cudaFree(L.dinv); cudaFree(L.b); cudaFree(L.x); cudaFree(L.r); cudaFree(L.d0); cudaFree(L.d1);
     cudaFree(L.coarse_inv);
@@ -1223,5 +1226,29 @@ double vcycle_bytes(const Hierarchy& H) {
   }
   const Level& C = H.lv[L - 1];
   b += 8.0 * (double)C.g.nq * C.g.nq + 4.0 * 8.0 * C.g.nq;  // dense coarse solve
+  return b;
+}
+
+// fp32 V-cycle algorithmic bytes: 8 B per stored entry + 4 B index... i.e. values 4 B + index 4 B,
+// fp32 vectors (half of the fp64 vector traffic)
+double vcycle_bytes_f32(const Hierarchy& H) {
+  double b = 0.0;
+  const int L = (int)H.lv.size();
+  const int deg = H.degree;
+  for (int l = 0; l < L - 1; ++l) {
+    const Level& lv = H.lv[l];
+    const double nq = lv.nrows, mat = 8.0 * lv.A.nnz + 4.0 * lv.A.nslices * SELL_C + 4.0 * nq;
+    const double v = 4.0 * 2 * nq;
+    if (l == 0) b += 4.0 * nq + 2 * v;
+    for (int k = 0; k < deg; ++k) b += mat + v * ((k == 0 ? 2 : 3) + (k == deg - 1 ? 2 : 3));
+    const double nqc = H.lv[l + 1].nrows, vc = 4.0 * 2 * nqc;
+    b += v + 2 * vc + 4.0 * nqc;
+    b += 2 * vc + 2 * v;
+    b += mat + 2 * v + 2 * v;
+    for (int k = 0; k < deg - 1; ++k) b += mat + v * (3 + (k == deg - 2 ? 2 : 3));
+    if (l == 0) b += 2 * v + v;
+  }
+  const Level& C = H.lv[L - 1];
+  b += 4.0 * (double)C.nrows * C.nrows + 4.0 * 4.0 * C.nrows;
   return b;
 }

@@ -73,6 +73,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "etq_two_stage_solve": ([P, VP, VP, D, D, I32, I32, C.POINTER(Report), C.POINTER(Report),
                                  C.POINTER(D)], I32),
         "etq_apply_pcd_schur": ([P, VP, VP], I32),
+        "etq_est_minres": ([VP, VP, I32, C.POINTER(D)], I32),
+        "etq_apply_saddle_f32": ([P, I32, VP, VP], I32),
+        "etq_apply_vcycle_f32": ([P, VP, VP], I32),
         "etq_time_kernel": ([P, I32, I32, C.POINTER(D), C.POINTER(D)], I32),
         "etq_status_string": ([I32], C.c_char_p),
         "etq_destroy": ([P], None),
@@ -107,6 +110,17 @@ def launch_count() -> int:
     return c.value
 
 
+def est_minres(delta, gamma):
+    """EST-MINRES gamma^2 from a MINRES report's delta/gamma arrays (etq_est_minres)."""
+    import numpy as np
+    d = np.ascontiguousarray(delta, dtype=np.float64)
+    g = np.ascontiguousarray(gamma, dtype=np.float64)
+    out = C.c_double()
+    _check(lib().etq_est_minres(C.c_void_p(d.ctypes.data), C.c_void_p(g.ctypes.data), len(d), C.byref(out)),
+           "etq_est_minres")
+    return out.value
+
+
 def status_string(s: int) -> str:
     return lib().etq_status_string(int(s)).decode()
 
@@ -123,6 +137,13 @@ def _ptr(t):
     import torch
     if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
         raise ValueError("expected a contiguous float64 CUDA tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def _fptr(t):
+    import torch
+    if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        raise ValueError("expected a contiguous float32 CUDA tensor")
     return C.c_void_p(t.data_ptr())
 
 
@@ -246,6 +267,14 @@ class Problem:
         s = _check(lib().etq_minres_solve_host(self.h, kind, pb, px, rtol, maxit, C.byref(rep)),
                    "etq_minres_solve_host")
         return self._report_dict(rep, hist, dl, gm, s)
+
+    def apply_saddle_f32(self, x, y, reduced=False):
+        _check(lib().etq_apply_saddle_f32(self.h, int(reduced), _fptr(x), _fptr(y)), "etq_apply_saddle_f32")
+        return y
+
+    def apply_vcycle_f32(self, r_u, z_u):
+        _check(lib().etq_apply_vcycle_f32(self.h, _fptr(r_u), _fptr(z_u)), "etq_apply_vcycle_f32")
+        return z_u
 
     def apply_pcd_schur(self, r_p1, z_p1):
         _check(lib().etq_apply_pcd_schur(self.h, _ptr(r_p1), _ptr(z_p1)), "etq_apply_pcd_schur")

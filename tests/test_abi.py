@@ -16,7 +16,7 @@ def test_library_exports_every_header_symbol():
 
 
 def test_binding_mirrors_header_names():
-    methods = set(dir(etq.Problem)) | {"assemble", "status_string", "destroy", "sizes", "launch_count"}
+    methods = set(dir(etq.Problem)) | {"assemble", "status_string", "destroy", "sizes", "launch_count", "est_minres"}
     for n in etq.header_functions():
         short = n[len("etq_"):]
         assert short in methods or short == "status_string", short
@@ -35,3 +35,19 @@ def test_product_path_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_est_minres_host_matches_oracle():
+    """etq_est_minres is host-side: check it against oracle.krylov.est_minres_gamma2 on CPU."""
+    import numpy as np
+    from oracle import krylov
+    rng = np.random.default_rng(3)
+    for k in (1, 2, 5, 30):
+        d = rng.standard_normal(k)
+        g = np.abs(rng.standard_normal(k)) + 0.1          # gamma_2 .. gamma_{k+1}
+        ref = krylov.est_minres_gamma2(d, np.concatenate([[1.0], g]))
+        got = etq.est_minres(d, g)
+        if np.isnan(ref):
+            assert np.isnan(got)
+        else:
+            assert abs(got - ref) <= 1e-10 * max(1.0, abs(ref))

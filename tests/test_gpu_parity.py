@@ -309,3 +309,38 @@ def test_full_size_properties_c3():
         rb = L.getrow(500 + i + m * (500 + j))
         v16 = sorted(r16.data.tolist()); vb = sorted(rb.data.tolist())
         np.testing.assert_allclose(vb, v16, rtol=1e-13, atol=1e-15)
+
+
+def test_est_minres_c1():
+    """EST-MINRES (NEXT-1): the GPU MINRES Lanczos scalars give the same gamma^2 as the oracle's,
+    and both approximate the deflated generalised eigenvalue of Eq. (7)."""
+    n = 8
+    s = oracle_system(n)
+    P = etq.Problem(n)
+    P.precond_setup(etq.PC_P1_EXACT)
+    b = torch.zeros(P.N, dtype=torch.float64, device=DEV)
+    P.build_rhs(b)
+    x = torch.zeros(P.N, dtype=torch.float64, device=DEV)
+    rep = P.minres_solve(etq.PC_P1_EXACT, b, x, rtol=1e-12, maxit=400)
+    g2 = etq.est_minres(rep["delta"], rep["gamma"])
+    xo, ro = krylov.minres(lambda v: s.K @ v, s.b, precond.StokesP1(s), rtol=1e-12, maxit=400)
+    assert g2 == pytest.approx(krylov.est_minres_gamma2(ro.delta, ro.gamma), rel=1e-8)
+    from tests.test_oracle_estminres import deflated_infsup
+    assert g2 == pytest.approx(deflated_infsup(s), rel=1e-3)
+
+
+@pytest.mark.parametrize("n", [16, 64])
+def test_fp32_sweep_variants(n):
+    """c5 fp32-value variants (BASELINE.json configs[4]) against the fp64 oracle at 1e-5."""
+    s = oracle_system(n)
+    P = etq.Problem(n)
+    _p2(P, 0.01)
+    x = synth.random_vector(P.N, seed=31)
+    y = torch.zeros(P.N, dtype=torch.float32, device=DEV)
+    P.apply_saddle_f32(torch.as_tensor(x, dtype=torch.float32, device=DEV), y)
+    assert rel_err(host(y).astype(np.float64), s.K @ x) < 1e-5
+    h = mg.Hierarchy(n)
+    r = synth.random_vector(P.n_u, seed=32)
+    z = torch.zeros(P.n_u, dtype=torch.float32, device=DEV)
+    P.apply_vcycle_f32(torch.as_tensor(r, dtype=torch.float32, device=DEV), z)
+    assert rel_err(host(z).astype(np.float64), h.apply_velocity(r)) < 1e-5
