@@ -1,0 +1,130 @@
+"""Edge cases and full-size sampled parity (BASELINE.json sizes, bench launch configuration)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import fem, krylov, mg, normalize, oseen, precond  # noqa: E402
+from paper_2303_10233_b200 import etq  # noqa: E402
+import synth  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=DEV)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def zeros(n):
+    return torch.zeros(n, dtype=torch.float64, device=DEV)
+
+
+def test_invalid_arguments():
+    with pytest.raises(etq.EtqError) as e:
+        etq.Problem(1)
+    assert e.value.status == -1
+    with pytest.raises(etq.EtqError):
+        etq.Problem(8, bc=0, viscosity=-1.0, wind=1)
+    P = etq.Problem(6)                                    # not a power of two: no multigrid
+    with pytest.raises(etq.EtqError):
+        P.precond_setup(etq.PC_P2_GMG)
+    P = etq.Problem(8)
+    b = zeros(P.N); x = zeros(P.N)
+    with pytest.raises(etq.EtqError) as e:                # not set up
+        P.minres_solve(etq.PC_P2_GMG, b, x)
+    assert e.value.status == -6
+    with pytest.raises(etq.EtqError):                     # Oseen kinds on a Stokes problem
+        P.precond_setup(etq.PC_OSEEN_M1)
+
+
+def test_zero_rhs_and_maxit_status():
+    P = etq.Problem(8)
+    P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.005))
+    b = zeros(P.N); x = zeros(P.N)
+    rep = P.minres_solve(etq.PC_P2_GMG, b, x, rtol=1e-8, maxit=50)
+    assert rep["iterations"] == 0 and rep["converged"] and float(x.abs().max()) == 0.0
+    P.build_rhs(b)
+    rep = P.minres_solve(etq.PC_P2_GMG, b, x, rtol=1e-8, maxit=3)
+    assert rep["iterations"] == 3 and not rep["converged"] and rep["status"] == etq.ETQ_NOT_CONVERGED
+
+
+@pytest.mark.parametrize("kind", [etq.PC_P1_EXACT, etq.PC_P2_GMG])
+def test_minres_n2_and_warm_start(kind):
+    """Smallest grid (n = 2: one interior Q2 node per element row) and a non-zero initial guess."""
+    for n in (2, 8):
+        s = fem.assemble_system(n)
+        g = s.g
+        P = etq.Problem(n)
+        if kind == etq.PC_P1_EXACT:
+            P.precond_setup(kind); Pr = precond.StokesP1(s)
+        else:
+            P.precond_setup(kind, etq.make_params(cheb_sgs_lo=0.03)); Pr = precond.StokesP2(s, 0.03)
+        b = zeros(P.N); P.build_rhs(b)
+        x0 = synth.random_vector(P.N, seed=41)
+        x = dev(x0)
+        rep = P.minres_solve(kind, b, x, rtol=1e-10, maxit=300)
+        xo, ro = krylov.minres(lambda v: s.K @ v, s.b, Pr, rtol=1e-10, maxit=300, x0=x0)
+        assert rep["converged"] and ro.converged and abs(rep["iterations"] - ro.iterations) <= 2
+        k = fem.null_vector_k(g)
+        xg = normalize.normalise_solution(host(x), g.n_u, s.MQ, k)
+        xr = normalize.normalise_solution(xo, g.n_u, s.MQ, k)
+        assert np.abs(xg - xr).max() <= 1e-8 * np.abs(xr).max()
+
+
+def test_c3_full_size_sampled_parity():
+    """c3 (n = 1024, the bench configuration): the first MINRES iterations match the oracle's
+    |eta_j|, delta_j, gamma_j; the complete GPU solve meets rtol and its true residual is small."""
+    n = 1024
+    a = 0.005
+    s = fem.assemble_system(n)
+    h = mg.Hierarchy(n)
+    Pr = precond.StokesP2(s, a, hierarchy=h)
+    _, ro = krylov.minres(lambda v: s.K @ v, s.b, Pr, rtol=0.0, maxit=3)
+    P = etq.Problem(n)
+    P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=a))
+    b = zeros(P.N); P.build_rhs(b)
+    x = zeros(P.N)
+    rep = P.minres_solve(etq.PC_P2_GMG, b, x, rtol=1e-8, maxit=5000)
+    np.testing.assert_allclose(rep["history"][:3], ro.history[1:4], rtol=1e-9)
+    np.testing.assert_allclose(rep["delta"][:3], ro.delta[:3], rtol=1e-9)
+    np.testing.assert_allclose(rep["gamma"][:3], ro.gamma[1:4], rtol=1e-9)
+    assert rep["converged"] and rep["rel_res"] < 1e-8
+    y = zeros(P.N); P.apply_saddle(x, y)
+    # preconditioned residual 1e-8 ~ Euclidean residual a few orders larger at most
+    assert float(torch.linalg.norm(b - y) / torch.linalg.norm(b)) < 1e-5
+    # local mass conservation of the GPU solution
+    g0 = s.b[s.g.n_u + s.g.n_k:]
+    assert np.abs(s.B0 @ host(x)[:s.g.n_u] - g0).max() <= 10 * 1e-8 * np.linalg.norm(s.b)
+
+
+def test_c4_full_size_sampled_parity():
+    """c4 (n = 512 Oseen, two-stage): the first Step-I GMRES residual estimates match the oracle;
+    the full GPU two-stage solve meets eta = 1e-6 and Prop 3.3."""
+    n, nu = 512, 0.01
+    s = fem.assemble_system(n, nu=nu)
+    hF = oseen.velocity_hierarchy(n, nu, n_coarse=32)
+    nr = s.g.n_u + s.g.n_k
+    Kr = fem.reduced_operator(s)
+    _, ro = krylov.gmres(lambda v: Kr @ v, s.b[:nr], oseen.OseenPCD1(s, hF, oseen.PCDSchur(s, nu)),
+                         tol_abs=0.0, restart=50, maxit=3)
+    P = etq.Problem(n, bc=0, viscosity=nu, wind=1)
+    P.precond_setup(etq.PC_OSEEN_M1); P.precond_setup(etq.PC_OSEEN_PCD1)
+    b = zeros(P.N); P.build_rhs(b)
+    x = zeros(P.N)
+    rep = P.gmres_solve(etq.PC_OSEEN_PCD1, b, x, rtol=1e-30, restart=50, maxit=3, reduced=True)
+    np.testing.assert_allclose(rep["history"][:4], ro.history[:4], rtol=1e-9)
+    x.zero_()
+    out = P.two_stage_solve(b, x, eta=1e-6, c=10.0, restart=50, maxit=2000)
+    assert out["step1"]["converged"] and out["step2"]["converged"]
+    assert out["zstar"] <= out["bound"] * (1 + 1e-9)
+    y = zeros(P.N); P.apply_saddle(x, y)
+    assert float(torch.linalg.norm(b - y) / torch.linalg.norm(b)) <= 1e-6 * (1 + 1e-6)
