@@ -174,6 +174,21 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------------ multi-rank timing
+def aggregate(ms, its, world, device=None):
+    """Max of the per-rank timed region and sum of the per-rank MINRES iterations (contract:
+    value = units all ranks processed / max-over-ranks time).  Works with nccl or gloo."""
+    if world == 1:
+        return float(ms), float(its)
+    import torch
+    import torch.distributed as dist
+    t_ms = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    t_it = torch.tensor([float(its)], dtype=torch.float64, device=device)
+    dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t_it, op=dist.ReduceOp.SUM)
+    return t_ms.item(), t_it.item()
+
+
 # ------------------------------------------------------------------ ours (GPU)
 def run_ours(args):
     import numpy as np
@@ -192,13 +207,6 @@ def run_ours(args):
     def barrier():
         if world > 1:
             dist.barrier()
-
-    def allreduce(v, op):
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=op)
-        return t.item()
 
     n = args.n
     t0 = time.perf_counter()
@@ -239,8 +247,7 @@ def run_ours(args):
     L1 = etq.launch_count()
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
-    ms_max = allreduce(ms, dist.ReduceOp.MAX if world > 1 else None)
-    its_all = allreduce(float(its), dist.ReduceOp.SUM if world > 1 else None)
+    ms_max, its_all = aggregate(ms, its, world, dev)
     value = its_all / (ms_max / 1000.0)
     last = reps[-1]
 
@@ -261,8 +268,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
         barrier()
-        el_max = allreduce(el, dist.ReduceOp.MAX if world > 1 else None)
-        e_all = allreduce(float(e_its), dist.ReduceOp.SUM if world > 1 else None)
+        el_max, e_all = aggregate(el, e_its, world, dev)
         e2e = {"value": e_all / el_max, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * P.N,
                "d2h_bytes_per_step": 8 * P.N,
                "note": "etq_minres_solve_host: b and x0 copied H2D, x copied D2H each step (pinned host)"}
