@@ -34,6 +34,8 @@ void sell_free(Sell& s) {
   if (s.col) cudaFree(s.col);
   if (s.val) cudaFree(s.val);
   if (s.fval) cudaFree(s.fval);
+  if (s.skind) cudaFree(s.skind);
+  if (s.stoff) cudaFree(s.stoff);
   s = Sell{};
 }
 
@@ -154,6 +156,7 @@ etq_status etq_assemble(const etq_grid* grid, double viscosity, const etq_wind* 
   int64_t nsl = 0;
   A_TRY(build_node_perm(P.g, &P.node_perm, &nsl, P.stream));
   A_TRY(assemble_velocity_op(P.g, P.oseen, P.nu, P.wind, P.node_perm, nsl, &P.Lv, P.stream));
+  A_TRY(mark_implicit(P.g, P.oseen, P.Lv, P.stream));
   A_TRY(assemble_bt(P.g, 0, 0, P.node_perm, nsl, &P.BxT1, P.stream));
   A_TRY(assemble_bt(P.g, 1, 0, P.node_perm, nsl, &P.ByT1, P.stream));
   A_TRY(assemble_bt(P.g, 0, 1, P.node_perm, nsl, &P.BxT0, P.stream));
@@ -556,7 +559,7 @@ etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* 
   *ms = (double)t / reps;
   const double nnz_all = (double)(P.Lv.nnz + P.BxT1.nnz + P.ByT1.nnz + P.BxT0.nnz + P.ByT0.nnz + P.B.nnz);
   switch (which) {
-    case 0: *bytes = 12.0 * nnz_all + 4.0 * P.Lv.nslices * SELL_C + 16.0 * P.N; break;
+    case 0: *bytes = 12.0 * nnz_all - 4.0 * P.Lv.nnz_implicit + 4.0 * P.Lv.nslices * SELL_C + 16.0 * P.N; break;
     case 1: *bytes = cheb_step_bytes(P.mg.lv[0]); break;
     case 2: case 4: *bytes = vcycle_bytes(P.mg); break;
     case 5: *bytes = 8.0 * nnz_all + 4.0 * P.Lv.nslices * SELL_C + 8.0 * P.N; break;

@@ -16,6 +16,7 @@
 #include "etq_internal.cuh"
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 namespace {
 
@@ -518,6 +519,34 @@ __global__ void k_sell_diag_inv(Sell A, double* dinv) {
   }
   dinv[row] = 1.0 / d;
 }
+// A slice is implicit when every lane holds a row of the same node class whose stored columns are
+// exactly row + off[class][k] (the full interior stencil in enumeration order).
+__global__ void k_mark_implicit(Sell S, const int* off, const int* len, int8_t* skind, unsigned long long* nimp) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t s = t / SELL_C;
+  if (s >= S.nslices) return;
+  const int lane = (int)(t % SELL_C);
+  const int row = S.perm[t];
+  int cls = -1;
+  bool ok = row >= 0;
+  const int m = len[4];                       // nodes per grid row
+  if (ok) {
+    const int i = row % m, j = row / m;
+    cls = (i & 1) + 2 * (j & 1);
+    ok = S.slen[s] == len[cls];
+    for (int k = 0; ok && k < len[cls]; ++k) {
+      const int64_t e = S.sptr[s] + lane + (int64_t)k * SELL_C;
+      if (S.col[e] != row + off[cls * 32 + k] || S.val[e] == 0.0) ok = false;
+    }
+  }
+  const int c0 = __shfl_sync(0xffffffffu, cls, 0);
+  const bool all = __all_sync(0xffffffffu, ok && cls == c0);
+  if (lane == 0) {
+    skind[s] = all ? (int8_t)(c0 + 1) : (int8_t)0;
+    if (all) atomicAdd(nimp, (unsigned long long)SELL_C * len[c0]);
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- host entry points
@@ -602,5 +631,43 @@ etq_status assemble_f1(const Geo& g, double nu, int wind, Sell* out, cudaStream_
 etq_status sell_diag_inv(const Sell& A, double* dinv, cudaStream_t st) {
   k_sell_diag_inv<<<(unsigned)((A.nslices * SELL_C + 255) / 256), 256, 0, st>>>(A, dinv); etq_count_launch();
   ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
+// Per-class interior stencil offsets in vel_row's enumeration order (dj outer, di inner), then
+// mark the slices whose stored columns follow them (implicit column indices in the kernels).
+etq_status mark_implicit(const Geo& g, bool oseen, Sell& S, cudaStream_t st) {
+  if (!S.perm) return ETQ_OK;
+  std::vector<int> off(4 * 32, 0), len(5, 0);
+  for (int c = 0; c < 4; ++c) {
+    const int px = c & 1, py = c >> 1, rx = px ? 1 : 2, ry = py ? 1 : 2;
+    int k = 0;
+    for (int dj = -ry; dj <= ry; ++dj)
+      for (int di = -rx; di <= rx; ++di) {
+        if (!oseen) {
+          if ((di == 2 || di == -2) && dj == 0 && py) continue;
+          if ((dj == 2 || dj == -2) && di == 0 && px) continue;
+        }
+        off[c * 32 + k++] = di + g.m * dj;
+      }
+    len[c] = k;
+  }
+  len[4] = g.m;
+  int* dlen;
+  unsigned long long* dn;
+  ETQ_TRY(dalloc(&S.stoff, 4 * 32));
+  ETQ_TRY(dalloc(&dlen, 5));
+  ETQ_TRY(dalloc(&S.skind, S.nslices));
+  ETQ_TRY(dalloc(&dn, 1));
+  ETQ_CHECK(cudaMemcpyAsync(S.stoff, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice, st));
+  ETQ_CHECK(cudaMemcpyAsync(dlen, len.data(), sizeof(int) * len.size(), cudaMemcpyHostToDevice, st));
+  ETQ_CHECK(cudaMemsetAsync(dn, 0, sizeof(unsigned long long), st));
+  k_mark_implicit<<<(unsigned)((S.nslices * SELL_C + 255) / 256), 256, 0, st>>>(S, S.stoff, dlen, S.skind, dn);
+  etq_count_launch();
+  unsigned long long h = 0;
+  ETQ_CHECK(cudaMemcpyAsync(&h, dn, sizeof(h), cudaMemcpyDeviceToHost, st));
+  ETQ_CHECK(cudaStreamSynchronize(st));
+  cudaFree(dlen); cudaFree(dn);
+  S.nnz_implicit = (int64_t)h;
   return ETQ_OK;
 }

@@ -92,30 +92,12 @@ __device__ __forceinline__ T ld_mat(const T* p) {
   return __ldg(p);
 #endif
 }
-#ifndef SELL_PRED
-#define SELL_PRED 0
-#endif
-// all rows of a slice have the same length, so chunk predicates are warp-uniform
 __device__ __forceinline__ double sell_row1(const Sell& A, int64_t s, int lane, const double* __restrict__ x) {
   const int64_t base = A.sptr[s] + lane;
   const int len = A.slen[s];
   const int* __restrict__ cp = A.col + base;
   const double* __restrict__ vp = A.val + base;
   double acc = 0.0;
-#if SELL_PRED
-  for (int k = 0; k < len; k += SELL_U) {
-    int c[SELL_U]; double v[SELL_U];
-#pragma unroll
-    for (int u = 0; u < SELL_U; ++u) {
-      const bool ok = k + u < len;
-      c[u] = ok ? ld_mat(cp + (k + u) * SELL_C) : 0;
-      v[u] = ok ? ld_mat(vp + (k + u) * SELL_C) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < SELL_U; ++u)
-      if (k + u < len) acc = fma(v[u], __ldg(x + c[u]), acc);
-  }
-#else
   int k = 0;
   for (; k + SELL_U <= len; k += SELL_U) {
     int c[SELL_U]; double v[SELL_U];
@@ -125,30 +107,32 @@ __device__ __forceinline__ double sell_row1(const Sell& A, int64_t s, int lane, 
     for (int u = 0; u < SELL_U; ++u) acc = fma(v[u], __ldg(x + c[u]), acc);
   }
   for (; k < len; ++k) acc = fma(ld_mat(vp + k * SELL_C), __ldg(x + ld_mat(cp + k * SELL_C)), acc);
-#endif
   return acc;
 }
 
-__device__ __forceinline__ void sell_row2(const Sell& A, int64_t s, int lane, const double* __restrict__ x0,
+__device__ __forceinline__ void sell_row2(const Sell& A, int64_t s, int lane, int row, const double* __restrict__ x0,
                                           const double* __restrict__ x1, double& a0, double& a1) {
   const int64_t base = A.sptr[s] + lane;
   const int len = A.slen[s];
-  const int* __restrict__ cp = A.col + base;
   const double* __restrict__ vp = A.val + base;
-#if SELL_PRED
-  for (int k = 0; k < len; k += SELL_U) {
-    int c[SELL_U]; double v[SELL_U];
+  const int kind = A.skind ? (int)A.skind[s] : 0;
+  if (kind) {   // implicit columns: col = row + offset (warp-uniform branch)
+    const int* __restrict__ off = A.stoff + (kind - 1) * 32;
+    int k = 0;
+    for (; k + SELL_U <= len; k += SELL_U) {
+      int c[SELL_U]; double v[SELL_U];
 #pragma unroll
-    for (int u = 0; u < SELL_U; ++u) {
-      const bool ok = k + u < len;
-      c[u] = ok ? ld_mat(cp + (k + u) * SELL_C) : 0;
-      v[u] = ok ? ld_mat(vp + (k + u) * SELL_C) : 0.0;
+      for (int u = 0; u < SELL_U; ++u) { c[u] = row + __ldg(off + k + u); v[u] = ld_mat(vp + (k + u) * SELL_C); }
+#pragma unroll
+      for (int u = 0; u < SELL_U; ++u) { a0 = fma(v[u], __ldg(x0 + c[u]), a0); a1 = fma(v[u], __ldg(x1 + c[u]), a1); }
     }
-#pragma unroll
-    for (int u = 0; u < SELL_U; ++u)
-      if (k + u < len) { a0 = fma(v[u], __ldg(x0 + c[u]), a0); a1 = fma(v[u], __ldg(x1 + c[u]), a1); }
+    for (; k < len; ++k) {
+      const int c = row + __ldg(off + k); const double v = ld_mat(vp + k * SELL_C);
+      a0 = fma(v, __ldg(x0 + c), a0); a1 = fma(v, __ldg(x1 + c), a1);
+    }
+    return;
   }
-#else
+  const int* __restrict__ cp = A.col + base;
   int k = 0;
   for (; k + SELL_U <= len; k += SELL_U) {
     int c[SELL_U]; double v[SELL_U];
@@ -161,6 +145,5 @@ __device__ __forceinline__ void sell_row2(const Sell& A, int64_t s, int lane, co
     const int c = ld_mat(cp + k * SELL_C); const double v = ld_mat(vp + k * SELL_C);
     a0 = fma(v, __ldg(x0 + c), a0); a1 = fma(v, __ldg(x1 + c), a1);
   }
-#endif
 }
 }  // namespace etqd

@@ -53,6 +53,11 @@ struct Sell {
   int* col = nullptr;      // [nnz_stored]
   double* val = nullptr;   // [nnz_stored]
   float* fval = nullptr;   // optional fp32 copy of val (c5 sweep)
+  // implicit column indices (velocity operators): slice s with skind[s] = c + 1 holds rows of node
+  // class c with the full interior stencil, so col = row + stoff[c * 32 + k] and col[] is not read
+  int8_t* skind = nullptr; // [nslices] or nullptr
+  int* stoff = nullptr;    // [4 * 32] stencil offsets per class
+  int64_t nnz_implicit = 0;
 };
 
 // ---------------------------------------------------------------- grid geometry
@@ -206,6 +211,7 @@ etq_status assemble_ap(const Geo& g, Sell* out, cudaStream_t st);
 etq_status assemble_f1(const Geo& g, double nu, int wind, Sell* out, cudaStream_t st);
 etq_status sell_diag_inv(const Sell& A, double* dinv, cudaStream_t st);
 etq_status build_rhs_dev(const Problem& P, const double* f_nodal, double* b);
+etq_status mark_implicit(const Geo& g, bool oseen, Sell& S, cudaStream_t st);
 
 // ops.cu
 void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y, const double* inv_scale,

@@ -15,6 +15,11 @@
 #include <complex>
 
 #include "device_common.cuh"
+// SpMV-type kernels: 8 resident 256-thread blocks per SM (<= 32 registers) gave the highest
+// bandwidth among the measured variants (unroll 2/4/8 x min-blocks 1/6/8, n = 1024).
+#ifndef SPMV_MINB
+#define SPMV_MINB 8
+#endif
 using namespace etqd;
 
 namespace {
@@ -47,7 +52,7 @@ __global__ void __launch_bounds__(BS) k_saddle(SaddleArgs a) {
     if (s < nsv) {
       const int row = a.L.perm[s * SELL_C + lane];
       double ax = 0.0, ay = 0.0;
-      sell_row2(a.L, s, lane, xu, xv, ax, ay);
+      sell_row2(a.L, s, lane, row, xu, xv, ax, ay);
       ax += sell_row1(a.BxT1, s, lane, p1);
       ay += sell_row1(a.ByT1, s, lane, p1);
       if (!a.reduced) {
@@ -85,7 +90,7 @@ __global__ void __launch_bounds__(BS) k_vel_spmv2(Sell A, int nq, const double* 
   for (int64_t s = gw; s < A.nslices; s += nw) {
     const int row = A.perm[s * SELL_C + lane];
     double a0 = 0.0, a1 = 0.0;
-    sell_row2(A, s, lane, x, x + nq, a0, a1);
+    sell_row2(A, s, lane, row, x, x + nq, a0, a1);
     if (row >= 0) { y[row] = a0; y[nq + row] = a1; }
   }
 }
@@ -107,7 +112,7 @@ struct ChebArgs {
   const double* done;
 };
 template <int NC>
-__global__ void __launch_bounds__(BS) k_cheb_step(ChebArgs a) {
+__global__ void __launch_bounds__(BS, SPMV_MINB) k_cheb_step(ChebArgs a) {
   if (is_done(a.done)) return;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -115,7 +120,7 @@ __global__ void __launch_bounds__(BS) k_cheb_step(ChebArgs a) {
   for (int64_t s = gw; s < a.A.nslices; s += nw) {
     const int row = sell_row_id(a.A, s, lane);
     double q[2] = {0.0, 0.0};
-    if (NC == 2) sell_row2(a.A, s, lane, a.d_in, a.d_in + a.nq, q[0], q[1]);
+    if (NC == 2) sell_row2(a.A, s, lane, row, a.d_in, a.d_in + a.nq, q[0], q[1]);
     else q[0] = sell_row1(a.A, s, lane, a.d_in);
     if (row < 0) continue;
     const double di = a.dinv[row];
@@ -133,7 +138,7 @@ __global__ void __launch_bounds__(BS) k_cheb_step(ChebArgs a) {
 
 // r = b - A x ; d = D^{-1} r / theta  (start of post-smoothing), NC components
 template <int NC>
-__global__ void __launch_bounds__(BS) k_post_residual(Sell A, const double* dinv, int nq, const double* b,
+__global__ void __launch_bounds__(BS, SPMV_MINB) k_post_residual(Sell A, const double* dinv, int nq, const double* b,
                                                       const double* x, double* r, double* d, double theta,
                                                       const double* done) {
   if (is_done(done)) return;
@@ -143,7 +148,7 @@ __global__ void __launch_bounds__(BS) k_post_residual(Sell A, const double* dinv
   for (int64_t s = gw; s < A.nslices; s += nw) {
     const int row = sell_row_id(A, s, lane);
     double q[2] = {0.0, 0.0};
-    if (NC == 2) sell_row2(A, s, lane, x, x + nq, q[0], q[1]);
+    if (NC == 2) sell_row2(A, s, lane, row, x, x + nq, q[0], q[1]);
     else q[0] = sell_row1(A, s, lane, x);
     if (row < 0) continue;
     const double di = dinv[row];
@@ -841,6 +846,7 @@ etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, do
       int* perm; int64_t nsl;
       ETQ_TRY(build_node_perm(L.g, &perm, &nsl, P.stream));
       ETQ_TRY(assemble_velocity_op(L.g, P.oseen, P.nu, P.wind, perm, nsl, &L.A, P.stream));
+      ETQ_TRY(mark_implicit(L.g, P.oseen, L.A, P.stream));
       L.A.own_perm = true;
     }
     ETQ_TRY(dalloc(&L.dinv, L.g.nq));
@@ -1202,7 +1208,7 @@ void cheb_step_level0(const Problem& P, const double* d_in, double* d_out, cudaS
 // row permutation (4 B per slot), every vector element the kernel must read or write once.
 double cheb_step_bytes(const Level& L) {
   const double nq = L.nrows;
-  return 12.0 * L.A.nnz + 4.0 * L.A.nslices * SELL_C + 8.0 * nq /*dinv*/ + 8.0 * 2 * nq * 6 /*d,r,x in; x,r,d out*/;
+  return 12.0 * L.A.nnz - 4.0 * L.A.nnz_implicit + 4.0 * L.A.nslices * SELL_C + 8.0 * nq /*dinv*/ + 8.0 * 2 * nq * 6 /*d,r,x in; x,r,d out*/;
 }
 
 double vcycle_bytes(const Hierarchy& H) {
@@ -1211,7 +1217,7 @@ double vcycle_bytes(const Hierarchy& H) {
   const int deg = H.degree;
   for (int l = 0; l < L - 1; ++l) {
     const Level& lv = H.lv[l];
-    const double nq = lv.g.nq, mat = 12.0 * lv.A.nnz + 4.0 * lv.A.nslices * SELL_C + 8.0 * nq;
+    const double nq = lv.g.nq, mat = 12.0 * lv.A.nnz - 4.0 * lv.A.nnz_implicit + 4.0 * lv.A.nslices * SELL_C + 8.0 * nq;
     const double v = 8.0 * 2 * nq;   // one two-component vector
     if (l == 0) b += 8.0 * nq + 2 * v;                       // init: dinv, b -> d
     for (int k = 0; k < deg; ++k)                            // pre-smoothing steps
