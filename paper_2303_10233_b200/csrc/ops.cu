@@ -437,8 +437,9 @@ struct SgsSmem {
   __device__ __forceinline__ double& cl(int la, int lc) const { return C[lc * SGS_W + la]; }
 };
 
-// update of colour (PX, PY) vertices owned by this thread: plane column i = tx, rows j = ty, ty + 16
-template <int PX, int PY>
+// update of colour (PX, PY) vertices owned by this thread: plane column i = tx, rows j = ty, ty + 16.
+// IN: the whole window lies strictly inside the domain (no boundary vertices, no range checks).
+template <int PX, int PY, bool IN>
 __device__ __forceinline__ void sgs_colour(const SgsSmem& S, const double (&rr)[2], int A0, int C0, int n,
                                            double w_in, double w_bd, double w_off, double rq, double c_dd,
                                            double c_ed, double inv_in2) {
@@ -450,9 +451,9 @@ __device__ __forceinline__ void sgs_colour(const SgsSmem& S, const double (&rr)[
     const int j = threadIdx.y + SGS_TY * m;
     const int lc = 2 * j + PY, gc = C0 + lc;
     if (la == 0 || la == SGS_W - 1 || lc == 0 || lc == SGS_W - 1) continue;   // window edge: garbage halo
-    if (ga < 0 || ga > n || gc < 0 || gc > n) continue;
+    if (!IN && (ga < 0 || ga > n || gc < 0 || gc > n)) continue;
     const int iw = i - 1 + PX, ie = i + PX, js = j - 1 + PY, jn = j + PY;
-    if (ga > 0 && ga < n && gc > 0 && gc < n) {
+    if (IN || (ga > 0 && ga < n && gc > 0 && gc < n)) {
       const double sd = S.v(cxy, iw, js) + S.v(cxy, ie, js) + S.v(cxy, iw, jn) + S.v(cxy, ie, jn);
       const double se = S.v(cx, iw, j) + S.v(cx, ie, j) + S.v(cy, i, js) + S.v(cy, i, jn);
       const double sc = S.cl(la - 1, lc - 1) + S.cl(la, lc - 1) + S.cl(la - 1, lc) + S.cl(la, lc);
@@ -481,46 +482,53 @@ __device__ __forceinline__ void sgs_colour(const SgsSmem& S, const double (&rr)[
   }
 }
 
-__global__ void __launch_bounds__(SGS_TX * SGS_TY, 2) k_sgs_tile(SgsTileArgs a) {
-  if (is_done(a.done)) return;
+template <bool IN>
+__device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, const SgsSmem& S, int A0, int C0) {
   constexpr int W = SGS_W, T = SGS_T, H = SGS_H;
-  extern __shared__ double sm[];
-  SgsSmem S{sm, sm + 4 * SGS_P * SGS_P};
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int n = a.g.n, n1 = n + 1, nk = a.g.nk;
-  const int A0 = (blockIdx.x % a.tiles_x) * T - H, C0 = (blockIdx.x / a.tiles_x) * T - H;
   const double alpha = a.kproj ? (*a.kproj * a.inv_kk) : 0.0;
-  // ---- load y (planes, cells) and this thread's right-hand sides into registers
-  double rv[4][2], rc[2][4];
+  const double* __restrict__ r1 = a.r;
+  const double* __restrict__ r0 = a.r + nk;
+  // ---- phase A: stage the vertex right-hand sides (coalesced rows) and take this thread's
+  //      colour-plane entries into registers
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int ga = A0 + 2 * tx + (c & 1);
+  for (int v = 0; v < 4; ++v) {
+    const int lc = ty + SGS_TY * v, gc = C0 + lc;
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      const int gc = C0 + 2 * (ty + SGS_TY * m) + (c >> 1);
-      const bool in = ga >= 0 && ga <= n && gc >= 0 && gc <= n;
-      const int idx = ga + n1 * gc;
-      S.v(c, tx, ty + SGS_TY * m) = (in && a.y) ? a.y[idx] : 0.0;
-      rv[c][m] = in ? __ldg(a.r + idx) - alpha : 0.0;
+    for (int u = 0; u < 2; ++u) {
+      const int la = tx + 32 * u, ga = A0 + la;
+      const bool in = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
+      S.cl(la, lc) = in ? __ldg(r1 + ga + n1 * gc) - alpha : 0.0;
     }
   }
+  __syncthreads();
+  double rv[4][2];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int la = tx + 32 * u, ga = A0 + la;
+  for (int c = 0; c < 4; ++c)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int lc = ty + SGS_TY * v, gc = C0 + lc;
-      const bool in = ga >= 0 && ga < n && gc >= 0 && gc < n;
-      const int idx = nk + ga + n * gc;
-      S.cl(la, lc) = (in && a.y) ? a.y[idx] : 0.0;
-      rc[u][v] = in ? __ldg(a.r + idx) + alpha : 0.0;
+    for (int m = 0; m < 2; ++m) rv[c][m] = S.cl(2 * tx + (c & 1), 2 * (ty + SGS_TY * m) + (c >> 1));
+  __syncthreads();
+  // ---- phase B: y (vertices into the planes, cells) and the cell right-hand sides, coalesced
+  double rc[2][4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int lc = ty + SGS_TY * v, gc = C0 + lc;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int la = tx + 32 * u, ga = A0 + la;
+      const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
+      const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
+      S.vl(la, lc) = (inv && a.y) ? a.y[ga + n1 * gc] : 0.0;
+      S.cl(la, lc) = (inc && a.y) ? a.y[nk + ga + n * gc] : 0.0;
+      rc[u][v] = inc ? __ldg(r0 + ga + n * gc) + alpha : 0.0;
     }
   }
   __syncthreads();
   const double h = a.g.h;
   const double w_in = 4.0 * h / 6.0, w_bd = 2.0 * h / 6.0, w_off = h / 6.0, rq = 0.25 * h * h;
   const double c_dd = w_off * w_off, c_ed = w_off * w_in, inv_in2 = 1.0 / (w_in * w_in), inv_q0 = 1.0 / (h * h);
-#define SGS_V(PX, PY) do { sgs_colour<PX, PY>(S, rv[PX + 2 * PY], A0, C0, n, w_in, w_bd, w_off, rq, c_dd, c_ed, inv_in2); __syncthreads(); } while (0)
+#define SGS_V(PX, PY) do { sgs_colour<PX, PY, IN>(S, rv[PX + 2 * PY], A0, C0, n, w_in, w_bd, w_off, rq, c_dd, c_ed, inv_in2); __syncthreads(); } while (0)
   SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
   // P0 cells (once: the backward sweep's P0 update would repeat it exactly)
 #pragma unroll
@@ -529,52 +537,58 @@ __global__ void __launch_bounds__(SGS_TX * SGS_TY, 2) k_sgs_tile(SgsTileArgs a) 
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int lc = ty + SGS_TY * v, gc = C0 + lc;
-      if (la == W - 1 || lc == W - 1 || ga < 0 || ga >= n || gc < 0 || gc >= n) continue;
+      if (la == W - 1 || lc == W - 1) continue;
+      if (!IN && (ga < 0 || ga >= n || gc < 0 || gc >= n)) continue;
       S.cl(la, lc) = (rc[u][v] - rq * (S.vl(la, lc) + S.vl(la + 1, lc) + S.vl(la, lc + 1) + S.vl(la + 1, lc + 1))) * inv_q0;
     }
   }
   __syncthreads();
   SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
 #undef SGS_V
-  // ---- write the tile with the semi-iteration update
+  // ---- write the tile (coalesced rows) with the semi-iteration update
   double kd = 0.0;
+  for (int lc = H + ty; lc < H + T; lc += SGS_TY) {
+    const int gc = C0 + lc;
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int la = 2 * tx + (c & 1), ga = A0 + la;
-#pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      const int lc = 2 * (ty + SGS_TY * m) + (c >> 1), gc = C0 + lc;
-      if (la < H || la >= H + T || lc < H || lc >= H + T || ga > n || gc > n) continue;
-      const int idx = ga + n1 * gc;
-      const double v = S.v(c, tx, ty + SGS_TY * m);
-      double o = v;
-      if (a.mode) {
-        const double y = a.y ? a.y[idx] : 0.0, yp = a.yp ? a.yp[idx] : 0.0;
-        o = a.omega * (a.gam * (v - y) + y - yp) + yp;
+    for (int u = 0; u < 2; ++u) {
+      const int la = H + tx + 32 * u, ga = A0 + la;
+      if (la >= H + T) continue;
+      if (IN || (ga <= n && gc <= n)) {
+        const int idx = ga + n1 * gc;
+        const double v = S.vl(la, lc);
+        double o = v;
+        if (a.mode) {
+          const double y = a.y ? a.y[idx] : 0.0, yp = a.yp ? a.yp[idx] : 0.0;
+          o = a.omega * (a.gam * (v - y) + y - yp) + yp;
+        }
+        a.out[idx] = o;
+        kd += o;
       }
-      a.out[idx] = o;
-      kd += o;
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int la = tx + 32 * u, ga = A0 + la;
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int lc = ty + SGS_TY * v, gc = C0 + lc;
-      if (la < H || la >= H + T || lc < H || lc >= H + T || ga >= n || gc >= n) continue;
-      const int idx = nk + ga + n * gc;
-      const double val = S.cl(la, lc);
-      double o = val;
-      if (a.mode) {
-        const double y = a.y ? a.y[idx] : 0.0, yp = a.yp ? a.yp[idx] : 0.0;
-        o = a.omega * (a.gam * (val - y) + y - yp) + yp;
+      if (IN || (ga < n && gc < n)) {
+        const int idx = nk + ga + n * gc;
+        const double v = S.cl(la, lc);
+        double o = v;
+        if (a.mode) {
+          const double y = a.y ? a.y[idx] : 0.0, yp = a.yp ? a.yp[idx] : 0.0;
+          o = a.omega * (a.gam * (v - y) + y - yp) + yp;
+        }
+        a.out[idx] = o;
+        kd -= o;
       }
-      a.out[idx] = o;
-      kd -= o;
     }
   }
   if (a.kout) { double v[1] = {kd}; reduce_finish<1>(v, a.site, a.slot, a.kout); }
+}
+
+__global__ void __launch_bounds__(SGS_TX * SGS_TY, 2) k_sgs_tile(SgsTileArgs a) {
+  if (is_done(a.done)) return;
+  extern __shared__ double sm[];
+  const SgsSmem S{sm, sm + 4 * SGS_P * SGS_P};
+  const int n = a.g.n;
+  const int A0 = (blockIdx.x % a.tiles_x) * SGS_T - SGS_H, C0 = (blockIdx.x / a.tiles_x) * SGS_T - SGS_H;
+  const bool interior = A0 >= 1 && A0 + SGS_W - 1 <= n - 1 && C0 >= 1 && C0 + SGS_W - 1 <= n - 1;
+  if (interior) sgs_tile_body<true>(a, S, A0, C0);
+  else sgs_tile_body<false>(a, S, A0, C0);
 }
 
 // k^T x
@@ -1052,14 +1066,24 @@ void mass_apply(const Geo& g, const double* x, double* y, cudaStream_t st) {
 }
 
 static void launch_sgs_tile(SgsTileArgs a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static bool smem_set = false;
+  if (!smem_set) {
     cudaFuncSetAttribute(k_sgs_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, SGS_SMEM);
-    attr = true;
+    smem_set = true;
   }
   a.tiles_x = (a.g.n + 1 + SGS_T - 1) / SGS_T;
   const int tiles = a.tiles_x * a.tiles_x;
-  k_sgs_tile<<<tiles, dim3(SGS_TX, SGS_TY), SGS_SMEM, st>>>(a); etq_count_launch();
+  // the latency-bound pressure chain runs at the lowest priority so that the concurrent,
+  // bandwidth-bound V-cycle blocks are scheduled first (the attribute is kept by graph capture)
+  static int lo_prio = 1;
+  if (lo_prio == 1) { int hi; cudaDeviceGetStreamPriorityRange(&lo_prio, &hi); }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles); cfg.blockDim = dim3(SGS_TX, SGS_TY); cfg.dynamicSmemBytes = SGS_SMEM; cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributePriority;
+  attr[0].val.priority = lo_prio;
+  cfg.attrs = attr; cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_sgs_tile, a); etq_count_launch();
 }
 
 // z = S(y) (one symmetric sweep from y; y nullable = 0); t is scratch for the in-place case
