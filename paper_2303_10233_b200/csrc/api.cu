@@ -338,24 +338,19 @@ etq_status etq_minres_solve_host(etq_problem* h, etq_pc_kind kind, const double*
                                  double rtol, int32_t maxit, etq_report* report) {
   if (!h || !b_host || !x_host) return ETQ_EINVAL;
   Problem& P = h->P;
-  double *db, *dx;
-  ETQ_TRY(dalloc(&db, P.N));
-  ETQ_TRY(dalloc(&dx, P.N));
-  etq_status s;
-  {
-    StreamScope sc(P);
-    ETQ_CHECK(cudaMemcpyAsync(db, b_host, sizeof(double) * P.N, cudaMemcpyHostToDevice, P.stream));
-    ETQ_CHECK(cudaMemcpyAsync(dx, x_host, sizeof(double) * P.N, cudaMemcpyHostToDevice, P.stream));
-    s = minres_run(P, kind, db, dx, rtol, maxit, report);
-    if (s >= 0) {
-      ETQ_CHECK(cudaMemcpyAsync(x_host, dx, sizeof(double) * P.N, cudaMemcpyDeviceToHost, P.stream));
-      ETQ_CHECK(cudaStreamSynchronize(P.stream));
-    }
+  // persistent device staging buffers (the cached MINRES graphs stay valid across calls)
+  if (!P.kv[7]) ETQ_TRY(dalloc(&P.kv[7], P.N));
+  if (!P.kv[8]) ETQ_TRY(dalloc(&P.kv[8], P.N));
+  double* db = P.kv[7];
+  double* dx = P.kv[8];
+  StreamScope sc(P);
+  ETQ_CHECK(cudaMemcpyAsync(db, b_host, sizeof(double) * P.N, cudaMemcpyHostToDevice, P.stream));
+  ETQ_CHECK(cudaMemcpyAsync(dx, x_host, sizeof(double) * P.N, cudaMemcpyHostToDevice, P.stream));
+  const etq_status s = minres_run(P, kind, db, dx, rtol, maxit, report);
+  if (s >= 0) {
+    ETQ_CHECK(cudaMemcpyAsync(x_host, dx, sizeof(double) * P.N, cudaMemcpyDeviceToHost, P.stream));
+    ETQ_CHECK(cudaStreamSynchronize(P.stream));
   }
-  cudaFree(db); cudaFree(dx);
-  // the cached graphs referenced dx
-  for (int g = 0; g < 2; ++g)
-    if (P.minres_graph[g]) { cudaGraphExecDestroy(P.minres_graph[g]); P.minres_graph[g] = nullptr; }
   return s;
 }
 
@@ -587,7 +582,7 @@ void etq_destroy(etq_problem* h) {
   cudaFree(P.red[0].partials); cudaFree(P.red[0].counter);
   cudaFree(P.dscal); cudaFree(P.dhist); cudaFree(P.tk); cudaFree(P.tkf);
   if (P.hscal) cudaFreeHost(P.hscal);
-  for (int i = 0; i < P.nkv; ++i) cudaFree(P.kv[i]);
+  for (int i = 0; i < 10; ++i) cudaFree(P.kv[i]);
   cudaEvent_t evs[6] = {P.ev_in, P.ev_out, P.ev_fork, P.ev_join, P.ev_t0, P.ev_t1};
   for (auto e : evs) if (e) cudaEventDestroy(e);
   if (P.aux) cudaStreamDestroy(P.aux);
