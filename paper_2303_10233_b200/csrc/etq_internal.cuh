@@ -99,6 +99,12 @@ struct Level {
   float* f_coarse = nullptr;
 };
 
+// device-side description of one level of the fused coarse-level tail (ops.cu)
+struct TailLevel {
+  Sell A; const double* dinv; double *b, *x, *r, *d0, *d1;
+  int nq, m; double c1[4], c2[4]; const double* coarse_inv;
+};
+
 struct Hierarchy {
   std::vector<Level> lv;
   double lo = 0.16, hi = 1.6;
@@ -107,6 +113,8 @@ struct Hierarchy {
   int ncomp = 2;
   bool built = false;
   bool f32 = false;           // fp32 copies present
+  int tail_start = -1;        // first level run by the fused coarse-level tail kernel (-1: none)
+  TailLevel* tail = nullptr;  // device array, levels tail_start .. L-1
 };
 
 // ---------------------------------------------------------------- device scalars (MINRES / GMRES)

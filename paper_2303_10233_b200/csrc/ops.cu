@@ -819,7 +819,146 @@ etq_status p1_build_mass_inverse(const Geo& g, double* W, cudaStream_t st) {
   return ETQ_OK;
 }
 
+// ---------------------------------------------------------------- coarse-level tail
+// Levels with n <= TAIL_N are latency-bound (~55 us per level for ~10 tiny launches); one
+// 1024-thread CTA runs them all with __syncthreads() between the same per-row operations as the
+// level kernels (same formulas and order, so the results are identical).
+namespace {
+constexpr int TAIL_N = 16;
+constexpr int TAIL_THREADS = 1024;
+
+__device__ void tail_cheb_step(const TailLevel& L, const double* d_in, const double* r_in, const double* x_in,
+                               double* x_out, double* r_out, double* d_out, double c1, double c2) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = TAIL_THREADS / 32;
+  for (int64_t s = w; s < L.A.nslices; s += nw) {
+    const int row = L.A.perm[s * SELL_C + lane];
+    double q0 = 0.0, q1 = 0.0;
+    sell_row2(L.A, s, lane, row, d_in, d_in + L.nq, q0, q1);
+    if (row < 0) continue;
+    const double di = L.dinv[row];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int64_t idx = (int64_t)c * L.nq + row;
+      const double dd = d_in[idx];
+      const double ro = r_in[idx] - (c == 0 ? q0 : q1);
+      x_out[idx] = (x_in ? x_in[idx] : 0.0) + dd;
+      if (r_out) r_out[idx] = ro;
+      if (d_out) d_out[idx] = c1 * dd + c2 * (di * ro);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(const TailLevel* lvs, int nlev, int degree, double theta,
+                                                              const double* done) {
+  if (is_done(done)) return;
+  const int tid = threadIdx.x;
+  // ---- down (level 0 of the tail: b and d0 were written by the restriction kernel above it)
+  for (int l = 0; l < nlev - 1; ++l) {
+    const TailLevel& L = lvs[l];
+    double* din = L.d0; double* dout = L.d1;
+    for (int k = 0; k < degree; ++k) {
+      tail_cheb_step(L, din, k == 0 ? L.b : L.r, k == 0 ? nullptr : L.x, L.x, L.r, k == degree - 1 ? nullptr : dout,
+                     L.c1[k], L.c2[k]);
+      __syncthreads();
+      double* t = din; din = dout; dout = t;
+    }
+    const TailLevel& Cv = lvs[l + 1];
+    for (int t = tid; t < Cv.nq; t += TAIL_THREADS) {
+      const int I = t % Cv.m, J = t / Cv.m;
+      if (I == 0 || J == 0 || I == Cv.m - 1 || J == Cv.m - 1) {
+        Cv.b[t] = 0.0; Cv.b[Cv.nq + t] = 0.0; Cv.d0[t] = 0.0; Cv.d0[Cv.nq + t] = 0.0;
+        continue;
+      }
+      int ox[5], oy[5]; double wx[5], wy[5];
+      const int nx = restrict_taps(I, ox, wx), ny = restrict_taps(J, oy, wy);
+      double s0 = 0.0, s1 = 0.0;
+      for (int q = 0; q < ny; ++q) {
+        const int64_t rowf = (int64_t)(2 * J + oy[q]) * L.m;
+        double t0 = 0.0, t1 = 0.0;
+        for (int p = 0; p < nx; ++p) {
+          const int64_t f = rowf + 2 * I + ox[p];
+          t0 = fma(wx[p], L.r[f], t0);
+          t1 = fma(wx[p], L.r[L.nq + f], t1);
+        }
+        s0 = fma(wy[q], t0, s0);
+        s1 = fma(wy[q], t1, s1);
+      }
+      Cv.b[t] = s0; Cv.b[Cv.nq + t] = s1;
+      const double di = Cv.dinv[t];
+      Cv.d0[t] = di * s0 / theta; Cv.d0[Cv.nq + t] = di * s1 / theta;
+    }
+    __syncthreads();
+  }
+  // ---- coarse solve x = C^{-1} b (warp per row, both components)
+  {
+    const TailLevel& C = lvs[nlev - 1];
+    const int lane = tid & 31, w = tid >> 5;
+    for (int r = w; r < C.nq; r += TAIL_THREADS / 32)
+      for (int c = 0; c < 2; ++c) {
+        double s = 0.0;
+        for (int j = lane; j < C.nq; j += 32) s = fma(C.coarse_inv[(int64_t)r * C.nq + j], C.b[(int64_t)c * C.nq + j], s);
+        s = warp_sum(s);
+        if (lane == 0) C.x[(int64_t)c * C.nq + r] = s;
+      }
+    __syncthreads();
+  }
+  // ---- up
+  const double* pend_c = nullptr;
+  for (int l = nlev - 2; l >= 0; --l) {
+    const TailLevel& L = lvs[l];
+    const TailLevel& Cv = lvs[l + 1];
+    for (int64_t t = tid; t < L.nq; t += TAIL_THREADS) {
+      const int k = (int)(t % L.m), ll = (int)(t / L.m);
+      if (k == 0 || ll == 0 || k == L.m - 1 || ll == L.m - 1) continue;
+      int ix[3], iy[3]; double wx[3], wy[3];
+      const int nx = prolong_taps(k, ix, wx), ny = prolong_taps(ll, iy, wy);
+      double s0 = 0.0, s1 = 0.0;
+      for (int q = 0; q < ny; ++q) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int p = 0; p < nx; ++p) {
+          const int64_t c = (int64_t)iy[q] * Cv.m + ix[p];
+          const double v0 = pend_c ? Cv.x[c] + pend_c[c] : Cv.x[c];
+          const double v1 = pend_c ? Cv.x[Cv.nq + c] + pend_c[Cv.nq + c] : Cv.x[Cv.nq + c];
+          t0 = fma(wx[p], v0, t0);
+          t1 = fma(wx[p], v1, t1);
+        }
+        s0 = fma(wy[q], t0, s0);
+        s1 = fma(wy[q], t1, s1);
+      }
+      L.x[t] += s0; L.x[L.nq + t] += s1;
+    }
+    __syncthreads();
+    {   // r = b - A x ; d = D^{-1} r / theta
+      const int lane = tid & 31, w = tid >> 5;
+      for (int64_t s = w; s < L.A.nslices; s += TAIL_THREADS / 32) {
+        const int row = L.A.perm[s * SELL_C + lane];
+        double q0 = 0.0, q1 = 0.0;
+        sell_row2(L.A, s, lane, row, L.x, L.x + L.nq, q0, q1);
+        if (row < 0) continue;
+        const double di = L.dinv[row];
+        const double r0 = L.b[row] - q0, r1 = L.b[L.nq + row] - q1;
+        L.r[row] = r0; L.r[L.nq + row] = r1;
+        L.d0[row] = di * r0 / theta; L.d0[L.nq + row] = di * r1 / theta;
+      }
+    }
+    __syncthreads();
+    double* din = L.d0; double* dout = L.d1;
+    for (int k = 0; k < degree - 1; ++k) {
+      tail_cheb_step(L, din, L.r, L.x, L.x, k == degree - 2 ? nullptr : L.r, dout, L.c1[k], L.c2[k]);
+      __syncthreads();
+      double* t = din; din = dout; dout = t;
+    }
+    pend_c = din;
+  }
+  // ---- complete level 0 of the tail: x += pending correction (the caller prolongs from x)
+  const TailLevel& L0 = lvs[0];
+  for (int64_t i = tid; i < 2LL * L0.nq; i += TAIL_THREADS) L0.x[i] += pend_c[i];
+}
+}  // namespace
+
 // ---------------------------------------------------------------- hierarchy
+static void cheb_coeffs(double lo, double hi, double bim, int degree, std::vector<double>& c1, std::vector<double>& c2);
+
 static etq_status alloc_level_vectors(Level& L, int nc, bool need_b) {
   const size_t nv = (size_t)nc * L.nrows;
   if (need_b) ETQ_TRY(dalloc(&L.b, nv));
@@ -875,6 +1014,26 @@ etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, do
   if (P.oseen) ETQ_TRY(dense_inverse_pivot(C.coarse_inv, C.g.nq, P.stream));
   else ETQ_TRY(dense_inverse_spd(C.coarse_inv, C.g.nq, P.stream));
   H.lo = lo; H.hi = hi; H.degree = degree; H.built = true;
+  // coarse-level tail: first level l >= 1 with n <= TAIL_N (degree <= 4)
+  H.tail_start = -1;
+  if (degree <= 4)
+    for (size_t l = 1; l < H.lv.size(); ++l)
+      if (H.lv[l].g.n <= TAIL_N && H.lv.size() - l >= 2) { H.tail_start = (int)l; break; }
+  if (H.tail_start > 0) {
+    std::vector<TailLevel> tl;
+    std::vector<double> c1, c2;
+    for (size_t l = H.tail_start; l < H.lv.size(); ++l) {
+      const Level& lv = H.lv[l];
+      TailLevel t{};
+      t.A = lv.A; t.dinv = lv.dinv; t.b = lv.b; t.x = lv.x; t.r = lv.r; t.d0 = lv.d0; t.d1 = lv.d1;
+      t.nq = lv.nrows; t.m = lv.g.m; t.coarse_inv = lv.coarse_inv;
+      cheb_coeffs(lo, hi, lv.bim, degree, c1, c2);
+      for (int k = 0; k < degree; ++k) { t.c1[k] = c1[k]; t.c2[k] = c2[k]; }
+      tl.push_back(t);
+    }
+    ETQ_TRY(dalloc(&H.tail, tl.size()));
+    ETQ_CHECK(cudaMemcpy(H.tail, tl.data(), sizeof(TailLevel) * tl.size(), cudaMemcpyHostToDevice));
+  }
   ETQ_CHECK(cudaStreamSynchronize(P.stream));
   return ETQ_OK;
 }
@@ -924,6 +1083,7 @@ void free_hierarchy(Hierarchy& H) {
     cudaFree(L.dinv); cudaFree(L.b); cudaFree(L.x); cudaFree(L.r); cudaFree(L.d0); cudaFree(L.d1);
     cudaFree(L.coarse_inv);
   }
+  cudaFree(H.tail);
   H = Hierarchy{};
 }
 
@@ -973,8 +1133,10 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
   std::vector<const double*> bvec(L);
   std::vector<const double*> pend(L, nullptr);
   std::vector<double> c1, c2;
+  const bool use_tail = H.kind == 0 && nc == 2 && H.tail_start > 0 && H.tail != nullptr;
+  const int Ld = use_tail ? H.tail_start + 1 : L;   // levels handled by the per-level kernels (+1)
   // ---- down
-  for (int l = 0; l < L - 1; ++l) {
+  for (int l = 0; l < Ld - 1; ++l) {
     const Level& lv = H.lv[l];
     const int nq = lv.nrows;
     cheb_coeffs(H.lo, H.hi, lv.bim, H.degree, c1, c2);
@@ -1006,14 +1168,17 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     }
     etq_count_launch();
   }
-  // ---- coarse
-  {
+  // ---- coarse (or the fused coarse-level tail, which leaves a complete x on its first level)
+  if (use_tail) {
+    k_vcycle_tail<<<1, TAIL_THREADS, 0, st>>>(H.tail, L - H.tail_start, H.degree, theta, done); etq_count_launch();
+    pend[Ld - 1] = nullptr;
+  } else {
     const Level& C = H.lv[L - 1];
     dense_gemv(C.coarse_inv, C.nrows, nc, C.b, C.nrows, C.x, C.nrows, done, st);
     pend[L - 1] = nullptr;
   }
   // ---- up
-  for (int l = L - 2; l >= 0; --l) {
+  for (int l = Ld - 2; l >= 0; --l) {
     const Level& lv = H.lv[l];
     const Level& cv = H.lv[l + 1];
     const int nq = lv.nrows;
