@@ -43,8 +43,12 @@ enum {
 
 /* Grid: n x n squares on [-1,1]^2, h = 2/n.
  * bc = 0: regularised lid u = (1 - x^4, 0) on y = 1, no-slip elsewhere (reading R1);
- * bc = 1: homogeneous Dirichlet velocity on the whole boundary. */
-typedef struct { int32_t n; int32_t bc; } etq_grid;
+ * bc = 1: homogeneous Dirichlet velocity on the whole boundary.
+ * storage (velocity operators; results are bitwise identical in all modes):
+ *   0 = compressed: interior SELL slices keep neither column indices (col = row + per-class
+ *       offset) nor values when these equal the per-class stencil bitwise;
+ *   1 = implicit column indices only;  2 = explicit SELL (indices and values stored). */
+typedef struct { int32_t n; int32_t bc; int32_t storage; } etq_grid;
 
 /* Convection field of the Oseen problem.
  * kind = 0: none (Stokes, viscosity ignored);

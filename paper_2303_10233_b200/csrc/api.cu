@@ -36,6 +36,7 @@ void sell_free(Sell& s) {
   if (s.fval) cudaFree(s.fval);
   if (s.skind) cudaFree(s.skind);
   if (s.stoff) cudaFree(s.stoff);
+  if (s.stval) cudaFree(s.stval);
   s = Sell{};
 }
 
@@ -120,6 +121,7 @@ etq_status etq_assemble(const etq_grid* grid, double viscosity, const etq_wind* 
                         etq_problem** out) {
   if (!grid || !out) return ETQ_EINVAL;
   if (grid->n < 2 || grid->n > 4096 || (grid->bc != 0 && grid->bc != 1)) return ETQ_EINVAL;
+  if (grid->storage < 0 || grid->storage > 2) return ETQ_EINVAL;
   const bool oseen = wind && wind->kind != 0;
   if (oseen && !(viscosity > 0.0)) return ETQ_EINVAL;
   if (wind && (wind->kind < 0 || wind->kind > 1)) return ETQ_EINVAL;
@@ -128,6 +130,7 @@ etq_status etq_assemble(const etq_grid* grid, double viscosity, const etq_wind* 
   Problem& P = h->P;
   P.g = make_geo(grid->n);
   P.bc = grid->bc;
+  P.storage = grid->storage;
   P.oseen = oseen;
   P.wind = oseen ? wind->kind : 0;
   P.nu = oseen ? viscosity : 1.0;
@@ -159,7 +162,7 @@ etq_status etq_assemble(const etq_grid* grid, double viscosity, const etq_wind* 
   int64_t nsl = 0;
   A_TRY(build_node_perm(P.g, &P.node_perm, &nsl, P.stream));
   A_TRY(assemble_velocity_op(P.g, P.oseen, P.nu, P.wind, P.node_perm, nsl, &P.Lv, P.stream));
-  A_TRY(mark_implicit(P.g, P.oseen, P.Lv, P.stream));
+  if (P.storage < 2) A_TRY(mark_implicit(P.g, P.oseen, P.nu, P.wind, P.Lv, P.stream, P.storage == 0));
   A_TRY(assemble_bt(P.g, 0, 0, P.node_perm, nsl, &P.BxT1, P.stream));
   A_TRY(assemble_bt(P.g, 1, 0, P.node_perm, nsl, &P.ByT1, P.stream));
   A_TRY(assemble_bt(P.g, 0, 1, P.node_perm, nsl, &P.BxT0, P.stream));
@@ -557,7 +560,7 @@ etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* 
   *ms = (double)t / reps;
   const double nnz_all = (double)(P.Lv.nnz + P.BxT1.nnz + P.ByT1.nnz + P.BxT0.nnz + P.ByT0.nnz + P.B.nnz);
   switch (which) {
-    case 0: *bytes = 12.0 * nnz_all - 4.0 * P.Lv.nnz_implicit + 4.0 * P.Lv.nslices * SELL_C + 16.0 * P.N; break;
+    case 0: *bytes = 12.0 * nnz_all - 4.0 * P.Lv.nnz_implicit - 8.0 * P.Lv.nnz_implicit_vals + 4.0 * P.Lv.nslices * SELL_C + 16.0 * P.N; break;
     case 1: *bytes = cheb_step_bytes(P.mg.lv[0]); break;
     case 2: case 4: *bytes = vcycle_bytes(P.mg); break;
     case 5: *bytes = 8.0 * nnz_all + 4.0 * P.Lv.nslices * SELL_C + 8.0 * P.N; break;

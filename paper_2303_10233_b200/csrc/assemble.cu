@@ -521,14 +521,28 @@ __global__ void k_sell_diag_inv(Sell A, double* dinv) {
 }
 // A slice is implicit when every lane holds a row of the same node class whose stored columns are
 // exactly row + off[class][k] (the full interior stencil in enumeration order).
-__global__ void k_mark_implicit(Sell S, const int* off, const int* len, int8_t* skind, unsigned long long* nimp) {
+// reference values of the interior rows of each node class (node (4 + px, 4 + py))
+struct RefEmit {
+  double* out; int k;
+  __device__ void operator()(int, double v) { out[k++] = v; }
+};
+__global__ void k_ref_values(VelParams P, double* stval) {
+  const int c = threadIdx.x;
+  if (c >= 4) return;
+  const int px = c & 1, py = c >> 1;
+  RefEmit e{stval + c * 32, 0};
+  vel_row(P, (4 + px) + P.g.m * (4 + py), e);
+}
+
+__global__ void k_mark_implicit(Sell S, const int* off, const int* len, const double* stval, int8_t* skind,
+                                unsigned long long* nimp) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t s = t / SELL_C;
   if (s >= S.nslices) return;
   const int lane = (int)(t % SELL_C);
   const int row = S.perm[t];
   int cls = -1;
-  bool ok = row >= 0;
+  bool ok = row >= 0, vok = ok && stval != nullptr;
   const int m = len[4];                       // nodes per grid row
   if (ok) {
     const int i = row % m, j = row / m;
@@ -537,13 +551,16 @@ __global__ void k_mark_implicit(Sell S, const int* off, const int* len, int8_t* 
     for (int k = 0; ok && k < len[cls]; ++k) {
       const int64_t e = S.sptr[s] + lane + (int64_t)k * SELL_C;
       if (S.col[e] != row + off[cls * 32 + k] || S.val[e] == 0.0) ok = false;
+      if (vok && S.val[e] != stval[cls * 32 + k]) vok = false;
     }
   }
   const int c0 = __shfl_sync(0xffffffffu, cls, 0);
   const bool all = __all_sync(0xffffffffu, ok && cls == c0);
+  const bool allv = __all_sync(0xffffffffu, ok && vok && cls == c0);
   if (lane == 0) {
-    skind[s] = all ? (int8_t)(c0 + 1) : (int8_t)0;
+    skind[s] = allv ? (int8_t)(c0 + 5) : (all ? (int8_t)(c0 + 1) : (int8_t)0);
     if (all) atomicAdd(nimp, (unsigned long long)SELL_C * len[c0]);
+    if (allv) atomicAdd(nimp + 1, (unsigned long long)SELL_C * len[c0]);
   }
 }
 
@@ -636,7 +653,7 @@ etq_status sell_diag_inv(const Sell& A, double* dinv, cudaStream_t st) {
 
 // Per-class interior stencil offsets in vel_row's enumeration order (dj outer, di inner), then
 // mark the slices whose stored columns follow them (implicit column indices in the kernels).
-etq_status mark_implicit(const Geo& g, bool oseen, Sell& S, cudaStream_t st) {
+etq_status mark_implicit(const Geo& g, bool oseen, double nu, int wind, Sell& S, cudaStream_t st, bool values) {
   if (!S.perm) return ETQ_OK;
   std::vector<int> off(4 * 32, 0), len(5, 0);
   for (int c = 0; c < 4; ++c) {
@@ -658,16 +675,25 @@ etq_status mark_implicit(const Geo& g, bool oseen, Sell& S, cudaStream_t st) {
   ETQ_TRY(dalloc(&S.stoff, 4 * 32));
   ETQ_TRY(dalloc(&dlen, 5));
   ETQ_TRY(dalloc(&S.skind, S.nslices));
-  ETQ_TRY(dalloc(&dn, 1));
+  ETQ_TRY(dalloc(&dn, 2));
   ETQ_CHECK(cudaMemcpyAsync(S.stoff, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice, st));
   ETQ_CHECK(cudaMemcpyAsync(dlen, len.data(), sizeof(int) * len.size(), cudaMemcpyHostToDevice, st));
-  ETQ_CHECK(cudaMemsetAsync(dn, 0, sizeof(unsigned long long), st));
-  k_mark_implicit<<<(unsigned)((S.nslices * SELL_C + 255) / 256), 256, 0, st>>>(S, S.stoff, dlen, S.skind, dn);
+  ETQ_CHECK(cudaMemsetAsync(dn, 0, 2 * sizeof(unsigned long long), st));
+  // value dictionary only for the translation-invariant Stokes operator (n >= 4)
+  if (values && !oseen && g.n >= 4) {
+    ETQ_TRY(dalloc(&S.stval, 4 * 32));
+    ETQ_CHECK(cudaMemsetAsync(S.stval, 0, sizeof(double) * 4 * 32, st));
+    VelParams P{g, 0, 1.0};
+    k_ref_values<<<1, 32, 0, st>>>(P, S.stval); etq_count_launch();
+  }
+  (void)nu; (void)wind;
+  k_mark_implicit<<<(unsigned)((S.nslices * SELL_C + 255) / 256), 256, 0, st>>>(S, S.stoff, dlen, S.stval, S.skind, dn);
   etq_count_launch();
-  unsigned long long h = 0;
-  ETQ_CHECK(cudaMemcpyAsync(&h, dn, sizeof(h), cudaMemcpyDeviceToHost, st));
+  unsigned long long h[2] = {0, 0};
+  ETQ_CHECK(cudaMemcpyAsync(h, dn, sizeof(h), cudaMemcpyDeviceToHost, st));
   ETQ_CHECK(cudaStreamSynchronize(st));
   cudaFree(dlen); cudaFree(dn);
-  S.nnz_implicit = (int64_t)h;
+  S.nnz_implicit = (int64_t)h[0];
+  S.nnz_implicit_vals = (int64_t)h[1];
   return ETQ_OK;
 }

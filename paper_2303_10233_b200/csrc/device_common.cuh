@@ -116,6 +116,23 @@ __device__ __forceinline__ void sell_row2(const Sell& A, int64_t s, int lane, in
   const int len = A.slen[s];
   const double* __restrict__ vp = A.val + base;
   const int kind = A.skind ? (int)A.skind[s] : 0;
+  if (kind >= 5) {   // implicit columns and values (warp-uniform branch): nothing streamed
+    const int* __restrict__ off = A.stoff + (kind - 5) * 32;
+    const double* __restrict__ sv = A.stval + (kind - 5) * 32;
+    int k = 0;
+    for (; k + SELL_U <= len; k += SELL_U) {
+      int c[SELL_U]; double v[SELL_U];
+#pragma unroll
+      for (int u = 0; u < SELL_U; ++u) { c[u] = row + __ldg(off + k + u); v[u] = __ldg(sv + k + u); }
+#pragma unroll
+      for (int u = 0; u < SELL_U; ++u) { a0 = fma(v[u], __ldg(x0 + c[u]), a0); a1 = fma(v[u], __ldg(x1 + c[u]), a1); }
+    }
+    for (; k < len; ++k) {
+      const int c = row + __ldg(off + k); const double v = __ldg(sv + k);
+      a0 = fma(v, __ldg(x0 + c), a0); a1 = fma(v, __ldg(x1 + c), a1);
+    }
+    return;
+  }
   if (kind) {   // implicit columns: col = row + offset (warp-uniform branch)
     const int* __restrict__ off = A.stoff + (kind - 1) * 32;
     int k = 0;

@@ -55,9 +55,13 @@ struct Sell {
   float* fval = nullptr;   // optional fp32 copy of val (c5 sweep)
   // implicit column indices (velocity operators): slice s with skind[s] = c + 1 holds rows of node
   // class c with the full interior stencil, so col = row + stoff[c * 32 + k] and col[] is not read
+  //   skind[s] = c + 5: additionally every value equals stval[c * 32 + k] bitwise (translation-
+  //   invariant interior rows), so val[] is not read either
   int8_t* skind = nullptr; // [nslices] or nullptr
   int* stoff = nullptr;    // [4 * 32] stencil offsets per class
-  int64_t nnz_implicit = 0;
+  double* stval = nullptr; // [4 * 32] stencil values per class (Stokes), or nullptr
+  int64_t nnz_implicit = 0;        // entries without stored indices
+  int64_t nnz_implicit_vals = 0;   // entries without stored values
 };
 
 // ---------------------------------------------------------------- grid geometry
@@ -144,6 +148,7 @@ struct PcMass {               // Chebyshev-SGS on M_Q (P2 / M1 pressure block)
 struct Problem {
   Geo g;
   int bc = 0;
+  int storage = 0;                            // etq_grid.storage
   int wind = 0;
   double nu = 1.0;
   bool oseen = false;
@@ -219,7 +224,7 @@ etq_status assemble_ap(const Geo& g, Sell* out, cudaStream_t st);
 etq_status assemble_f1(const Geo& g, double nu, int wind, Sell* out, cudaStream_t st);
 etq_status sell_diag_inv(const Sell& A, double* dinv, cudaStream_t st);
 etq_status build_rhs_dev(const Problem& P, const double* f_nodal, double* b);
-etq_status mark_implicit(const Geo& g, bool oseen, Sell& S, cudaStream_t st);
+etq_status mark_implicit(const Geo& g, bool oseen, double nu, int wind, Sell& S, cudaStream_t st, bool values);
 
 // ops.cu
 void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y, const double* inv_scale,

@@ -999,7 +999,7 @@ etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, do
       int* perm; int64_t nsl;
       ETQ_TRY(build_node_perm(L.g, &perm, &nsl, P.stream));
       ETQ_TRY(assemble_velocity_op(L.g, P.oseen, P.nu, P.wind, perm, nsl, &L.A, P.stream));
-      ETQ_TRY(mark_implicit(L.g, P.oseen, L.A, P.stream));
+      if (P.storage < 2) ETQ_TRY(mark_implicit(L.g, P.oseen, P.nu, P.wind, L.A, P.stream, P.storage == 0));
       L.A.own_perm = true;
     }
     ETQ_TRY(dalloc(&L.dinv, L.g.nq));
@@ -1397,7 +1397,7 @@ void cheb_step_level0(const Problem& P, const double* d_in, double* d_out, cudaS
 // row permutation (4 B per slot), every vector element the kernel must read or write once.
 double cheb_step_bytes(const Level& L) {
   const double nq = L.nrows;
-  return 12.0 * L.A.nnz - 4.0 * L.A.nnz_implicit + 4.0 * L.A.nslices * SELL_C + 8.0 * nq /*dinv*/ + 8.0 * 2 * nq * 6 /*d,r,x in; x,r,d out*/;
+  return 12.0 * L.A.nnz - 4.0 * L.A.nnz_implicit - 8.0 * L.A.nnz_implicit_vals + 4.0 * L.A.nslices * SELL_C + 8.0 * nq /*dinv*/ + 8.0 * 2 * nq * 6 /*d,r,x in; x,r,d out*/;
 }
 
 double vcycle_bytes(const Hierarchy& H) {
@@ -1406,7 +1406,7 @@ double vcycle_bytes(const Hierarchy& H) {
   const int deg = H.degree;
   for (int l = 0; l < L - 1; ++l) {
     const Level& lv = H.lv[l];
-    const double nq = lv.g.nq, mat = 12.0 * lv.A.nnz - 4.0 * lv.A.nnz_implicit + 4.0 * lv.A.nslices * SELL_C + 8.0 * nq;
+    const double nq = lv.g.nq, mat = 12.0 * lv.A.nnz - 4.0 * lv.A.nnz_implicit - 8.0 * lv.A.nnz_implicit_vals + 4.0 * lv.A.nslices * SELL_C + 8.0 * nq;
     const double v = 8.0 * 2 * nq;   // one two-component vector
     if (l == 0) b += 8.0 * nq + 2 * v;                       // init: dinv, b -> d
     for (int k = 0; k < deg; ++k)                            // pre-smoothing steps

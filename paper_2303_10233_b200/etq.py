@@ -26,7 +26,7 @@ class EtqError(RuntimeError):
 
 
 class Grid(C.Structure):
-    _fields_ = [("n", C.c_int32), ("bc", C.c_int32)]
+    _fields_ = [("n", C.c_int32), ("bc", C.c_int32), ("storage", C.c_int32)]
 
 
 class Wind(C.Structure):
@@ -163,9 +163,9 @@ def make_params(**kw) -> PcParams:
 class Problem:
     """Owns an etq_problem (device matrices and workspaces)."""
 
-    def __init__(self, n: int, bc: int = 0, viscosity: float = 1.0, wind: int = 0):
+    def __init__(self, n: int, bc: int = 0, viscosity: float = 1.0, wind: int = 0, storage: int = 0):
         h = C.c_void_p()
-        g = Grid(n, bc)
+        g = Grid(n, bc, storage)
         w = Wind(wind)
         _check(lib().etq_assemble(C.byref(g), viscosity, C.byref(w), _stream(), C.byref(h)), "etq_assemble")
         self.h = h

@@ -87,12 +87,12 @@ def c4_case(n=512):
     return res
 
 
-def c5_case(nmax):
+def c5_case(nmax, storage=0):
     pk = peak()
     rows = []
     n = 64
     while n <= nmax:
-        P = etq.Problem(n, bc=0)
+        P = etq.Problem(n, bc=0, storage=storage)
         P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.005))
         row = {"n": n, "N": P.N}
         for which, name in ((0, "spmv"), (1, "cheb_step"), (2, "vcycle"), (5, "spmv_f32"), (6, "vcycle_f32")):
@@ -104,6 +104,7 @@ def c5_case(nmax):
         P.close()
         n *= 2
     return {"peak_GBps": pk, "dtype": "f64 (spmv, cheb_step, vcycle) and f32 values+vectors (*_f32)", "reps": 100,
+            "storage": {0: "compressed (implicit indices + value dictionary)", 2: "explicit SELL"}[storage],
             "rows": rows}
 
 
@@ -124,6 +125,7 @@ def main():
         res["c4"] = c4_case(512)
     if "c5" in which:
         res["c5"] = c5_case(args.c5_max)
+        res["c5_explicit_sell"] = c5_case(args.c5_max, storage=2)
     print(json.dumps(res, indent=1))
 
 

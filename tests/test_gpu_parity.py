@@ -344,3 +344,20 @@ def test_fp32_sweep_variants(n):
     z = torch.zeros(P.n_u, dtype=torch.float32, device=DEV)
     P.apply_vcycle_f32(torch.as_tensor(r, dtype=torch.float32, device=DEV), z)
     assert rel_err(host(z).astype(np.float64), h.apply_velocity(r)) < 1e-5
+
+
+@pytest.mark.parametrize("storage", [0, 1, 2])
+def test_storage_modes_bitwise_identical(storage):
+    """The compressed storage modes change what is streamed, not what is computed."""
+    n = 32
+    ref = etq.Problem(n, storage=2)
+    P = etq.Problem(n, storage=storage)
+    for Q in (ref, P):
+        _p2(Q, 0.005)
+    x = dev(synth.random_vector(P.N, seed=51))
+    y0 = torch.zeros(P.N, dtype=torch.float64, device=DEV); y1 = torch.zeros_like(y0)
+    ref.apply_saddle(x, y0); P.apply_saddle(x, y1)
+    assert torch.equal(y0, y1)
+    z0 = torch.zeros(P.N, dtype=torch.float64, device=DEV); z1 = torch.zeros_like(z0)
+    ref.apply_precond(etq.PC_P2_GMG, x, z0); P.apply_precond(etq.PC_P2_GMG, x, z1)
+    assert torch.equal(z0, z1)
