@@ -697,3 +697,42 @@ etq_status mark_implicit(const Geo& g, bool oseen, double nu, int wind, Sell& S,
   S.nnz_implicit_vals = (int64_t)h[1];
   return ETQ_OK;
 }
+
+// Interior stencil of a Stokes level: rectangle [4, m-5]^2, per-class weights
+// from the verified value dictionary, and a SELL over the remaining (frame) rows.
+etq_status build_stencil_level(const Geo& g, const Sell& A, StencilOp* so, Sell* frame, cudaStream_t st) {
+  if (!A.stval || !A.stoff || g.n < 16) return ETQ_EINVAL;
+  std::vector<double> sv(4 * 32);
+  ETQ_CHECK(cudaMemcpy(sv.data(), A.stval, sizeof(double) * sv.size(), cudaMemcpyDeviceToHost));
+  StencilOp o;
+  o.m = g.m; o.lo = 4; o.hi = g.m - 5;
+  o.nseg_x = (o.hi - o.lo + 1 + 31) / 32;
+  o.nseg = (int64_t)o.nseg_x * (o.hi - o.lo + 1);
+  for (int c = 0; c < 4; ++c) {
+    for (int t = 0; t < 25; ++t) o.w[c][t] = 0.0;
+    const int px = c & 1, py = c >> 1, rx = px ? 1 : 2, ry = py ? 1 : 2;
+    int k = 0;
+    for (int dj = -ry; dj <= ry; ++dj)
+      for (int di = -rx; di <= rx; ++di) {   // Stokes enumeration of vel_row (cancelled taps dropped)
+        if ((di == 2 || di == -2) && dj == 0 && py) continue;
+        if ((dj == 2 || dj == -2) && di == 0 && px) continue;
+        o.w[c][(dj + 2) * 5 + (di + 2)] = sv[c * 32 + k++];
+      }
+  }
+  // frame rows, class-major
+  std::vector<int> rows;
+  for (int c = 0; c < 4; ++c)
+    for (int j = (c >> 1); j < g.m; j += 2)
+      for (int i = (c & 1); i < g.m; i += 2)
+        if (i < o.lo || i > o.hi || j < o.lo || j > o.hi) rows.push_back(i + g.m * j);
+  const int64_t ns = ((int64_t)rows.size() + SELL_C - 1) / SELL_C;
+  rows.resize(ns * SELL_C, -1);
+  int* perm;
+  ETQ_TRY(dalloc(&perm, rows.size()));
+  ETQ_CHECK(cudaMemcpy(perm, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
+  VelFn fn{VelParams{g, 0, 1.0}};
+  ETQ_TRY(build_sell(fn, perm, g.nq, ns, frame, st));
+  frame->own_perm = true;
+  *so = o;
+  return ETQ_OK;
+}

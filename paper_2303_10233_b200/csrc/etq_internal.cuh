@@ -88,6 +88,16 @@ struct RedSite {
   int nslot = 0;
 };
 
+// ---------------------------------------------------------------- interior stencil
+// Interior rectangle [lo, hi]^2 of a translation-invariant (Stokes) level, processed in natural
+// node order with per-class tap weights (dj outer, di inner; 0 where a class has no tap), i.e.
+// the same summation order as the SELL rows, so the results are bitwise identical.
+struct StencilOp {
+  int m = 0, lo = 0, hi = -1, nseg_x = 0;
+  int64_t nseg = 0;
+  double w[4][25];
+};
+
 // ---------------------------------------------------------------- MG level
 struct Level {
   Geo g;
@@ -95,6 +105,9 @@ struct Level {
   double* dinv = nullptr;     // [nrows]
   int nrows = 0;              // nq (Q2 velocity) or nk (Q1 pressure)
   double bim = 0.0;           // imaginary semi-axis of the smoother ellipse (0: real interval)
+  bool st_on = false;         // interior stencil + frame SELL (Afr) instead of A for the smoother
+  StencilOp so;
+  Sell Afr;                   // rows outside the interior rectangle (own permutation)
   // two-component work vectors, each [2*nq]
   double *b = nullptr, *x = nullptr, *r = nullptr, *d0 = nullptr, *d1 = nullptr;
   double* coarse_inv = nullptr;   // dense inverse (coarsest level only), nq x nq row-major
@@ -225,6 +238,7 @@ etq_status assemble_f1(const Geo& g, double nu, int wind, Sell* out, cudaStream_
 etq_status sell_diag_inv(const Sell& A, double* dinv, cudaStream_t st);
 etq_status build_rhs_dev(const Problem& P, const double* f_nodal, double* b);
 etq_status mark_implicit(const Geo& g, bool oseen, double nu, int wind, Sell& S, cudaStream_t st, bool values);
+etq_status build_stencil_level(const Geo& g, const Sell& A, StencilOp* so, Sell* frame, cudaStream_t st);
 
 // ops.cu
 void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y, const double* inv_scale,

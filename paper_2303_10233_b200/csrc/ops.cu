@@ -136,6 +136,80 @@ __global__ void __launch_bounds__(BS, SPMV_MINB) k_cheb_step(ChebArgs a) {
   }
 }
 
+// ---- interior stencil path (Stokes levels): natural node order, contiguous gathers
+// acc_c = sum_{dj, di} w[class][dj][di] x_c[(i+di) + m (j+dj)] in the SELL row order
+__device__ __forceinline__ void stencil_row2(const StencilOp& so, int i, int j, const double* __restrict__ x0,
+                                             const double* __restrict__ x1, double& a0, double& a1) {
+  const int ce = (j & 1) * 2, cl = ce + (i & 1);
+  const int node = i + so.m * j;
+  a0 = 0.0; a1 = 0.0;
+#pragma unroll
+  for (int dj = -2; dj <= 2; ++dj) {
+    if ((j & 1) && (dj == 2 || dj == -2)) continue;   // classes 2, 3 have no |dj| = 2 taps (warp-uniform)
+    const int rb = node + dj * so.m;
+#pragma unroll
+    for (int di = -2; di <= 2; ++di) {
+      const double w = so.w[cl][(dj + 2) * 5 + (di + 2)];
+      const double v0 = __ldg(x0 + rb + di), v1 = __ldg(x1 + rb + di);
+      a0 = fma(w, v0, a0);
+      a1 = fma(w, v1, a1);
+    }
+  }
+}
+
+struct ChebStArgs {
+  StencilOp so; Sell F; const double* dinv; int nq;
+  const double* d_in; const double* r_in; const double* x_in;
+  double* x_out; double* r_out; double* d_out;
+  double c1, c2; int post; double theta;   // post: r = b - A x, d = D^{-1} r / theta (x_in = x, r_in = b)
+  const double* done;
+};
+__device__ __forceinline__ void cheb_update2(const ChebStArgs& a, int row, double q0, double q1) {
+  const double di = a.dinv[row];
+  if (a.post) {
+    const double r0 = a.r_in[row] - q0, r1 = a.r_in[a.nq + row] - q1;
+    a.r_out[row] = r0; a.r_out[a.nq + row] = r1;
+    a.d_out[row] = di * r0 / a.theta; a.d_out[a.nq + row] = di * r1 / a.theta;
+    return;
+  }
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int64_t idx = (int64_t)c * a.nq + row;
+    const double dd = a.d_in[idx];
+    const double ro = a.r_in[idx] - (c == 0 ? q0 : q1);
+    a.x_out[idx] = (a.x_in ? a.x_in[idx] : 0.0) + dd;
+    if (a.r_out) a.r_out[idx] = ro;
+    if (a.d_out) a.d_out[idx] = a.c1 * dd + a.c2 * (di * ro);
+  }
+}
+// one launch: interior segments (32 consecutive nodes of one grid row per warp) + frame SELL slices
+#ifndef STENCIL_MINB
+#define STENCIL_MINB 6
+#endif
+__global__ void __launch_bounds__(BS, STENCIL_MINB) k_cheb_step_st(ChebStArgs a) {
+  if (is_done(a.done)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const double* g = a.post ? a.x_in : a.d_in;   // gathered vector
+  for (int64_t s = gw; s < a.so.nseg + a.F.nslices; s += nw) {
+    if (s < a.so.nseg) {
+      const int j = a.so.lo + (int)(s / a.so.nseg_x);
+      const int i = a.so.lo + (int)(s % a.so.nseg_x) * 32 + lane;
+      if (i > a.so.hi) continue;
+      double q0, q1;
+      stencil_row2(a.so, i, j, g, g + a.nq, q0, q1);
+      cheb_update2(a, i + a.so.m * j, q0, q1);
+    } else {
+      const int64_t sf = s - a.so.nseg;
+      const int row = a.F.perm[sf * SELL_C + lane];
+      double q0 = 0.0, q1 = 0.0;
+      sell_row2(a.F, sf, lane, row, g, g + a.nq, q0, q1);
+      if (row >= 0) cheb_update2(a, row, q0, q1);
+    }
+  }
+}
+
 // r = b - A x ; d = D^{-1} r / theta  (start of post-smoothing), NC components
 template <int NC>
 __global__ void __launch_bounds__(BS, SPMV_MINB) k_post_residual(Sell A, const double* dinv, int nq, const double* b,
@@ -1014,6 +1088,14 @@ etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, do
   if (P.oseen) ETQ_TRY(dense_inverse_pivot(C.coarse_inv, C.g.nq, P.stream));
   else ETQ_TRY(dense_inverse_spd(C.coarse_inv, C.g.nq, P.stream));
   H.lo = lo; H.hi = hi; H.degree = degree; H.built = true;
+  // interior stencil path for translation-invariant levels with n > TAIL_N
+  for (size_t l = 0; l < H.lv.size(); ++l) {
+    Level& lv = H.lv[l];
+    if (!P.oseen && P.storage == 0 && lv.g.n > TAIL_N && lv.A.stval && l + 1 < H.lv.size()) {
+      ETQ_TRY(build_stencil_level(lv.g, lv.A, &lv.so, &lv.Afr, P.stream));
+      lv.st_on = true;
+    }
+  }
   // coarse-level tail: first level l >= 1 with n <= TAIL_N (degree <= 4)
   H.tail_start = -1;
   if (degree <= 4)
@@ -1080,6 +1162,7 @@ void free_hierarchy(Hierarchy& H) {
     cudaFree(L.f_dinv); cudaFree(L.f_b); cudaFree(L.f_x); cudaFree(L.f_r); cudaFree(L.f_d0); cudaFree(L.f_d1);
     cudaFree(L.f_coarse);
     if (H.kind == 1 || l > 0) sell_free(L.A);
+    sell_free(L.Afr);
     cudaFree(L.dinv); cudaFree(L.b); cudaFree(L.x); cudaFree(L.r); cudaFree(L.d0); cudaFree(L.d1);
     cudaFree(L.coarse_inv);
   }
@@ -1110,6 +1193,15 @@ static void cheb_coeffs(double lo, double hi, double bim, int degree, std::vecto
     c1[k] = (rn * rho).real(); c2[k] = (2.0 * rn / delta).real();
     rho = rn;
   }
+}
+
+static void launch_cheb_st(const Level& lv, const ChebArgs& c, bool post, double theta, cudaStream_t st) {
+  ChebStArgs a;
+  a.so = lv.so; a.F = lv.Afr; a.dinv = c.dinv; a.nq = c.nq;
+  a.d_in = c.d_in; a.r_in = c.r_in; a.x_in = c.x_in; a.x_out = c.x_out; a.r_out = c.r_out; a.d_out = c.d_out;
+  a.c1 = c.c1; a.c2 = c.c2; a.post = post ? 1 : 0; a.theta = theta; a.done = c.done;
+  const int64_t warps = lv.so.nseg + lv.Afr.nslices;
+  k_cheb_step_st<<<grid_for(warps * 32, BS, 4096), BS, 0, st>>>(a);
 }
 
 // One V-cycle (readings R9/R9'/R13) on H.ncomp components: z = V(r); optional partial
@@ -1153,7 +1245,8 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       a.d_in = din; a.r_in = (k == 0) ? b : lv.r; a.x_in = (k == 0) ? nullptr : lv.x;
       a.x_out = lv.x; a.r_out = lv.r; a.d_out = (k == H.degree - 1) ? nullptr : dout;
       a.c1 = c1[k]; a.c2 = c2[k]; a.done = done;
-      if (nc == 2) k_cheb_step<2><<<gs, BS, 0, st>>>(a);
+      if (lv.st_on) launch_cheb_st(lv, a, false, theta, st);
+      else if (nc == 2) k_cheb_step<2><<<gs, BS, 0, st>>>(a);
       else k_cheb_step<1><<<gs, BS, 0, st>>>(a);
       etq_count_launch();
       std::swap(din, dout);
@@ -1190,8 +1283,16 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     }
     etq_count_launch();
     const int gs = grid_for(lv.A.nslices * 32, BS, 4096);
-    if (nc == 2) k_post_residual<2><<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, theta, done);
-    else k_post_residual<1><<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, theta, done);
+    if (lv.st_on) {
+      ChebArgs a{};
+      a.A = lv.A; a.dinv = lv.dinv; a.nq = nq; a.x_in = lv.x; a.r_in = bvec[l]; a.r_out = lv.r; a.d_out = lv.d0;
+      a.done = done;
+      launch_cheb_st(lv, a, true, theta, st);
+    } else if (nc == 2) {
+      k_post_residual<2><<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, theta, done);
+    } else {
+      k_post_residual<1><<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, theta, done);
+    }
     etq_count_launch();
     double* din = lv.d0; double* dout = lv.d1;
     for (int k = 0; k < H.degree - 1; ++k) {
@@ -1200,7 +1301,8 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       a.d_in = din; a.r_in = lv.r; a.x_in = lv.x;
       a.x_out = lv.x; a.r_out = (k == H.degree - 2) ? nullptr : lv.r; a.d_out = dout;
       a.c1 = c1[k]; a.c2 = c2[k]; a.done = done;
-      if (nc == 2) k_cheb_step<2><<<gs, BS, 0, st>>>(a);
+      if (lv.st_on) launch_cheb_st(lv, a, false, theta, st);
+      else if (nc == 2) k_cheb_step<2><<<gs, BS, 0, st>>>(a);
       else k_cheb_step<1><<<gs, BS, 0, st>>>(a);
       etq_count_launch();
       std::swap(din, dout);
@@ -1390,7 +1492,9 @@ void cheb_step_level0(const Problem& P, const double* d_in, double* d_out, cudaS
   a.A = lv.A; a.dinv = lv.dinv; a.nq = lv.g.nq;
   a.d_in = d_in; a.r_in = lv.r; a.x_in = lv.x; a.x_out = lv.x; a.r_out = lv.r; a.d_out = d_out;
   a.c1 = 0.5; a.c2 = 0.1; a.done = nullptr;
-  k_cheb_step<2><<<grid_for(lv.A.nslices * 32, BS, 4096), BS, 0, st>>>(a); etq_count_launch();
+  if (lv.st_on) launch_cheb_st(lv, a, false, 0.0, st);
+  else k_cheb_step<2><<<grid_for(lv.A.nslices * 32, BS, 4096), BS, 0, st>>>(a);
+  etq_count_launch();
 }
 
 // Algorithmic bytes: every stored value/index once (12 B per true nnz), the
