@@ -145,13 +145,10 @@ etq_status etq_assemble(const etq_grid* grid, double viscosity, const etq_wind* 
   {
     // the bandwidth-bound velocity V-cycle (main stream) has the higher priority; the latency-bound
     // pressure chain (aux stream) fills the SMs around it (measured: P2 apply 2.99 -> 2.69 ms, n=1024)
-#ifndef ETQ_AUX_HIGH
-#define ETQ_AUX_HIGH 0
-#endif
     int lo_prio = 0, hi_prio = 0;
     A_CHECK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-    A_CHECK(cudaStreamCreateWithPriority(&P.stream, cudaStreamNonBlocking, ETQ_AUX_HIGH ? lo_prio : hi_prio));
-    A_CHECK(cudaStreamCreateWithPriority(&P.aux, cudaStreamNonBlocking, ETQ_AUX_HIGH ? hi_prio : lo_prio));
+    A_CHECK(cudaStreamCreateWithPriority(&P.stream, cudaStreamNonBlocking, hi_prio));
+    A_CHECK(cudaStreamCreateWithPriority(&P.aux, cudaStreamNonBlocking, lo_prio));
   }
   cudaEvent_t* evs[4] = {&P.ev_in, &P.ev_out, &P.ev_fork, &P.ev_join};
   for (auto e : evs) A_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));

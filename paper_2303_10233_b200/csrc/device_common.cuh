@@ -74,24 +74,16 @@ __device__ void reduce_finish(const double (&v)[NV], RedSite site, int slot, dou
 }
 
 // ---------------------------------------------------------------- SELL row products
-// One thread per row; entry k of the row at base + 32 k.  The matrix is streamed once per apply,
-// so its values and indices are loaded with the evict-first hint (__ldcs) to keep the gathered
-// vectors in L1/L2; SELL_U entries are loaded before their gathers to keep SELL_U x 12 B of
-// matrix data plus SELL_U gathers in flight per thread.
+// One thread per row; entry k of the row at base + 32 k.  SELL_U entries are loaded before their
+// gathers so SELL_U x 12 B of matrix data plus SELL_U gathers are in flight per thread (U = 4
+// measured best among 2/4/6/8 and predicated variants, n = 1024).  Slices may carry implicit
+// column indices (col = row + per-class offset) and implicit values (per-class dictionary).
 #ifndef SELL_U
 #define SELL_U 4
 #endif
-#ifndef SELL_STREAM
-#define SELL_STREAM 0
-#endif
+// matrix loads: read-only path (measured faster than the evict-first hint, variants A/E)
 template <class T>
-__device__ __forceinline__ T ld_mat(const T* p) {
-#if SELL_STREAM
-  return __ldcs(p);
-#else
-  return __ldg(p);
-#endif
-}
+__device__ __forceinline__ T ld_mat(const T* p) { return __ldg(p); }
 __device__ __forceinline__ double sell_row1(const Sell& A, int64_t s, int lane, const double* __restrict__ x) {
   const int64_t base = A.sptr[s] + lane;
   const int len = A.slen[s];

@@ -654,7 +654,10 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, const SgsSme
   if (a.kout) { double v[1] = {kd}; reduce_finish<1>(v, a.site, a.slot, a.kout); }
 }
 
-__global__ void __launch_bounds__(SGS_TX * SGS_TY, 2) k_sgs_tile(SgsTileArgs a) {
+#ifndef SGS_MINB
+#define SGS_MINB 2
+#endif
+__global__ void __launch_bounds__(SGS_TX * SGS_TY, SGS_MINB) k_sgs_tile(SgsTileArgs a) {
   if (is_done(a.done)) return;
   extern __shared__ double sm[];
   const SgsSmem S{sm, sm + 4 * SGS_P * SGS_P};
