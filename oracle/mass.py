@@ -176,3 +176,48 @@ def cheb_lo_rule(lam_est: float, m: int) -> float:
     ~1/m^2, and measured MINRES counts are lower with this floor than with a = lam_min
     (n = 32: 42 vs 74 iterations at m = 20)."""
     return max(float(lam_est), 2.0 / (m * m))
+
+
+class SparseAugmentedMassSolver:
+    """Exact solve of [[M_Q, k], [k^T, 0]] [z; lam] = [r; 0] by sparse LU of the bordered matrix
+    (same system as AugmentedMassSolver, usable at larger n)."""
+
+    def __init__(self, MQ, k):
+        import scipy.sparse.linalg as spla
+        n = MQ.shape[0]
+        kk = sp.csr_matrix(k.reshape(-1, 1))
+        Aug = sp.bmat([[MQ, kk], [kk.T, None]]).tocsc()
+        self.lu = spla.splu(Aug)
+        self.n = n
+
+    def solve(self, r):
+        return self.lu.solve(np.concatenate([r, [0.0]]))[:self.n]
+
+
+def schur_mass(g: fem.Grid):
+    """S_k = Qk - R^T Q0^{-1} R on the Q1 vertices (symmetric PSD, null space = constants)."""
+    MQ, Qk, R, Q0 = fem.pressure_mass(g)
+    S = (Qk - R.T @ sp.diags(1.0 / Q0.diagonal()) @ R).tocsr()
+    S.sort_indices()
+    return S
+
+
+def augmented_via_schur(g: fem.Grid, r, S_pinv_solve):
+    """The augmented M_Q solve written through the Schur complement S_k (the reduction the GPU
+    uses; derived in DESIGN.md §3 'NEXT-2'):  with a = 1 + R^T 1 / h^2,
+        lam = k^T r / 1^T a,  g = r_k - R^T r_0 / h^2 - lam a,  zhat = S_k^+ g,
+        beta = ((1^T r_0 + lam n_0) / h^2 - a^T zhat) / 1^T a,  z_k = zhat + beta 1,
+        z_0 = (r_0 - R z_k + lam 1) / h^2.
+    S_pinv_solve(g) must return a solution of S_k x = g (any constant shift)."""
+    MQ, Qk, R, Q0 = fem.pressure_mass(g)
+    h2 = g.h * g.h
+    rk, r0 = r[:g.n_k], r[g.n_k:]
+    one_k = np.ones(g.n_k)
+    a = one_k + (R.T @ np.ones(g.n_0)) / h2
+    lam = (rk.sum() - r0.sum()) / a.sum()
+    gg = rk - (R.T @ r0) / h2 - lam * a
+    zhat = S_pinv_solve(gg)
+    beta = ((r0.sum() + lam * g.n_0) / h2 - a @ zhat) / a.sum()
+    zk = zhat + beta * one_k
+    z0 = (r0 - R @ zk + lam) / h2
+    return np.concatenate([zk, z0])

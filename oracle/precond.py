@@ -49,3 +49,16 @@ class StokesP2:
 
     def __call__(self, r):
         return np.concatenate([self.velocity(r[:self.n_u]), self.pressure(r[self.n_u:])])
+
+
+class StokesP3:
+    """NEXT-2 hybrid: z_u = one Q2-GMG V-cycle per component (as P2),
+    z_p = exact augmented M_Q solve (as P1)."""
+
+    def __init__(self, s: fem.SaddleSystem, hierarchy=None):
+        self.n_u = s.g.n_u
+        self.h = hierarchy if hierarchy is not None else mg.Hierarchy(s.g.n)
+        self.aug = mass.SparseAugmentedMassSolver(s.MQ, fem.null_vector_k(s.g))
+
+    def __call__(self, r):
+        return np.concatenate([self.h.apply_velocity(r[:self.n_u]), self.aug.solve(r[self.n_u:])])

@@ -188,3 +188,24 @@ def test_ellipse_chebyshev_closed_form():
     x0, _ = mg.chebyshev_smooth_ellipse(A, np.ones(12), b, None, lo, hi, 0.0, 3)
     x1, _ = mg.chebyshev_smooth(A, np.ones(12), b, None, lo, hi, 3)
     np.testing.assert_array_equal(x0, x1)
+
+
+@pytest.mark.parametrize("n", [2, 5, 8])
+def test_schur_reduction_equals_augmented_solve(n):
+    """The Schur-complement reduction of the augmented M_Q system (used by the GPU's exact M_Q
+    solve, NEXT-2) reproduces the bordered dense LU solve; S_k is PSD with null space
+    the constants and lambda_max(diag(S_k)^{-1} S_k) = 12/7."""
+    g = fem.Grid(n)
+    s = fem.assemble_system(n)
+    k = fem.null_vector_k(g)
+    S = mass.schur_mass(g).toarray()
+    ev = np.linalg.eigvalsh(S)
+    assert abs(ev[0]) < 1e-14 * ev[-1] and ev[1] > 1e-9 * ev[-1]
+    assert np.abs(S @ np.ones(g.n_k)).max() < 1e-15
+    lam = np.linalg.eigvals(np.diag(1 / np.diag(S)) @ S).real
+    assert lam.max() == pytest.approx(12 / 7, rel=1e-12)
+    Sp = np.linalg.pinv(S, rcond=1e-12)
+    r = np.random.default_rng(8).standard_normal(g.n_p)
+    z = mass.augmented_via_schur(g, r, lambda v: Sp @ v)
+    np.testing.assert_allclose(z, mass.AugmentedMassSolver(s.MQ, k).solve(r), atol=1e-10 * np.abs(z).max())
+    np.testing.assert_allclose(z, mass.SparseAugmentedMassSolver(s.MQ, k).solve(r), atol=1e-10 * np.abs(z).max())
