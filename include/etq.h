@@ -59,7 +59,11 @@ typedef enum {
     ETQ_PC_P1_EXACT = 0,   /* P1 = diag(A, M_Q): exact A^{-1}, exact augmented M_Q solve; n <= 32 */
     ETQ_PC_P2_GMG = 1,     /* P2 = diag(one Q2-GMG V-cycle, Pi C Pi) with C = m-step Chebyshev-SGS */
     ETQ_PC_OSEEN_M1 = 2,   /* M1 = [[V-cycle(F), B^T], [0, -(1/nu) M_Q~]] block upper triangular */
-    ETQ_PC_OSEEN_PCD1 = 3  /* Step-I PCD: [[V-cycle(F), B1^T], [0, -Ap^{-1} F1 Mp^{-1}]] */
+    ETQ_PC_OSEEN_PCD1 = 3, /* Step-I PCD: [[V-cycle(F), B1^T], [0, -Ap^{-1} F1 Mp^{-1}]] */
+    ETQ_PC_P1_ITER = 4,    /* P1 at any n: A^{-1} by V-cycle-preconditioned CG and the
+                              exact augmented M_Q solve through S_k (reading R21), both to inner_rtol */
+    ETQ_PC_P3 = 5          /* diag(one Q2-GMG V-cycle, exact M_Q solve through S_k): P2's velocity block with
+                              P1's pressure block (NEXT-2; mesh-independent MINRES counts) */
 } etq_pc_kind;
 
 /* Preconditioner parameters (defaults in brackets; readings R7, R9, R13). */
@@ -74,6 +78,9 @@ typedef struct {
     int32_t coarse_n;         /* coarsest V-cycle grid [2 Stokes, 32 Oseen] */
     int32_t mass_cheb_steps;  /* m_p, Chebyshev-Jacobi steps for Mp^{-1} in PCD [10] (reading R13) */
     int32_t use_graphs;       /* capture solver iterations in CUDA graphs [1] */
+    double  inner_rtol;       /* relative residual of the inner CG solves of P1_ITER / P3 [1e-10] */
+    int32_t inner_maxit;      /* iteration cap of each inner CG solve [100] */
+    int32_t inner_coarse_n;   /* coarsest grid of the Q1 S_k hierarchy [16] (reading R21) */
 } etq_pc_params;
 
 /* Solve report; history/lanczos buffers are caller-owned HOST arrays and may be NULL. */
@@ -123,6 +130,16 @@ etq_status etq_apply_precond(const etq_problem* p, etq_pc_kind kind, const doubl
  *                       M_Q z = r_p from y_p (reading R7); y may equal z (in place). */
 etq_status etq_apply_vcycle(const etq_problem* p, etq_pc_kind kind, const double* r_u, double* z_u);
 etq_status etq_apply_mass_pc(const etq_problem* p, const double* r_p, double* z_p);
+
+/* Exact augmented M_Q solve at any n through the Schur complement S_k = Q_k - R^T Q_0^{-1} R
+ * (reading R21): z_p with M_Q z_p + lambda k = r_p and k^T z_p = 0, to the inner CG tolerance of the
+ * P3 / P1_ITER setup (either kind).  r_p, z_p: device, length n_p, must not alias.  Synchronises; if
+ * cg_iterations is non-NULL it receives the CG iterations this call took (host). */
+etq_status etq_apply_mass_exact(const etq_problem* p, const double* r_p, double* z_p, int32_t* cg_iterations);
+
+/* Counters of the inner CG solves since setup: which = 0 exact M_Q solve, 1 velocity CG (P1_ITER).
+ * Host outputs: total CG iterations and number of solves. */
+etq_status etq_inner_stats(const etq_problem* p, int32_t which, double* iterations, double* solves);
 etq_status etq_apply_mass(const etq_problem* p, const double* x_p, double* y_p);
 etq_status etq_sgs_sweep(const etq_problem* p, const double* r_p, const double* y_p, double* z_p);
 
@@ -134,7 +151,7 @@ etq_status etq_estimate_sgs_lo(etq_problem* p, const double* v0, int32_t steps, 
 etq_status etq_get_cheb_sgs_lo(const etq_problem* p, double* a);
 
 /* Preconditioned MINRES, Algorithm 1 with stopping test |eta|/gamma_1 < rtol
- * (P:511-514).  x is the initial guess on input and the solution on output (device).
+ * (P:511-514); kind = P1_EXACT, P2_GMG, P3 or P1_ITER (Stokes).  x is the initial guess on input and the solution on output (device).
  * Returns ETQ_OK, ETQ_NOT_CONVERGED or an error.  report may be NULL. */
 etq_status etq_minres_solve(etq_problem* p, etq_pc_kind kind, const double* b, double* x,
                             double rtol, int32_t maxit, etq_report* report);
@@ -146,7 +163,7 @@ etq_status etq_minres_solve_host(etq_problem* p, etq_pc_kind kind, const double*
 /* Export an assembled operator to caller-owned HOST CSR buffers (tests).  which:
  *   0 = scalar velocity operator with Dirichlet rows (L or F_s) of MG level `level`,
  *   1 = B (n_p x n_u), 2 = B^T (n_u x n_p), 3 = Ap of Q1 level `level` (PCD set up),
- *   4 = F1 (PCD set up).
+ *   4 = F1 (PCD set up), 5 = S_k / 4^level of Q1 level `level` (P3 or P1_ITER set up, reading R21).
  * Call with rowptr == NULL to query *nrows and *nnz. */
 etq_status etq_export_operator(const etq_problem* p, int32_t which, int32_t level,
                                int64_t* nrows, int64_t* nnz,

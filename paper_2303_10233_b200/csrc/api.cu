@@ -66,6 +66,9 @@ etq_pc_params default_params(const Problem& P) {
   d.coarse_n = P.oseen ? 32 : 2;
   d.mass_cheb_steps = 10;
   d.use_graphs = 1;
+  d.inner_rtol = 1e-10;
+  d.inner_maxit = 100;
+  d.inner_coarse_n = 16;
   return d;
 }
 
@@ -81,6 +84,9 @@ etq_pc_params merge_params(const Problem& P, const etq_pc_params* in) {
   if (in->coarse_n > 0) d.coarse_n = in->coarse_n;
   if (in->mass_cheb_steps > 0) d.mass_cheb_steps = in->mass_cheb_steps;
   d.use_graphs = in->use_graphs;
+  if (in->inner_rtol > 0) d.inner_rtol = in->inner_rtol;
+  if (in->inner_maxit > 0) d.inner_maxit = in->inner_maxit;
+  if (in->inner_coarse_n > 0) d.inner_coarse_n = in->inner_coarse_n;
   return d;
 }
 
@@ -209,6 +215,22 @@ etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_para
   StreamScope sc(P);
   const etq_pc_params prm = merge_params(P, params);
   P.params = prm;
+  // cached MINRES graphs bake in hierarchy buffers that a new setup may replace
+  for (int g = 0; g < 2; ++g) {
+    if (P.minres_graph[g]) { cudaGraphExecDestroy(P.minres_graph[g]); P.minres_graph[g] = nullptr; }
+  }
+  P.minres_graph_kind = -1;
+  if (kind == ETQ_PC_P3 || kind == ETQ_PC_P1_ITER) {
+    if (P.oseen) return ETQ_EINVAL;
+    if (!is_pow2(P.g.n) || !is_pow2(prm.coarse_n) || prm.coarse_n > P.g.n || !is_pow2(prm.inner_coarse_n))
+      return ETQ_EINVAL;
+    if (P.mg.built) free_hierarchy(P.mg);
+    ETQ_TRY(build_hierarchy(P, P.mg, prm.coarse_n, prm.smooth_lo, prm.smooth_hi, prm.smooth_degree));
+    ETQ_TRY(exact_mass_setup(P));
+    if (kind == ETQ_PC_P1_ITER) ETQ_TRY(vel_iter_setup(P));
+    ETQ_CHECK(cudaStreamSynchronize(P.stream));
+    return ETQ_OK;
+  }
   if (kind == ETQ_PC_P1_EXACT) {
     if (P.oseen || P.g.nq > 4225) return ETQ_EINVAL;   // dense exact solves: n <= 32
     if (!P.p1.Ainv) {
@@ -293,6 +315,26 @@ etq_status etq_apply_mass_pc(const etq_problem* h, const double* r_p, double* z_
   return mass_pc_apply_ex(P, r_p, z_p, &P.red[0], 2, nullptr, nullptr, nullptr, P.stream);
 }
 
+etq_status etq_apply_mass_exact(const etq_problem* h, const double* r_p, double* z_p, int32_t* cg_iterations) {
+  if (!h || !r_p || !z_p || r_p == z_p) return ETQ_EINVAL;
+  const Problem& P = h->P;
+  if (!P.mx.ready) return ETQ_ENOTSETUP;
+  StreamScope sc(P);
+  double i0, c0, i1, c1;
+  ETQ_TRY(pcg_stats(P, 0, &i0, &c0));
+  ETQ_TRY(exact_mass_apply(P, r_p, z_p, nullptr, 0, nullptr, nullptr, nullptr, P.stream));
+  ETQ_CHECK(cudaStreamSynchronize(P.stream));
+  ETQ_TRY(pcg_stats(P, 0, &i1, &c1));
+  if (cg_iterations) *cg_iterations = (int32_t)(i1 - i0);
+  return ETQ_OK;
+}
+
+etq_status etq_inner_stats(const etq_problem* h, int32_t which, double* iterations, double* solves) {
+  if (!h || !iterations || !solves || which < 0 || which > 1) return ETQ_EINVAL;
+  cudaStreamSynchronize(h->P.stream);
+  return pcg_stats(h->P, which, iterations, solves);
+}
+
 etq_status etq_apply_mass(const etq_problem* h, const double* x_p, double* y_p) {
   if (!h || !x_p || !y_p || x_p == y_p) return ETQ_EINVAL;
   const Problem& P = h->P;
@@ -328,7 +370,8 @@ etq_status etq_get_cheb_sgs_lo(const etq_problem* h, double* a) {
 etq_status etq_minres_solve(etq_problem* h, etq_pc_kind kind, const double* b, double* x, double rtol,
                             int32_t maxit, etq_report* report) {
   if (!h || !b || !x || !(rtol > 0.0) || maxit < 1) return ETQ_EINVAL;
-  if (kind != ETQ_PC_P1_EXACT && kind != ETQ_PC_P2_GMG) return ETQ_EINVAL;
+  if (kind != ETQ_PC_P1_EXACT && kind != ETQ_PC_P2_GMG && kind != ETQ_PC_P3 && kind != ETQ_PC_P1_ITER)
+    return ETQ_EINVAL;
   Problem& P = h->P;
   StreamScope sc(P);
   return minres_run(P, kind, b, x, rtol, maxit, report);
@@ -336,7 +379,9 @@ etq_status etq_minres_solve(etq_problem* h, etq_pc_kind kind, const double* b, d
 
 etq_status etq_minres_solve_host(etq_problem* h, etq_pc_kind kind, const double* b_host, double* x_host,
                                  double rtol, int32_t maxit, etq_report* report) {
-  if (!h || !b_host || !x_host) return ETQ_EINVAL;
+  if (!h || !b_host || !x_host || !(rtol > 0.0) || maxit < 1) return ETQ_EINVAL;
+  if (kind != ETQ_PC_P1_EXACT && kind != ETQ_PC_P2_GMG && kind != ETQ_PC_P3 && kind != ETQ_PC_P1_ITER)
+    return ETQ_EINVAL;
   Problem& P = h->P;
   // persistent device staging buffers (the cached MINRES graphs stay valid across calls)
   if (!P.kv[7]) ETQ_TRY(dalloc(&P.kv[7], P.N));
@@ -427,6 +472,10 @@ etq_status etq_export_operator(const etq_problem* h, int32_t which, int32_t leve
     if (!P.apH.built || level < 0 || level >= (int)P.apH.lv.size()) return ETQ_EINVAL;
     parts.push_back({&P.apH.lv[level].A, {0, 0}});
     R = P.apH.lv[level].A.nrows;
+  } else if (which == 5) {
+    if (!P.mx.sH.built || level < 0 || level >= (int)P.mx.sH.lv.size()) return ETQ_EINVAL;
+    parts.push_back({&P.mx.sH.lv[level].A, {0, 0}});
+    R = P.mx.sH.lv[level].A.nrows;
   } else if (which == 4) {
     if (!P.pcd_ready) return ETQ_EINVAL;
     parts.push_back({&P.F1, {0, 0}});
@@ -573,6 +622,7 @@ void etq_destroy(etq_problem* h) {
   if (P.stream) cudaStreamSynchronize(P.stream);
   for (int g = 0; g < 2; ++g) if (P.minres_graph[g]) cudaGraphExecDestroy(P.minres_graph[g]);
   free_hierarchy(P.mg);
+  exact_free(P);
   oseen_free(P);
   P.Lv.perm = nullptr; P.BxT1.perm = nullptr; P.ByT1.perm = nullptr; P.BxT0.perm = nullptr; P.ByT0.perm = nullptr;
   sell_free(P.Lv); sell_free(P.BxT1); sell_free(P.ByT1); sell_free(P.BxT0); sell_free(P.ByT0); sell_free(P.B);

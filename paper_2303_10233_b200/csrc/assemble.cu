@@ -229,6 +229,35 @@ __device__ int ap_row(const ApParams& P, int row, Emit& emit) {
   return cnt;
 }
 
+// S_k = Q_k - R^T Q_0^{-1} R on the Q1 vertices (the Schur complement of the Q0 block of M_Q,
+// P:287-294 with R = h^2/4, Q0 = h^2): per cell T, (h^2/36) m_x m_y - h^2/16 for each vertex pair
+// of T (m = 2 on the same 1D index, else 1); interior stencil (h^2/144) [-5 -2 -5; -2 28 -2; -5 -2 -5].
+// `scale` multiplies the operator (4^-l on hierarchy level l, reading R21).
+struct SkParams { Geo g; double scale; };
+template <class Emit>
+__device__ int sk_row(const SkParams& P, int row, Emit& emit) {
+  const int n = P.g.n; const double h2 = P.g.h * P.g.h;
+  const int a = row % (n + 1), c = row / (n + 1);
+  double acc[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) acc[k] = 0.0;
+  for (int f = max(0, c - 1); f <= min(n - 1, c); ++f)
+    for (int e = max(0, a - 1); e <= min(n - 1, a); ++e)
+      for (int cc = f; cc <= f + 1; ++cc)
+        for (int aa = e; aa <= e + 1; ++aa) {
+          const double mx = aa == a ? 2.0 : 1.0, my = cc == c ? 2.0 : 1.0;
+          acc[(cc - c + 1) * 3 + (aa - a + 1)] += h2 * (mx * my / 36.0 - 1.0 / 16.0);
+        }
+  int cnt = 0;
+  for (int dc = -1; dc <= 1; ++dc)
+    for (int da = -1; da <= 1; ++da) {
+      const int aa = a + da, cc = c + dc;
+      if (aa < 0 || aa > n || cc < 0 || cc > n) continue;
+      emit(aa + (n + 1) * cc, P.scale * acc[(dc + 1) * 3 + (da + 1)]); ++cnt;
+    }
+  return cnt;
+}
+
 // F1 = nu int grad psi_j . grad psi_i + int (w . grad psi_j) psi_i on Q1, natural
 // boundary (reading R13); for the separable cavity wind the convection part is
 // Aq (x) Tq - Tq (x) Aq with Aq = int (1-x^2) N_b' N_a, Tq = int 2x N_b N_a (3-point Gauss, exact).
@@ -283,6 +312,7 @@ struct VelFn { VelParams p; template <class E> __device__ int operator()(int r, 
 struct BtFn { BtParams p; template <class E> __device__ int operator()(int r, E& e) const { return bt_row(p, r, e); } };
 struct BFn { BParams p; template <class E> __device__ int operator()(int r, E& e) const { return b_row(p, r, e); } };
 struct ApFn { ApParams p; template <class E> __device__ int operator()(int r, E& e) const { return ap_row(p, r, e); } };
+struct SkFn { SkParams p; template <class E> __device__ int operator()(int r, E& e) const { return sk_row(p, r, e); } };
 struct F1Fn { F1Params p; template <class E> __device__ int operator()(int r, E& e) const { return f1_row(p, r, e); } };
 
 template <class Fn>
@@ -637,6 +667,11 @@ etq_status oseen_gershgorin(const Geo& g, double nu, int wind, double* bim, cuda
 
 etq_status assemble_ap(const Geo& g, Sell* out, cudaStream_t st) {
   ApFn fn{ApParams{g}};
+  return build_sell(fn, nullptr, g.nk, ((int64_t)g.nk + SELL_C - 1) / SELL_C, out, st);
+}
+
+etq_status assemble_sk(const Geo& g, double scale, Sell* out, cudaStream_t st) {
+  SkFn fn{SkParams{g, scale}};
   return build_sell(fn, nullptr, g.nk, ((int64_t)g.nk + SELL_C - 1) / SELL_C, out, st);
 }
 

@@ -44,8 +44,10 @@ static __device__ double block_sum(double v) {
 
 // Store this block's partial of NV sums into `site` and, in the last block to finish, sum the
 // gridDim.x partials in a fixed order into out[0..NV).  Deterministic for a fixed grid.
+// Returns true in exactly one thread (thread 0 of the last block) after out[] is written, so
+// the caller can derive scalars from the finished sums.
 template <int NV>
-__device__ void reduce_finish(const double (&v)[NV], RedSite site, int slot, double* out) {
+__device__ bool reduce_finish(const double (&v)[NV], RedSite site, int slot, double* out) {
   __shared__ bool last;
   const int t = lin_tid(), bs = lin_bs();
   double tot[NV];
@@ -71,6 +73,7 @@ __device__ void reduce_finish(const double (&v)[NV], RedSite site, int slot, dou
     }
     if (t == 0) site.counter[slot] = 0u;
   }
+  return last && t == 0;
 }
 
 // ---------------------------------------------------------------- SELL row products

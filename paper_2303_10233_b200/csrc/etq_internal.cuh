@@ -158,6 +158,35 @@ struct PcMass {               // Chebyshev-SGS on M_Q (P2 / M1 pressure block)
   double *t = nullptr, *y0 = nullptr, *y1 = nullptr, *rr = nullptr;   // n_p work vectors
 };
 
+// ---------------------------------------------------------------- PCG inner solves (exact.cu)
+enum PcgScalar {
+  PG_R0 = 0, PG_RZ0, PG_RZ1, PG_PQ, PG_RR, PG_DONE, PG_IT, PG_TOL2, PG_MAXIT, PG_ITTOT, PG_CALLS,
+  PG_COUNT = 16
+};
+struct PcgWs {                // one preconditioned CG instance: device scalars, vectors, own slots
+  int64_t n = 0;
+  double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
+  double* sc = nullptr;       // [PG_COUNT]
+  RedSite red{};              // RED_SLOTS slots: 0 r0, 1 rz, 2 pq, 3 rr, 4.. callers
+  cudaStream_t cs = nullptr;  // stream used to capture the conditional loop body
+  double rtol = 1e-10;
+  int maxit = 50;
+  int64_t body_nodes = 0;     // kernel launches per loop iteration (captured body)
+  int64_t fixed_nodes = 0;    // kernel launches outside the loop per call
+};
+struct PcExactMass {          // exact augmented M_Q solve through S_k (NEXT-2, reading R21)
+  bool ready = false;
+  Hierarchy sH;               // Q1 hierarchy of S_k (level l scaled by 4^-l)
+  PcgWs cg;
+  double* g = nullptr;        // [n_k] reduced right-hand side
+  double* zh = nullptr;       // [n_k] S_k^+ g
+  double* sc = nullptr;       // [8] sums, lambda, a^T zhat, beta
+};
+struct PcVelIter {            // A^{-1} by V-cycle-preconditioned CG (P1 at scale)
+  bool ready = false;
+  PcgWs cg;
+};
+
 struct Problem {
   Geo g;
   int bc = 0;
@@ -206,6 +235,10 @@ struct Problem {
   cudaGraphExec_t gmres_graph = nullptr; int gmres_graph_key = -1;
   int64_t gmres_graph_nodes = 0;
 
+  // NEXT-2: exact M_Q solve (P3, P1_ITER) and iterative A^{-1} (P1_ITER)
+  PcExactMass mx;
+  PcVelIter vi;
+
   // Krylov workspace (length N each)
   double* kv[10] = {nullptr};
   int nkv = 0;
@@ -235,6 +268,7 @@ etq_status velocity_dinv_dev(const Geo& g, bool oseen, double nu, int wind, doub
 etq_status oseen_gershgorin(const Geo& g, double nu, int wind, double* bim, cudaStream_t st);
 etq_status assemble_ap(const Geo& g, Sell* out, cudaStream_t st);
 etq_status assemble_f1(const Geo& g, double nu, int wind, Sell* out, cudaStream_t st);
+etq_status assemble_sk(const Geo& g, double scale, Sell* out, cudaStream_t st);
 etq_status sell_diag_inv(const Sell& A, double* dinv, cudaStream_t st);
 etq_status build_rhs_dev(const Problem& P, const double* f_nodal, double* b);
 etq_status mark_implicit(const Geo& g, bool oseen, double nu, int wind, Sell& S, cudaStream_t st, bool values);
@@ -247,7 +281,7 @@ void launch_vel_spmv(const Sell& A, const double* x, double* y, int nq, cudaStre
 void launch_dot(const double* a, const double* b, int64_t n, RedSite* site, int slot, double* out,
                 const double* done, cudaStream_t st);
 etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, double hi, int degree);
-etq_status build_ap_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, double hi, int degree);
+etq_status build_ap_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, double hi, int degree, int op = 0);
 void free_hierarchy(Hierarchy& H);
 etq_status dense_inverse_pivot(double* A, int m, cudaStream_t st);
 etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r_u, double* z_u,
@@ -298,3 +332,14 @@ etq_status precond_apply_ex(const Problem& P, etq_pc_kind kind, const double* r,
                             double* out_u, double* out_p, const double* done, cudaStream_t st);
 etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, double rtol,
                       int maxit, etq_report* rep);
+
+// exact.cu (NEXT-2: exact M_Q solve through S_k, iterative A^{-1}, preconditioners P3 / P1_ITER)
+etq_status exact_mass_setup(Problem& P);
+etq_status vel_iter_setup(Problem& P);
+void exact_free(Problem& P);
+etq_status exact_mass_apply(const Problem& P, const double* r_p, double* z_p, const RedSite* site, int slot,
+                            double* dot_out, const double* dot_with, const double* done, cudaStream_t st);
+etq_status vel_iter_apply(const Problem& P, const double* r_u, double* z_u, const RedSite* site, int slot,
+                          double* dot_out, const double* dot_with, const double* done, cudaStream_t st);
+etq_status pcg_stats(const Problem& P, int which, double* it_total, double* calls);
+int64_t pcg_launches_since(const Problem& P, double it0_m, double calls0_m, double it0_v, double calls0_v);

@@ -1129,9 +1129,10 @@ __global__ void k_add_ones(double* A, int m, double v) {
     A[t] += v;
 }
 
-// Pressure hierarchy for Ap = B1 Mdiag^{-1} B1^T (reading R13): Q1 levels n ... coarse_n,
-// nested bilinear transfers, real Chebyshev smoother, coarse pseudo-inverse.
-etq_status build_ap_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, double hi, int degree) {
+// Pressure hierarchy for Ap = B1 Mdiag^{-1} B1^T (reading R13; op 0) or the mass Schur complement
+// S_k (reading R21; op 1, level l scaled by 4^-l so that it approximates the Galerkin product):
+// Q1 levels n ... coarse_n, nested bilinear transfers, real Chebyshev smoother, coarse pseudo-inverse.
+etq_status build_ap_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, double hi, int degree, int op) {
   std::vector<int> ns;
   ETQ_TRY(level_sizes(P.g.n, coarse_n, ns));
   H.kind = 1; H.ncomp = 1;
@@ -1140,7 +1141,8 @@ etq_status build_ap_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo,
     Level& L = H.lv[l];
     L.g = make_geo(ns[l]);
     L.nrows = L.g.nk;
-    ETQ_TRY(assemble_ap(L.g, &L.A, P.stream));
+    if (op == 0) ETQ_TRY(assemble_ap(L.g, &L.A, P.stream));
+    else ETQ_TRY(assemble_sk(L.g, std::ldexp(1.0, -2 * (int)l), &L.A, P.stream));   // S_k / 4^l (R21)
     ETQ_TRY(dalloc(&L.dinv, L.g.nk));
     ETQ_TRY(sell_diag_inv(L.A, L.dinv, P.stream));
     L.bim = 0.0;
@@ -1150,9 +1152,12 @@ etq_status build_ap_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo,
   const int m = C.g.nk;
   ETQ_TRY(dalloc(&C.coarse_inv, (size_t)m * m));
   ETQ_TRY(dense_from_sell(C.A, m, C.coarse_inv, P.stream));
-  k_add_ones<<<grid_for((int64_t)m * m, BS, 4096), BS, 0, P.stream>>>(C.coarse_inv, m, 1.0); etq_count_launch();
+  // c 1 1^T with c m ~ the operator's diagonal keeps A + c 1 1^T as well conditioned as A on 1^perp
+  // (Ap: diagonal O(1); S_k / 4^l: diagonal (28/144) h_0^2 on every level)
+  const double cs = op == 0 ? 1.0 : (28.0 / 144.0) * P.g.h * P.g.h / m;
+  k_add_ones<<<grid_for((int64_t)m * m, BS, 4096), BS, 0, P.stream>>>(C.coarse_inv, m, cs); etq_count_launch();
   ETQ_TRY(dense_inverse_spd(C.coarse_inv, m, P.stream));
-  k_add_ones<<<grid_for((int64_t)m * m, BS, 4096), BS, 0, P.stream>>>(C.coarse_inv, m, -1.0 / ((double)m * m)); etq_count_launch();
+  k_add_ones<<<grid_for((int64_t)m * m, BS, 4096), BS, 0, P.stream>>>(C.coarse_inv, m, -1.0 / (cs * m * m)); etq_count_launch();
   H.lo = lo; H.hi = hi; H.degree = degree; H.built = true;
   ETQ_CHECK(cudaStreamSynchronize(P.stream));
   return ETQ_OK;

@@ -141,6 +141,18 @@ etq_status precond_apply_ex(const Problem& P, etq_pc_kind kind, const double* r,
     if (out_p) launch_dot(z + nu, w + nu, np, const_cast<RedSite*>(site), 2, out_p, done, st);
     return ETQ_OK;
   }
+  if (kind == ETQ_PC_P3 || kind == ETQ_PC_P1_ITER) {
+    if (!P.mx.ready || (kind == ETQ_PC_P1_ITER && !P.vi.ready)) return ETQ_ENOTSETUP;
+    // exact M_Q solve on the aux stream, velocity block (one V-cycle or V-cycle-PCG) on the main stream
+    ETQ_CHECK(cudaEventRecord(P.ev_fork, st));
+    ETQ_CHECK(cudaStreamWaitEvent(P.aux, P.ev_fork, 0));
+    ETQ_TRY(exact_mass_apply(P, r + nu, z + nu, site, 2, out_p, w ? w + nu : nullptr, done, P.aux));
+    if (kind == ETQ_PC_P3) ETQ_TRY(vcycle_apply_ex(P, P.mg, r, z, site, 1, out_u, w, done, st));
+    else ETQ_TRY(vel_iter_apply(P, r, z, site, 1, out_u, w, done, st));
+    ETQ_CHECK(cudaEventRecord(P.ev_join, P.aux));
+    ETQ_CHECK(cudaStreamWaitEvent(st, P.ev_join, 0));
+    return ETQ_OK;
+  }
   if (kind == ETQ_PC_P2_GMG) {
     if (!P.p2_ready) return ETQ_ENOTSETUP;
     // pressure branch on the aux stream, velocity V-cycle on the main stream
@@ -237,6 +249,13 @@ etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, 
     P.minres_graph_kind = (int)kind;
     P.minres_graph_x = x;
   }
+  double pi0m = 0, pc0m = 0, pi0v = 0, pc0v = 0;   // inner CG counters (loop bodies run a variable count)
+  const bool inner = kind == ETQ_PC_P3 || kind == ETQ_PC_P1_ITER;
+  if (inner) {
+    ETQ_CHECK(cudaStreamSynchronize(st));
+    ETQ_TRY(pcg_stats(P, 0, &pi0m, &pc0m));
+    ETQ_TRY(pcg_stats(P, 1, &pi0v, &pc0v));
+  }
   int cur = 1;
   int it = 0;
   for (;;) {
@@ -254,6 +273,7 @@ etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, 
   ETQ_CHECK(cudaEventRecord(P.ev_t1, st));
   ETQ_CHECK(cudaMemcpyAsync(P.hscal, sc, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost, st));
   ETQ_CHECK(cudaStreamSynchronize(st));
+  if (inner && graphs) etq_count_launch(pcg_launches_since(P, pi0m, pc0m, pi0v, pc0v));
   const int iters = (int)P.hscal[S_IT];
   const int status = (int)P.hscal[S_STATUS];
   const double g1 = P.hscal[S_GAMMA1];

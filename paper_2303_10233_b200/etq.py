@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("ETQ_LIB", os.path.join(_HERE, "libetq.so"))
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "etq.h")
 
 ETQ_OK, ETQ_NOT_CONVERGED = 0, 1
-PC_P1_EXACT, PC_P2_GMG, PC_OSEEN_M1, PC_OSEEN_PCD1 = 0, 1, 2, 3
+PC_P1_EXACT, PC_P2_GMG, PC_OSEEN_M1, PC_OSEEN_PCD1, PC_P1_ITER, PC_P3 = 0, 1, 2, 3, 4, 5
 
 
 class EtqError(RuntimeError):
@@ -36,7 +36,8 @@ class Wind(C.Structure):
 class PcParams(C.Structure):
     _fields_ = [("cheb_sgs_steps", C.c_int32), ("cheb_sgs_lo", C.c_double), ("lanczos_steps", C.c_int32),
                 ("smooth_degree", C.c_int32), ("smooth_hi", C.c_double), ("smooth_lo", C.c_double),
-                ("coarse_n", C.c_int32), ("mass_cheb_steps", C.c_int32), ("use_graphs", C.c_int32)]
+                ("coarse_n", C.c_int32), ("mass_cheb_steps", C.c_int32), ("use_graphs", C.c_int32),
+                ("inner_rtol", C.c_double), ("inner_maxit", C.c_int32), ("inner_coarse_n", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -62,6 +63,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "etq_apply_vcycle": ([P, I32, VP, VP], I32),
         "etq_apply_mass_pc": ([P, VP, VP], I32),
         "etq_apply_mass": ([P, VP, VP], I32),
+        "etq_apply_mass_exact": ([P, VP, VP, C.POINTER(I32)], I32),
+        "etq_inner_stats": ([P, I32, C.POINTER(D), C.POINTER(D)], I32),
         "etq_sgs_sweep": ([P, VP, VP, VP], I32),
         "etq_estimate_sgs_lo": ([P, VP, I32, C.POINTER(D)], I32),
         "etq_get_cheb_sgs_lo": ([P, C.POINTER(D)], I32),
@@ -213,6 +216,18 @@ class Problem:
         _check(lib().etq_apply_mass_pc(self.h, _ptr(r_p), _ptr(z_p)), "etq_apply_mass_pc")
         return z_p
 
+    def apply_mass_exact(self, r_p, z_p):
+        """Exact augmented M_Q solve through S_k (P3 / P1_ITER set up); returns the CG iterations."""
+        it = C.c_int32()
+        _check(lib().etq_apply_mass_exact(self.h, _ptr(r_p), _ptr(z_p), C.byref(it)), "etq_apply_mass_exact")
+        return it.value
+
+    def inner_stats(self, which=0):
+        """(total inner CG iterations, solves) since setup; which 0 = M_Q, 1 = velocity."""
+        it, calls = C.c_double(), C.c_double()
+        _check(lib().etq_inner_stats(self.h, which, C.byref(it), C.byref(calls)), "etq_inner_stats")
+        return it.value, calls.value
+
     def apply_mass(self, x_p, y_p):
         _check(lib().etq_apply_mass(self.h, _ptr(x_p), _ptr(y_p)), "etq_apply_mass")
         return y_p
@@ -312,5 +327,5 @@ class Problem:
         _check(lib().etq_export_operator(self.h, which, level, C.byref(nr), C.byref(nz),
                                          C.c_void_p(rp.ctypes.data), C.c_void_p(col.ctypes.data),
                                          C.c_void_p(val.ctypes.data)), "etq_export_operator")
-        ncol = {0: nr.value, 1: self.n_u, 2: self.n_p, 3: nr.value, 4: nr.value}[which]
+        ncol = {0: nr.value, 1: self.n_u, 2: self.n_p, 3: nr.value, 4: nr.value, 5: nr.value}[which]
         return sp.csr_matrix((val[:nz.value], col[:nz.value], rp), shape=(nr.value, ncol))
