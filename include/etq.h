@@ -218,7 +218,9 @@ etq_status etq_launch_count(int64_t* count);
  *        2 = one V-cycle on both velocity components (P2 set up);
  *        3 = one Pi C Pi pressure apply (P2 set up; L2-resident, bytes reported as 0);
  *        4 = one P2 preconditioner apply (velocity and pressure branches concurrently);
- *        5 = fp32 fused saddle SpMV; 6 = fp32 V-cycle (P2 set up).
+ *        5 = fp32 fused saddle SpMV; 6 = fp32 V-cycle (P2 set up);
+ *        7 = one exact M_Q solve through S_k (P3/P1_ITER set up; replays of one captured graph);
+ *        8 = one Q1-GMG V-cycle on S_k; 9 = one P3 preconditioner apply (graph replays).
  * Host outputs: *ms = average device time per launch, *bytes = algorithmic bytes per launch. */
 etq_status etq_time_kernel(etq_problem* p, int32_t which, int32_t reps, double* ms, double* bytes);
 

@@ -564,8 +564,9 @@ etq_status etq_launch_count(int64_t* count) {
 etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* ms, double* bytes) {
   if (!h || reps < 1 || !ms || !bytes) return ETQ_EINVAL;
   Problem& P = h->P;
-  if ((which >= 2 && which != 5) && !P.p2_ready) return ETQ_ENOTSETUP;
-  if (which < 0 || which > 6) return ETQ_EINVAL;
+  if (which < 0 || which > 9) return ETQ_EINVAL;
+  if ((which >= 2 && which <= 6 && which != 5) && !P.p2_ready) return ETQ_ENOTSETUP;
+  if (which >= 7 && !P.mx.ready) return ETQ_ENOTSETUP;
   if (which >= 5) {
     ETQ_TRY(ensure_f32(P));
     if (!P.tkf) {
@@ -593,17 +594,38 @@ etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* 
       case 4: ETQ_TRY(precond_apply_ex(P, ETQ_PC_P2_GMG, a, c, nullptr, nullptr, nullptr, nullptr, st)); break;
       case 5: launch_saddle_f32(P, false, P.tkf, P.tkf + P.N, st); break;
       case 6: ETQ_TRY(vcycle_f32(P, P.tkf, P.tkf + P.N, st)); break;
+      case 7: ETQ_TRY(exact_mass_apply(P, a + P.n_u, b + P.n_u, nullptr, 0, nullptr, nullptr, nullptr, st)); break;
+      case 8: ETQ_TRY(vcycle_apply_ex(P, P.mx.sH, a + P.n_u, b + P.n_u, nullptr, 0, nullptr, nullptr, nullptr, st)); break;
+      case 9: ETQ_TRY(precond_apply_ex(P, ETQ_PC_P3, a, c, nullptr, nullptr, nullptr, nullptr, st)); break;
     }
     return ETQ_OK;
   };
-  ETQ_TRY(one(0));   // warm-up
+  cudaGraphExec_t gx = nullptr;
+  if (which == 7 || which == 9) {   // the inner CG loops are graph while-nodes: time replays of one graph
+    cudaGraph_t g;
+    ETQ_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    etq_status s1 = one(0);
+    cudaError_t e = cudaStreamEndCapture(st, &g);
+    if (s1 < 0) return s1;
+    ETQ_CHECK(e);
+    cudaError_t ei = cudaGraphInstantiate(&gx, g, 0);
+    cudaGraphDestroy(g);
+    ETQ_CHECK(ei);
+    ETQ_CHECK(cudaGraphLaunch(gx, st));   // warm-up
+  } else {
+    ETQ_TRY(one(0));   // warm-up
+  }
   ETQ_CHECK(cudaEventRecord(P.ev_t0, st));
-  for (int k = 0; k < reps; ++k) ETQ_TRY(one(k));
+  for (int k = 0; k < reps; ++k) {
+    if (gx) ETQ_CHECK(cudaGraphLaunch(gx, st));
+    else ETQ_TRY(one(k));
+  }
   ETQ_CHECK(cudaEventRecord(P.ev_t1, st));
   ETQ_CHECK(cudaEventSynchronize(P.ev_t1));
   float t = 0.f;
   ETQ_CHECK(cudaEventElapsedTime(&t, P.ev_t0, P.ev_t1));
   *ms = (double)t / reps;
+  if (gx) cudaGraphExecDestroy(gx);
   const double nnz_all = (double)(P.Lv.nnz + P.BxT1.nnz + P.ByT1.nnz + P.BxT0.nnz + P.ByT0.nnz + P.B.nnz);
   switch (which) {
     case 0: *bytes = 12.0 * nnz_all - 4.0 * P.Lv.nnz_implicit - 8.0 * P.Lv.nnz_implicit_vals + 4.0 * P.Lv.nslices * SELL_C + 16.0 * P.N; break;

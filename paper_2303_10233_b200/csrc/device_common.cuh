@@ -158,4 +158,34 @@ __device__ __forceinline__ void sell_row2(const Sell& A, int64_t s, int lane, in
     a0 = fma(v, __ldg(x0 + c), a0); a1 = fma(v, __ldg(x1 + c), a1);
   }
 }
+
+// ---------------------------------------------------------------- matrix-free S_k (reading R21)
+// (S_k v)_p / w with w = h_0^2 / 144 on every level of the scaled hierarchy (S_l / 4^l): per cell
+// T of the Q1 vertex p = (a, c), (36^-1 m_x m_y - 16^-1) h^2 for each vertex pair of T, i.e.
+//   7 ca cc v_p - cc (v_{p-1} + v_{p+1}) - ca (v_{p-n1} + v_{p+n1}) - 5 (corner neighbours)
+// with ca, cc the numbers of cells adjacent to p along x and y (missing neighbours dropped).
+// Returns the sum; *diag7 = 7 ca cc (the diagonal / w).
+__device__ __forceinline__ double sk_stencil(int64_t p, int a, int c, int n, const double* __restrict__ v,
+                                             double* diag7) {
+  const int n1 = n + 1;
+  const int ca = (a > 0) + (a < n), cc = (c > 0) + (c < n);
+  const double d7 = 7.0 * (double)(ca * cc);
+  double acc = d7 * __ldg(v + p);
+  double ex = 0.0, ey = 0.0, co = 0.0;
+  if (a > 0) ex += __ldg(v + p - 1);
+  if (a < n) ex += __ldg(v + p + 1);
+  if (c > 0) {
+    ey += __ldg(v + p - n1);
+    if (a > 0) co += __ldg(v + p - n1 - 1);
+    if (a < n) co += __ldg(v + p - n1 + 1);
+  }
+  if (c < n) {
+    ey += __ldg(v + p + n1);
+    if (a > 0) co += __ldg(v + p + n1 - 1);
+    if (a < n) co += __ldg(v + p + n1 + 1);
+  }
+  acc -= (double)cc * ex + (double)ca * ey + 5.0 * co;
+  *diag7 = d7;
+  return acc;
+}
 }  // namespace etqd

@@ -126,7 +126,9 @@ struct Hierarchy {
   std::vector<Level> lv;
   double lo = 0.16, hi = 1.6;
   int degree = 3;
-  int kind = 0;               // 0: Q2 velocity (2 components, Dirichlet rows); 1: Q1 pressure (Ap)
+  int kind = 0;               // 0: Q2 velocity (2 components, Dirichlet rows); 1: Q1 pressure (Ap / S_k)
+  int op = 0;                 // kind 1: 0 = Ap (SELL), 1 = S_k / 4^l (matrix-free stencil kernels)
+  double sk_w = 0.0;          // op 1: h_0^2 / 144, the stencil scale shared by all levels
   int ncomp = 2;
   bool built = false;
   bool f32 = false;           // fp32 copies present

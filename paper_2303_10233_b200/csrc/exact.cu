@@ -105,6 +105,25 @@ __global__ void __launch_bounds__(BS) k_pcg_spmv(Sell A, int nq, const double* p
   reduce_finish<1>(a, site, SL_PQ, sc + PG_PQ);
 }
 
+// q = S_k p (matrix-free, level 0 of the S_k hierarchy: w = h^2 / 144), pq = p^T q
+__global__ void __launch_bounds__(BS) k_pcg_spmv_sk(int n, double w, const double* p, double* q, RedSite site,
+                                                    double* sc) {
+  if (pcg_done(sc)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc[PG_RZ0] = sc[PG_RZ1];
+  const int n1 = n + 1;
+  const int64_t nk = (int64_t)n1 * n1;
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nk; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / n1), a = (int)(i - (int64_t)c * n1);
+    double d7;
+    const double v = w * sk_stencil(i, a, c, n, p, &d7);
+    q[i] = v;
+    s += v * p[i];
+  }
+  double a[1] = {s};
+  reduce_finish<1>(a, site, SL_PQ, sc + PG_PQ);
+}
+
 // alpha = rz / pq; x += alpha p; r -= alpha q; stop test ||r||^2 <= tol^2 ||b||^2 or it >= maxit
 __global__ void __launch_bounds__(BS) k_pcg_xr(double* x, double* r, const double* p, const double* q, int64_t n,
                                                RedSite site, double* sc, cudaGraphConditionalHandle h, int use_h) {
@@ -212,7 +231,9 @@ struct PcgOps {
 
 static void pcg_apply_A(const PcgWs& W, const PcgOps& o, cudaStream_t st) {
   const int gs = grid_for(o.A->nslices * 32, BS, 4096);
-  if (o.nc == 2) k_pcg_spmv<2><<<gs, BS, 0, st>>>(*o.A, o.nq, W.p, W.q, W.red, W.sc);
+  if (o.nc == 1 && o.H->op == 1)
+    k_pcg_spmv_sk<<<grid_for(W.n, BS, RED_BLOCKS * 2), BS, 0, st>>>(o.H->lv[0].g.n, o.H->sk_w, W.p, W.q, W.red, W.sc);
+  else if (o.nc == 2) k_pcg_spmv<2><<<gs, BS, 0, st>>>(*o.A, o.nq, W.p, W.q, W.red, W.sc);
   else k_pcg_spmv<1><<<gs, BS, 0, st>>>(*o.A, o.nq, W.p, W.q, W.red, W.sc);
   etq_count_launch();
 }

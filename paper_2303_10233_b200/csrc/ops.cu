@@ -236,6 +236,38 @@ __global__ void __launch_bounds__(BS, SPMV_MINB) k_post_residual(Sell A, const d
   }
 }
 
+// Matrix-free S_k Chebyshev step / post-smoothing residual on a Q1 level (reading R21):
+// same contract as k_cheb_step<1> (post = 0) and k_post_residual<1> (post = 1, v = x, r_in = b).
+struct SkChebArgs {
+  int n; double w;
+  const double* v;                         // vector the operator is applied to (d_in, or x if post)
+  const double* d_in; const double* r_in; const double* x_in;
+  double* x_out; double* r_out; double* d_out;
+  double c1, c2, theta; int post;
+  const double* done;
+};
+__global__ void __launch_bounds__(BS) k_cheb_sk(SkChebArgs a) {
+  if (is_done(a.done)) return;
+  const int n1 = a.n + 1;
+  const int64_t nk = (int64_t)n1 * n1;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nk; p += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(p / n1), ai = (int)(p - (int64_t)c * n1);
+    double d7;
+    const double q = a.w * sk_stencil(p, ai, c, a.n, a.v, &d7);
+    const double di = 1.0 / (a.w * d7);
+    const double ro = a.r_in[p] - q;
+    if (a.post) {
+      a.r_out[p] = ro;
+      a.d_out[p] = di * ro / a.theta;
+    } else {
+      const double dd = a.d_in[p];
+      a.x_out[p] = (a.x_in ? a.x_in[p] : 0.0) + dd;
+      if (a.r_out) a.r_out[p] = ro;
+      if (a.d_out) a.d_out[p] = a.c1 * dd + a.c2 * (di * ro);
+    }
+  }
+}
+
 // d = D^{-1} b / theta (start of pre-smoothing from x = 0), NC components
 __global__ void k_cheb_init(const double* dinv, int nq, int nc, const double* b, double* d, double theta,
                             const double* done) {
@@ -1159,6 +1191,7 @@ etq_status build_ap_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo,
   ETQ_TRY(dense_inverse_spd(C.coarse_inv, m, P.stream));
   k_add_ones<<<grid_for((int64_t)m * m, BS, 4096), BS, 0, P.stream>>>(C.coarse_inv, m, -1.0 / (cs * m * m)); etq_count_launch();
   H.lo = lo; H.hi = hi; H.degree = degree; H.built = true;
+  H.op = op; H.sk_w = P.g.h * P.g.h / 144.0;
   ETQ_CHECK(cudaStreamSynchronize(P.stream));
   return ETQ_OK;
 }
@@ -1214,6 +1247,17 @@ static void launch_cheb_st(const Level& lv, const ChebArgs& c, bool post, double
 
 // One V-cycle (readings R9/R9'/R13) on H.ncomp components: z = V(r); optional partial
 // <z, dot_with> into (site, slot) -> dot_out.
+static void launch_cheb_sk(const Hierarchy& H, const Level& lv, const ChebArgs& c, int post, double theta,
+                           cudaStream_t st) {
+  SkChebArgs a;
+  a.n = lv.g.n; a.w = H.sk_w;
+  a.v = post ? c.x_in : c.d_in;
+  a.d_in = c.d_in; a.r_in = c.r_in; a.x_in = c.x_in;
+  a.x_out = c.x_out; a.r_out = c.r_out; a.d_out = c.d_out;
+  a.c1 = c.c1; a.c2 = c.c2; a.theta = theta; a.post = post; a.done = c.done;
+  k_cheb_sk<<<grid_for((int64_t)lv.g.nk, BS, 8 * 148), BS, 0, st>>>(a);
+}
+
 etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r_u, double* z_u,
                            const RedSite* site, int slot, double* dot_out, const double* dot_with,
                            const double* done, cudaStream_t st) {
@@ -1254,6 +1298,7 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       a.x_out = lv.x; a.r_out = lv.r; a.d_out = (k == H.degree - 1) ? nullptr : dout;
       a.c1 = c1[k]; a.c2 = c2[k]; a.done = done;
       if (lv.st_on) launch_cheb_st(lv, a, false, theta, st);
+      else if (H.op == 1) launch_cheb_sk(H, lv, a, 0, theta, st);
       else if (nc == 2) k_cheb_step<2><<<gs, BS, 0, st>>>(a);
       else k_cheb_step<1><<<gs, BS, 0, st>>>(a);
       etq_count_launch();
@@ -1296,6 +1341,10 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       a.A = lv.A; a.dinv = lv.dinv; a.nq = nq; a.x_in = lv.x; a.r_in = bvec[l]; a.r_out = lv.r; a.d_out = lv.d0;
       a.done = done;
       launch_cheb_st(lv, a, true, theta, st);
+    } else if (H.op == 1) {
+      ChebArgs a{};
+      a.x_in = lv.x; a.r_in = bvec[l]; a.r_out = lv.r; a.d_out = lv.d0; a.done = done;
+      launch_cheb_sk(H, lv, a, 1, theta, st);
     } else if (nc == 2) {
       k_post_residual<2><<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, theta, done);
     } else {
@@ -1310,6 +1359,7 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       a.x_out = lv.x; a.r_out = (k == H.degree - 2) ? nullptr : lv.r; a.d_out = dout;
       a.c1 = c1[k]; a.c2 = c2[k]; a.done = done;
       if (lv.st_on) launch_cheb_st(lv, a, false, theta, st);
+      else if (H.op == 1) launch_cheb_sk(H, lv, a, 0, theta, st);
       else if (nc == 2) k_cheb_step<2><<<gs, BS, 0, st>>>(a);
       else k_cheb_step<1><<<gs, BS, 0, st>>>(a);
       etq_count_launch();
