@@ -33,7 +33,9 @@
   } while (0)
 
 void etq_last_cuda_error(cudaError_t e, const char* file, int line);
-void etq_count_launch(int64_t k = 1);   // host-side launch counter (etq_launch_count)
+void etq_count_launch(int64_t k = 1);
+extern bool g_cheb_tile_enabled;          // api.cu; etq_set_option(0)
+extern int g_cheb_tile_min_n;             // api.cu; etq_set_option(1)   // host-side launch counter (etq_launch_count)
 
 constexpr int SELL_C = 32;           // slice height = warp size
 constexpr int RED_BLOCKS = 592;      // 4 x 148 SMs: grid of plain reduction kernels
@@ -96,6 +98,7 @@ struct StencilOp {
   int m = 0, lo = 0, hi = -1, nseg_x = 0;
   int64_t nseg = 0;
   double w[4][25];
+  double dcls[4] = {0.0, 0.0, 0.0, 0.0};   // D^-1 of the non-Dirichlet rows per class
 };
 
 // ---------------------------------------------------------------- MG level

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <vector>
+#include <utility>
 #include <complex>
 
 #include "device_common.cuh"
@@ -161,7 +162,7 @@ struct ChebStArgs {
   StencilOp so; Sell F; const double* dinv; int nq;
   const double* d_in; const double* r_in; const double* x_in;
   double* x_out; double* r_out; double* d_out;
-  double c1, c2; int post; double theta;   // post: r = b - A x, d = D^{-1} r / theta (x_in = x, r_in = b)
+  double c1, c2; int post; double itheta;   // post: r = b - A x, d = D^{-1} r / theta (x_in = x, r_in = b; itheta = 1 / theta)
   const double* done;
 };
 __device__ __forceinline__ void cheb_update2(const ChebStArgs& a, int row, double q0, double q1) {
@@ -169,7 +170,7 @@ __device__ __forceinline__ void cheb_update2(const ChebStArgs& a, int row, doubl
   if (a.post) {
     const double r0 = a.r_in[row] - q0, r1 = a.r_in[a.nq + row] - q1;
     a.r_out[row] = r0; a.r_out[a.nq + row] = r1;
-    a.d_out[row] = di * r0 / a.theta; a.d_out[a.nq + row] = di * r1 / a.theta;
+    a.d_out[row] = di * r0 * a.itheta; a.d_out[a.nq + row] = di * r1 * a.itheta;
     return;
   }
 #pragma unroll
@@ -210,10 +211,259 @@ __global__ void __launch_bounds__(BS, STENCIL_MINB) k_cheb_step_st(ChebStArgs a)
   }
 }
 
+// ---- temporally blocked Chebyshev smoothing (Stokes levels, storage 0): all three steps of a
+// pre- or post-smoothing pass in one kernel.  A CTA owns a CT_T x CT_T tile of one velocity
+// component and stages a CT_R x CT_R window (halo CT_H = 3 steps x stencil radius 2) of each
+// vector in shared memory; each step shrinks the valid region by 2.  Within a step a lane owns
+// a column pair (even i, odd i + 1) and a warp walks a strip of rows with a 5-row x 6-column
+// register window (one 128-bit shared load per two values, each value reused by up to 25 taps).
+// Row parity is compile-time in the unrolled walk, so the four stencil classes' weights are
+// compile-time constant-bank operands.  Every non-Dirichlet row of a translation-invariant
+// Stokes level equals its class stencil with the Dirichlet-node taps removed (identity rows and
+// eliminated columns, reading R2): the level is matrix-free.  Per-row arithmetic and summation
+// order are those of k_cheb_step_st / k_post_residual (interior rows bitwise identical).
+// Bytes per node and component: pre 24 (b in; x, r out), post 32 (x, b in; x, d out) instead of
+// 3 x ~52 + 16 for the unfused steps.
+constexpr int CT_T = 56, CT_H = 6, CT_R = CT_T + 2 * CT_H, CT_THREADS = 256, CT_STRIP = 8;
+constexpr int CT_ARR = CT_R * CT_R;            // one staged array, row-major (stride CT_R, even)
+constexpr int CT_SMEM = 3 * CT_ARR * (int)sizeof(double);
+static_assert(CT_R % 2 == 0 && CT_H % 2 == 0 && CT_T % 2 == 0, "column pairs need even offsets");
+static_assert((CT_R - 4) / 2 <= 32, "a warp covers the widest step region with column pairs");
+static_assert((CT_R - 4) <= CT_STRIP * (CT_THREADS / 32), "the warps' strips cover the widest step region");
+struct ChebTileArgs {
+  StencilOp so; int nq; int tiles_x;
+  const double* b; const double* x_in;
+  double* x_out; double* r_out; double* d_out;
+  double itheta, c1[3], c2[3];
+  const double* done;
+};
+
+// class stencil of one output from the register window: win[slot][col], rows jj-2..jj+2 in
+// slots (R0 + dj) % 5 (R0: slot of the output row, compile-time), cols ii-2..ii+3 with the
+// output at column offset OC
+template <int C, int OC, int R0>
+__device__ __forceinline__ double ct_tap_sum(const StencilOp& so, const double (&win)[5][6]) {
+  constexpr int PI = C & 1, PJ = C >> 1, RX = PI ? 1 : 2, RY = PJ ? 1 : 2;
+  double a = 0.0;
+#pragma unroll
+  for (int dj = -RY; dj <= RY; ++dj) {
+#pragma unroll
+    for (int di = -RX; di <= RX; ++di)
+      a = fma(so.w[C][(dj + 2) * 5 + di + 2], win[(R0 + dj + 5) % 5][OC + di + 2], a);
+  }
+  return a;
+}
+
+// window row load: columns ii-2 .. ii+3 of window row jj (three 128-bit loads); EDGE: Dirichlet
+// nodes read as 0 (their columns are eliminated from every non-Dirichlet row)
+template <bool EDGE>
+__device__ __forceinline__ void ct_load_row(const double* __restrict__ v, int ii, int jj, int i, int j, int m,
+                                            double (&dst)[6]) {
+  const double2* p = reinterpret_cast<const double2*>(v + (ii - 2) + CT_R * jj);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double2 t = p[k];
+    dst[2 * k] = t.x; dst[2 * k + 1] = t.y;
+  }
+  if (EDGE) {
+    const bool rowd = j <= 0 || j >= m - 1;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const int it = i - 2 + k;
+      if (rowd || it <= 0 || it >= m - 1) dst[k] = 0.0;
+    }
+  }
+}
+
+// row t of a warp's strip (compile-time t: window slots and stencil classes are constants)
+template <int S, int MODE, bool EDGE, int t>
+__device__ __forceinline__ void ct_row_t(const ChebTileArgs& a, int i0, int j0, double* RS, const double* v,
+                                         const double* din, double* dout, double c1, double c2, int jb, int ii,
+                                         int i, bool lok, double (&win)[5][6]) {
+  const int m = a.so.m;
+  const int jj = jb + t;
+  if (jj >= CT_R - S) return;                          // W even, strips even: whole pairs
+  if (jj + 2 < CT_R) ct_load_row<EDGE>(v, ii, jj + 2, i, j0 + jj + 2, m, win[(t + 4) % 5]);
+  constexpr int RSLOT = (t + 2) % 5;
+  double qq[2];
+  if ((t & 1) == 0) {                                  // jj even (jb even): classes 0 (i even), 1 (i odd)
+    qq[0] = ct_tap_sum<0, 0, RSLOT>(a.so, win);
+    qq[1] = ct_tap_sum<1, 1, RSLOT>(a.so, win);
+  } else {
+    qq[0] = ct_tap_sum<2, 0, RSLOT>(a.so, win);
+    qq[1] = ct_tap_sum<3, 1, RSLOT>(a.so, win);
+  }
+  const int j = j0 + jj;
+  if (!lok || j < 0 || j >= m) return;
+  constexpr int C0 = (t & 1) * 2;
+  const int base = ii + CT_R * jj;
+  const double2 rr = *reinterpret_cast<const double2*>(RS + base);
+  double ro[2] = {rr.x, rr.y};
+  double outd[2];
+  double dd[2] = {0.0, 0.0};
+  if (MODE == 0 && dout) {
+    const double2 t2 = *reinterpret_cast<const double2*>(din + base);
+    dd[0] = t2.x; dd[1] = t2.y;
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int ik = i + k;
+    const bool dir = ik == 0 || j == 0 || ik == m - 1 || j == m - 1;
+    if (EDGE && dir) qq[k] = fma(1.0, v[base + k], 0.0);   // identity row (unmasked centre)
+    const double di = dir ? 1.0 : a.so.dcls[C0 + k];
+    ro[k] = ro[k] - qq[k];
+    if (MODE == 1) outd[k] = di * ro[k] * a.itheta;
+    else outd[k] = c1 * dd[k] + c2 * (di * ro[k]);
+  }
+  // the odd column of the last pair may lie outside the domain (never read by valid rows)
+  *reinterpret_cast<double2*>(RS + base) = make_double2(ro[0], ro[1]);
+  if (MODE == 1 || dout) *reinterpret_cast<double2*>(dout + base) = make_double2(outd[0], outd[1]);
+}
+
+template <int S, int MODE, bool EDGE, int... Ts>
+__device__ __forceinline__ void ct_rows(const ChebTileArgs& a, int i0, int j0, double* RS, const double* v,
+                                        const double* din, double* dout, double c1, double c2, int jb, int ii,
+                                        int i, bool lok, double (&win)[5][6], std::integer_sequence<int, Ts...>) {
+  (ct_row_t<S, MODE, EDGE, Ts>(a, i0, j0, RS, v, din, dout, c1, c2, jb, ii, i, lok, win), ...);
+}
+
+// One Chebyshev update over the square [S, CT_R - S)^2 of the window.  MODE 0: r <- r - A v,
+// dout <- c1 din + c2 D^-1 r (dout null: r only); MODE 1 (post-smoothing start, v = x):
+// r <- b - A x (r holds b), dout <- D^-1 r / theta.
+template <int S, int MODE, bool EDGE>
+__device__ __forceinline__ void ct_step(const ChebTileArgs& a, int i0, int j0, double* RS, const double* v,
+                                        const double* din, double* dout, double c1, double c2) {
+  constexpr int W = CT_R - 2 * S;
+  const int m = a.so.m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int jb = S + CT_STRIP * warp;                 // first row of this warp's strip (even)
+  if (jb >= CT_R - S) return;
+  const bool lok = lane < W / 2;
+  const int ii = S + 2 * (lok ? lane : 0);            // even column of the pair
+  const int i = i0 + ii;
+  double win[5][6];
+  // rows jb-2 .. jb+1 into slots 0..3 (slot of row jj = (jj - jb + 2) % 5)
+#pragma unroll
+  for (int r = 0; r < 4; ++r) ct_load_row<EDGE>(v, ii, jb - 2 + r, i, j0 + jb - 2 + r, m, win[r]);
+  ct_rows<S, MODE, EDGE>(a, i0, j0, RS, v, din, dout, c1, c2, jb, ii, i, lok, win,
+                         std::make_integer_sequence<int, CT_STRIP>{});
+}
+
+template <int POST>
+__global__ void __launch_bounds__(CT_THREADS, 2) k_cheb_tile(ChebTileArgs a) {
+  if (is_done(a.done)) return;
+  extern __shared__ __align__(16) double ct_sm[];
+  double* D0 = ct_sm;
+  double* D1 = ct_sm + CT_ARR;     // POST: holds x until the second step overwrites it
+  double* RS = ct_sm + 2 * CT_ARR;
+  const int m = a.so.m;
+  const int comp = blockIdx.y;
+  const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
+  const int i0 = tx * CT_T - CT_H, j0 = ty * CT_T - CT_H;
+  const int64_t off = (int64_t)comp * a.nq;
+  const double* b = a.b + off;
+  const int tid = threadIdx.x;
+  const bool edge = i0 < 3 || j0 < 3 || i0 + CT_R > m - 3 || j0 + CT_R > m - 3;   // block-uniform
+  // ---- stage the window (coalesced along i); outside the domain everything is 0.  All of a
+  // thread's global loads are issued before any is used (one memory latency per CTA, not 19).
+  constexpr int NST = (CT_ARR + CT_THREADS - 1) / CT_THREADS;
+  double lb[NST], lx[NST];
+#pragma unroll
+  for (int k = 0; k < NST; ++k) {
+    const int idx = tid + k * CT_THREADS;
+    const int ii = idx % CT_R, jj = idx / CT_R;
+    const int i = i0 + ii, j = j0 + jj;
+    const bool in = idx < CT_ARR && i >= 0 && j >= 0 && i < m && j < m;
+    const int node = in ? i + m * j : 0;
+    lb[k] = in ? __ldg(b + node) : 0.0;
+    if (POST) lx[k] = in ? __ldg(a.x_in + off + node) : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < NST; ++k) {
+    const int idx = tid + k * CT_THREADS;
+    if (idx >= CT_ARR) break;
+    const int ii = idx % CT_R, jj = idx / CT_R;
+    const int i = i0 + ii, j = j0 + jj;
+    const double bv = lb[k];
+    RS[idx] = bv;
+    if (POST) {
+      D1[idx] = lx[k];
+      D0[idx] = 0.0;
+    } else {
+      const bool in = i >= 0 && j >= 0 && i < m && j < m;
+      double di = 1.0;
+      if (!(i == 0 || j == 0 || i == m - 1 || j == m - 1)) di = a.so.dcls[(i & 1) + 2 * (j & 1)];
+      D0[idx] = in ? di * bv * a.itheta : 0.0;   // k_cheb_init
+      D1[idx] = 0.0;
+    }
+  }
+  __syncthreads();
+  // x lives in the output array between steps (T region only; L2-resident re-reads)
+  constexpr int NTP = (CT_T * CT_T + CT_THREADS - 1) / CT_THREADS;
+  auto tile_pos = [&](int k, int& w, int64_t& g) {
+    const int o = tid + k * CT_THREADS;
+    const int ii = CT_H + o % CT_T, jj = CT_H + o / CT_T;
+    const int i = i0 + ii, j = j0 + jj;
+    w = ii + CT_R * jj;
+    g = off + i + (int64_t)m * j;
+    return o < CT_T * CT_T && i < m && j < m;
+  };
+  auto tile_pass = [&](auto&& f) {
+#pragma unroll
+    for (int k = 0; k < NTP; ++k) {
+      int w; int64_t g;
+      if (tile_pos(k, w, g)) f(w, g);
+    }
+  };
+  // x_out[T] += D[T] with all loads first
+  auto tile_accum = [&](const double* D) {
+    double xv[NTP];
+#pragma unroll
+    for (int k = 0; k < NTP; ++k) {
+      int w; int64_t g;
+      xv[k] = tile_pos(k, w, g) ? a.x_out[g] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < NTP; ++k) {
+      int w; int64_t g;
+      if (tile_pos(k, w, g)) a.x_out[g] = xv[k] + D[w];
+    }
+  };
+#define CT_STEP(S_, MODE_, RS_, V_, DIN_, DOUT_, C1_, C2_)                              \
+  do {                                                                                  \
+    if (edge) ct_step<S_, MODE_, true>(a, i0, j0, RS_, V_, DIN_, DOUT_, C1_, C2_);      \
+    else ct_step<S_, MODE_, false>(a, i0, j0, RS_, V_, DIN_, DOUT_, C1_, C2_);          \
+  } while (0)
+  if (!POST) {
+    CT_STEP(2, 0, RS, D0, D0, D1, a.c1[0], a.c2[0]);
+    __syncthreads();
+    tile_pass([&](int w, int64_t g) { a.x_out[g] = (0.0 + D0[w]) + D1[w]; });   // x2 = (0 + d0) + d1
+    __syncthreads();
+    CT_STEP(4, 0, RS, D1, D1, D0, a.c1[1], a.c2[1]);
+    __syncthreads();
+    tile_accum(D0);                                                              // x3 = x2 + d2
+    CT_STEP(6, 0, RS, D0, D0, (double*)nullptr, 0.0, 0.0);
+    __syncthreads();
+    tile_pass([&](int w, int64_t g) { a.r_out[g] = RS[w]; });
+  } else {
+    CT_STEP(2, 1, RS, D1, (const double*)nullptr, D0, 0.0, 0.0);   // r0 = b - A x, d0 = D^-1 r0 / theta
+    __syncthreads();
+    tile_pass([&](int w, int64_t g) { a.x_out[g] = D1[w] + D0[w]; });   // x += d0
+    __syncthreads();                                                     // x (in D1) no longer read
+    CT_STEP(4, 0, RS, D0, D0, D1, a.c1[0], a.c2[0]);
+    __syncthreads();
+    tile_accum(D1);                                                      // x += d1
+    CT_STEP(6, 0, RS, D1, D1, D0, a.c1[1], a.c2[1]);                   // d2 (deferred)
+    __syncthreads();
+    tile_pass([&](int w, int64_t g) { a.d_out[g] = D0[w]; });
+  }
+#undef CT_STEP
+}
+
 // r = b - A x ; d = D^{-1} r / theta  (start of post-smoothing), NC components
 template <int NC>
 __global__ void __launch_bounds__(BS, SPMV_MINB) k_post_residual(Sell A, const double* dinv, int nq, const double* b,
-                                                      const double* x, double* r, double* d, double theta,
+                                                      const double* x, double* r, double* d, double itheta,
                                                       const double* done) {
   if (is_done(done)) return;
   const int lane = threadIdx.x & 31;
@@ -231,7 +481,7 @@ __global__ void __launch_bounds__(BS, SPMV_MINB) k_post_residual(Sell A, const d
       const int64_t idx = (int64_t)c * nq + row;
       const double rr = b[idx] - q[c];
       r[idx] = rr;
-      d[idx] = di * rr / theta;
+      d[idx] = di * rr * itheta;
     }
   }
 }
@@ -243,7 +493,7 @@ struct SkChebArgs {
   const double* v;                         // vector the operator is applied to (d_in, or x if post)
   const double* d_in; const double* r_in; const double* x_in;
   double* x_out; double* r_out; double* d_out;
-  double c1, c2, theta; int post;
+  double c1, c2, itheta; int post;
   const double* done;
 };
 __global__ void __launch_bounds__(BS) k_cheb_sk(SkChebArgs a) {
@@ -258,7 +508,7 @@ __global__ void __launch_bounds__(BS) k_cheb_sk(SkChebArgs a) {
     const double ro = a.r_in[p] - q;
     if (a.post) {
       a.r_out[p] = ro;
-      a.d_out[p] = di * ro / a.theta;
+      a.d_out[p] = di * ro * a.itheta;
     } else {
       const double dd = a.d_in[p];
       a.x_out[p] = (a.x_in ? a.x_in[p] : 0.0) + dd;
@@ -269,20 +519,20 @@ __global__ void __launch_bounds__(BS) k_cheb_sk(SkChebArgs a) {
 }
 
 // d = D^{-1} b / theta (start of pre-smoothing from x = 0), NC components
-__global__ void k_cheb_init(const double* dinv, int nq, int nc, const double* b, double* d, double theta,
+__global__ void k_cheb_init(const double* dinv, int nq, int nc, const double* b, double* d, double itheta,
                             const double* done) {
   if (is_done(done)) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)nc * nq;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int row = (int)(i % nq);
-    d[i] = dinv[row] * b[i] / theta;
+    d[i] = dinv[row] * b[i] * itheta;
   }
 }
 
 // Q1 (pressure) transfers: nested bilinear interpolation, no boundary rows (no pressure BC)
 // b_c = P^T r_f and d0_c = D_c^{-1} b_c / theta
 __global__ void k_restrict_q1(int mf, int mc, const double* rf, double* bc, double* d0c, const double* dinvc,
-                              double theta, const double* done) {
+                              double itheta, const double* done) {
   if (is_done(done)) return;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)mc * mc;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -301,7 +551,7 @@ __global__ void k_restrict_q1(int mf, int mc, const double* rf, double* bc, doub
       s = fma(wy, tt, s);
     }
     bc[t] = s;
-    d0c[t] = dinvc[t] * s / theta;
+    d0c[t] = dinvc[t] * s * itheta;
   }
 }
 // x_f += P (x_c + d_c)
@@ -346,7 +596,7 @@ __device__ __forceinline__ int restrict_taps(int I, int* off, double* w) {
 
 // b_c = Z_c P^T r_f (both components) and d0_c = D_c^{-1} b_c / theta
 __global__ void k_restrict(int mf, int mc, int nqf, int nqc, const double* rf, double* bc, double* d0c,
-                           const double* dinvc, double theta, const double* done) {
+                           const double* dinvc, double itheta, const double* done) {
   if (is_done(done)) return;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)nqc;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -371,7 +621,7 @@ __global__ void k_restrict(int mf, int mc, int nqf, int nqc, const double* rf, d
     }
     bc[t] = s0; bc[nqc + t] = s1;
     const double di = dinvc[t];
-    d0c[t] = di * s0 / theta; d0c[nqc + t] = di * s1 / theta;
+    d0c[t] = di * s0 * itheta; d0c[nqc + t] = di * s1 * itheta;
   }
 }
 
@@ -957,7 +1207,7 @@ __device__ void tail_cheb_step(const TailLevel& L, const double* d_in, const dou
   }
 }
 
-__global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(const TailLevel* lvs, int nlev, int degree, double theta,
+__global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(const TailLevel* lvs, int nlev, int degree, double itheta,
                                                               const double* done) {
   if (is_done(done)) return;
   const int tid = threadIdx.x;
@@ -994,7 +1244,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(const TailLevel* l
       }
       Cv.b[t] = s0; Cv.b[Cv.nq + t] = s1;
       const double di = Cv.dinv[t];
-      Cv.d0[t] = di * s0 / theta; Cv.d0[Cv.nq + t] = di * s1 / theta;
+      Cv.d0[t] = di * s0 * itheta; Cv.d0[Cv.nq + t] = di * s1 * itheta;
     }
     __syncthreads();
   }
@@ -1047,7 +1297,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(const TailLevel* l
         const double di = L.dinv[row];
         const double r0 = L.b[row] - q0, r1 = L.b[L.nq + row] - q1;
         L.r[row] = r0; L.r[L.nq + row] = r1;
-        L.d0[row] = di * r0 / theta; L.d0[L.nq + row] = di * r1 / theta;
+        L.d0[row] = di * r0 * itheta; L.d0[L.nq + row] = di * r1 * itheta;
       }
     }
     __syncthreads();
@@ -1128,6 +1378,12 @@ etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, do
     Level& lv = H.lv[l];
     if (!P.oseen && P.storage == 0 && lv.g.n > TAIL_N && lv.A.stval && l + 1 < H.lv.size()) {
       ETQ_TRY(build_stencil_level(lv.g, lv.A, &lv.so, &lv.Afr, P.stream));
+      // D^-1 per stencil class, read at interior reference nodes (the tiled smoother's diagonal)
+      for (int c = 0; c < 4; ++c) {
+        const int64_t node = (int64_t)(lv.so.lo + (c & 1)) + (int64_t)lv.g.m * (lv.so.lo + (c >> 1));
+        ETQ_CHECK(cudaMemcpyAsync(&lv.so.dcls[c], lv.dinv + node, sizeof(double), cudaMemcpyDeviceToHost, P.stream));
+      }
+      ETQ_CHECK(cudaStreamSynchronize(P.stream));
       lv.st_on = true;
     }
   }
@@ -1240,9 +1496,36 @@ static void launch_cheb_st(const Level& lv, const ChebArgs& c, bool post, double
   ChebStArgs a;
   a.so = lv.so; a.F = lv.Afr; a.dinv = c.dinv; a.nq = c.nq;
   a.d_in = c.d_in; a.r_in = c.r_in; a.x_in = c.x_in; a.x_out = c.x_out; a.r_out = c.r_out; a.d_out = c.d_out;
-  a.c1 = c.c1; a.c2 = c.c2; a.post = post ? 1 : 0; a.theta = theta; a.done = c.done;
+  a.c1 = c.c1; a.c2 = c.c2; a.post = post ? 1 : 0; a.itheta = 1.0 / theta; a.done = c.done;
   const int64_t warps = lv.so.nseg + lv.Afr.nslices;
   k_cheb_step_st<<<grid_for(warps * 32, BS, 4096), BS, 0, st>>>(a);
+}
+
+// Temporally blocked smoothing pass on an interior-stencil level (degree 3, real interval).
+static void launch_cheb_tile(const Level& lv, bool post, const double* b, const double* x_in, double* x_out,
+                             double* r_out, double* d_out, const std::vector<double>& c1,
+                             const std::vector<double>& c2, double theta, const double* done, cudaStream_t st) {
+  static bool smem_set = false;
+  if (!smem_set) {
+    cudaFuncSetAttribute(k_cheb_tile<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM);
+    cudaFuncSetAttribute(k_cheb_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM);
+    smem_set = true;
+  }
+  ChebTileArgs a;
+  a.so = lv.so; a.nq = lv.g.nq;
+  a.tiles_x = (lv.g.m + CT_T - 1) / CT_T;
+  a.b = b; a.x_in = x_in; a.x_out = x_out; a.r_out = r_out; a.d_out = d_out;
+  a.itheta = 1.0 / theta;
+  for (int k = 0; k < 3; ++k) { a.c1[k] = c1[k]; a.c2[k] = c2[k]; }
+  a.done = done;
+  dim3 grid(a.tiles_x * a.tiles_x, 2);
+  if (post) k_cheb_tile<1><<<grid, CT_THREADS, CT_SMEM, st>>>(a);
+  else k_cheb_tile<0><<<grid, CT_THREADS, CT_SMEM, st>>>(a);
+}
+
+static bool tile_ok(const Hierarchy& H, const Level& lv) {
+  return lv.st_on && H.degree == 3 && lv.bim == 0.0 && H.ncomp == 2 && g_cheb_tile_enabled &&
+         lv.g.n >= g_cheb_tile_min_n;
 }
 
 // One V-cycle (readings R9/R9'/R13) on H.ncomp components: z = V(r); optional partial
@@ -1254,7 +1537,7 @@ static void launch_cheb_sk(const Hierarchy& H, const Level& lv, const ChebArgs& 
   a.v = post ? c.x_in : c.d_in;
   a.d_in = c.d_in; a.r_in = c.r_in; a.x_in = c.x_in;
   a.x_out = c.x_out; a.r_out = c.r_out; a.d_out = c.d_out;
-  a.c1 = c.c1; a.c2 = c.c2; a.theta = theta; a.post = post; a.done = c.done;
+  a.c1 = c.c1; a.c2 = c.c2; a.itheta = 1.0 / theta; a.post = post; a.done = c.done;
   k_cheb_sk<<<grid_for((int64_t)lv.g.nk, BS, 8 * 148), BS, 0, st>>>(a);
 }
 
@@ -1286,12 +1569,16 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     cheb_coeffs(H.lo, H.hi, lv.bim, H.degree, c1, c2);
     const double* b = (l == 0) ? r_u : lv.b;
     bvec[l] = b;
-    if (l == 0) {
-      k_cheb_init<<<grid_for((int64_t)nc * nq, BS, 4096), BS, 0, st>>>(lv.dinv, nq, nc, b, lv.d0, theta, done); etq_count_launch();
+    const bool tiled = tile_ok(H, lv);
+    if (tiled) {
+      launch_cheb_tile(lv, false, b, nullptr, lv.x, lv.r, nullptr, c1, c2, theta, done, st); etq_count_launch();
+    }
+    if (l == 0 && !tiled) {
+      k_cheb_init<<<grid_for((int64_t)nc * nq, BS, 4096), BS, 0, st>>>(lv.dinv, nq, nc, b, lv.d0, 1.0 / theta, done); etq_count_launch();
     }
     const int gs = grid_for(lv.A.nslices * 32, BS, 4096);
     double* din = lv.d0; double* dout = lv.d1;
-    for (int k = 0; k < H.degree; ++k) {
+    for (int k = 0; k < (tiled ? 0 : H.degree); ++k) {
       ChebArgs a;
       a.A = lv.A; a.dinv = lv.dinv; a.nq = nq;
       a.d_in = din; a.r_in = (k == 0) ? b : lv.r; a.x_in = (k == 0) ? nullptr : lv.x;
@@ -1307,16 +1594,16 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     const Level& cv = H.lv[l + 1];
     if (H.kind == 0) {
       k_restrict<<<grid_for(cv.g.nq, BS, 4096), BS, 0, st>>>(lv.g.m, cv.g.m, nq, cv.g.nq, lv.r, cv.b, cv.d0,
-                                                            cv.dinv, theta, done);
+                                                            cv.dinv, 1.0 / theta, done);
     } else {
       k_restrict_q1<<<grid_for(cv.g.nk, BS, 4096), BS, 0, st>>>(lv.g.n + 1, cv.g.n + 1, lv.r, cv.b, cv.d0,
-                                                               cv.dinv, theta, done);
+                                                               cv.dinv, 1.0 / theta, done);
     }
     etq_count_launch();
   }
   // ---- coarse (or the fused coarse-level tail, which leaves a complete x on its first level)
   if (use_tail) {
-    k_vcycle_tail<<<1, TAIL_THREADS, 0, st>>>(H.tail, L - H.tail_start, H.degree, theta, done); etq_count_launch();
+    k_vcycle_tail<<<1, TAIL_THREADS, 0, st>>>(H.tail, L - H.tail_start, H.degree, 1.0 / theta, done); etq_count_launch();
     pend[Ld - 1] = nullptr;
   } else {
     const Level& C = H.lv[L - 1];
@@ -1324,18 +1611,27 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     pend[L - 1] = nullptr;
   }
   // ---- up
+  std::vector<const double*> xres(L, nullptr);   // where each level's smoothed x ends up
+  for (int l = 0; l < L; ++l) xres[l] = H.lv[l].x;
   for (int l = Ld - 2; l >= 0; --l) {
     const Level& lv = H.lv[l];
     const Level& cv = H.lv[l + 1];
     const int nq = lv.nrows;
     cheb_coeffs(H.lo, H.hi, lv.bim, H.degree, c1, c2);
     if (H.kind == 0) {
-      k_prolong<<<grid_for(nq, BS, 4096), BS, 0, st>>>(lv.g.m, cv.g.m, nq, cv.g.nq, cv.x, pend[l + 1], lv.x, done);
+      k_prolong<<<grid_for(nq, BS, 4096), BS, 0, st>>>(lv.g.m, cv.g.m, nq, cv.g.nq, xres[l + 1], pend[l + 1], lv.x, done);
     } else {
-      k_prolong_q1<<<grid_for(nq, BS, 4096), BS, 0, st>>>(lv.g.n + 1, cv.g.n + 1, cv.x, pend[l + 1], lv.x, done);
+      k_prolong_q1<<<grid_for(nq, BS, 4096), BS, 0, st>>>(lv.g.n + 1, cv.g.n + 1, xres[l + 1], pend[l + 1], lv.x, done);
     }
     etq_count_launch();
     const int gs = grid_for(lv.A.nslices * 32, BS, 4096);
+    if (tile_ok(H, lv)) {
+      // residual + two steps in one pass; x goes to d1 (tiles read x halos), deferred d2 to d0
+      launch_cheb_tile(lv, true, bvec[l], lv.x, lv.d1, nullptr, lv.d0, c1, c2, theta, done, st); etq_count_launch();
+      xres[l] = lv.d1;
+      pend[l] = lv.d0;
+      continue;
+    }
     if (lv.st_on) {
       ChebArgs a{};
       a.A = lv.A; a.dinv = lv.dinv; a.nq = nq; a.x_in = lv.x; a.r_in = bvec[l]; a.r_out = lv.r; a.d_out = lv.d0;
@@ -1346,9 +1642,9 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       a.x_in = lv.x; a.r_in = bvec[l]; a.r_out = lv.r; a.d_out = lv.d0; a.done = done;
       launch_cheb_sk(H, lv, a, 1, theta, st);
     } else if (nc == 2) {
-      k_post_residual<2><<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, theta, done);
+      k_post_residual<2><<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, 1.0 / theta, done);
     } else {
-      k_post_residual<1><<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, theta, done);
+      k_post_residual<1><<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, 1.0 / theta, done);
     }
     etq_count_launch();
     double* din = lv.d0; double* dout = lv.d1;
@@ -1369,7 +1665,7 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
   }
   const Level& F = H.lv[0];
   const int64_t nv = (int64_t)nc * F.nrows;
-  k_final_add<<<grid_for(nv, BS, RED_BLOCKS), BS, 0, st>>>(F.x, pend[0], z_u, nv, dot_with,
+  k_final_add<<<grid_for(nv, BS, RED_BLOCKS), BS, 0, st>>>(xres[0], pend[0], z_u, nv, dot_with,
                                                           site ? *site : dummy, slot, dot_out, done); etq_count_launch();
   return ETQ_OK;
 }

@@ -80,6 +80,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "etq_apply_saddle_f32": ([P, I32, VP, VP], I32),
         "etq_apply_vcycle_f32": ([P, VP, VP], I32),
         "etq_time_kernel": ([P, I32, I32, C.POINTER(D), C.POINTER(D)], I32),
+        "etq_set_option": ([I32, I32], I32),
         "etq_status_string": ([I32], C.c_char_p),
         "etq_destroy": ([P], None),
     }
@@ -122,6 +123,11 @@ def est_minres(delta, gamma):
     _check(lib().etq_est_minres(C.c_void_p(d.ctypes.data), C.c_void_p(g.ctypes.data), len(d), C.byref(out)),
            "etq_est_minres")
     return out.value
+
+
+def set_option(option: int, value: int):
+    """Process-wide implementation switch (etq_set_option); 0 = temporally blocked smoothing."""
+    _check(lib().etq_set_option(option, value), "etq_set_option")
 
 
 def status_string(s: int) -> str:

@@ -16,7 +16,9 @@ def test_library_exports_every_header_symbol():
 
 
 def test_binding_mirrors_header_names():
-    methods = set(dir(etq.Problem)) | {"assemble", "status_string", "destroy", "sizes", "launch_count", "est_minres"}
+    methods = set(dir(etq.Problem)) | {"assemble", "status_string", "destroy", "sizes", "launch_count", "est_minres",
+                                        "set_option"}
+    assert callable(etq.set_option)
     for n in etq.header_functions():
         short = n[len("etq_"):]
         assert short in methods or short == "status_string", short
