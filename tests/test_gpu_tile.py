@@ -1,0 +1,57 @@
+"""The temporally blocked Chebyshev smoother (one kernel per pre/post-smoothing pass on the
+Stokes interior-stencil levels) against the one-kernel-per-step path: bitwise-identical V-cycles
+(same per-row arithmetic and summation order, reading R2's eliminated Dirichlet columns) and the
+oracle V-cycle within the apply tolerance."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import mg  # noqa: E402
+from paper_2303_10233_b200 import etq  # noqa: E402
+import synth  # noqa: E402
+
+
+def _vcycle(n, tile, bc=0, min_n=32):
+    etq.set_option(0, 1 if tile else 0)
+    etq.set_option(1, min_n)
+    try:
+        P = etq.Problem(n, bc=bc)
+        P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.005))
+        r = torch.as_tensor(synth.random_vector(P.n_u, seed=21), device="cuda")
+        z = torch.zeros(P.n_u, dtype=torch.float64, device="cuda")
+        P.apply_vcycle(etq.PC_P2_GMG, r, z)
+        torch.cuda.synchronize()
+        out = z.cpu().numpy()
+        P.close()
+        return out
+    finally:
+        etq.set_option(0, 1)
+        etq.set_option(1, 64)
+
+
+@pytest.mark.parametrize("n,bc", [(32, 0), (64, 1), (128, 0), (512, 0)])
+def test_tiled_smoother_bitwise_equal(n, bc):
+    a = _vcycle(n, True, bc)
+    b = _vcycle(n, False, bc)
+    np.testing.assert_array_equal(a, b)
+
+
+def test_tiled_vcycle_matches_oracle():
+    n = 64
+    z = _vcycle(n, True)
+    h = mg.Hierarchy(n)
+    r = synth.random_vector(2 * (2 * n + 1) ** 2, seed=21)
+    ref = h.apply_velocity(r)
+    assert np.abs(z - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_set_option_rejects_unknown():
+    with pytest.raises(etq.EtqError):
+        etq.set_option(7, 1)
+    with pytest.raises(etq.EtqError):
+        etq.set_option(1, 0)
