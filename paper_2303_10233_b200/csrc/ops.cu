@@ -1509,6 +1509,8 @@ static void launch_cheb_tile(const Level& lv, bool post, const double* b, const 
   if (!smem_set) {
     cudaFuncSetAttribute(k_cheb_tile<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM);
     cudaFuncSetAttribute(k_cheb_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM);
+    cudaFuncSetAttribute(k_cheb_tile<0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_cheb_tile<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     smem_set = true;
   }
   ChebTileArgs a;
