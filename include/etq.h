@@ -220,7 +220,9 @@ etq_status etq_launch_count(int64_t* count);
  *        4 = one P2 preconditioner apply (velocity and pressure branches concurrently);
  *        5 = fp32 fused saddle SpMV; 6 = fp32 V-cycle (P2 set up);
  *        7 = one exact M_Q solve through S_k (P3/P1_ITER set up; replays of one captured graph);
- *        8 = one Q1-GMG V-cycle on S_k; 9 = one P3 preconditioner apply (graph replays).
+ *        8 = one Q1-GMG V-cycle on S_k; 9 = one P3 preconditioner apply (graph replays);
+ *        10 = one Chebyshev-SGS step on the pressure vectors (the SGS tile kernel, P2 set up);
+ *        11 / 12 = the finest level's temporally blocked pre- / post-smoothing pass (P2 set up).
  * Host outputs: *ms = average device time per launch, *bytes = algorithmic bytes per launch. */
 etq_status etq_time_kernel(etq_problem* p, int32_t which, int32_t reps, double* ms, double* bytes);
 

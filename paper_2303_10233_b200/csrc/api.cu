@@ -566,9 +566,10 @@ etq_status etq_launch_count(int64_t* count) {
 etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* ms, double* bytes) {
   if (!h || reps < 1 || !ms || !bytes) return ETQ_EINVAL;
   Problem& P = h->P;
-  if (which < 0 || which > 9) return ETQ_EINVAL;
+  if (which < 0 || which > 12) return ETQ_EINVAL;
   if ((which >= 2 && which <= 6 && which != 5) && !P.p2_ready) return ETQ_ENOTSETUP;
-  if (which >= 7 && !P.mx.ready) return ETQ_ENOTSETUP;
+  if (which >= 10 && !P.p2_ready) return ETQ_ENOTSETUP;
+  if (which >= 7 && which <= 9 && !P.mx.ready) return ETQ_ENOTSETUP;
   if (which >= 5) {
     ETQ_TRY(ensure_f32(P));
     if (!P.tkf) {
@@ -599,6 +600,9 @@ etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* 
       case 7: ETQ_TRY(exact_mass_apply(P, a + P.n_u, b + P.n_u, nullptr, 0, nullptr, nullptr, nullptr, st)); break;
       case 8: ETQ_TRY(vcycle_apply_ex(P, P.mx.sH, a + P.n_u, b + P.n_u, nullptr, 0, nullptr, nullptr, nullptr, st)); break;
       case 9: ETQ_TRY(precond_apply_ex(P, ETQ_PC_P3, a, c, nullptr, nullptr, nullptr, nullptr, st)); break;
+      case 10: sgs_step_bench(P, a + P.n_u, b + P.n_u, c + P.n_u, (k & 1) ? b + P.n_u : c + P.n_u, st); break;
+      case 11: ETQ_TRY(cheb_tile_bench(P, false, a, nullptr, b, c, st)); break;
+      case 12: ETQ_TRY(cheb_tile_bench(P, true, a, b, nullptr, nullptr, st)); break;
     }
     return ETQ_OK;
   };
@@ -635,6 +639,9 @@ etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* 
     case 2: case 4: *bytes = vcycle_bytes(P.mg); break;
     case 5: *bytes = 8.0 * nnz_all + 4.0 * P.Lv.nslices * SELL_C + 8.0 * P.N; break;
     case 6: *bytes = vcycle_bytes_f32(P.mg); break;
+    case 10: *bytes = 32.0 * (double)P.n_p; break;            // r, y, yp in; out
+    case 11: *bytes = 48.0 * (double)P.g.nq; break;           // b in; x, r out (2 components)
+    case 12: *bytes = 64.0 * (double)P.g.nq; break;           // x, b in; x, d out (2 components)
     default: *bytes = 0.0;
   }
   return ETQ_OK;

@@ -308,6 +308,10 @@ int64_t etq_launch_total();
 void cheb_step_level0(const Problem& P, const double* d_in, double* d_out, cudaStream_t st);
 double vcycle_bytes(const Hierarchy& H);
 double cheb_step_bytes(const Level& L);
+void sgs_step_bench(const Problem& P, const double* r, const double* y, const double* yp, double* out,
+                    cudaStream_t st);
+etq_status cheb_tile_bench(const Problem& P, bool post, const double* in_b, const double* in_x, double* o1,
+                           double* o2, cudaStream_t st);
 
 // oseen.cu
 etq_status oseen_setup(Problem& P, etq_pc_kind kind);

@@ -1762,6 +1762,32 @@ etq_status mass_pc_apply_ex(const Problem& P, const double* r_p, double* z_p, co
   return ETQ_OK;
 }
 
+// ---- bench helpers (etq_time_kernel 10-12)
+// one Chebyshev-SGS step (mode 1: the semi-iteration combination) on the pressure vectors
+void sgs_step_bench(const Problem& P, const double* r, const double* y, const double* yp, double* out,
+                    cudaStream_t st) {
+  SgsTileArgs a{};
+  a.g = mass_geo(P.g); a.r = r; a.kproj = nullptr; a.inv_kk = 0.0;
+  a.y = y; a.yp = yp; a.out = out; a.mode = 1; a.omega = 1.2; a.gam = 1.1;
+  a.site = RedSite{}; a.slot = 0; a.kout = nullptr; a.done = nullptr;
+  launch_sgs_tile(a, st);
+}
+
+// the finest level's temporally blocked pre- (post = false) or post-smoothing pass
+etq_status cheb_tile_bench(const Problem& P, bool post, const double* in_b, const double* in_x, double* o1,
+                           double* o2, cudaStream_t st) {
+  const Hierarchy& H = P.mg;
+  if (!H.built || !tile_ok(H, H.lv[0])) return ETQ_ENOTSETUP;
+  std::vector<double> c1, c2;
+  cheb_coeffs(H.lo, H.hi, H.lv[0].bim, H.degree, c1, c2);
+  const double theta = 0.5 * (H.hi + H.lo);
+  // post: outputs into the level's own scratch (x -> d1, deferred d -> d0) exactly as in the V-cycle
+  if (post) launch_cheb_tile(H.lv[0], true, in_b, in_x, H.lv[0].d1, nullptr, H.lv[0].d0, c1, c2, theta, nullptr, st);
+  else launch_cheb_tile(H.lv[0], false, in_b, nullptr, o1, o2, nullptr, c1, c2, theta, nullptr, st);
+  etq_count_launch();
+  return ETQ_OK;
+}
+
 etq_status mass_pc_alloc(Problem& P) {
   const int64_t np = P.n_p;
   PcMass& M = P.pm;
@@ -1868,15 +1894,22 @@ double vcycle_bytes(const Hierarchy& H) {
     const Level& lv = H.lv[l];
     const double nq = lv.g.nq, mat = 12.0 * lv.A.nnz - 4.0 * lv.A.nnz_implicit - 8.0 * lv.A.nnz_implicit_vals + 4.0 * lv.A.nslices * SELL_C + 8.0 * nq;
     const double v = 8.0 * 2 * nq;   // one two-component vector
-    if (l == 0) b += 8.0 * nq + 2 * v;                       // init: dinv, b -> d
-    for (int k = 0; k < deg; ++k)                            // pre-smoothing steps
-      b += mat + v * ((k == 0 ? 2 : 3) + (k == deg - 1 ? 2 : 3));
+    const bool tiled = tile_ok(H, lv);
+    if (tiled) b += 3 * v;                                   // fused pre pass: b -> x, r (matrix-free)
+    else {
+      if (l == 0) b += 8.0 * nq + 2 * v;                     // init: dinv, b -> d
+      for (int k = 0; k < deg; ++k)                          // pre-smoothing steps
+        b += mat + v * ((k == 0 ? 2 : 3) + (k == deg - 1 ? 2 : 3));
+    }
     const double nqc = H.lv[l + 1].g.nq, vc = 8.0 * 2 * nqc;
     b += v + 2 * vc + 8.0 * nqc;                             // restriction: r -> b_c, d0_c
     b += 2 * vc + 2 * v;                                     // prolongation: x_c + d_c -> x += P e
-    b += mat + 2 * v + 2 * v;                                // post residual: b, x -> r, d
-    for (int k = 0; k < deg - 1; ++k)                        // post steps
-      b += mat + v * (3 + (k == deg - 2 ? 2 : 3));
+    if (tiled) b += 4 * v;                                   // fused post pass: x, b -> x, d
+    else {
+      b += mat + 2 * v + 2 * v;                              // post residual: b, x -> r, d
+      for (int k = 0; k < deg - 1; ++k)                      // post steps
+        b += mat + v * (3 + (k == deg - 2 ? 2 : 3));
+    }
     if (l == 0) b += 2 * v + v;                              // final: x + d -> z
   }
   const Level& C = H.lv[L - 1];
