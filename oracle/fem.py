@@ -290,7 +290,7 @@ class SaddleSystem:
 
 
 def assemble_system(n: int, bc: str = "lid", nu: float | None = None, wind=None,
-                    f_nodal=None) -> SaddleSystem:
+                    f_nodal=None, convection_matrix=None) -> SaddleSystem:
     """Assemble the Stokes (nu=None) or Oseen system and its right-hand side.
 
     Stokes velocity block A = I_2 (x) L; Oseen F = I_2 (x) (nu L + N)
@@ -298,13 +298,15 @@ def assemble_system(n: int, bc: str = "lid", nu: float | None = None, wind=None,
     values into f and g, then zero boundary rows/columns of A (identity
     diagonal, f = u_bc there) and zero the boundary columns of B.
     Body force (reading R10 / O5): f = M_v f_nodal, rows on the boundary set to 0.
+    convection_matrix: a precomputed scalar N (e.g. a Picard wind, oracle.picard) instead of wind.
     """
     g = Grid(n)
     s = SaddleSystem()
     s.g = g
     L = laplacian(g)
     if nu is not None:
-        Nc = convection(g, wind if wind is not None else cavity_wind)
+        Nc = convection_matrix if convection_matrix is not None else \
+            convection(g, wind if wind is not None else cavity_wind)
         Ls = (nu * L + Nc).tocsr()
     else:
         Ls = L
