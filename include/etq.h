@@ -52,7 +52,10 @@ typedef struct { int32_t n; int32_t bc; int32_t storage; } etq_grid;
 
 /* Convection field of the Oseen problem.
  * kind = 0: none (Stokes, viscosity ignored);
- * kind = 1: frozen cavity wind w = (2y(1-x^2), -2x(1-y^2)) (BASELINE.json configs[3]). */
+ * kind = 1: frozen cavity wind w = (2y(1-x^2), -2x(1-y^2)) (BASELINE.json configs[3]);
+ * kind = 2: a nodal Q2 wind given later by etq_set_wind (zero until then), e.g. the previous
+ *           Picard iterate.  Velocity operators are stored
+ *           explicitly (grid.storage is taken as 2). */
 typedef struct { int32_t kind; } etq_wind;
 
 typedef enum {
@@ -187,6 +190,21 @@ etq_status etq_gmres_solve(etq_problem* p, int32_t reduced, etq_pc_kind kind, co
 etq_status etq_two_stage_solve(etq_problem* p, const double* b, double* x, double eta, double c,
                                int32_t restart, int32_t maxit, etq_report* st1, etq_report* st2,
                                double bound_out[2]);
+
+/* Nodal wind (wind kind 2): w = [w_x | w_y] on the Q2 nodes (device, length n_u).  Rebuilds F = nu L +
+ * N(w) on every MG level (4 x 4 Gauss points per square, exact for a Q2 wind; coarse winds by
+ * injection), the smoother ellipses (reading R9'), the coarse inverse and, if PCD is set up, F1;
+ * the next etq_build_rhs lifts with the new F.  Synchronises.  ETQ_EINVAL for other wind kinds. */
+etq_status etq_set_wind(etq_problem* p, const double* w);
+
+/* Picard loop of the steady Navier-Stokes problem: x^0 = solution of the
+ * wind-0 system (its velocity is the Stokes velocity), then `steps` Oseen solves, solve k with the
+ * wind u^{k-1}; each solve is etq_two_stage_solve(eta, c, restart, maxit) on the RHS of that
+ * system.  Wind kind 2, M1 and PCD1 set up.  x: device, length N, receives x^steps (its wind
+ * state is u^{steps-1}).  its (host, 2 (steps+1), may be NULL): Step I / II GMRES iterations per
+ * solve; res (host, steps+1, may be NULL): true ||b_k - K_k x^k|| / ||b_k||; ms_total: device ms. */
+etq_status etq_picard_solve(etq_problem* p, int32_t steps, double eta, double c, int32_t restart,
+                            int32_t maxit, double* x, int32_t* its, double* res, double* ms_total);
 
 /* z_p1 = M_S1^{-1} r_p1 = Ap^{-1} F1 Mp^{-1} r_p1 on the Q1 pressure block (length n_k; PCD set up;
  * paper order of Eq. (discrete-commutator1x), reading R11).  Test hook of the Step-I Schur apply. */

@@ -5,7 +5,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["assemble.cu", "ops.cu", "solvers.cu", "oseen.cu", "sweep32.cu", "exact.cu", "api.cu"]
+SOURCES = ["assemble.cu", "ops.cu", "solvers.cu", "oseen.cu", "sweep32.cu", "exact.cu", "picard.cu", "api.cu"]
 OUT = os.path.join(HERE, "libetq.so")
 
 

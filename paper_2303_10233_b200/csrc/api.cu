@@ -132,13 +132,13 @@ etq_status etq_assemble(const etq_grid* grid, double viscosity, const etq_wind* 
   if (grid->storage < 0 || grid->storage > 2) return ETQ_EINVAL;
   const bool oseen = wind && wind->kind != 0;
   if (oseen && !(viscosity > 0.0)) return ETQ_EINVAL;
-  if (wind && (wind->kind < 0 || wind->kind > 1)) return ETQ_EINVAL;
+  if (wind && (wind->kind < 0 || wind->kind > 2)) return ETQ_EINVAL;
   etq_problem* h = new (std::nothrow) etq_problem();
   if (!h) return ETQ_ENOMEM;
   Problem& P = h->P;
   P.g = make_geo(grid->n);
   P.bc = grid->bc;
-  P.storage = grid->storage;
+  P.storage = (oseen && wind->kind == 2) ? 2 : grid->storage;   // nodal winds refill explicit values
   P.oseen = oseen;
   P.wind = oseen ? wind->kind : 0;
   P.nu = oseen ? viscosity : 1.0;
@@ -287,6 +287,7 @@ etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_para
       P.pm.ready = true;
     }
     ETQ_TRY(oseen_setup(P, kind));
+    if (P.wind == 2) ETQ_TRY(picard_refresh(P));   // new levels / F1 get the current nodal wind
     if (P.gmres_graph) { cudaGraphExecDestroy(P.gmres_graph); P.gmres_graph = nullptr; }
     ETQ_CHECK(cudaStreamSynchronize(P.stream));
     return ETQ_OK;
@@ -451,6 +452,21 @@ etq_status etq_two_stage_solve(etq_problem* h, const double* b, double* x, doubl
   Problem& P = h->P;
   StreamScope sc(P);
   return two_stage_run(P, b, x, eta, c, restart, maxit, st1, st2, bound_out);
+}
+
+etq_status etq_set_wind(etq_problem* h, const double* w) {
+  if (!h || !w) return ETQ_EINVAL;
+  Problem& P = h->P;
+  StreamScope sc(P);
+  return picard_set_wind(P, w);
+}
+
+etq_status etq_picard_solve(etq_problem* h, int32_t steps, double eta, double c, int32_t restart, int32_t maxit,
+                            double* x, int32_t* its, double* res, double* ms_total) {
+  if (!h || !x || steps < 0 || !(eta > 0.0) || !(c > 0.0) || restart < 1 || maxit < 1) return ETQ_EINVAL;
+  Problem& P = h->P;
+  StreamScope sc(P);
+  return picard_run(P, steps, eta, c, restart, maxit, x, its, res, ms_total);
 }
 
 etq_status etq_export_operator(const etq_problem* h, int32_t which, int32_t level, int64_t* nrows, int64_t* nnz,
@@ -661,6 +677,7 @@ void etq_destroy(etq_problem* h) {
   free_hierarchy(P.mg);
   exact_free(P);
   oseen_free(P);
+  cudaFree(P.wnod); cudaFree(P.lv_lap); cudaFree(P.f1_lap);
   P.Lv.perm = nullptr; P.BxT1.perm = nullptr; P.ByT1.perm = nullptr; P.BxT0.perm = nullptr; P.ByT0.perm = nullptr;
   sell_free(P.Lv); sell_free(P.BxT1); sell_free(P.ByT1); sell_free(P.BxT0); sell_free(P.ByT0); sell_free(P.B);
   if (P.node_perm) cudaFree(P.node_perm);

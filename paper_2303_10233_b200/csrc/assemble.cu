@@ -99,14 +99,16 @@ __device__ double w1(double h, int e, int i) {
   return (i >= 2 * e && i <= 2 * e + 2) ? cW[i - 2 * e] * h : 0.0;
 }
 
-struct VelParams { Geo g; int oseen; double nu; };
+struct VelParams { Geo g; int oseen; double nu; };   // oseen: 0 Stokes, 1 cavity wind, 2 nodal wind (nu L part)
 
 // entry of the scalar velocity operator between nodes (i,j) and (ii,jj), no Dirichlet masking
 __device__ double vel_entry(const VelParams& P, int i, int j, int ii, int jj) {
   const int n = P.g.n; const double h = P.g.h;
   double v = m1(n, h, j, jj) * k1(n, h, i, ii) + k1(n, h, j, jj) * m1(n, h, i, ii);
-  if (P.oseen) {
+  if (P.oseen == 1) {
     v = P.nu * v + osn1(0, n, h, i, ii) * osn1(1, n, h, j, jj) - osn1(1, n, h, i, ii) * osn1(0, n, h, j, jj);
+  } else if (P.oseen == 2) {   // nodal (Picard) wind: nu L here, the convection is added by picard.cu
+    v = P.nu * v;
   }
   return v;
 }
@@ -617,7 +619,7 @@ etq_status build_node_perm(const Geo& g, int** perm, int64_t* nslices, cudaStrea
 
 etq_status assemble_velocity_op(const Geo& g, bool oseen, double nu, int wind, int* perm,
                                 int64_t nslices, Sell* out, cudaStream_t st) {
-  VelFn fn{VelParams{g, (oseen && wind == 1) ? 1 : 0, oseen ? nu : 1.0}};
+  VelFn fn{VelParams{g, oseen ? (wind == 1 ? 1 : 2) : 0, oseen ? nu : 1.0}};
   return build_sell(fn, perm, g.nq, nslices, out, st);
 }
 
@@ -634,22 +636,24 @@ etq_status assemble_b(const Geo& g, Sell* out, cudaStream_t st) {
 }
 
 etq_status velocity_dinv_dev(const Geo& g, bool oseen, double nu, int wind, double* dinv, cudaStream_t st) {
-  VelParams P{g, (oseen && wind == 1) ? 1 : 0, oseen ? nu : 1.0};
+  VelParams P{g, oseen ? (wind == 1 ? 1 : 2) : 0, oseen ? nu : 1.0};
   k_vel_dinv<<<(g.nq + 255) / 256, 256, 0, st>>>(P, dinv); etq_count_launch();
   ETQ_CHECK(cudaGetLastError());
   return ETQ_OK;
 }
 
 etq_status build_rhs_dev(const Problem& P, const double* f_nodal, double* b) {
-  VelParams vp{P.g, (P.oseen && P.wind == 1) ? 1 : 0, P.oseen ? P.nu : 1.0};
+  VelParams vp{P.g, P.oseen ? (P.wind == 1 ? 1 : 2) : 0, P.oseen ? P.nu : 1.0};
   k_rhs_velocity<<<(P.g.nq + 255) / 256, 256, 0, P.stream>>>(vp, P.bc, f_nodal, b); etq_count_launch();
   ETQ_CHECK(cudaGetLastError());
   k_rhs_pressure<<<(unsigned)((P.n_p + 255) / 256), 256, 0, P.stream>>>(P.g, P.bc, b + P.n_u); etq_count_launch();
   ETQ_CHECK(cudaGetLastError());
+  if (P.oseen && P.wind == 2) ETQ_TRY(picard_rhs_convection(P, b));   // - N(w)[:, boundary] u_boundary
   return ETQ_OK;
 }
 
 etq_status oseen_gershgorin(const Geo& g, double nu, int wind, double* bim, cudaStream_t st) {
+  if (wind == 2) { *bim = 0.0; return ETQ_OK; }   // nodal wind: picard.cu recomputes it from the values
   VelParams P{g, wind == 1 ? 1 : 0, nu};
   unsigned long long* d;
   ETQ_TRY(dalloc(&d, 1));

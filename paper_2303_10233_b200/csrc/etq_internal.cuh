@@ -114,6 +114,8 @@ struct Level {
   // two-component work vectors, each [2*nq]
   double *b = nullptr, *x = nullptr, *r = nullptr, *d0 = nullptr, *d1 = nullptr;
   double* coarse_inv = nullptr;   // dense inverse (coarsest level only), nq x nq row-major
+  double* wind = nullptr;         // nodal Q2 wind on this level (Picard, levels >= 1; injection)
+  double* lapval = nullptr;       // nu L values of A as assembled (Picard refills F = nu L + N)
   // fp32 copies for the c5 sweep (sweep32.cu)
   float *f_dinv = nullptr, *f_b = nullptr, *f_x = nullptr, *f_r = nullptr, *f_d0 = nullptr, *f_d1 = nullptr;
   float* f_coarse = nullptr;
@@ -240,6 +242,11 @@ struct Problem {
   cudaGraphExec_t gmres_graph = nullptr; int gmres_graph_key = -1;
   int64_t gmres_graph_nodes = 0;
 
+  // NEXT-3: nodal (Picard) wind, wind kind 2 (picard.cu)
+  double* wnod = nullptr;                     // [n_u] Q2 nodal wind [w_x | w_y]
+  double* lv_lap = nullptr;                   // nu L values of Lv as assembled
+  double* f1_lap = nullptr;                   // diffusion values of F1 as assembled
+
   // NEXT-2: exact M_Q solve (P3, P1_ITER) and iterative A^{-1} (P1_ITER)
   PcExactMass mx;
   PcVelIter vi;
@@ -352,3 +359,11 @@ etq_status vel_iter_apply(const Problem& P, const double* r_u, double* z_u, cons
                           double* dot_out, const double* dot_with, const double* done, cudaStream_t st);
 etq_status pcg_stats(const Problem& P, int which, double* it_total, double* calls);
 int64_t pcg_launches_since(const Problem& P, double it0_m, double calls0_m, double it0_v, double calls0_v);
+
+// picard.cu (NEXT-3: nodal Q2 wind, Picard loop)
+etq_status picard_refresh(Problem& P);
+etq_status picard_set_wind(Problem& P, const double* w);
+etq_status picard_rhs_convection(const Problem& P, double* b);
+etq_status picard_run(Problem& P, int steps, double eta, double c, int restart, int maxit, double* x,
+                      int* its, double* res, double* ms_total);
+etq_status refresh_tail(Hierarchy& H);   // ops.cu: rewrite the fused tail's level table (c1, c2)

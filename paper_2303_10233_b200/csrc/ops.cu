@@ -1392,22 +1392,28 @@ etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, do
   if (degree <= 4)
     for (size_t l = 1; l < H.lv.size(); ++l)
       if (H.lv[l].g.n <= TAIL_N && H.lv.size() - l >= 2) { H.tail_start = (int)l; break; }
-  if (H.tail_start > 0) {
-    std::vector<TailLevel> tl;
-    std::vector<double> c1, c2;
-    for (size_t l = H.tail_start; l < H.lv.size(); ++l) {
-      const Level& lv = H.lv[l];
-      TailLevel t{};
-      t.A = lv.A; t.dinv = lv.dinv; t.b = lv.b; t.x = lv.x; t.r = lv.r; t.d0 = lv.d0; t.d1 = lv.d1;
-      t.nq = lv.nrows; t.m = lv.g.m; t.coarse_inv = lv.coarse_inv;
-      cheb_coeffs(lo, hi, lv.bim, degree, c1, c2);
-      for (int k = 0; k < degree; ++k) { t.c1[k] = c1[k]; t.c2[k] = c2[k]; }
-      tl.push_back(t);
-    }
-    ETQ_TRY(dalloc(&H.tail, tl.size()));
-    ETQ_CHECK(cudaMemcpy(H.tail, tl.data(), sizeof(TailLevel) * tl.size(), cudaMemcpyHostToDevice));
-  }
+  if (H.tail_start > 0) ETQ_TRY(refresh_tail(H));
   ETQ_CHECK(cudaStreamSynchronize(P.stream));
+  return ETQ_OK;
+}
+
+// (Re)write the fused tail's level table: operators, vectors and Chebyshev coefficients (the
+// latter change when a Picard wind changes the smoother ellipses, picard.cu)
+etq_status refresh_tail(Hierarchy& H) {
+  if (H.tail_start <= 0) return ETQ_OK;
+  std::vector<TailLevel> tl;
+  std::vector<double> c1, c2;
+  for (size_t l = H.tail_start; l < H.lv.size(); ++l) {
+    const Level& lv = H.lv[l];
+    TailLevel t{};
+    t.A = lv.A; t.dinv = lv.dinv; t.b = lv.b; t.x = lv.x; t.r = lv.r; t.d0 = lv.d0; t.d1 = lv.d1;
+    t.nq = lv.nrows; t.m = lv.g.m; t.coarse_inv = lv.coarse_inv;
+    cheb_coeffs(H.lo, H.hi, lv.bim, H.degree, c1, c2);
+    for (int k = 0; k < H.degree; ++k) { t.c1[k] = c1[k]; t.c2[k] = c2[k]; }
+    tl.push_back(t);
+  }
+  if (!H.tail) ETQ_TRY(dalloc(&H.tail, tl.size()));
+  ETQ_CHECK(cudaMemcpy(H.tail, tl.data(), sizeof(TailLevel) * tl.size(), cudaMemcpyHostToDevice));
   return ETQ_OK;
 }
 
@@ -1462,6 +1468,7 @@ void free_hierarchy(Hierarchy& H) {
     sell_free(L.Afr);
     cudaFree(L.dinv); cudaFree(L.b); cudaFree(L.x); cudaFree(L.r); cudaFree(L.d0); cudaFree(L.d1);
     cudaFree(L.coarse_inv);
+    cudaFree(L.wind); cudaFree(L.lapval);
   }
   cudaFree(H.tail);
   H = Hierarchy{};

@@ -76,6 +76,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "etq_two_stage_solve": ([P, VP, VP, D, D, I32, I32, C.POINTER(Report), C.POINTER(Report),
                                  C.POINTER(D)], I32),
         "etq_apply_pcd_schur": ([P, VP, VP], I32),
+        "etq_set_wind": ([P, VP], I32),
+        "etq_picard_solve": ([P, I32, D, D, I32, I32, VP, VP, VP, C.POINTER(D)], I32),
         "etq_est_minres": ([VP, VP, I32, C.POINTER(D)], I32),
         "etq_apply_saddle_f32": ([P, I32, VP, VP], I32),
         "etq_apply_vcycle_f32": ([P, VP, VP], I32),
@@ -319,6 +321,22 @@ class Problem:
         st1 = self._report_dict(r1, h1, d1, g1, s); st1["history"] = h1[:r1.iterations + 1].copy()
         st2 = self._report_dict(r2, h2, d2, g2, s); st2["history"] = h2[:r2.iterations + 1].copy()
         return {"status": s, "step1": st1, "step2": st2, "zstar": bound[0], "bound": bound[1]}
+
+    def set_wind(self, w):
+        """Nodal Q2 wind [w_x | w_y] (device tensor, length n_u) of a wind-kind-2 problem."""
+        _check(lib().etq_set_wind(self.h, _ptr(w)), "etq_set_wind")
+
+    def picard_solve(self, x, steps=5, eta=1e-6, c=10.0, restart=50, maxit=2000):
+        """Picard loop (etq_picard_solve); x receives the last iterate."""
+        import numpy as np
+        its = np.zeros(2 * (steps + 1), dtype=np.int32)
+        res = np.zeros(steps + 1)
+        ms = C.c_double()
+        s = _check(lib().etq_picard_solve(self.h, steps, eta, c, restart, maxit, _ptr(x),
+                                          C.c_void_p(its.ctypes.data), C.c_void_p(res.ctypes.data),
+                                          C.byref(ms)), "etq_picard_solve")
+        return {"status": s, "step1_its": its[0::2].copy(), "step2_its": its[1::2].copy(), "rel_res": res,
+                "ms_total": ms.value}
 
     def export_operator(self, which, level=0):
         """Assembled operator as a scipy CSR matrix (host copy; tests only)."""

@@ -4,7 +4,8 @@
 
 c1: n=16 lid, P1 MINRES; c2: n=256 homogeneous BC + N(0,1) nodal force (seed 0), P2 MINRES;
 c3: n=1024 lid, P2 MINRES (also bench.py's headline); c4: n=512 Oseen nu=0.01 cavity wind,
-two-stage PCD with GMRES(50), eta=1e-6, c=10; c5: fused saddle SpMV and one V-cycle for
+two-stage PCD with GMRES(50), eta=1e-6, c=10; c4p (NEXT-3): the Picard loop at n=512, nu=0.01,
+5 Oseen solves with the previous iterate as wind; c5: fused saddle SpMV and one V-cycle for
 n = 64 ... c5-max (fp64), GB/s of algorithmic bytes against the measured HBM peak.
 """
 import argparse
@@ -87,6 +88,27 @@ def c4_case(n=512):
     return res
 
 
+def c4p_case(n=512, steps=5):
+    """NEXT-3: the Picard loop of the cavity at nu = 0.01: Stokes start +
+    `steps` Oseen solves with the previous iterate as wind, two-stage PCD with GMRES(50), eta 1e-6."""
+    t0 = time.perf_counter()
+    P = etq.Problem(n, bc=0, viscosity=0.01, wind=2)
+    P.precond_setup(etq.PC_OSEEN_M1)
+    P.precond_setup(etq.PC_OSEEN_PCD1)
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    x = zeros(P.N)
+    t0 = time.perf_counter()
+    out = P.picard_solve(x, steps=steps, eta=1e-6, c=10.0, restart=50, maxit=3000)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    res = {"n": n, "N": P.N, "steps": steps, "setup_s": setup, "wall_s": wall, "device_ms": out["ms_total"],
+           "status": out["status"], "step1_its": out["step1_its"].tolist(), "step2_its": out["step2_its"].tolist(),
+           "true_rel_res": out["rel_res"].tolist()}
+    P.close()
+    return res
+
+
 def c5_case(nmax, storage=0):
     pk = peak()
     rows = []
@@ -110,7 +132,7 @@ def c5_case(nmax, storage=0):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c1,c2,c3,c4,c5")
+    ap.add_argument("--only", default="c1,c2,c3,c4,c4p,c5")
     ap.add_argument("--c5-max", type=int, default=2048)
     args = ap.parse_args()
     which = set(args.only.split(","))
@@ -123,6 +145,8 @@ def main():
         res["c3"] = minres_case(1024, 0, False, etq.PC_P2_GMG, 5000)
     if "c4" in which:
         res["c4"] = c4_case(512)
+    if "c4p" in which:
+        res["c4p"] = c4p_case(512)
     if "c5" in which:
         res["c5"] = c5_case(args.c5_max)
         res["c5_explicit_sell"] = c5_case(args.c5_max, storage=2)
