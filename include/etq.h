@@ -65,8 +65,12 @@ typedef enum {
     ETQ_PC_OSEEN_PCD1 = 3, /* Step-I PCD: [[V-cycle(F), B1^T], [0, -Ap^{-1} F1 Mp^{-1}]] */
     ETQ_PC_P1_ITER = 4,    /* P1 at any n: A^{-1} by V-cycle-preconditioned CG and the
                               exact augmented M_Q solve through S_k (reading R21), both to inner_rtol */
-    ETQ_PC_P3 = 5          /* diag(one Q2-GMG V-cycle, exact M_Q solve through S_k): P2's velocity block with
+    ETQ_PC_P3 = 5,         /* diag(one Q2-GMG V-cycle, exact M_Q solve through S_k): P2's velocity block with
                               P1's pressure block (NEXT-2; mesh-independent MINRES counts) */
+    ETQ_PC_OSEEN_M2 = 6,   /* M2 = [[V-cycle(F), B^T], [0, -M_S]], two-field PCD M_S = diag(Q1,Q0) diag(F1,F0)^-1
+                              B M^-1 B^T (NEXT-4; stagnates) */
+    ETQ_PC_OSEEN_LSC = 7   /* M3 = [[V-cycle(F), B^T], [0, -M_S]], least-squares commutator M_S with H = M
+                              (NEXT-4, reading R26) */
 } etq_pc_kind;
 
 /* Preconditioner parameters (defaults in brackets; readings R7, R9, R13). */
@@ -166,7 +170,8 @@ etq_status etq_minres_solve_host(etq_problem* p, etq_pc_kind kind, const double*
 /* Export an assembled operator to caller-owned HOST CSR buffers (tests).  which:
  *   0 = scalar velocity operator with Dirichlet rows (L or F_s) of MG level `level`,
  *   1 = B (n_p x n_u), 2 = B^T (n_u x n_p), 3 = Ap of Q1 level `level` (PCD set up),
- *   4 = F1 (PCD set up), 5 = S_k / 4^level of Q1 level `level` (P3 or P1_ITER set up, reading R21).
+ *   4 = F1 (PCD set up), 5 = S_k / 4^level of Q1 level `level` (P3 or P1_ITER set up, reading R21),
+ *   6 = the two-field Laplacian B Mdiag^-1 B^T on [Q1; P0] of level `level` (M2 or LSC set up).
  * Call with rowptr == NULL to query *nrows and *nnz. */
 etq_status etq_export_operator(const etq_problem* p, int32_t which, int32_t level,
                                int64_t* nrows, int64_t* nnz,
@@ -175,7 +180,8 @@ etq_status etq_export_operator(const etq_problem* p, int32_t which, int32_t leve
 /* Right-preconditioned restarted GMRES(m) with classical Gram-Schmidt applied twice (
  * readings R14, R18) on the Oseen system [F B^T; B 0] (reduced = 0, kind = ETQ_PC_OSEEN_M1) or the
  * reduced Taylor-Hood system [F B1^T; B1 0] (reduced = 1, kind = ETQ_PC_OSEEN_PCD1; the p_0 block of
- * b is ignored and x's p_0 block is left unchanged).  Stops when the residual estimate
+ * b is ignored and x's p_0 block is left unchanged); kinds ETQ_PC_OSEEN_M2 / ETQ_PC_OSEEN_LSC precondition the
+ * full system (reduced = 0) with the NEXT-4 Schur approximations.  Stops when the residual estimate
  * |g_{j+1}| <= rtol * ||b||_2 (Euclidean residual); report.abs_res is the true
  * ||b - K x||_2 after the last restart, report.history the estimates (entry 0 = ||r_0||).
  * x is the initial guess on input (device).  Returns ETQ_OK, ETQ_NOT_CONVERGED or an error. */

@@ -275,7 +275,7 @@ etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_para
     ETQ_CHECK(cudaStreamSynchronize(P.stream));
     return ETQ_OK;
   }
-  if (kind == ETQ_PC_OSEEN_M1 || kind == ETQ_PC_OSEEN_PCD1) {
+  if (kind == ETQ_PC_OSEEN_M1 || kind == ETQ_PC_OSEEN_PCD1 || kind == ETQ_PC_OSEEN_M2 || kind == ETQ_PC_OSEEN_LSC) {
     if (!P.oseen) return ETQ_EINVAL;
     if (!is_pow2(P.g.n)) return ETQ_EINVAL;
     if (kind == ETQ_PC_OSEEN_M1) {   // Chebyshev-SGS for the -(1/nu) M_Q~ block
@@ -431,7 +431,9 @@ etq_status etq_apply_pcd_schur(const etq_problem* h, const double* r_p1, double*
 etq_status etq_gmres_solve(etq_problem* h, int32_t reduced, etq_pc_kind kind, const double* b, double* x,
                            double rtol, int32_t restart, int32_t maxit, etq_report* report) {
   if (!h || !b || !x || !(rtol > 0.0) || restart < 1 || maxit < 1) return ETQ_EINVAL;
-  if (kind != ETQ_PC_OSEEN_M1 && kind != ETQ_PC_OSEEN_PCD1) return ETQ_EINVAL;
+  if (kind != ETQ_PC_OSEEN_M1 && kind != ETQ_PC_OSEEN_PCD1 && kind != ETQ_PC_OSEEN_M2 && kind != ETQ_PC_OSEEN_LSC)
+    return ETQ_EINVAL;
+  if ((kind == ETQ_PC_OSEEN_M2 || kind == ETQ_PC_OSEEN_LSC) && reduced) return ETQ_EINVAL;   // full system only
   if (kind == ETQ_PC_OSEEN_PCD1 && !reduced) return ETQ_EINVAL;   // PCD1 preconditions the reduced system
   Problem& P = h->P;
   StreamScope sc(P);
@@ -490,6 +492,10 @@ etq_status etq_export_operator(const etq_problem* h, int32_t which, int32_t leve
     if (!P.apH.built || level < 0 || level >= (int)P.apH.lv.size()) return ETQ_EINVAL;
     parts.push_back({&P.apH.lv[level].A, {0, 0}});
     R = P.apH.lv[level].A.nrows;
+  } else if (which == 6) {
+    if (!P.lp.H.built || level < 0 || level >= (int)P.lp.H.lv.size()) return ETQ_EINVAL;
+    parts.push_back({&P.lp.H.lv[level].A, {0, 0}});
+    R = P.lp.H.lv[level].A.nrows;
   } else if (which == 5) {
     if (!P.mx.sH.built || level < 0 || level >= (int)P.mx.sH.lv.size()) return ETQ_EINVAL;
     parts.push_back({&P.mx.sH.lv[level].A, {0, 0}});

@@ -231,6 +231,80 @@ __device__ int ap_row(const ApParams& P, int row, Emit& emit) {
   return cnt;
 }
 
+// Two-field pressure Laplacian Lp = B Mdiag^{-1} B^T on [Q1; P0] (NEXT-4: the B M^{-1} B^T of the
+// two-field PCD and LSC approximations).  A Q1 row gathers over the
+// interior velocity nodes of its B1 support into a 5 x 5 vertex window and a 4 x 4 cell window; a P0
+// row over the interior nodes of its square into 4 x 4 vertices and 3 x 3 cells.  Q1 columns first.
+struct LpParams { Geo g; };
+template <class Emit>
+__device__ int lp_row(const LpParams& P, int row, Emit& emit) {
+  const int m = P.g.m, n = P.g.n; const double h = P.g.h;
+  const int nk = P.g.nk;
+  double acck[25], acc0[16];
+#pragma unroll
+  for (int k = 0; k < 25; ++k) acck[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc0[k] = 0.0;
+  const bool q1 = row < nk;
+  int a, c, i0, i1, j0, j1, kw, ko, cw, co;   // vertex window (width kw, origin ko), cell window (cw, co)
+  if (q1) {
+    a = row % (n + 1); c = row / (n + 1);
+    i0 = max(1, 2 * a - 2); i1 = min(m - 2, 2 * a + 2); j0 = max(1, 2 * c - 2); j1 = min(m - 2, 2 * c + 2);
+    kw = 5; ko = 2; cw = 4; co = 2;
+  } else {
+    const int t = row - nk;
+    a = t % n; c = t / n;
+    i0 = max(1, 2 * a); i1 = min(m - 2, 2 * a + 2); j0 = max(1, 2 * c); j1 = min(m - 2, 2 * c + 2);
+    kw = 4; ko = 1; cw = 3; co = 1;
+  }
+  for (int jj = j0; jj <= j1; ++jj) {
+    for (int ii = i0; ii <= i1; ++ii) {
+      double bx, by;
+      if (q1) { bx = -g1(n, a, ii) * h1(n, h, c, jj); by = -h1(n, h, a, ii) * g1(n, c, jj); }
+      else { bx = -e1(a, ii) * w1(h, c, jj); by = -w1(h, a, ii) * e1(c, jj); }
+      if (bx == 0.0 && by == 0.0) continue;
+      const double md = m1(n, h, ii, ii) * m1(n, h, jj, jj);   // diagonal of the Q2 mass
+      const double wx = bx / md, wy = by / md;
+      for (int cc = max(0, jj / 2 - 1); cc <= min(n, jj / 2 + 1); ++cc) {
+        if (cc - c + ko < 0 || cc - c + ko >= kw) continue;
+        for (int aa = max(0, ii / 2 - 1); aa <= min(n, ii / 2 + 1); ++aa) {
+          if (aa - a + ko < 0 || aa - a + ko >= kw) continue;
+          const double qx = -g1(n, aa, ii) * h1(n, h, cc, jj), qy = -h1(n, h, aa, ii) * g1(n, cc, jj);
+          acck[(cc - c + ko) * kw + (aa - a + ko)] += wx * qx + wy * qy;
+        }
+      }
+      for (int ff = max(0, (jj - 1) / 2); ff <= min(n - 1, jj / 2); ++ff) {
+        if (2 * ff > jj || 2 * ff + 2 < jj || ff - c + co < 0 || ff - c + co >= cw) continue;
+        for (int ee = max(0, (ii - 1) / 2); ee <= min(n - 1, ii / 2); ++ee) {
+          if (2 * ee > ii || 2 * ee + 2 < ii || ee - a + co < 0 || ee - a + co >= cw) continue;
+          const double px = -e1(ee, ii) * w1(h, ff, jj), py = -w1(h, ee, ii) * e1(ff, jj);
+          acc0[(ff - c + co) * cw + (ee - a + co)] += wx * px + wy * py;
+        }
+      }
+    }
+  }
+  int cnt = 0;
+  for (int dc = 0; dc < kw; ++dc)
+    for (int da = 0; da < kw; ++da) {
+      const double v = acck[dc * kw + da];
+      if (v != 0.0) { emit((a + da - ko) + (n + 1) * (c + dc - ko), v); ++cnt; }
+    }
+  for (int df = 0; df < cw; ++df)
+    for (int de = 0; de < cw; ++de) {
+      const double v = acc0[df * cw + de];
+      if (v != 0.0) { emit(nk + (a + de - co) + n * (c + df - co), v); ++cnt; }
+    }
+  return cnt;
+}
+
+// 1 / diagonal of the scalar Q2 velocity mass (M = Mdiag of P:922-923), Dirichlet nodes 0
+__global__ void k_vel_mdiag_inv(Geo g, double* out) {
+  const int node = blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= g.nq) return;
+  const int m = g.m, i = node % m, j = node / m;
+  out[node] = (i == 0 || j == 0 || i == m - 1 || j == m - 1) ? 0.0 : 1.0 / (m1(g.n, g.h, i, i) * m1(g.n, g.h, j, j));
+}
+
 // S_k = Q_k - R^T Q_0^{-1} R on the Q1 vertices (the Schur complement of the Q0 block of M_Q,
 // P:287-294 with R = h^2/4, Q0 = h^2): per cell T, (h^2/36) m_x m_y - h^2/16 for each vertex pair
 // of T (m = 2 on the same 1D index, else 1); interior stencil (h^2/144) [-5 -2 -5; -2 28 -2; -5 -2 -5].
@@ -314,6 +388,7 @@ struct VelFn { VelParams p; template <class E> __device__ int operator()(int r, 
 struct BtFn { BtParams p; template <class E> __device__ int operator()(int r, E& e) const { return bt_row(p, r, e); } };
 struct BFn { BParams p; template <class E> __device__ int operator()(int r, E& e) const { return b_row(p, r, e); } };
 struct ApFn { ApParams p; template <class E> __device__ int operator()(int r, E& e) const { return ap_row(p, r, e); } };
+struct LpFn { LpParams p; template <class E> __device__ int operator()(int r, E& e) const { return lp_row(p, r, e); } };
 struct SkFn { SkParams p; template <class E> __device__ int operator()(int r, E& e) const { return sk_row(p, r, e); } };
 struct F1Fn { F1Params p; template <class E> __device__ int operator()(int r, E& e) const { return f1_row(p, r, e); } };
 
@@ -672,6 +747,18 @@ etq_status oseen_gershgorin(const Geo& g, double nu, int wind, double* bim, cuda
 etq_status assemble_ap(const Geo& g, Sell* out, cudaStream_t st) {
   ApFn fn{ApParams{g}};
   return build_sell(fn, nullptr, g.nk, ((int64_t)g.nk + SELL_C - 1) / SELL_C, out, st);
+}
+
+etq_status assemble_lp(const Geo& g, Sell* out, cudaStream_t st) {
+  LpFn fn{LpParams{g}};
+  const int64_t nr = (int64_t)g.nk + g.n0;
+  return build_sell(fn, nullptr, nr, (nr + SELL_C - 1) / SELL_C, out, st);
+}
+
+etq_status velocity_mdiag_inv(const Geo& g, double* out, cudaStream_t st) {
+  k_vel_mdiag_inv<<<(g.nq + 255) / 256, 256, 0, st>>>(g, out); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
 }
 
 etq_status assemble_sk(const Geo& g, double scale, Sell* out, cudaStream_t st) {

@@ -189,6 +189,13 @@ struct PcExactMass {          // exact augmented M_Q solve through S_k (NEXT-2, 
   double* zh = nullptr;       // [n_k] S_k^+ g
   double* sc = nullptr;       // [8] sums, lambda, a^T zhat, beta
 };
+struct PcLp {                 // Lp^+ for the two-field PCD / LSC Schur approximations (NEXT-4)
+  bool ready = false;
+  Hierarchy H;                // Q1 + P0 hierarchy of Lp = B Mdiag^-1 B^T
+  PcgWs cg;
+  double* rp = nullptr;       // [n_p] projected right-hand side
+  double* sc = nullptr;       // [8] field sums
+};
 struct PcVelIter {            // A^{-1} by V-cycle-preconditioned CG (P1 at scale)
   bool ready = false;
   PcgWs cg;
@@ -250,6 +257,9 @@ struct Problem {
   // NEXT-2: exact M_Q solve (P3, P1_ITER) and iterative A^{-1} (P1_ITER)
   PcExactMass mx;
   PcVelIter vi;
+  PcLp lp;                                    // NEXT-4: Lp^+ (oseen2 Schur approximations)
+  double* minv = nullptr;                     // [nq] 1 / Mdiag (scalar velocity mass diagonal)
+  double* s2w[4] = {nullptr, nullptr, nullptr, nullptr};   // [n_u] work vectors of M2 / LSC
 
   // Krylov workspace (length N each)
   double* kv[10] = {nullptr};
@@ -281,6 +291,8 @@ etq_status oseen_gershgorin(const Geo& g, double nu, int wind, double* bim, cuda
 etq_status assemble_ap(const Geo& g, Sell* out, cudaStream_t st);
 etq_status assemble_f1(const Geo& g, double nu, int wind, Sell* out, cudaStream_t st);
 etq_status assemble_sk(const Geo& g, double scale, Sell* out, cudaStream_t st);
+etq_status assemble_lp(const Geo& g, Sell* out, cudaStream_t st);
+etq_status velocity_mdiag_inv(const Geo& g, double* out, cudaStream_t st);
 etq_status sell_diag_inv(const Sell& A, double* dinv, cudaStream_t st);
 etq_status build_rhs_dev(const Problem& P, const double* f_nodal, double* b);
 etq_status mark_implicit(const Geo& g, bool oseen, double nu, int wind, Sell& S, cudaStream_t st, bool values);
@@ -367,3 +379,8 @@ etq_status picard_rhs_convection(const Problem& P, double* b);
 etq_status picard_run(Problem& P, int steps, double eta, double c, int restart, int maxit, double* x,
                       int* its, double* res, double* ms_total);
 etq_status refresh_tail(Hierarchy& H);   // ops.cu: rewrite the fused tail's level table (c1, c2)
+etq_status lp_setup(Problem& P);
+etq_status lp_pinv_apply(const Problem& P, const double* r, double* z, const double* done, cudaStream_t st);
+void lp_free(Problem& P);
+etq_status schur2_apply(const Problem& P, etq_pc_kind kind, const double* r_p, double* z_p, const double* done,
+                        cudaStream_t st);

@@ -220,6 +220,25 @@ __global__ void __launch_bounds__(BS) k_mq_final(const double* zh, const double*
   if (out) { double a[1] = {dot}; reduce_finish<1>(a, site, slot, out); }
 }
 
+// ---------------------------------------------------------------- two-field Lp^+ (NEXT-4)
+// sums of the Q1 and P0 parts of x -> out[0], out[1]
+__global__ void __launch_bounds__(BS) k_field_sums(const double* x, int nk, int n0, RedSite site, int slot,
+                                                   double* out, const double* done) {
+  if (is_done(done)) return;
+  double s[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nk + n0; i += (int64_t)gridDim.x * blockDim.x)
+    s[i < nk ? 0 : 1] += x[i];
+  reduce_finish<2>(s, site, slot, out);
+}
+// y = x - (mean of each field) (projection onto range(Lp) = the zero-mean fields)
+__global__ void __launch_bounds__(BS) k_field_sub(const double* x, double* y, int nk, int n0, const double* sums,
+                                                  const double* done) {
+  if (is_done(done)) return;
+  const double m1 = sums[0] / nk, m0 = sums[1] / n0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nk + n0; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = x[i] - (i < nk ? m1 : m0);
+}
+
 // ---------------------------------------------------------------- PCG driver
 // A and M issue their launches on the given stream; M must write z = M r and the dot r^T z into
 // sc[PG_RZ1] through (site, SL_RZ) and honour done = sc + PG_DONE.
@@ -379,6 +398,21 @@ static etq_status vel_iter_issue(PcVelIter& V, const Problem& P, const double* r
   return ETQ_OK;
 }
 
+static etq_status lp_pinv_issue(PcLp& X, const Problem& P, const double* r, double* z, const double* done,
+                                cudaStream_t st) {
+  const int nk = P.g.nk, n0 = P.g.n0;
+  const int64_t np = (int64_t)nk + n0;
+  const int gs = grid_for(np, BS, RED_BLOCKS);
+  k_field_sums<<<gs, BS, 0, st>>>(r, nk, n0, X.cg.red, SL_SUMS, X.sc, done); etq_count_launch();
+  k_field_sub<<<grid_for(np, BS, 4096), BS, 0, st>>>(r, X.rp, nk, n0, X.sc, done); etq_count_launch();
+  PcgOps o{1, &X.H.lv[0].A, (int)np, &P, &X.H};
+  ETQ_TRY(pcg_captured(X.cg, o, X.rp, z, done, st));
+  k_field_sums<<<gs, BS, 0, st>>>(z, nk, n0, X.cg.red, SL_SUMS, X.sc + 2, done); etq_count_launch();
+  k_field_sub<<<grid_for(np, BS, 4096), BS, 0, st>>>(z, z, nk, n0, X.sc + 2, done); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
 }  // namespace
 
 etq_status exact_mass_setup(Problem& P) {
@@ -448,4 +482,31 @@ int64_t pcg_launches_since(const Problem& P, double it0_m, double calls0_m, doub
   if (pcg_stats(P, 0, &im, &cm) < 0 || pcg_stats(P, 1, &iv, &cv) < 0) return 0;
   const double em = (im - it0_m) - (cm - calls0_m), ev = (iv - it0_v) - (cv - calls0_v);
   return (int64_t)(std::max(0.0, em) * (double)P.mx.cg.body_nodes + std::max(0.0, ev) * (double)P.vi.cg.body_nodes);
+}
+
+// ---------------------------------------------------------------- Lp^+ (NEXT-4)
+// Two-field pressure Laplacian Lp = B Mdiag^-1 B^T: Q1 + P0 multigrid (rediscretised Lp, bilinear and
+// piecewise-constant transfers, Chebyshev-3 on [0.21, 2.1] in D^-1 Lp: lambda_max = 1.93 on fine
+// levels, reading R25), coarse pseudo-inverse at n_c = 2; CG to inner_rtol on the zero-mean fields.
+etq_status lp_setup(Problem& P) {
+  PcLp& X = P.lp;
+  if (X.ready) return ETQ_OK;
+  ETQ_TRY(build_ap_hierarchy(P, X.H, 2, 0.21, 2.1, 3, 2));
+  if (!X.rp) { ETQ_TRY(dalloc(&X.rp, P.n_p)); ETQ_TRY(dalloc(&X.sc, 8)); }
+  ETQ_TRY(pcg_alloc(X.cg, P.n_p, P.params.inner_rtol, P.params.inner_maxit));
+  X.ready = true;
+  return ETQ_OK;
+}
+
+etq_status lp_pinv_apply(const Problem& P, const double* r, double* z, const double* done, cudaStream_t st) {
+  if (!P.lp.ready) return ETQ_ENOTSETUP;
+  PcLp& X = const_cast<PcLp&>(P.lp);
+  return run_graphed(P, st, [&](cudaStream_t s) { return lp_pinv_issue(X, P, r, z, done, s); });
+}
+
+void lp_free(Problem& P) {
+  if (P.lp.H.built) free_hierarchy(P.lp.H);
+  cudaFree(P.lp.rp); cudaFree(P.lp.sc);
+  pcg_free(P.lp.cg);
+  P.lp = PcLp{};
 }

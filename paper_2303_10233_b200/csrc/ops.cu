@@ -575,6 +575,36 @@ __global__ void k_prolong_q1(int mf, int mc, const double* xc, const double* dc,
     xf[t] += s;
   }
 }
+// P0 (cell) transfers of the two-field hierarchy (NEXT-4): piecewise-constant prolongation
+// (a coarse cell's value on its 4 children) and its transpose (sum of the 4 children)
+__global__ void k_restrict_p0(int nf, int nc, const double* rf, double* bc, double* d0c, const double* dinvc,
+                              double itheta, const double* done) {
+  if (is_done(done)) return;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)nc * nc;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int E = (int)(t % nc), F = (int)(t / nc);
+    const int64_t f0 = (int64_t)(2 * F) * nf + 2 * E;
+    const double s = (rf[f0] + rf[f0 + 1]) + (rf[f0 + nf] + rf[f0 + nf + 1]);
+    bc[t] = s;
+    d0c[t] = dinvc[t] * s * itheta;
+  }
+}
+__global__ void k_prolong_p0(int nf, int nc, const double* xc, const double* dc, double* xf, const double* done) {
+  if (is_done(done)) return;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)nf * nf;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(t % nf), f = (int)(t / nf);
+    const int64_t c = (int64_t)(f >> 1) * nc + (e >> 1);
+    xf[t] += dc ? xc[c] + dc[c] : xc[c];
+  }
+}
+// A[i][j] += v for i, j in [r0, r1) (coarse pseudo-inverse of the two-field Laplacian)
+__global__ void k_add_block(double* A, int m, int r0, int r1, double v) {
+  const int w = r1 - r0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)w * w; t += (int64_t)gridDim.x * blockDim.x)
+    A[(int64_t)(r0 + t / w) * m + r0 + t % w] += v;
+}
+
 // z -= (sum / n) 1 (mean-zero projection after the Ap V-cycle, reading R13)
 __global__ void k_sub_mean(double* z, int64_t n, const double* sum, const double* done) {
   if (is_done(done)) return;
@@ -1434,18 +1464,32 @@ etq_status build_ap_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo,
   for (size_t l = 0; l < ns.size(); ++l) {
     Level& L = H.lv[l];
     L.g = make_geo(ns[l]);
-    L.nrows = L.g.nk;
+    L.nrows = op == 2 ? L.g.nk + L.g.n0 : L.g.nk;
     if (op == 0) ETQ_TRY(assemble_ap(L.g, &L.A, P.stream));
-    else ETQ_TRY(assemble_sk(L.g, std::ldexp(1.0, -2 * (int)l), &L.A, P.stream));   // S_k / 4^l (R21)
+    else if (op == 1) ETQ_TRY(assemble_sk(L.g, std::ldexp(1.0, -2 * (int)l), &L.A, P.stream));   // S_k / 4^l (R21)
+    else ETQ_TRY(assemble_lp(L.g, &L.A, P.stream));                                                // two-field Lp
+    if (op == 2) { ETQ_TRY(dalloc(&L.dinv, L.nrows)); ETQ_TRY(sell_diag_inv(L.A, L.dinv, P.stream));
+                   L.bim = 0.0; ETQ_TRY(alloc_level_vectors(L, 1, true)); continue; }
     ETQ_TRY(dalloc(&L.dinv, L.g.nk));
     ETQ_TRY(sell_diag_inv(L.A, L.dinv, P.stream));
     L.bim = 0.0;
     ETQ_TRY(alloc_level_vectors(L, 1, true));
   }
   Level& C = H.lv.back();
-  const int m = C.g.nk;
+  const int m = C.nrows;
   ETQ_TRY(dalloc(&C.coarse_inv, (size_t)m * m));
   ETQ_TRY(dense_from_sell(C.A, m, C.coarse_inv, P.stream));
+  if (op == 2) {   // null space: the Q1 and the P0 constants; (A + sum c_i e_i e_i^T)^-1 - sum e_i e_i^T / (c_i |e_i|^4)
+    const int nk = C.g.nk, n0 = C.g.n0;
+    k_add_block<<<grid_for((int64_t)nk * nk, BS, 4096), BS, 0, P.stream>>>(C.coarse_inv, m, 0, nk, 1.0 / nk); etq_count_launch();
+    k_add_block<<<grid_for((int64_t)n0 * n0, BS, 4096), BS, 0, P.stream>>>(C.coarse_inv, m, nk, m, 1.0 / n0); etq_count_launch();
+    ETQ_TRY(dense_inverse_spd(C.coarse_inv, m, P.stream));
+    k_add_block<<<grid_for((int64_t)nk * nk, BS, 4096), BS, 0, P.stream>>>(C.coarse_inv, m, 0, nk, -1.0 / nk); etq_count_launch();
+    k_add_block<<<grid_for((int64_t)n0 * n0, BS, 4096), BS, 0, P.stream>>>(C.coarse_inv, m, nk, m, -1.0 / n0); etq_count_launch();
+    H.lo = lo; H.hi = hi; H.degree = degree; H.built = true; H.op = op;
+    ETQ_CHECK(cudaStreamSynchronize(P.stream));
+    return ETQ_OK;
+  }
   // c 1 1^T with c m ~ the operator's diagonal keeps A + c 1 1^T as well conditioned as A on 1^perp
   // (Ap: diagonal O(1); S_k / 4^l: diagonal (28/144) h_0^2 on every level)
   const double cs = op == 0 ? 1.0 : (28.0 / 144.0) * P.g.h * P.g.h / m;
@@ -1607,6 +1651,12 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     } else {
       k_restrict_q1<<<grid_for(cv.g.nk, BS, 4096), BS, 0, st>>>(lv.g.n + 1, cv.g.n + 1, lv.r, cv.b, cv.d0,
                                                                cv.dinv, 1.0 / theta, done);
+      if (H.op == 2) {
+        etq_count_launch();
+        const int nkf = lv.g.nk, nkc = cv.g.nk;
+        k_restrict_p0<<<grid_for(cv.g.n0, BS, 4096), BS, 0, st>>>(lv.g.n, cv.g.n, lv.r + nkf, cv.b + nkc, cv.d0 + nkc,
+                                                                  cv.dinv + nkc, 1.0 / theta, done);
+      }
     }
     etq_count_launch();
   }
@@ -1630,7 +1680,13 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     if (H.kind == 0) {
       k_prolong<<<grid_for(nq, BS, 4096), BS, 0, st>>>(lv.g.m, cv.g.m, nq, cv.g.nq, xres[l + 1], pend[l + 1], lv.x, done);
     } else {
-      k_prolong_q1<<<grid_for(nq, BS, 4096), BS, 0, st>>>(lv.g.n + 1, cv.g.n + 1, xres[l + 1], pend[l + 1], lv.x, done);
+      k_prolong_q1<<<grid_for(lv.g.nk, BS, 4096), BS, 0, st>>>(lv.g.n + 1, cv.g.n + 1, xres[l + 1], pend[l + 1], lv.x, done);
+      if (H.op == 2) {
+        etq_count_launch();
+        const int nkf = lv.g.nk, nkc = cv.g.nk;
+        k_prolong_p0<<<grid_for(lv.g.n0, BS, 4096), BS, 0, st>>>(lv.g.n, cv.g.n, xres[l + 1] + nkc,
+                                                                 pend[l + 1] ? pend[l + 1] + nkc : nullptr, lv.x + nkf, done);
+      }
     }
     etq_count_launch();
     const int gs = grid_for(lv.A.nslices * 32, BS, 4096);

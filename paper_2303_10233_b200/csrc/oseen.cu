@@ -102,6 +102,58 @@ __global__ void __launch_bounds__(BS) k_bt_sub(BtSubArgs a) {
   }
 }
 
+// t_u = minv o (B^T z_p) (both parts; minv = 1 / Mdiag, zero on Dirichlet nodes)
+__global__ void __launch_bounds__(BS) k_bt_minv(BtSubArgs a, const double* minv) {
+  if (is_done(a.done)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const double* p1 = a.z_p;
+  const double* p0 = a.z_p + a.nk;
+  for (int64_t s = gw; s < a.BxT1.nslices; s += nw) {
+    const int row = a.BxT1.perm[s * SELL_C + lane];
+    const double ax = sell_row1(a.BxT1, s, lane, p1) + sell_row1(a.BxT0, s, lane, p0);
+    const double ay = sell_row1(a.ByT1, s, lane, p1) + sell_row1(a.ByT0, s, lane, p0);
+    if (row >= 0) { a.t_u[row] = minv[row] * ax; a.t_u[a.nq + row] = minv[row] * ay; }
+  }
+}
+
+// y = minv o x on both velocity components
+__global__ void k_scale_minv(const double* x, const double* minv, double* y, int nq, const double* done) {
+  if (is_done(done)) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2LL * nq; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = minv[i % nq] * x[i];
+}
+
+// P0 convection-diffusion F0 (reading R25): y_T = sum over the interior edges e of T of
+// (nu - (w_e . n_e) h / 2) (x_T - x_T'), w_e the wind at the edge midpoint (a Q2 node)
+__global__ void k_f0_apply(Geo g, double nu, int wind, const double* wnod, const double* x, double* y,
+                           double scale, const double* done) {
+  if (is_done(done)) return;
+  const int n = g.n, m = g.m; const double h = g.h;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)n * n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(t % n), f = (int)(t / n);
+    const double xt = x[t] * scale;
+    double acc = 0.0;
+    for (int k = 0; k < 4; ++k) {
+      const int de = k == 0 ? 1 : (k == 1 ? -1 : 0), df = k == 2 ? 1 : (k == 3 ? -1 : 0);
+      const int e2 = e + de, f2 = f + df;
+      if (e2 < 0 || e2 >= n || f2 < 0 || f2 >= n) continue;
+      const int i = 2 * e + 1 + de, j = 2 * f + 1 + df;          // edge-midpoint Q2 node
+      double wx = 0.0, wy = 0.0;
+      if (wind == 1) {
+        const double xx = -1.0 + i * (0.5 * h), yy = -1.0 + j * (0.5 * h);
+        wx = 2.0 * yy * (1.0 - xx * xx); wy = -2.0 * xx * (1.0 - yy * yy);
+      } else if (wind == 2 && wnod) {
+        wx = wnod[i + m * j]; wy = wnod[g.nq + i + m * j];
+      }
+      const double flux = (wx * de + wy * df) * h / 2.0;
+      acc += (nu - flux) * (xt - x[e2 + (int64_t)n * f2] * scale);
+    }
+    y[t] = acc;
+  }
+}
+
 __global__ void k_fill(double* x, int64_t n, double v, const double* done) {
   if (is_done(done)) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) x[i] = v;
@@ -271,6 +323,40 @@ static void qk_cheb(const Problem& P, const double* r, double* out, int steps, c
   }
 }
 
+// z_p = -M_S^+ r_p for the two-field PCD (M2) or LSC (M3) approximation (NEXT-4, oracle.schur2)
+etq_status schur2_apply(const Problem& P, etq_pc_kind kind, const double* r_p, double* z_p, const double* done,
+                        cudaStream_t st) {
+  if (!P.lp.ready || !P.minv) return ETQ_ENOTSETUP;
+  const int nk = P.g.nk, n0 = P.g.n0, nq = P.g.nq;
+  const int64_t np = (int64_t)nk + n0;
+  double* u = P.s2w[0]; double* v = P.s2w[1]; double* w = P.s2w[2]; double* y = P.s2w[3];
+  if (kind == ETQ_PC_OSEEN_M2) {
+    if (!P.F1.val) return ETQ_ENOTSETUP;
+    // [F1 Q1^{-1} r_1 ; F0 Q0^{-1} r_0], Q1^{-1} as in the Step-I PCD (R13), Q0 = h^2 I
+    qk_cheb(P, r_p, v, P.params.mass_cheb_steps, done, st);
+    k_spmv1<<<grid_for(P.F1.nslices * 32, BS, 4096), BS, 0, st>>>(P.F1, v, u, 1.0, done); etq_count_launch();
+    k_f0_apply<<<grid_for(n0, BS, 4096), BS, 0, st>>>(P.g, P.nu, P.wind, P.wnod, r_p + nk, u + nk,
+                                                      1.0 / (P.g.h * P.g.h), done); etq_count_launch();
+    ETQ_TRY(lp_pinv_apply(P, u, z_p, done, st));
+  } else if (kind == ETQ_PC_OSEEN_LSC) {
+    // Lp^+ (B M^{-1} F M^{-1} B^T) Lp^+ r   (H = M, reading R26)
+    ETQ_TRY(lp_pinv_apply(P, r_p, u, done, st));
+    BtSubArgs a;
+    a.BxT1 = P.BxT1; a.ByT1 = P.ByT1; a.BxT0 = P.BxT0; a.ByT0 = P.ByT0; a.nq = nq; a.nk = nk; a.reduced = 0;
+    a.r_u = nullptr; a.z_p = u; a.t_u = v; a.done = done;
+    k_bt_minv<<<grid_for(P.BxT1.nslices * 32, BS, 4096), BS, 0, st>>>(a, P.minv); etq_count_launch();
+    launch_vel_spmv(P.Lv, v, w, nq, st);
+    k_scale_minv<<<grid_for(2LL * nq, BS, 4096), BS, 0, st>>>(w, P.minv, v, nq, done); etq_count_launch();
+    k_spmv1<<<grid_for(P.B.nslices * 32, BS, 4096), BS, 0, st>>>(P.B, v, y, 1.0, done); etq_count_launch();
+    ETQ_TRY(lp_pinv_apply(P, y, z_p, done, st));
+  } else {
+    return ETQ_EINVAL;
+  }
+  vec_scale_copy(z_p, z_p, -1.0, np, st);
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
 etq_status oseen_precond_apply(const Problem& P, etq_pc_kind kind, const double* r, double* z, cudaStream_t st) {
   const int64_t nu = P.n_u;
   const double* done = nullptr;
@@ -285,6 +371,8 @@ etq_status oseen_precond_apply(const Problem& P, etq_pc_kind kind, const double*
     // negate z_p1 and zero z_p0
     vec_scale_copy(z + nu, z + nu, -1.0, P.g.nk, st);
     k_fill<<<grid_for(P.g.n0, BS, 4096), BS, 0, st>>>(z + nu + P.g.nk, P.g.n0, 0.0, done); etq_count_launch();
+  } else if (kind == ETQ_PC_OSEEN_M2 || kind == ETQ_PC_OSEEN_LSC) {
+    ETQ_TRY(schur2_apply(P, kind, r + nu, z + nu, done, st));
   } else if (kind == ETQ_PC_OSEEN_M1) {
     if (!P.m1_ready) return ETQ_ENOTSETUP;
     // z_p = -nu Pi C Pi r_p  ( -(1/nu) M_Q~ z_p = r_p, P:1006 )
@@ -322,10 +410,27 @@ etq_status oseen_setup(Problem& P, etq_pc_kind kind) {
     P.m1_ready = true;
     return ETQ_OK;
   }
+  if (kind == ETQ_PC_OSEEN_M2 || kind == ETQ_PC_OSEEN_LSC) {
+    ETQ_TRY(lp_setup(P));
+    if (!P.minv) {
+      ETQ_TRY(dalloc(&P.minv, P.g.nq));
+      ETQ_TRY(velocity_mdiag_inv(P.g, P.minv, P.stream));
+    }
+    for (int i = 0; i < 4; ++i) if (!P.s2w[i]) ETQ_TRY(dalloc(&P.s2w[i], P.n_u));
+    if (kind == ETQ_PC_OSEEN_M2) {
+      if (!P.F1.val) ETQ_TRY(assemble_f1(P.g, P.nu, P.wind, &P.F1, P.stream));
+      for (int i = 0; i < 3; ++i) if (!P.pw[i]) ETQ_TRY(dalloc(&P.pw[i], P.g.nk));
+    }
+    ETQ_CHECK(cudaStreamSynchronize(P.stream));
+    return ETQ_OK;
+  }
   return ETQ_EINVAL;
 }
 
 void oseen_free(Problem& P) {
+  lp_free(P);
+  cudaFree(P.minv); P.minv = nullptr;
+  for (int i = 0; i < 4; ++i) { cudaFree(P.s2w[i]); P.s2w[i] = nullptr; }
   free_hierarchy(P.apH);
   sell_free(P.F1);
   for (int i = 0; i < 3; ++i) { cudaFree(P.pw[i]); P.pw[i] = nullptr; }

@@ -298,7 +298,7 @@ etq_status picard_refresh(Problem& P) {
     ETQ_TRY(dense_inverse_pivot(C.coarse_inv, C.g.nq, st));
     ETQ_TRY(refresh_tail(H));
   }
-  if (P.pcd_ready) {
+  if (P.F1.val) {
     double* nl1;
     ETQ_TRY(dalloc(&nl1, (size_t)16 * P.g.n * P.g.n));
     const int64_t nt = (int64_t)P.g.n * P.g.n * 4;

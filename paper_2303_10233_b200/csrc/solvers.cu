@@ -132,7 +132,8 @@ etq_status precond_apply_ex(const Problem& P, etq_pc_kind kind, const double* r,
                             double* out_u, double* out_p, const double* done, cudaStream_t st) {
   const RedSite* site = &P.red[0];
   const int64_t nu = P.n_u, np = P.n_p;
-  if (kind == ETQ_PC_OSEEN_M1 || kind == ETQ_PC_OSEEN_PCD1) return oseen_precond_apply(P, kind, r, z, st);
+  if (kind == ETQ_PC_OSEEN_M1 || kind == ETQ_PC_OSEEN_PCD1 || kind == ETQ_PC_OSEEN_M2 || kind == ETQ_PC_OSEEN_LSC)
+    return oseen_precond_apply(P, kind, r, z, st);
   if (kind == ETQ_PC_P1_EXACT) {
     if (!P.p1.ready) return ETQ_ENOTSETUP;
     dense_gemv(P.p1.Ainv, P.g.nq, 2, r, P.g.nq, z, P.g.nq, done, st);

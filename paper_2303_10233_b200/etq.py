@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("ETQ_LIB", os.path.join(_HERE, "libetq.so"))
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "etq.h")
 
 ETQ_OK, ETQ_NOT_CONVERGED = 0, 1
-PC_P1_EXACT, PC_P2_GMG, PC_OSEEN_M1, PC_OSEEN_PCD1, PC_P1_ITER, PC_P3 = 0, 1, 2, 3, 4, 5
+PC_P1_EXACT, PC_P2_GMG, PC_OSEEN_M1, PC_OSEEN_PCD1, PC_P1_ITER, PC_P3, PC_OSEEN_M2, PC_OSEEN_LSC = 0, 1, 2, 3, 4, 5, 6, 7
 
 
 class EtqError(RuntimeError):
@@ -351,5 +351,5 @@ class Problem:
         _check(lib().etq_export_operator(self.h, which, level, C.byref(nr), C.byref(nz),
                                          C.c_void_p(rp.ctypes.data), C.c_void_p(col.ctypes.data),
                                          C.c_void_p(val.ctypes.data)), "etq_export_operator")
-        ncol = {0: nr.value, 1: self.n_u, 2: self.n_p, 3: nr.value, 4: nr.value, 5: nr.value}[which]
+        ncol = {0: nr.value, 1: self.n_u, 2: self.n_p, 3: nr.value, 4: nr.value, 5: nr.value, 6: nr.value}[which]
         return sp.csr_matrix((val[:nz.value], col[:nz.value], rp), shape=(nr.value, ncol))

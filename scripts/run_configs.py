@@ -109,6 +109,28 @@ def c4p_case(n=512, steps=5):
     return res
 
 
+def c4s_case(n=512, maxit=400):
+    """NEXT-4: c4's Oseen system with GMRES(50) and the one-stage Schur approximations M2 (two-field
+    PCD) and M3 (LSC), against M1, from x = 0 to ||r|| <= 1e-6 ||b||."""
+    out = {"n": n}
+    for name, kind in (("M1", etq.PC_OSEEN_M1), ("M2", etq.PC_OSEEN_M2), ("LSC", etq.PC_OSEEN_LSC)):
+        P = etq.Problem(n, bc=0, viscosity=0.01, wind=1)
+        t0 = time.perf_counter()
+        P.precond_setup(kind)
+        torch.cuda.synchronize()
+        setup = time.perf_counter() - t0
+        b = zeros(P.N)
+        P.build_rhs(b)
+        x = zeros(P.N)
+        r = P.gmres_solve(kind, b, x, rtol=1e-6, restart=50, maxit=maxit)
+        h = r["history"]
+        out[name] = {"iterations": r["iterations"], "converged": r["converged"], "ms_total": r["ms_total"],
+                     "setup_s": setup, "rel_res_true": r["abs_res"] / float(torch.linalg.norm(b)),
+                     "history_every_25": [float(h[k] / h[0]) for k in range(0, len(h), 25)]}
+        P.close()
+    return out
+
+
 def c5_case(nmax, storage=0):
     pk = peak()
     rows = []
@@ -132,7 +154,7 @@ def c5_case(nmax, storage=0):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c1,c2,c3,c4,c4p,c5")
+    ap.add_argument("--only", default="c1,c2,c3,c4,c4p,c4s,c5")
     ap.add_argument("--c5-max", type=int, default=2048)
     args = ap.parse_args()
     which = set(args.only.split(","))
@@ -147,6 +169,8 @@ def main():
         res["c4"] = c4_case(512)
     if "c4p" in which:
         res["c4p"] = c4p_case(512)
+    if "c4s" in which:
+        res["c4s"] = c4s_case(512)
     if "c5" in which:
         res["c5"] = c5_case(args.c5_max)
         res["c5_explicit_sell"] = c5_case(args.c5_max, storage=2)

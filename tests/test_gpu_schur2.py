@@ -1,0 +1,102 @@
+"""GPU parity of SURVEY §8(f) NEXT-4: the two-field pressure Laplacian and its multigrid-CG
+pseudo-inverse, the two-field PCD preconditioner M2 (with the P0 operator F0, reading R25) and the
+LSC preconditioner M3 (H = M, reading R26), against oracle.schur2 (exact Lp^+ by sparse LU)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import fem, krylov, oseen, schur2  # noqa: E402
+from paper_2303_10233_b200 import etq  # noqa: E402
+import synth  # noqa: E402
+
+DEV = torch.device("cuda:0")
+NU = 0.01
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device=DEV)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def sp_rel_diff(A, B):
+    D = (A - B).tocsr()
+    return (np.abs(D.data).max() if D.nnz else 0.0) / np.abs(B.data).max()
+
+
+def _problem(n, kind, **kw):
+    P = etq.Problem(n, bc=0, viscosity=NU, wind=1)
+    P.precond_setup(kind, etq.make_params(**kw))
+    return P
+
+
+@pytest.mark.parametrize("n", [4, 16])
+def test_two_field_laplacian_levels_entrywise(n):
+    P = _problem(n, etq.PC_OSEEN_LSC)
+    l, m = 0, n
+    while True:
+        ref = schur2.two_field_laplacian(fem.assemble_system(m))
+        assert sp_rel_diff(P.export_operator(6, l), ref) < 1e-13, m
+        if m <= 2:
+            break
+        l, m = l + 1, m // 2
+
+
+@pytest.mark.parametrize("kind", [etq.PC_OSEEN_M2, etq.PC_OSEEN_LSC])
+@pytest.mark.parametrize("n", [8, 32])
+def test_block_triangular_apply_matches_oracle(kind, n):
+    """z = M^{-1} r for M2 / M3 (block upper-triangular) with the inner Lp CG at 1e-13."""
+    s = fem.assemble_system(n, nu=NU)
+    g = s.g
+    x, y = g.node_xy()
+    wx, wy = fem.cavity_wind(x, y)
+    hF = oseen.velocity_hierarchy(n, NU)
+    if kind == etq.PC_OSEEN_M2:
+        S = schur2.TwoFieldPCD(s, NU, fem.pcd_f1(g, NU), schur2.f0_jump(g, NU, wx, wy))
+    else:
+        S = schur2.LSCSchur(s)
+    Mo = schur2.OseenBlockTriangular(s, hF, S)
+    P = _problem(n, kind, inner_rtol=1e-13)
+    r = synth.random_vector(g.N, seed=41)
+    z = torch.zeros(g.N, dtype=torch.float64, device=DEV)
+    P.apply_precond(kind, dev(r), z)
+    zg, zr = host(z), Mo(r)
+    np.testing.assert_allclose(zg[g.n_u:], zr[g.n_u:], rtol=0, atol=1e-9 * np.abs(zr[g.n_u:]).max())
+    np.testing.assert_allclose(zg, zr, rtol=0, atol=1e-9 * np.abs(zr).max())
+
+
+def test_gmres_m2_stagnates_and_lsc_converges_like_the_oracle():
+    """GMRES on the c4-type cavity (n = 16, nu = 0.01): M2's residual path follows the oracle's
+    (fast initial phase, then stagnation); M3 converges in the oracle's count."""
+    n = 16
+    s = fem.assemble_system(n, nu=NU)
+    g = s.g
+    x, y = g.node_xy()
+    wx, wy = fem.cavity_wind(x, y)
+    hF = oseen.velocity_hierarchy(n, NU)
+    nb = np.linalg.norm(s.b)
+    for kind, S in ((etq.PC_OSEEN_M2, schur2.TwoFieldPCD(s, NU, fem.pcd_f1(g, NU), schur2.f0_jump(g, NU, wx, wy))),
+                    (etq.PC_OSEEN_LSC, schur2.LSCSchur(s))):
+        _, ro = krylov.gmres(lambda v: s.K @ v, s.b, schur2.OseenBlockTriangular(s, hF, S), tol_abs=1e-6 * nb,
+                             restart=50, maxit=120)
+        P = _problem(n, kind, inner_rtol=1e-13)
+        b = torch.zeros(P.N, dtype=torch.float64, device=DEV)
+        P.build_rhs(b)
+        xg = torch.zeros(P.N, dtype=torch.float64, device=DEV)
+        rep = P.gmres_solve(kind, b, xg, rtol=1e-6, restart=50, maxit=120)
+        hg = rep["history"]
+        k = min(40, len(hg), len(ro.history))
+        np.testing.assert_allclose(hg[:k], ro.history[:k], rtol=1e-6)
+        if kind == etq.PC_OSEEN_M2:
+            assert not rep["converged"] and hg[-1] > 1e-3 * hg[0] and hg[10] < 1e-2 * hg[0]
+        else:
+            assert rep["converged"] and abs(rep["iterations"] - ro.iterations) <= 2
