@@ -253,7 +253,8 @@ etq_status etq_time_kernel(etq_problem* p, int32_t which, int32_t reps, double* 
 /* Process-wide implementation switches (A/B tests; results are bitwise identical either way):
  *   option 0 = temporally blocked Chebyshev smoothing on the Stokes interior-stencil levels
  *              (value 1 = on [default], 0 = one kernel per Chebyshev step);
- *   option 1 = coarsest level n that uses it [64] (smaller grids are launch-latency bound).
+ *   option 1 = coarsest level n that uses it [64] (smaller grids are launch-latency bound);
+ *   option 2 = launch priority of the Chebyshev-SGS pressure kernels (0 = lowest [default], 1 = highest).
  * Applies to solves whose CUDA graphs are captured afterwards (re-run etq_precond_setup). */
 etq_status etq_set_option(int32_t option, int32_t value);
 

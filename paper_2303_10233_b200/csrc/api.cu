@@ -12,6 +12,7 @@ struct etq_problem { Problem P; };
 static std::atomic<int64_t> g_launches{0};
 bool g_cheb_tile_enabled = true;   // etq_set_option(0): temporally blocked smoothing on/off
 int g_cheb_tile_min_n = 64;         // etq_set_option(1): coarsest level n that uses it
+bool g_sgs_high_prio = false;       // etq_set_option(2): Chebyshev-SGS kernels at the highest priority
 void etq_count_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 int64_t etq_launch_total() { return g_launches.load(std::memory_order_relaxed); }
 
@@ -672,6 +673,7 @@ etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* 
 etq_status etq_set_option(int32_t option, int32_t value) {
   if (option == 0) { g_cheb_tile_enabled = value != 0; return ETQ_OK; }
   if (option == 1) { if (value < 2) return ETQ_EINVAL; g_cheb_tile_min_n = value; return ETQ_OK; }
+  if (option == 2) { g_sgs_high_prio = value != 0; return ETQ_OK; }
   return ETQ_EINVAL;
 }
 

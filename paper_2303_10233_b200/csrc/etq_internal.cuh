@@ -35,7 +35,8 @@
 void etq_last_cuda_error(cudaError_t e, const char* file, int line);
 void etq_count_launch(int64_t k = 1);
 extern bool g_cheb_tile_enabled;          // api.cu; etq_set_option(0)
-extern int g_cheb_tile_min_n;             // api.cu; etq_set_option(1)   // host-side launch counter (etq_launch_count)
+extern int g_cheb_tile_min_n;             // api.cu; etq_set_option(1)
+extern bool g_sgs_high_prio;              // api.cu; etq_set_option(2)   // host-side launch counter (etq_launch_count)
 
 constexpr int SELL_C = 32;           // slice height = warp size
 constexpr int RED_BLOCKS = 592;      // 4 x 148 SMs: grid of plain reduction kernels

@@ -931,10 +931,30 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, const SgsSme
   __syncthreads();
   SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
 #undef SGS_V
-  // ---- write the tile (coalesced rows) with the semi-iteration update
+  // ---- write the tile (coalesced rows) with the semi-iteration update.  The y / y_prev loads of all
+  //      of this thread's outputs are issued before any is used (one memory latency, not six).
+  constexpr int NL = (T + SGS_TY - 1) / SGS_TY;   // 3 row passes
+  double yv[NL][2][2], ypv[NL][2][2];           // [pass][u][vertex, cell]
+#pragma unroll
+  for (int q = 0; q < NL; ++q) {
+    const int lc = H + ty + SGS_TY * q, gc = C0 + lc;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int la = H + tx + 32 * u, ga = A0 + la;
+      const bool okt = lc < H + T && la < H + T;
+      const bool okv = okt && (IN || (ga <= n && gc <= n)), okc = okt && (IN || (ga < n && gc < n));
+      const int iv = okv ? ga + n1 * gc : 0, ic = okc ? nk + ga + n * gc : 0;
+      yv[q][u][0] = (a.mode && a.y && okv) ? a.y[iv] : 0.0;
+      yv[q][u][1] = (a.mode && a.y && okc) ? a.y[ic] : 0.0;
+      ypv[q][u][0] = (a.mode && a.yp && okv) ? a.yp[iv] : 0.0;
+      ypv[q][u][1] = (a.mode && a.yp && okc) ? a.yp[ic] : 0.0;
+    }
+  }
   double kd = 0.0;
-  for (int lc = H + ty; lc < H + T; lc += SGS_TY) {
-    const int gc = C0 + lc;
+#pragma unroll
+  for (int q = 0; q < NL; ++q) {
+    const int lc = H + ty + SGS_TY * q, gc = C0 + lc;
+    if (lc >= H + T) continue;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int la = H + tx + 32 * u, ga = A0 + la;
@@ -944,7 +964,7 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, const SgsSme
         const double v = S.vl(la, lc);
         double o = v;
         if (a.mode) {
-          const double y = a.y ? a.y[idx] : 0.0, yp = a.yp ? a.yp[idx] : 0.0;
+          const double y = yv[q][u][0], yp = ypv[q][u][0];
           o = a.omega * (a.gam * (v - y) + y - yp) + yp;
         }
         a.out[idx] = o;
@@ -955,7 +975,7 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, const SgsSme
         const double v = S.cl(la, lc);
         double o = v;
         if (a.mode) {
-          const double y = a.y ? a.y[idx] : 0.0, yp = a.yp ? a.yp[idx] : 0.0;
+          const double y = yv[q][u][1], yp = ypv[q][u][1];
           o = a.omega * (a.gam * (v - y) + y - yp) + yp;
         }
         a.out[idx] = o;
@@ -1761,13 +1781,13 @@ static void launch_sgs_tile(SgsTileArgs a, cudaStream_t st) {
   const int tiles = a.tiles_x * a.tiles_x;
   // the latency-bound pressure chain runs at the lowest priority so that the concurrent,
   // bandwidth-bound V-cycle blocks are scheduled first (the attribute is kept by graph capture)
-  static int lo_prio = 1;
-  if (lo_prio == 1) { int hi; cudaDeviceGetStreamPriorityRange(&lo_prio, &hi); }
+  static int lo_prio = 1, hi_prio = 0;
+  if (lo_prio == 1) cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles); cfg.blockDim = dim3(SGS_TX, SGS_TY); cfg.dynamicSmemBytes = SGS_SMEM; cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributePriority;
-  attr[0].val.priority = lo_prio;
+  attr[0].val.priority = g_sgs_high_prio ? hi_prio : lo_prio;
   cfg.attrs = attr; cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k_sgs_tile, a); etq_count_launch();
 }
