@@ -12,6 +12,7 @@ struct etq_problem { Problem P; };
 static std::atomic<int64_t> g_launches{0};
 bool g_cheb_tile_enabled = true;   // etq_set_option(0): temporally blocked smoothing on/off
 int g_cheb_tile_min_n = 64;         // etq_set_option(1): coarsest level n that uses it
+bool g_saddle_mf = true;            // etq_set_option(2): matrix-free Stokes saddle apply
 bool g_sgs_high_prio = false;       // etq_set_option(2): Chebyshev-SGS kernels at the highest priority
 void etq_count_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 int64_t etq_launch_total() { return g_launches.load(std::memory_order_relaxed); }
@@ -169,6 +170,11 @@ etq_status etq_assemble(const etq_grid* grid, double viscosity, const etq_wind* 
   A_TRY(build_node_perm(P.g, &P.node_perm, &nsl, P.stream));
   A_TRY(assemble_velocity_op(P.g, P.oseen, P.nu, P.wind, P.node_perm, nsl, &P.Lv, P.stream));
   if (P.storage < 2) A_TRY(mark_implicit(P.g, P.oseen, P.nu, P.wind, P.Lv, P.stream, P.storage == 0));
+  if (!P.oseen && P.storage == 0 && P.g.n >= 16 && P.Lv.stval) {   // matrix-free Stokes saddle apply
+    A_TRY(class_weights(P.g, P.Lv, &P.so0));
+    A_TRY(saddle_weights(P.g, &P.sst, P.stream));
+    P.mf_on = true;
+  }
   A_TRY(assemble_bt(P.g, 0, 0, P.node_perm, nsl, &P.BxT1, P.stream));
   A_TRY(assemble_bt(P.g, 1, 0, P.node_perm, nsl, &P.ByT1, P.stream));
   A_TRY(assemble_bt(P.g, 0, 1, P.node_perm, nsl, &P.BxT0, P.stream));
@@ -673,6 +679,7 @@ etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* 
 etq_status etq_set_option(int32_t option, int32_t value) {
   if (option == 0) { g_cheb_tile_enabled = value != 0; return ETQ_OK; }
   if (option == 1) { if (value < 2) return ETQ_EINVAL; g_cheb_tile_min_n = value; return ETQ_OK; }
+  if (option == 2) { g_saddle_mf = value != 0; return ETQ_OK; }
   if (option == 2) { g_sgs_high_prio = value != 0; return ETQ_OK; }
   return ETQ_EINVAL;
 }

@@ -826,6 +826,76 @@ etq_status mark_implicit(const Geo& g, bool oseen, double nu, int wind, Sell& S,
 
 // Interior stencil of a Stokes level: rectangle [4, m-5]^2, per-class weights
 // from the verified value dictionary, and a SELL over the remaining (frame) rows.
+// B / B^T weights at deep-interior reference positions (the same 1-D table products as bt_row / b_row;
+// every non-Dirichlet row equals them, so the saddle operator can be applied matrix-free)
+__global__ void k_saddle_weights(Geo g, SaddleSt* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int n = g.n; const double h = g.h;
+  const int r = n / 2;
+  for (int c = 0; c < 4; ++c) {
+    const int i = 2 * r + (c & 1), j = 2 * r + (c >> 1);
+    for (int dc = -1; dc <= 1; ++dc)
+      for (int da = -1; da <= 1; ++da) {
+        const int a = i / 2 + da, cc = j / 2 + dc;
+        out->bt1[c][0][(dc + 1) * 3 + da + 1] = -g1(n, a, i) * h1(n, h, cc, j);
+        out->bt1[c][1][(dc + 1) * 3 + da + 1] = -h1(n, h, a, i) * g1(n, cc, j);
+      }
+    for (int df = -1; df <= 0; ++df)
+      for (int de = -1; de <= 0; ++de) {
+        const int e = i / 2 + de, f = j / 2 + df;
+        out->bt0[c][0][(df + 1) * 2 + de + 1] = -e1(e, i) * w1(h, f, j);
+        out->bt0[c][1][(df + 1) * 2 + de + 1] = -w1(h, e, i) * e1(f, j);
+      }
+  }
+  for (int dj = -2; dj <= 2; ++dj) {
+    const int jj = 2 * r + dj;
+    const double hc = h1(n, h, r, jj), gc = g1(n, r, jj);
+    for (int di = -2; di <= 2; ++di) {
+      const int ii = 2 * r + di;
+      out->b1[0][(dj + 2) * 5 + di + 2] = -g1(n, r, ii) * hc;
+      out->b1[1][(dj + 2) * 5 + di + 2] = -h1(n, h, r, ii) * gc;
+    }
+  }
+  for (int dj = 0; dj <= 2; ++dj)
+    for (int di = 0; di <= 2; ++di) {
+      const int ii = 2 * r + di, jj = 2 * r + dj;
+      out->b0[0][dj * 3 + di] = -e1(r, ii) * w1(h, r, jj);
+      out->b0[1][dj * 3 + di] = -w1(h, r, ii) * e1(r, jj);
+    }
+}
+
+etq_status saddle_weights(const Geo& g, SaddleSt* out, cudaStream_t st) {
+  SaddleSt* d;
+  ETQ_TRY(dalloc(&d, 1));
+  k_saddle_weights<<<1, 32, 0, st>>>(g, d); etq_count_launch();
+  ETQ_CHECK(cudaMemcpyAsync(out, d, sizeof(SaddleSt), cudaMemcpyDeviceToHost, st));
+  ETQ_CHECK(cudaStreamSynchronize(st));
+  cudaFree(d);
+  return ETQ_OK;
+}
+
+// class stencil w[4][25] of a Stokes velocity operator from its per-class dictionary (stval)
+etq_status class_weights(const Geo& g, const Sell& A, StencilOp* so) {
+  if (!A.stval || !A.stoff) return ETQ_EINVAL;
+  std::vector<double> sv(4 * 32);
+  ETQ_CHECK(cudaMemcpy(sv.data(), A.stval, sizeof(double) * sv.size(), cudaMemcpyDeviceToHost));
+  StencilOp o;
+  o.m = g.m; o.lo = 4; o.hi = g.m - 5;
+  for (int c = 0; c < 4; ++c) {
+    for (int t = 0; t < 25; ++t) o.w[c][t] = 0.0;
+    const int px = c & 1, py = c >> 1, rx = px ? 1 : 2, ry = py ? 1 : 2;
+    int k = 0;
+    for (int dj = -ry; dj <= ry; ++dj)
+      for (int di = -rx; di <= rx; ++di) {   // Stokes enumeration of vel_row (cancelled taps dropped)
+        if ((di == 2 || di == -2) && dj == 0 && py) continue;
+        if ((dj == 2 || dj == -2) && di == 0 && px) continue;
+        o.w[c][(dj + 2) * 5 + (di + 2)] = sv[c * 32 + k++];
+      }
+  }
+  *so = o;
+  return ETQ_OK;
+}
+
 etq_status build_stencil_level(const Geo& g, const Sell& A, StencilOp* so, Sell* frame, cudaStream_t st) {
   if (!A.stval || !A.stoff || g.n < 16) return ETQ_EINVAL;
   std::vector<double> sv(4 * 32);

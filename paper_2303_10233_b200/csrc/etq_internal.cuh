@@ -36,6 +36,7 @@ void etq_last_cuda_error(cudaError_t e, const char* file, int line);
 void etq_count_launch(int64_t k = 1);
 extern bool g_cheb_tile_enabled;          // api.cu; etq_set_option(0)
 extern int g_cheb_tile_min_n;             // api.cu; etq_set_option(1)
+extern bool g_saddle_mf;                  // api.cu; etq_set_option(2)
 extern bool g_sgs_high_prio;              // api.cu; etq_set_option(2)   // host-side launch counter (etq_launch_count)
 
 constexpr int SELL_C = 32;           // slice height = warp size
@@ -100,6 +101,14 @@ struct StencilOp {
   int64_t nseg = 0;
   double w[4][25];
   double dcls[4] = {0.0, 0.0, 0.0, 0.0};   // D^-1 of the non-Dirichlet rows per class
+};
+
+// translation-invariant B / B^T weights of the Stokes saddle operator (matrix-free k_saddle_mf)
+struct SaddleSt {
+  double bt1[4][2][9];        // B^T Q1 part per velocity class: vertices (i/2 + da, j/2 + dc), dc outer
+  double bt0[4][2][4];        // B^T P0 part per velocity class: cells (i/2 + de, j/2 + df), de, df in {-1, 0}
+  double b1[2][25];           // B Q1 rows: velocity nodes (2a + di, 2c + dj), dj outer, per component
+  double b0[2][9];            // B P0 rows: velocity nodes (2e + di, 2f + dj), di, dj in {0, 1, 2}
 };
 
 // ---------------------------------------------------------------- MG level
@@ -219,6 +228,9 @@ struct Problem {
   Sell Lv;                                    // scalar velocity operator, level-0 rows, node perm
   Sell BxT1, ByT1, BxT0, ByT0;                // B^T split by component and pressure part
   Sell B;                                     // pressure rows (Q1 then P0) over [u_x; u_y]
+  bool mf_on = false;                         // Stokes storage 0: matrix-free saddle apply (k_saddle_mf)
+  StencilOp so0;                              // class stencil of L (level 0)
+  SaddleSt sst;                               // B / B^T weights
   int* node_perm = nullptr;                   // shared by Lv and the B^T blocks
 
   Hierarchy mg;                               // velocity-block V-cycle
@@ -298,6 +310,8 @@ etq_status sell_diag_inv(const Sell& A, double* dinv, cudaStream_t st);
 etq_status build_rhs_dev(const Problem& P, const double* f_nodal, double* b);
 etq_status mark_implicit(const Geo& g, bool oseen, double nu, int wind, Sell& S, cudaStream_t st, bool values);
 etq_status build_stencil_level(const Geo& g, const Sell& A, StencilOp* so, Sell* frame, cudaStream_t st);
+etq_status saddle_weights(const Geo& g, SaddleSt* out, cudaStream_t st);
+etq_status class_weights(const Geo& g, const Sell& A, StencilOp* so);
 
 // ops.cu
 void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y, const double* inv_scale,

@@ -83,6 +83,135 @@ __global__ void __launch_bounds__(BS) k_saddle(SaddleArgs a) {
   }
 }
 
+// Matrix-free saddle apply for the Stokes operator (storage 0): every non-Dirichlet row of L, B^T and
+// B is a translation-invariant class stencil (Dirichlet columns removed, reading R2), so only the
+// vectors are streamed: 16 B per unknown (x in, y out) plus cached neighbour gathers, instead of the
+// ~0.9 GB of B / B^T entries per apply at n = 1024.  Per-row arithmetic and summation order are those
+// of k_saddle over the stored rows (bitwise-identical results).
+struct SaddleMfArgs {
+  StencilOp so; SaddleSt w;
+  int nq, nk; int64_t n_u, n_p; int reduced;
+  const double* x; double* y; const double* inv_scale;
+  RedSite site; int slot; double* dot_out; const double* done;
+};
+__global__ void __launch_bounds__(BS) k_saddle_mf(SaddleMfArgs a) {
+  if (is_done(a.done)) return;
+  const double sc = a.inv_scale ? *a.inv_scale : 1.0;
+  const int m = a.so.m, n = (m - 1) / 2, n1 = n + 1;
+  const double* xu = a.x;
+  const double* xv = a.x + a.nq;
+  const double* p1 = a.x + a.n_u;
+  const double* p0 = p1 + a.nk;
+  double dot = 0.0;
+  const int64_t tot = (int64_t)a.nq + a.n_p;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < a.nq) {
+      const int node = (int)t, i = node % m, j = node / m;
+      double ax, ay;
+      if (i == 0 || j == 0 || i == m - 1 || j == m - 1) {   // identity row; B^T rows are empty
+        ax = fma(1.0, xu[node], 0.0) + 0.0;
+        ay = fma(1.0, xv[node], 0.0) + 0.0;
+        if (!a.reduced) { ax += 0.0; ay += 0.0; }
+      } else {
+        const int cl = (j & 1) * 2 + (i & 1);
+        const double* w = a.so.w[cl];
+        const bool near = i < 3 || j < 3 || i > m - 4 || j > m - 4;
+        double a0 = 0.0, a1 = 0.0;
+        for (int dj = -2; dj <= 2; ++dj) {
+          if ((j & 1) && (dj == 2 || dj == -2)) continue;
+          const int jt = j + dj;
+          if (near && (jt <= 0 || jt >= m - 1)) continue;
+          const int rb = node + dj * m;
+#pragma unroll
+          for (int di = -2; di <= 2; ++di) {
+            if (near && (i + di <= 0 || i + di >= m - 1)) continue;
+            const double wv = w[(dj + 2) * 5 + (di + 2)];
+            a0 = fma(wv, __ldg(xu + rb + di), a0);
+            a1 = fma(wv, __ldg(xv + rb + di), a1);
+          }
+        }
+        // B^T Q1 part: vertices (i/2 + da, j/2 + dc) in [0, n]^2, dc outer
+        double bx = 0.0, by = 0.0;
+        const int ia = i / 2, jc = j / 2;
+#pragma unroll
+        for (int dc = -1; dc <= 1; ++dc) {
+          const int c = jc + dc;
+          if (c < 0 || c > n) continue;
+#pragma unroll
+          for (int da = -1; da <= 1; ++da) {
+            const int aa = ia + da;
+            if (aa < 0 || aa > n) continue;
+            const double pv = __ldg(p1 + aa + (int64_t)n1 * c);
+            bx = fma(a.w.bt1[cl][0][(dc + 1) * 3 + da + 1], pv, bx);
+            by = fma(a.w.bt1[cl][1][(dc + 1) * 3 + da + 1], pv, by);
+          }
+        }
+        ax = a0 + bx; ay = a1 + by;
+        if (!a.reduced) {
+          double cx = 0.0, cy = 0.0;
+#pragma unroll
+          for (int df = -1; df <= 0; ++df) {
+            const int f = jc + df;
+            if (f < 0 || f >= n) continue;
+#pragma unroll
+            for (int de = -1; de <= 0; ++de) {
+              const int e = ia + de;
+              if (e < 0 || e >= n) continue;
+              const double pv = __ldg(p0 + e + (int64_t)n * f);
+              cx = fma(a.w.bt0[cl][0][(df + 1) * 2 + de + 1], pv, cx);
+              cy = fma(a.w.bt0[cl][1][(df + 1) * 2 + de + 1], pv, cy);
+            }
+          }
+          ax += cx; ay += cy;
+        }
+      }
+      ax *= sc; ay *= sc;
+      a.y[node] = ax; a.y[a.nq + node] = ay;
+      if (a.dot_out) dot += ax * (sc * xu[node]) + ay * (sc * xv[node]);
+    } else {
+      const int64_t row = t - a.nq;
+      double acc = 0.0;
+      if (row < a.nk) {
+        const int aa = (int)(row % n1), c = (int)(row / n1);
+        for (int dj = -2; dj <= 2; ++dj) {
+          const int jj = 2 * c + dj;
+          if (jj < 1 || jj > m - 2) continue;
+#pragma unroll
+          for (int di = -2; di <= 2; ++di) {
+            const int ii = 2 * aa + di;
+            if (ii < 1 || ii > m - 2) continue;
+            const int64_t v = ii + (int64_t)m * jj;
+            acc = fma(a.w.b1[0][(dj + 2) * 5 + di + 2], __ldg(xu + v), acc);
+            acc = fma(a.w.b1[1][(dj + 2) * 5 + di + 2], __ldg(xv + v), acc);
+          }
+        }
+      } else {
+        const int tt = (int)(row - a.nk), e = tt % n, f = tt / n;
+        for (int dj = 0; dj <= 2; ++dj) {
+          const int jj = 2 * f + dj;
+          if (jj < 1 || jj > m - 2) continue;
+#pragma unroll
+          for (int di = 0; di <= 2; ++di) {
+            const int ii = 2 * e + di;
+            if (ii < 1 || ii > m - 2) continue;
+            const int64_t v = ii + (int64_t)m * jj;
+            acc = fma(a.w.b0[0][dj * 3 + di], __ldg(xu + v), acc);
+            acc = fma(a.w.b0[1][dj * 3 + di], __ldg(xv + v), acc);
+          }
+        }
+      }
+      acc *= sc;
+      if (a.reduced && row >= a.nk) acc = 0.0;
+      a.y[a.n_u + row] = acc;
+      if (a.dot_out) dot += acc * (sc * p1[row]);
+    }
+  }
+  if (a.dot_out) {
+    double v[1] = {dot};
+    reduce_finish<1>(v, a.site, a.slot, a.dot_out);
+  }
+}
+
 // scalar operator on two components: y_c = A x_c
 __global__ void __launch_bounds__(BS) k_vel_spmv2(Sell A, int nq, const double* x, double* y) {
   const int lane = threadIdx.x & 31;
@@ -1096,6 +1225,14 @@ void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y
   a.nq = P.g.nq; a.nk = P.g.nk; a.n_u = P.n_u; a.n_p = P.n_p; a.reduced = reduced ? 1 : 0;
   a.x = x; a.y = y; a.inv_scale = inv_scale;
   a.site = site ? *site : RedSite{}; a.slot = slot; a.dot_out = dot_out; a.done = done;
+  if (P.mf_on && g_saddle_mf) {
+    SaddleMfArgs b;
+    b.so = P.so0; b.w = P.sst;
+    b.nq = P.g.nq; b.nk = P.g.nk; b.n_u = P.n_u; b.n_p = P.n_p; b.reduced = a.reduced;
+    b.x = x; b.y = y; b.inv_scale = inv_scale; b.site = a.site; b.slot = slot; b.dot_out = dot_out; b.done = done;
+    k_saddle_mf<<<grid_for(P.N, BS, 8 * 148 * 2), BS, 0, st>>>(b); etq_count_launch();
+    return;
+  }
   const int64_t warps = P.Lv.nslices + P.B.nslices;
   const int grid = grid_for(warps * 32, BS);
   k_saddle<<<grid, BS, 0, st>>>(a); etq_count_launch();

@@ -55,3 +55,26 @@ def test_set_option_rejects_unknown():
         etq.set_option(7, 1)
     with pytest.raises(etq.EtqError):
         etq.set_option(1, 0)
+
+
+@pytest.mark.parametrize("n", [16, 64, 256])
+def test_matrix_free_saddle_bitwise_equal(n):
+    """The matrix-free Stokes saddle apply (class stencils of L, B^T and B) equals the stored-row
+    apply bitwise, full and reduced."""
+    ys = {}
+    x = None
+    for opt in (0, 1):
+        etq.set_option(2, opt)
+        try:
+            P = etq.Problem(n)
+            x = torch.as_tensor(synth.random_vector(P.N, seed=7), device="cuda")
+            for red in (False, True):
+                y = torch.zeros(P.N, dtype=torch.float64, device="cuda")
+                P.apply_saddle(x, y, reduced=red)
+                torch.cuda.synchronize()
+                ys[(opt, red)] = y.cpu().numpy()
+            P.close()
+        finally:
+            etq.set_option(2, 1)
+    for red in (False, True):
+        np.testing.assert_array_equal(ys[(0, red)], ys[(1, red)])
