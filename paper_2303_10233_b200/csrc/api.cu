@@ -13,6 +13,7 @@ static std::atomic<int64_t> g_launches{0};
 bool g_cheb_tile_enabled = true;   // etq_set_option(0): temporally blocked smoothing on/off
 int g_cheb_tile_min_n = 64;         // etq_set_option(1): coarsest level n that uses it
 bool g_saddle_mf = true;            // etq_set_option(2): matrix-free Stokes saddle apply
+bool g_minres_devloop = true;       // etq_set_option(3): MINRES loop as a CUDA-graph while node
 bool g_sgs_high_prio = false;       // etq_set_option(2): Chebyshev-SGS kernels at the highest priority
 void etq_count_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 int64_t etq_launch_total() { return g_launches.load(std::memory_order_relaxed); }
@@ -229,6 +230,8 @@ etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_para
     if (P.minres_graph[g]) { cudaGraphExecDestroy(P.minres_graph[g]); P.minres_graph[g] = nullptr; }
   }
   P.minres_graph_kind = -1;
+  if (P.minres_wgraph) { cudaGraphExecDestroy(P.minres_wgraph); P.minres_wgraph = nullptr; }
+  P.minres_wgraph_kind = -1;
   if (kind == ETQ_PC_P3 || kind == ETQ_PC_P1_ITER) {
     if (P.oseen) return ETQ_EINVAL;
     if (!is_pow2(P.g.n) || !is_pow2(prm.coarse_n) || prm.coarse_n > P.g.n || !is_pow2(prm.inner_coarse_n))
@@ -680,6 +683,7 @@ etq_status etq_set_option(int32_t option, int32_t value) {
   if (option == 0) { g_cheb_tile_enabled = value != 0; return ETQ_OK; }
   if (option == 1) { if (value < 2) return ETQ_EINVAL; g_cheb_tile_min_n = value; return ETQ_OK; }
   if (option == 2) { g_saddle_mf = value != 0; return ETQ_OK; }
+  if (option == 3) { g_minres_devloop = value != 0; return ETQ_OK; }
   if (option == 2) { g_sgs_high_prio = value != 0; return ETQ_OK; }
   return ETQ_EINVAL;
 }
@@ -689,6 +693,8 @@ void etq_destroy(etq_problem* h) {
   Problem& P = h->P;
   if (P.stream) cudaStreamSynchronize(P.stream);
   for (int g = 0; g < 2; ++g) if (P.minres_graph[g]) cudaGraphExecDestroy(P.minres_graph[g]);
+  if (P.minres_wgraph) cudaGraphExecDestroy(P.minres_wgraph);
+  if (P.wcs) cudaStreamDestroy(P.wcs);
   free_hierarchy(P.mg);
   exact_free(P);
   oseen_free(P);

@@ -36,6 +36,7 @@ void etq_last_cuda_error(cudaError_t e, const char* file, int line);
 void etq_count_launch(int64_t k = 1);
 extern bool g_cheb_tile_enabled;          // api.cu; etq_set_option(0)
 extern int g_cheb_tile_min_n;             // api.cu; etq_set_option(1)
+extern bool g_minres_devloop;             // api.cu; etq_set_option(3)
 extern bool g_saddle_mf;                  // api.cu; etq_set_option(2)
 extern bool g_sgs_high_prio;              // api.cu; etq_set_option(2)   // host-side launch counter (etq_launch_count)
 
@@ -281,6 +282,11 @@ struct Problem {
   int minres_graph_kind = -1;
   const double* minres_graph_x = nullptr;     // graphs bake in the caller's x pointer
   int64_t minres_graph_nodes[2] = {0, 0};     // kernel launches per graph launch
+  cudaGraphExec_t minres_wgraph = nullptr;    // device-side loop: while (!done) { 2 iterations }
+  int minres_wgraph_kind = -1;
+  const double* minres_wgraph_x = nullptr;
+  int64_t minres_wbody_nodes = 0, minres_wfixed_nodes = 0;
+  cudaStream_t wcs = nullptr;                 // capture stream of the loop body
   double* tk = nullptr;                       // scratch for etq_time_kernel (3 x N)
   float* tkf = nullptr;                       // fp32 scratch (2 x N)
 };

@@ -168,6 +168,12 @@ etq_status precond_apply_ex(const Problem& P, etq_pc_kind kind, const double* r,
   return ETQ_ENOTSETUP;
 }
 
+// device-side MINRES loop: the WHILE node's condition is "not done" (set before the loop and at the
+// end of every two-iteration body)
+__global__ void k_minres_cond(const double* sc, cudaGraphConditionalHandle h) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) cudaGraphSetConditional(h, sc[S_DONE] != 0.0 ? 0u : 1u);
+}
+
 static etq_status minres_alloc(Problem& P) {
   if (P.nkv >= 7) return ETQ_OK;
   for (int i = P.nkv; i < 7; ++i) ETQ_TRY(dalloc(&P.kv[i], P.N));
@@ -230,7 +236,58 @@ etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, 
   ETQ_CHECK(cudaGetLastError());
 
   const bool graphs = P.params.use_graphs != 0;
-  if (graphs && (P.minres_graph_kind != (int)kind || P.minres_graph_x != x || !P.minres_graph[0])) {
+  const bool devloop = graphs && g_minres_devloop;
+  if (devloop && (P.minres_wgraph_kind != (int)kind || P.minres_wgraph_x != x || !P.minres_wgraph)) {
+    // one graph: while (!done) { iteration(cur = 1); iteration(cur = 0); cond = !done }
+    if (P.minres_wgraph) { cudaGraphExecDestroy(P.minres_wgraph); P.minres_wgraph = nullptr; }
+    if (!P.wcs) ETQ_CHECK(cudaStreamCreateWithFlags(&P.wcs, cudaStreamNonBlocking));
+    cudaGraph_t graph;
+    const int64_t before = etq_launch_total();
+    ETQ_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    cudaStreamCaptureStatus cst;
+    cudaGraph_t cg;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    etq_status s = ETQ_OK;
+    cudaGraphConditionalHandle hc;
+    cudaError_t e = cudaStreamGetCaptureInfo(st, &cst, nullptr, &cg, &deps, &nd);
+    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hc, cg, 1u, cudaGraphCondAssignDefault);
+    if (e == cudaSuccess) { k_minres_cond<<<1, 32, 0, st>>>(sc, hc); etq_count_launch(); e = cudaGetLastError(); }
+    if (e == cudaSuccess) e = cudaStreamGetCaptureInfo(st, &cst, nullptr, &cg, &deps, &nd);
+    cudaGraphNode_t node;
+    cudaGraphNodeParams np = {};
+    if (e == cudaSuccess) {
+      np.type = cudaGraphNodeTypeConditional;
+      np.conditional.handle = hc;
+      np.conditional.type = cudaGraphCondTypeWhile;
+      np.conditional.size = 1;
+      e = cudaGraphAddNode(&node, cg, deps, nd, &np);
+    }
+    const int64_t b0 = etq_launch_total();
+    if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(P.wcs, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                            cudaStreamCaptureModeRelaxed);
+    if (e == cudaSuccess) {
+      s = minres_iteration(P, kind, 1, x, P.wcs);
+      if (s >= 0) s = minres_iteration(P, kind, 0, x, P.wcs);
+      if (s >= 0) { k_minres_cond<<<1, 32, 0, P.wcs>>>(sc, hc); etq_count_launch(); }
+      cudaGraph_t tmp;
+      cudaError_t e2 = cudaStreamEndCapture(P.wcs, &tmp);
+      if (e == cudaSuccess) e = e2;
+    }
+    P.minres_wbody_nodes = etq_launch_total() - b0;
+    if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies);
+    cudaError_t e3 = cudaStreamEndCapture(st, &graph);
+    P.minres_wfixed_nodes = (etq_launch_total() - before) - P.minres_wbody_nodes;
+    etq_count_launch(-(etq_launch_total() - before));   // captured, not launched
+    if (s < 0) return s;
+    ETQ_CHECK(e);
+    ETQ_CHECK(e3);
+    ETQ_CHECK(cudaGraphInstantiate(&P.minres_wgraph, graph, 0));
+    cudaGraphDestroy(graph);
+    P.minres_wgraph_kind = (int)kind;
+    P.minres_wgraph_x = x;
+  }
+  if (graphs && !devloop && (P.minres_graph_kind != (int)kind || P.minres_graph_x != x || !P.minres_graph[0])) {
     for (int g = 0; g < 2; ++g) {
       if (P.minres_graph[g]) { cudaGraphExecDestroy(P.minres_graph[g]); P.minres_graph[g] = nullptr; }
     }
@@ -259,7 +316,14 @@ etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, 
   }
   int cur = 1;
   int it = 0;
-  for (;;) {
+  if (devloop) {
+    ETQ_CHECK(cudaGraphLaunch(P.minres_wgraph, st));
+    ETQ_CHECK(cudaStreamSynchronize(st));
+    ETQ_CHECK(cudaMemcpy(P.hscal, sc, sizeof(double) * 20, cudaMemcpyDeviceToHost));
+    const int its = (int)P.hscal[S_IT];
+    etq_count_launch(P.minres_wfixed_nodes + (int64_t)((its + 1) / 2) * P.minres_wbody_nodes);
+  }
+  for (; !devloop;) {
     ETQ_CHECK(cudaMemcpyAsync(P.hscal, sc, sizeof(double) * 20, cudaMemcpyDeviceToHost, st));
     ETQ_CHECK(cudaStreamSynchronize(st));
     if (P.hscal[S_DONE] != 0.0) break;

@@ -78,3 +78,26 @@ def test_matrix_free_saddle_bitwise_equal(n):
             etq.set_option(2, 1)
     for red in (False, True):
         np.testing.assert_array_equal(ys[(0, red)], ys[(1, red)])
+
+
+@pytest.mark.parametrize("kind", [etq.PC_P2_GMG, etq.PC_P3])
+def test_device_minres_loop_matches_host_loop(kind):
+    """MINRES as one CUDA graph with a while node (no host round trip per iteration) gives the same
+    iterates as one graph launch plus one flag read-back per iteration."""
+    n = 32
+    xs, its = [], []
+    for opt in (0, 1):
+        etq.set_option(3, opt)
+        try:
+            P = etq.Problem(n)
+            P.precond_setup(kind, etq.make_params(cheb_sgs_lo=0.005))
+            b = torch.zeros(P.N, dtype=torch.float64, device="cuda")
+            P.build_rhs(b)
+            x = torch.zeros(P.N, dtype=torch.float64, device="cuda")
+            rep = P.minres_solve(kind, b, x, rtol=1e-8, maxit=500)
+            xs.append(x.cpu().numpy()); its.append(rep["iterations"])
+            P.close()
+        finally:
+            etq.set_option(3, 1)
+    assert its[0] == its[1]
+    np.testing.assert_array_equal(xs[0], xs[1])
