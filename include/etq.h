@@ -254,7 +254,12 @@ etq_status etq_time_kernel(etq_problem* p, int32_t which, int32_t reps, double* 
  *   option 0 = temporally blocked Chebyshev smoothing on the Stokes interior-stencil levels
  *              (value 1 = on [default], 0 = one kernel per Chebyshev step);
  *   option 1 = coarsest level n that uses it [64] (smaller grids are launch-latency bound);
- *   option 2 = launch priority of the Chebyshev-SGS pressure kernels (0 = lowest [default], 1 = highest).
+ *   option 2 = matrix-free Stokes saddle apply (1 [default]) or the stored SELL rows (0);
+ *   option 3 = MINRES loop as one CUDA graph with a device-side while node (1 [default]) or one
+ *              graph launch and one flag read-back per iteration (0);
+ *   option 4 = launch priority of the Chebyshev-SGS pressure kernels (0 = lowest [default], 1 = highest);
+ *   option 5 = coarse V-cycle levels (n <= 16) in one CTA with every vector in shared memory and
+ *              the class stencils (1 [default], Stokes only) or through the stored rows in global memory (0).
  * Applies to solves whose CUDA graphs are captured afterwards (re-run etq_precond_setup). */
 etq_status etq_set_option(int32_t option, int32_t value);
 

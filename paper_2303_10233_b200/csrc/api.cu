@@ -14,7 +14,8 @@ bool g_cheb_tile_enabled = true;   // etq_set_option(0): temporally blocked smoo
 int g_cheb_tile_min_n = 64;         // etq_set_option(1): coarsest level n that uses it
 bool g_saddle_mf = true;            // etq_set_option(2): matrix-free Stokes saddle apply
 bool g_minres_devloop = true;       // etq_set_option(3): MINRES loop as a CUDA-graph while node
-bool g_sgs_high_prio = false;       // etq_set_option(2): Chebyshev-SGS kernels at the highest priority
+bool g_sgs_high_prio = false;       // etq_set_option(4): Chebyshev-SGS kernels at the highest priority
+bool g_tail_sm = true;              // etq_set_option(5): shared-memory matrix-free coarse-level tail
 void etq_count_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 int64_t etq_launch_total() { return g_launches.load(std::memory_order_relaxed); }
 
@@ -684,7 +685,8 @@ etq_status etq_set_option(int32_t option, int32_t value) {
   if (option == 1) { if (value < 2) return ETQ_EINVAL; g_cheb_tile_min_n = value; return ETQ_OK; }
   if (option == 2) { g_saddle_mf = value != 0; return ETQ_OK; }
   if (option == 3) { g_minres_devloop = value != 0; return ETQ_OK; }
-  if (option == 2) { g_sgs_high_prio = value != 0; return ETQ_OK; }
+  if (option == 4) { g_sgs_high_prio = value != 0; return ETQ_OK; }
+  if (option == 5) { g_tail_sm = value != 0; return ETQ_OK; }
   return ETQ_EINVAL;
 }
 

@@ -38,7 +38,8 @@ extern bool g_cheb_tile_enabled;          // api.cu; etq_set_option(0)
 extern int g_cheb_tile_min_n;             // api.cu; etq_set_option(1)
 extern bool g_minres_devloop;             // api.cu; etq_set_option(3)
 extern bool g_saddle_mf;                  // api.cu; etq_set_option(2)
-extern bool g_sgs_high_prio;              // api.cu; etq_set_option(2)   // host-side launch counter (etq_launch_count)
+extern bool g_sgs_high_prio;              // api.cu; etq_set_option(4)
+extern bool g_tail_sm;                    // api.cu; etq_set_option(5)
 
 constexpr int SELL_C = 32;           // slice height = warp size
 constexpr int RED_BLOCKS = 592;      // 4 x 148 SMs: grid of plain reduction kernels
@@ -138,6 +139,20 @@ struct TailLevel {
   int nq, m; double c1[4], c2[4]; const double* coarse_inv;
 };
 
+// the same tail with its vectors in shared memory and the class stencils (Stokes levels only)
+constexpr int TAIL_SM_MAXLEV = 8;
+struct TailSmArgs {
+  StencilOp so;               // class stencils and D^-1 (identical on every Stokes level)
+  int nlev = 0, degree = 3;
+  int m[TAIL_SM_MAXLEV];
+  double c1[TAIL_SM_MAXLEV][4], c2[TAIL_SM_MAXLEV][4];
+  double itheta = 0.0;
+  const double* b0 = nullptr; const double* d00 = nullptr; double* x0 = nullptr;   // first tail level (global)
+  const double* coarse_inv = nullptr;
+  const double* done = nullptr;
+  int smem_bytes = 0;
+};
+
 struct Hierarchy {
   std::vector<Level> lv;
   double lo = 0.16, hi = 1.6;
@@ -150,6 +165,8 @@ struct Hierarchy {
   bool f32 = false;           // fp32 copies present
   int tail_start = -1;        // first level run by the fused coarse-level tail kernel (-1: none)
   TailLevel* tail = nullptr;  // device array, levels tail_start .. L-1
+  bool tail_sm = false;       // shared-memory matrix-free tail available (Stokes, storage 0)
+  TailSmArgs tsm;             // its launch arguments (done filled per launch)
 };
 
 // ---------------------------------------------------------------- device scalars (MINRES / GMRES)

@@ -912,20 +912,50 @@ __global__ void k_mass_apply(MassGeo g, const double* x, double* y) {
 // One launch = one symmetric Gauss-Seidel sweep S(y) on M_Q z = r' (r' = r - alpha k, reading R6)
 // in the colour order 0,1,2,3,P0 | P0,3,2,1,0 (reading R7; the repeated P0 update is idempotent
 // and done once), fused with the Chebyshev semi-iteration update of P:455 (mode 1):
-//     out = omega (gam (S(y) - y) + y - yp) + yp          (mode 0: out = S(y)).
+//     out = omega (gam (S(y) - y) + y - yp) + yp = co_s S(y) + (co_y y + co_p yp)   (mode 0: S(y)).
 // Each CTA owns a T x T tile of Q1 vertices (and the P0 cells whose lower-left vertex is in the
-// tile), loads it with a halo of SGS_H = 9 (the dependency radius of the 9 colour steps) into
+// tile), stages a W x W window (the tile plus the halo the 9 colour steps need, below) in
 // shared memory, runs all colour steps there and writes only its tile: the 16.8 MB pressure
 // vectors are read once per Chebyshev step instead of once per colour step.
-constexpr int SGS_H = 10;             // halo >= 9 (dependency radius of the 9 colour steps); even
-constexpr int SGS_W = 64;              // loaded window
-constexpr int SGS_T = SGS_W - 2 * SGS_H;   // 44: tile origin A0 = 44 t - 10 is even
-constexpr int SGS_P = SGS_W / 2;       // colour-plane side (32)
+//
+// Layout: vertices AND cells are stored as four parity planes each (local (la, lc) -> plane
+// (la & 1) + 2 (lc & 1), entry (lc >> 1, la >> 1)), and thread (tx, ty) owns plane entries
+// (tx, ty + 16 m), m = 0, 1, of every plane in every phase (staging, sweeps, cells, output).  So a
+// vertex update reads its 8 vertex and 4 cell neighbours at compile-time offsets from one base
+// address, each warp access is 32 consecutive words (no bank conflicts), and the interior path
+// (tiles away from the domain boundary) has no branches: the window-edge entries compute
+// finite garbage that the halo absorbs.  On
+// boundary tiles the 1D mass diagonal (2h/6 on the boundary) and the out-of-domain zeros are
+// selects.  Every row uses the same operation sequence on both paths.
+// Halo: garbage entering at the window edge moves one entry per colour step only when the
+// updated colour has the parity of the entry next to the front, so along x (colour parities
+// 0,1,0,1 | 1,0,1,0) it travels 7 entries from the left edge and 6 from the right, along y
+// (0,0,1,1 | 1,1,0,0) only 3 from below and 2 from above (tests/test_sgs_halo.py simulates the
+// dependency cone).  Halos 8 / 6 (x) and 4 / 2 (y) keep tile origins even (the colour of a local
+// entry is its global colour): 50 x 58 tiles from a 64 x 64 window (1.5x the 44 x 44 tiles of
+// a symmetric halo of 10).
+constexpr int SGS_W = 64;              // staged window (both directions)
+constexpr int SGS_HX = 8, SGS_HY = 4;  // left / bottom halo (right / top: 6 / 2)
+constexpr int SGS_TTX = 50, SGS_TTY = 58;   // tile
+constexpr int SGS_P = SGS_W / 2;       // plane side (32)
+constexpr int SGS_PL = SGS_P * SGS_P;  // one plane
+constexpr int SGS_I0 = SGS_HX / 2, SGS_NI = SGS_TTX / 2;   // tile in plane entries: i in [4, 29)
+constexpr int SGS_J0 = SGS_HY / 2, SGS_NJ = SGS_TTY / 2;   //                       j in [2, 31)
+constexpr int SGS_QP = SGS_NI * SGS_NJ;    // one Q plane
+constexpr int SGS_PAD = 64;            // zeroed words before the vertex planes (edge reads at -33)
 constexpr int SGS_TX = 32, SGS_TY = 16;
-constexpr int SGS_SMEM = (4 * SGS_P * SGS_P + SGS_W * SGS_W) * (int)sizeof(double);
+constexpr int SGS_SMEM = (SGS_PAD + 8 * SGS_PL + 8 * SGS_QP) * (int)sizeof(double);
+static_assert(SGS_W - SGS_HX - SGS_TTX >= 6 && SGS_W - SGS_HY - SGS_TTY >= 2, "right / top halo");
+static_assert(SGS_HX % 2 == 0 && SGS_HY % 2 == 0 && SGS_TTX % 2 == 0 && SGS_TTY % 2 == 0, "even origins");
+static_assert(SGS_TX == SGS_P && 2 * SGS_TY == SGS_P, "one thread per plane column, two rows");
+
+struct SgsK {                 // M_Q coefficients (Qk = Mlin x Mlin, R = h^2/4, Q0 = h^2)
+  double w_in, w_bd, w_off, rq, c_dd, c_ed, inv_in2, inv_inbd, inv_bd2, inv_q0;
+};
 
 struct SgsTileArgs {
   MassGeo g;
+  SgsK k;                   // filled by launch_sgs_tile (kernel parameters: constant-bank operands)
   const double* r;          // right-hand side (n_p)
   const double* kproj;      // optional device scalar k^T r: r' = r - (kproj / k^T k) k
   double inv_kk;
@@ -939,178 +969,162 @@ struct SgsTileArgs {
   const double* done;
 };
 
-// Shared-memory layout: the 64 x 64 window of Q1 vertices is stored as four 32 x 32 colour
-// planes V[c][j][i] <-> local vertex (2i + px, 2j + py), c = px + 2 py, so a warp updating one
-// colour touches consecutive words; cells are one 64 x 64 plane C[lc][la] (lower-left vertex).
-struct SgsSmem {
-  double* V;   // [4][32][32]
-  double* C;   // [64][64]
-  __device__ __forceinline__ double& v(int c, int i, int j) const { return V[(c * SGS_P + j) * SGS_P + i]; }
-  __device__ __forceinline__ double& vl(int la, int lc) const {   // by local vertex coordinates
-    return V[((((la & 1) + 2 * (lc & 1)) * SGS_P) + (lc >> 1)) * SGS_P + (la >> 1)];
-  }
-  __device__ __forceinline__ double& cl(int la, int lc) const { return C[lc * SGS_W + la]; }
-};
 
-// update of colour (PX, PY) vertices owned by this thread: plane column i = tx, rows j = ty, ty + 16.
-// IN: the whole window lies strictly inside the domain (no boundary vertices, no range checks).
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool pred) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(pred ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+}
+
+// update of colour (PX, PY): plane entries (i, j), j = ty + 16 m; vertex (2i + PX, 2j + PY)
 template <int PX, int PY, bool IN>
-__device__ __forceinline__ void sgs_colour(const SgsSmem& S, const double (&rr)[2], int A0, int C0, int n,
-                                           double w_in, double w_bd, double w_off, double rq, double c_dd,
-                                           double c_ed, double inv_in2) {
+__device__ __forceinline__ void sgs_colour(double* __restrict__ V, const double* __restrict__ Cc,
+                                           const double (&rr)[2], int A0, int C0, int n, const SgsK& k) {
   constexpr int c = PX + 2 * PY, cx = (1 - PX) + 2 * PY, cy = PX + 2 * (1 - PY), cxy = (1 - PX) + 2 * (1 - PY);
+  constexpr int OW = PX - 1, OE = PX, OS = (PY - 1) * SGS_P, ON = PY * SGS_P;   // neighbour offsets
   const int i = threadIdx.x;
-  const int la = 2 * i + PX, ga = A0 + la;
 #pragma unroll
   for (int m = 0; m < 2; ++m) {
     const int j = threadIdx.y + SGS_TY * m;
-    const int lc = 2 * j + PY, gc = C0 + lc;
-    if (la == 0 || la == SGS_W - 1 || lc == 0 || lc == SGS_W - 1) continue;   // window edge: garbage halo
-    if (!IN && (ga < 0 || ga > n || gc < 0 || gc > n)) continue;
-    const int iw = i - 1 + PX, ie = i + PX, js = j - 1 + PY, jn = j + PY;
-    if (IN || (ga > 0 && ga < n && gc > 0 && gc < n)) {
-      const double sd = S.v(cxy, iw, js) + S.v(cxy, ie, js) + S.v(cxy, iw, jn) + S.v(cxy, ie, jn);
-      const double se = S.v(cx, iw, j) + S.v(cx, ie, j) + S.v(cy, i, js) + S.v(cy, i, jn);
-      const double sc = S.cl(la - 1, lc - 1) + S.cl(la, lc - 1) + S.cl(la - 1, lc) + S.cl(la, lc);
-      S.v(c, i, j) = (rr[m] - c_dd * sd - c_ed * se - rq * sc) * inv_in2;
-    } else {   // domain-boundary vertex: 1D mass diagonal 2h/6, neighbours only inside [0, n]
-      const double da0 = (ga == 0 || ga == n) ? w_bd : w_in;
-      const double dc0 = (gc == 0 || gc == n) ? w_bd : w_in;
-      double s = rr[m];
-      for (int dc = -1; dc <= 1; ++dc) {
-        if (gc + dc < 0 || gc + dc > n) continue;
-        const double wc = dc == 0 ? dc0 : w_off;
-        for (int da = -1; da <= 1; ++da) {
-          if ((da == 0 && dc == 0) || ga + da < 0 || ga + da > n) continue;
-          s -= wc * (da == 0 ? da0 : w_off) * S.vl(la + da, lc + dc);
-        }
-      }
-      for (int df = -1; df <= 0; ++df) {
-        if (gc + df < 0 || gc + df >= n) continue;
-        for (int de = -1; de <= 0; ++de) {
-          if (ga + de < 0 || ga + de >= n) continue;
-          s -= rq * S.cl(la + de, lc + df);
-        }
-      }
-      S.v(c, i, j) = s / (da0 * dc0);
+    const int B = j * SGS_P + i;
+    const double* vd = V + cxy * SGS_PL + B;
+    const double* vx = V + cx * SGS_PL + B;
+    const double* vy = V + cy * SGS_PL + B;
+    const double sd = (vd[OS + OW] + vd[OS + OE]) + (vd[ON + OW] + vd[ON + OE]);
+    const double sx = vx[OW] + vx[OE];
+    const double sy = vy[OS] + vy[ON];
+    // cells (la-1, lc-1), (la, lc-1), (la-1, lc), (la, lc)
+    const double sc = (Cc[cxy * SGS_PL + B + OS + OW] + Cc[cy * SGS_PL + B + OS]) +
+                      (Cc[cx * SGS_PL + B + OW] + Cc[c * SGS_PL + B]);
+    double wx = k.c_ed, wy = k.c_ed, inv = k.inv_in2;
+    bool in = true;
+    if (!IN) {
+      const int ga = A0 + 2 * i + PX, gc = C0 + 2 * j + PY;
+      in = ga >= 0 && ga <= n && gc >= 0 && gc <= n;
+      const bool bx = ga == 0 || ga == n, by = gc == 0 || gc == n;
+      wx = by ? k.w_off * k.w_bd : k.c_ed;   // x-neighbours: M(a, a +- 1) M(c, c)
+      wy = bx ? k.w_bd * k.w_off : k.c_ed;   // y-neighbours: M(a, a) M(c, c +- 1)
+      inv = bx ? (by ? k.inv_bd2 : k.inv_inbd) : (by ? k.inv_inbd : k.inv_in2);
     }
+    const double s = rr[m] - k.c_dd * sd - wx * sx - wy * sy - k.rq * sc;
+    V[c * SGS_PL + B] = in ? s * inv : 0.0;
+  }
+}
+
+// P0 cells of parity plane (PE, PF): cell (2i + PE, 2j + PF) from its four vertices
+template <int PE, int PF, bool IN>
+__device__ __forceinline__ void sgs_cells(const double* __restrict__ V, double* __restrict__ Cc,
+                                          const double (&rc)[2], int A0, int C0, int n, const SgsK& k) {
+  constexpr int p00 = PE + 2 * PF, p10 = (1 - PE) + 2 * PF, p01 = PE + 2 * (1 - PF), p11 = (1 - PE) + 2 * (1 - PF);
+  const int i = threadIdx.x;
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    const int j = threadIdx.y + SGS_TY * m;
+    const int B = j * SGS_P + i;
+    const double sv = (V[p00 * SGS_PL + B] + V[p10 * SGS_PL + B + PE]) +
+                      (V[p01 * SGS_PL + B + PF * SGS_P] + V[p11 * SGS_PL + B + PF * SGS_P + PE]);
+    const double z = (rc[m] - k.rq * sv) * k.inv_q0;
+    bool in = true;
+    if (!IN) {
+      const int e = A0 + 2 * i + PE, f = C0 + 2 * j + PF;
+      in = e >= 0 && e < n && f >= 0 && f < n;
+    }
+    Cc[p00 * SGS_PL + B] = in ? z : 0.0;
   }
 }
 
 template <bool IN>
-__device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, const SgsSmem& S, int A0, int C0) {
-  constexpr int W = SGS_W, T = SGS_T, H = SGS_H;
-  const int tx = threadIdx.x, ty = threadIdx.y;
+__device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, double* Cc, double* Q, int A0, int C0) {
+  const int i = threadIdx.x, ty = threadIdx.y;
   const int n = a.g.n, n1 = n + 1, nk = a.g.nk;
   const double alpha = a.kproj ? (*a.kproj * a.inv_kk) : 0.0;
   const double* __restrict__ r1 = a.r;
   const double* __restrict__ r0 = a.r + nk;
-  // ---- phase A: stage the vertex right-hand sides (coalesced rows) and take this thread's
-  //      colour-plane entries into registers
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    const int lc = ty + SGS_TY * v, gc = C0 + lc;
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int la = tx + 32 * u, ga = A0 + la;
-      const bool in = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
-      S.cl(la, lc) = in ? __ldg(r1 + ga + n1 * gc) - alpha : 0.0;
-    }
-  }
-  __syncthreads();
-  double rv[4][2];
+  const double co_y = a.mode ? a.omega * (1.0 - a.gam) : 0.0;
+  const double co_p = a.mode ? 1.0 - a.omega : 0.0;
+  const bool use_yp = a.mode && a.yp && co_p != 0.0;
+  const double* ys = a.y ? a.y : a.r;      // valid source address for the zero-filling copies
+  const double* yps = use_yp ? a.yp : a.r;
+  // ---- one staging phase (plane order): y by cp.async (vertices, cells), r into registers,
+  //      y_prev of the tile by cp.async into Q
+  double rv[4][2], rc[4][2];
 #pragma unroll
   for (int c = 0; c < 4; ++c)
 #pragma unroll
-    for (int m = 0; m < 2; ++m) rv[c][m] = S.cl(2 * tx + (c & 1), 2 * (ty + SGS_TY * m) + (c >> 1));
-  __syncthreads();
-  // ---- phase B: y (vertices into the planes, cells) and the cell right-hand sides, coalesced
-  double rc[2][4];
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    const int lc = ty + SGS_TY * v, gc = C0 + lc;
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int la = tx + 32 * u, ga = A0 + la;
+    for (int m = 0; m < 2; ++m) {
+      const int j = ty + SGS_TY * m;
+      const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
       const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
       const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
-      S.vl(la, lc) = (inv && a.y) ? a.y[ga + n1 * gc] : 0.0;
-      S.cl(la, lc) = (inc && a.y) ? a.y[nk + ga + n * gc] : 0.0;
-      rc[u][v] = inc ? __ldg(r0 + ga + n * gc) + alpha : 0.0;
+      const int64_t gv = inv ? ga + (int64_t)n1 * gc : 0, gq = inc ? ga + (int64_t)n * gc : 0;
+      cp_async8(V + c * SGS_PL + j * SGS_P + i, ys + gv, inv && a.y);
+      cp_async8(Cc + c * SGS_PL + j * SGS_P + i, ys + nk + gq, inc && a.y);
+      rv[c][m] = inv ? __ldg(r1 + gv) - alpha : 0.0;
+      rc[c][m] = inc ? __ldg(r0 + gq) + alpha : 0.0;
     }
+  const bool ti = i >= SGS_I0 && i < SGS_I0 + SGS_NI;
+  if (use_yp && ti) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int j = ty + SGS_TY * m;
+        if (j < SGS_J0 || j >= SGS_J0 + SGS_NJ) continue;
+        const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
+        const bool okv = IN || (ga <= n && gc <= n), okc = IN || (ga < n && gc < n);
+        const int qi = (j - SGS_J0) * SGS_NI + (i - SGS_I0);
+        cp_async8(Q + c * SGS_QP + qi, yps + (okv ? ga + (int64_t)n1 * gc : 0), okv);
+        cp_async8(Q + (4 + c) * SGS_QP + qi, yps + nk + (okc ? ga + (int64_t)n * gc : 0), okc);
+      }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // ---- the y / y_prev part of this thread's outputs, before the sweep overwrites y in place
+  if (ti) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int j = ty + SGS_TY * m;
+        if (j < SGS_J0 || j >= SGS_J0 + SGS_NJ) continue;
+        double* q = Q + c * SGS_QP + (j - SGS_J0) * SGS_NI + (i - SGS_I0);
+        const double yv = (c < 4 ? V : Cc)[(c & 3) * SGS_PL + j * SGS_P + i];
+        *q = fma(co_y, yv, use_yp ? co_p * *q : 0.0);
+      }
   }
   __syncthreads();
-  const double h = a.g.h;
-  const double w_in = 4.0 * h / 6.0, w_bd = 2.0 * h / 6.0, w_off = h / 6.0, rq = 0.25 * h * h;
-  const double c_dd = w_off * w_off, c_ed = w_off * w_in, inv_in2 = 1.0 / (w_in * w_in), inv_q0 = 1.0 / (h * h);
-#define SGS_V(PX, PY) do { sgs_colour<PX, PY, IN>(S, rv[PX + 2 * PY], A0, C0, n, w_in, w_bd, w_off, rq, c_dd, c_ed, inv_in2); __syncthreads(); } while (0)
+  const SgsK& k = a.k;
+#define SGS_V(PX, PY) do { sgs_colour<PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
   SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
-  // P0 cells (once: the backward sweep's P0 update would repeat it exactly)
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int la = tx + 32 * u, ga = A0 + la;
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int lc = ty + SGS_TY * v, gc = C0 + lc;
-      if (la == W - 1 || lc == W - 1) continue;
-      if (!IN && (ga < 0 || ga >= n || gc < 0 || gc >= n)) continue;
-      S.cl(la, lc) = (rc[u][v] - rq * (S.vl(la, lc) + S.vl(la + 1, lc) + S.vl(la, lc + 1) + S.vl(la + 1, lc + 1))) * inv_q0;
-    }
-  }
+  sgs_cells<0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);             // P0 (once: the backward sweep's
+  sgs_cells<1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);             // P0 update would repeat it exactly)
+  sgs_cells<0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
+  sgs_cells<1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
   __syncthreads();
   SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
 #undef SGS_V
-  // ---- write the tile (coalesced rows) with the semi-iteration update.  The y / y_prev loads of all
-  //      of this thread's outputs are issued before any is used (one memory latency, not six).
-  constexpr int NL = (T + SGS_TY - 1) / SGS_TY;   // 3 row passes
-  double yv[NL][2][2], ypv[NL][2][2];           // [pass][u][vertex, cell]
-#pragma unroll
-  for (int q = 0; q < NL; ++q) {
-    const int lc = H + ty + SGS_TY * q, gc = C0 + lc;
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int la = H + tx + 32 * u, ga = A0 + la;
-      const bool okt = lc < H + T && la < H + T;
-      const bool okv = okt && (IN || (ga <= n && gc <= n)), okc = okt && (IN || (ga < n && gc < n));
-      const int iv = okv ? ga + n1 * gc : 0, ic = okc ? nk + ga + n * gc : 0;
-      yv[q][u][0] = (a.mode && a.y && okv) ? a.y[iv] : 0.0;
-      yv[q][u][1] = (a.mode && a.y && okc) ? a.y[ic] : 0.0;
-      ypv[q][u][0] = (a.mode && a.yp && okv) ? a.yp[iv] : 0.0;
-      ypv[q][u][1] = (a.mode && a.yp && okc) ? a.yp[ic] : 0.0;
-    }
-  }
+  // ---- write the tile: out = co_s S(y) + Q (plane order; the two parities of a row land in the
+  //      same L2 sectors from the same warp)
+  const double co_s = a.mode ? a.omega * a.gam : 1.0;
   double kd = 0.0;
+  if (ti) {
 #pragma unroll
-  for (int q = 0; q < NL; ++q) {
-    const int lc = H + ty + SGS_TY * q, gc = C0 + lc;
-    if (lc >= H + T) continue;
+    for (int c = 0; c < 8; ++c)
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int la = H + tx + 32 * u, ga = A0 + la;
-      if (la >= H + T) continue;
-      if (IN || (ga <= n && gc <= n)) {
-        const int idx = ga + n1 * gc;
-        const double v = S.vl(la, lc);
-        double o = v;
-        if (a.mode) {
-          const double y = yv[q][u][0], yp = ypv[q][u][0];
-          o = a.omega * (a.gam * (v - y) + y - yp) + yp;
+      for (int m = 0; m < 2; ++m) {
+        const int j = ty + SGS_TY * m;
+        if (j < SGS_J0 || j >= SGS_J0 + SGS_NJ) continue;
+        const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + ((c & 3) >> 1);
+        const double o = fma(co_s, (c < 4 ? V : Cc)[(c & 3) * SGS_PL + j * SGS_P + i],
+                             Q[c * SGS_QP + (j - SGS_J0) * SGS_NI + (i - SGS_I0)]);
+        if (c < 4) {
+          if (IN || (ga <= n && gc <= n)) { a.out[ga + (int64_t)n1 * gc] = o; kd += o; }
+        } else {
+          if (IN || (ga < n && gc < n)) { a.out[nk + ga + (int64_t)n * gc] = o; kd -= o; }
         }
-        a.out[idx] = o;
-        kd += o;
       }
-      if (IN || (ga < n && gc < n)) {
-        const int idx = nk + ga + n * gc;
-        const double v = S.cl(la, lc);
-        double o = v;
-        if (a.mode) {
-          const double y = yv[q][u][1], yp = ypv[q][u][1];
-          o = a.omega * (a.gam * (v - y) + y - yp) + yp;
-        }
-        a.out[idx] = o;
-        kd -= o;
-      }
-    }
   }
   if (a.kout) { double v[1] = {kd}; reduce_finish<1>(v, a.site, a.slot, a.kout); }
 }
@@ -1121,12 +1135,16 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, const SgsSme
 __global__ void __launch_bounds__(SGS_TX * SGS_TY, SGS_MINB) k_sgs_tile(SgsTileArgs a) {
   if (is_done(a.done)) return;
   extern __shared__ double sm[];
-  const SgsSmem S{sm, sm + 4 * SGS_P * SGS_P};
+  double* V = sm + SGS_PAD;
+  double* Cc = V + 4 * SGS_PL;
+  double* Q = Cc + 4 * SGS_PL;
+  const int tid = threadIdx.x + SGS_TX * threadIdx.y;
+  if (tid < SGS_PAD) sm[tid] = 0.0;
   const int n = a.g.n;
-  const int A0 = (blockIdx.x % a.tiles_x) * SGS_T - SGS_H, C0 = (blockIdx.x / a.tiles_x) * SGS_T - SGS_H;
+  const int A0 = (blockIdx.x % a.tiles_x) * SGS_TTX - SGS_HX, C0 = (blockIdx.x / a.tiles_x) * SGS_TTY - SGS_HY;
   const bool interior = A0 >= 1 && A0 + SGS_W - 1 <= n - 1 && C0 >= 1 && C0 + SGS_W - 1 <= n - 1;
-  if (interior) sgs_tile_body<true>(a, S, A0, C0);
-  else sgs_tile_body<false>(a, S, A0, C0);
+  if (interior) sgs_tile_body<true>(a, V, Cc, Q, A0, C0);
+  else sgs_tile_body<false>(a, V, Cc, Q, A0, C0);
 }
 
 // k^T x
@@ -1500,6 +1518,186 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(const TailLevel* l
   const TailLevel& L0 = lvs[0];
   for (int64_t i = tid; i < 2LL * L0.nq; i += TAIL_THREADS) L0.x[i] += pend_c[i];
 }
+
+// ---- the tail in shared memory (Stokes): every level's b, x, r, d0, d1 (two components) stay in
+// shared memory, and each row product is the level's class stencil (the Q2 Laplacian is
+// h-independent, so one StencilOp serves every level) with Dirichlet nodes read as 0 and
+// identity rows on the boundary, summed in the tap order of stencil_row2 (= the stored row
+// order).  Global traffic: the first level's b and d0 in, its x out, the coarse inverse.  The
+// previous tail ran each of its ~40 dependent phases through L2 with index chains (~120 us).
+__device__ __forceinline__ double tsm_at(const double* v, int m, int i, int j) {
+  return (i <= 0 || j <= 0 || i >= m - 1 || j >= m - 1) ? 0.0 : v[i + m * j];
+}
+__device__ __forceinline__ void tsm_row2(const StencilOp& so, int m, int i, int j, const double* v0,
+                                         const double* v1, double& a0, double& a1) {
+  if (i == 0 || j == 0 || i == m - 1 || j == m - 1) {   // identity row
+    const int t = i + m * j;
+    a0 = fma(1.0, v0[t], 0.0); a1 = fma(1.0, v1[t], 0.0);
+    return;
+  }
+  const int cl = (i & 1) + 2 * (j & 1);
+  a0 = 0.0; a1 = 0.0;
+#pragma unroll
+  for (int dj = -2; dj <= 2; ++dj) {
+    if ((j & 1) && (dj == 2 || dj == -2)) continue;
+#pragma unroll
+    for (int di = -2; di <= 2; ++di) {
+      const double w = so.w[cl][(dj + 2) * 5 + (di + 2)];
+      a0 = fma(w, tsm_at(v0, m, i + di, j + dj), a0);
+      a1 = fma(w, tsm_at(v1, m, i + di, j + dj), a1);
+    }
+  }
+}
+__device__ __forceinline__ double tsm_dinv(const StencilOp& so, int m, int i, int j) {
+  return (i == 0 || j == 0 || i == m - 1 || j == m - 1) ? 1.0 : so.dcls[(i & 1) + 2 * (j & 1)];
+}
+// one Chebyshev update on a level (same formulas as tail_cheb_step)
+__device__ __forceinline__ void tsm_cheb_step(const StencilOp& so, int m, const double* d_in, const double* r_in,
+                                              const double* x_in, double* x_out, double* r_out, double* d_out,
+                                              double c1, double c2) {
+  const int nq = m * m;
+  for (int t = threadIdx.x; t < nq; t += TAIL_THREADS) {
+    const int i = t % m, j = t / m;
+    double q[2];
+    tsm_row2(so, m, i, j, d_in, d_in + nq, q[0], q[1]);
+    const double di = tsm_dinv(so, m, i, j);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int idx = c * nq + t;
+      const double dd = d_in[idx];
+      const double ro = r_in[idx] - q[c];
+      x_out[idx] = (x_in ? x_in[idx] : 0.0) + dd;
+      if (r_out) r_out[idx] = ro;
+      if (d_out) d_out[idx] = c1 * dd + c2 * (di * ro);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail_sm(TailSmArgs a) {
+  if (is_done(a.done)) return;
+  extern __shared__ double tsm[];
+  const int tid = threadIdx.x;
+  const int nlev = a.nlev, degree = a.degree;
+  const double itheta = a.itheta;
+  auto base = [&](int l) {
+    int o = 0;
+    for (int k = 0; k < l; ++k) o += 10 * a.m[k] * a.m[k];
+    return tsm + o;
+  };
+  // vectors of level l: b, x, r, d0, d1 at offsets 0, 2nq, 4nq, 6nq, 8nq
+  {
+    const int nq = a.m[0] * a.m[0];
+    double* B = base(0);
+    for (int i = tid; i < 2 * nq; i += TAIL_THREADS) { B[i] = a.b0[i]; B[6 * nq + i] = a.d00[i]; }
+  }
+  __syncthreads();
+  // ---- down
+  for (int l = 0; l < nlev - 1; ++l) {
+    const int m = a.m[l], nq = m * m;
+    double* B = base(l);
+    double *b = B, *x = B + 2 * nq, *r = B + 4 * nq;
+    double* din = B + 6 * nq; double* dout = B + 8 * nq;
+    for (int k = 0; k < degree; ++k) {
+      tsm_cheb_step(a.so, m, din, k == 0 ? b : r, k == 0 ? nullptr : x, x, r, k == degree - 1 ? nullptr : dout,
+                    a.c1[l][k], a.c2[l][k]);
+      __syncthreads();
+      double* t = din; din = dout; dout = t;
+    }
+    const int mc = a.m[l + 1], nqc = mc * mc;
+    double* Bc = base(l + 1);
+    for (int t = tid; t < nqc; t += TAIL_THREADS) {
+      const int I = t % mc, J = t / mc;
+      if (I == 0 || J == 0 || I == mc - 1 || J == mc - 1) {
+        Bc[t] = 0.0; Bc[nqc + t] = 0.0; Bc[6 * nqc + t] = 0.0; Bc[6 * nqc + nqc + t] = 0.0;
+        continue;
+      }
+      int ox[5], oy[5]; double wx[5], wy[5];
+      const int nx = restrict_taps(I, ox, wx), ny = restrict_taps(J, oy, wy);
+      double s0 = 0.0, s1 = 0.0;
+      for (int q = 0; q < ny; ++q) {
+        const int rowf = (2 * J + oy[q]) * m;
+        double t0 = 0.0, t1 = 0.0;
+        for (int p = 0; p < nx; ++p) {
+          const int f = rowf + 2 * I + ox[p];
+          t0 = fma(wx[p], r[f], t0);
+          t1 = fma(wx[p], r[nq + f], t1);
+        }
+        s0 = fma(wy[q], t0, s0);
+        s1 = fma(wy[q], t1, s1);
+      }
+      Bc[t] = s0; Bc[nqc + t] = s1;
+      const double di = tsm_dinv(a.so, mc, I, J);
+      Bc[6 * nqc + t] = di * s0 * itheta; Bc[6 * nqc + nqc + t] = di * s1 * itheta;
+    }
+    __syncthreads();
+  }
+  // ---- coarse solve x = C^{-1} b (warp per row, both components)
+  {
+    const int mc = a.m[nlev - 1], nqc = mc * mc;
+    double* B = base(nlev - 1);
+    const int lane = tid & 31, w = tid >> 5;
+    for (int rr = w; rr < nqc; rr += TAIL_THREADS / 32)
+      for (int c = 0; c < 2; ++c) {
+        double s = 0.0;
+        for (int j = lane; j < nqc; j += 32) s = fma(__ldg(a.coarse_inv + (int64_t)rr * nqc + j), B[c * nqc + j], s);
+        s = warp_sum(s);
+        if (lane == 0) B[2 * nqc + c * nqc + rr] = s;
+      }
+    __syncthreads();
+  }
+  // ---- up
+  const double* pend_c = nullptr;
+  for (int l = nlev - 2; l >= 0; --l) {
+    const int m = a.m[l], nq = m * m, mc = a.m[l + 1], nqc = mc * mc;
+    double* B = base(l);
+    double *b = B, *x = B + 2 * nq, *r = B + 4 * nq;
+    const double* xc = base(l + 1) + 2 * nqc;
+    for (int t = tid; t < nq; t += TAIL_THREADS) {
+      const int k = t % m, ll = t / m;
+      if (k == 0 || ll == 0 || k == m - 1 || ll == m - 1) continue;
+      int ix[3], iy[3]; double wx[3], wy[3];
+      const int nx = prolong_taps(k, ix, wx), ny = prolong_taps(ll, iy, wy);
+      double s0 = 0.0, s1 = 0.0;
+      for (int q = 0; q < ny; ++q) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int p = 0; p < nx; ++p) {
+          const int c = iy[q] * mc + ix[p];
+          const double v0 = pend_c ? xc[c] + pend_c[c] : xc[c];
+          const double v1 = pend_c ? xc[nqc + c] + pend_c[nqc + c] : xc[nqc + c];
+          t0 = fma(wx[p], v0, t0);
+          t1 = fma(wx[p], v1, t1);
+        }
+        s0 = fma(wy[q], t0, s0);
+        s1 = fma(wy[q], t1, s1);
+      }
+      x[t] += s0; x[nq + t] += s1;
+    }
+    __syncthreads();
+    for (int t = tid; t < nq; t += TAIL_THREADS) {   // r = b - A x ; d = D^{-1} r / theta
+      const int i = t % m, j = t / m;
+      double q0, q1;
+      tsm_row2(a.so, m, i, j, x, x + nq, q0, q1);
+      const double di = tsm_dinv(a.so, m, i, j);
+      const double r0 = b[t] - q0, r1 = b[nq + t] - q1;
+      r[t] = r0; r[nq + t] = r1;
+      B[6 * nq + t] = di * r0 * itheta; B[6 * nq + nq + t] = di * r1 * itheta;
+    }
+    __syncthreads();
+    double* din = B + 6 * nq; double* dout = B + 8 * nq;
+    for (int k = 0; k < degree - 1; ++k) {
+      tsm_cheb_step(a.so, m, din, r, x, x, k == degree - 2 ? nullptr : r, dout, a.c1[l][k], a.c2[l][k]);
+      __syncthreads();
+      double* t = din; din = dout; dout = t;
+    }
+    pend_c = din;
+  }
+  // ---- complete level 0 of the tail: x += pending correction, to global (the caller prolongs it)
+  {
+    const int nq = a.m[0] * a.m[0];
+    const double* x = base(0) + 2 * nq;
+    for (int i = tid; i < 2 * nq; i += TAIL_THREADS) a.x0[i] = x[i] + pend_c[i];
+  }
+}
 }  // namespace
 
 // ---------------------------------------------------------------- hierarchy
@@ -1580,6 +1778,33 @@ etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, do
     for (size_t l = 1; l < H.lv.size(); ++l)
       if (H.lv[l].g.n <= TAIL_N && H.lv.size() - l >= 2) { H.tail_start = (int)l; break; }
   if (H.tail_start > 0) ETQ_TRY(refresh_tail(H));
+  // shared-memory matrix-free tail: Stokes levels (translation invariant, the finest level's class
+  // stencils and D^-1 hold on every level), degree <= 4, vectors within the shared-memory budget
+  H.tail_sm = false;
+  if (H.tail_start > 0 && !P.oseen && P.storage == 0 && H.lv[0].st_on &&
+      (int)H.lv.size() - H.tail_start <= TAIL_SM_MAXLEV) {
+    TailSmArgs& t = H.tsm;
+    t = TailSmArgs{};
+    t.so = H.lv[0].so; t.nlev = (int)H.lv.size() - H.tail_start; t.degree = degree;
+    const double theta = 0.5 * (hi + lo);
+    t.itheta = 1.0 / theta;
+    std::vector<double> c1, c2;
+    int words = 0;
+    for (int k = 0; k < t.nlev; ++k) {
+      const Level& lv = H.lv[H.tail_start + k];
+      t.m[k] = lv.g.m;
+      words += 10 * lv.g.m * lv.g.m;
+      cheb_coeffs(lo, hi, lv.bim, degree, c1, c2);
+      for (int q = 0; q < degree; ++q) { t.c1[k][q] = c1[q]; t.c2[k][q] = c2[q]; }
+    }
+    const Level& l0 = H.lv[H.tail_start];
+    t.b0 = l0.b; t.d00 = l0.d0; t.x0 = l0.x; t.coarse_inv = H.lv.back().coarse_inv;
+    t.smem_bytes = words * (int)sizeof(double);
+    if (t.smem_bytes <= 200 * 1024) {
+      ETQ_CHECK(cudaFuncSetAttribute(k_vcycle_tail_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes));
+      H.tail_sm = true;
+    }
+  }
   ETQ_CHECK(cudaStreamSynchronize(P.stream));
   return ETQ_OK;
 }
@@ -1819,7 +2044,14 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
   }
   // ---- coarse (or the fused coarse-level tail, which leaves a complete x on its first level)
   if (use_tail) {
-    k_vcycle_tail<<<1, TAIL_THREADS, 0, st>>>(H.tail, L - H.tail_start, H.degree, 1.0 / theta, done); etq_count_launch();
+    if (H.tail_sm && g_tail_sm) {
+      TailSmArgs ta = H.tsm;
+      ta.done = done;
+      k_vcycle_tail_sm<<<1, TAIL_THREADS, ta.smem_bytes, st>>>(ta);
+    } else {
+      k_vcycle_tail<<<1, TAIL_THREADS, 0, st>>>(H.tail, L - H.tail_start, H.degree, 1.0 / theta, done);
+    }
+    etq_count_launch();
     pend[Ld - 1] = nullptr;
   } else {
     const Level& C = H.lv[L - 1];
@@ -1914,8 +2146,16 @@ static void launch_sgs_tile(SgsTileArgs a, cudaStream_t st) {
     cudaFuncSetAttribute(k_sgs_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, SGS_SMEM);
     smem_set = true;
   }
-  a.tiles_x = (a.g.n + 1 + SGS_T - 1) / SGS_T;
-  const int tiles = a.tiles_x * a.tiles_x;
+  a.tiles_x = (a.g.n + 1 + SGS_TTX - 1) / SGS_TTX;
+  const int tiles = a.tiles_x * ((a.g.n + 1 + SGS_TTY - 1) / SGS_TTY);
+  {
+    SgsK& k = a.k;
+    const double h = a.g.h;
+    k.w_in = 4.0 * h / 6.0; k.w_bd = 2.0 * h / 6.0; k.w_off = h / 6.0; k.rq = 0.25 * h * h;
+    k.c_dd = k.w_off * k.w_off; k.c_ed = k.w_off * k.w_in;
+    k.inv_in2 = 1.0 / (k.w_in * k.w_in); k.inv_inbd = 1.0 / (k.w_in * k.w_bd); k.inv_bd2 = 1.0 / (k.w_bd * k.w_bd);
+    k.inv_q0 = 1.0 / (h * h);
+  }
   // the latency-bound pressure chain runs at the lowest priority so that the concurrent,
   // bandwidth-bound V-cycle blocks are scheduled first (the attribute is kept by graph capture)
   static int lo_prio = 1, hi_prio = 0;

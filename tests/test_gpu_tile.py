@@ -101,3 +101,24 @@ def test_device_minres_loop_matches_host_loop(kind):
             etq.set_option(3, 1)
     assert its[0] == its[1]
     np.testing.assert_array_equal(xs[0], xs[1])
+
+
+@pytest.mark.parametrize("n", [32, 64, 256])
+def test_shared_memory_tail_bitwise_equal(n):
+    """The coarse-level tail run in shared memory with the class stencils (option 5) gives the same
+    V-cycle output, bit for bit, as the tail through the stored rows in global memory."""
+    zs = {}
+    for opt in (0, 1):
+        etq.set_option(5, opt)
+        try:
+            P = etq.Problem(n)
+            P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.005))
+            r = torch.as_tensor(synth.random_vector(P.n_u, seed=11), device="cuda")
+            z = torch.zeros(P.n_u, dtype=torch.float64, device="cuda")
+            P.apply_vcycle(etq.PC_P2_GMG, r, z)
+            torch.cuda.synchronize()
+            zs[opt] = z.cpu().numpy()
+            P.close()
+        finally:
+            etq.set_option(5, 1)
+    np.testing.assert_array_equal(zs[0], zs[1])
