@@ -47,18 +47,21 @@ static __device__ double block_sum(double v) {
 // Returns true in exactly one thread (thread 0 of the last block) after out[] is written, so
 // the caller can derive scalars from the finished sums.
 template <int NV>
-__device__ bool reduce_finish(const double (&v)[NV], RedSite site, int slot, double* out) {
+__device__ bool reduce_finish(const double (&v)[NV], RedSite site, int slot, double* out, bool grid2d = false) {
   __shared__ bool last;
   const int t = lin_tid(), bs = lin_bs();
+  // linear block index / count (2D grids: blockIdx.y-major)
+  const int bid = grid2d ? (int)(blockIdx.x + gridDim.x * blockIdx.y) : (int)blockIdx.x;
+  const int nb = grid2d ? (int)(gridDim.x * gridDim.y) : (int)gridDim.x;
   double tot[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) tot[k] = block_sum(v[k]);
   if (t == 0) {
 #pragma unroll
-    for (int k = 0; k < NV; ++k) site.partials[(int64_t)(slot + k) * MAXB + blockIdx.x] = tot[k];
+    for (int k = 0; k < NV; ++k) site.partials[(int64_t)(slot + k) * MAXB + bid] = tot[k];
     __threadfence();
     unsigned c = atomicAdd(site.counter + slot, 1u);
-    last = (c == gridDim.x - 1);
+    last = (c == (unsigned)nb - 1);
   }
   __syncthreads();
   if (last) {
@@ -66,7 +69,7 @@ __device__ bool reduce_finish(const double (&v)[NV], RedSite site, int slot, dou
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       double s = 0.0;
-      for (int i = t; i < (int)gridDim.x; i += bs)
+      for (int i = t; i < nb; i += bs)
         s += __ldcg(site.partials + (int64_t)(slot + k) * MAXB + i);
       s = block_sum(s);
       if (t == 0) out[k] = s;

@@ -365,6 +365,8 @@ struct ChebTileArgs {
   double* x_out; double* r_out; double* d_out;
   double itheta, c1[3], c2[3];
   const double* done;
+  // finest post pass only: z = x + d2 written here (instead of d_out) and <z, dot_with>
+  double* z_out; const double* dot_with; RedSite site; int slot; double* dot_out;
 };
 
 // class stencil of one output from the register window: win[slot][col], rows jj-2..jj+2 in
@@ -584,7 +586,28 @@ __global__ void __launch_bounds__(CT_THREADS, 2) k_cheb_tile(ChebTileArgs a) {
     tile_accum(D1);                                                      // x += d1
     CT_STEP(6, 0, RS, D1, D1, D0, a.c1[1], a.c2[1]);                   // d2 (deferred)
     __syncthreads();
-    tile_pass([&](int w, int64_t g) { a.d_out[g] = D0[w]; });
+    if (a.z_out) {   // finest level: the V-cycle's result z = x + d2 (k_final_add fused), <z, w>
+      double xv[NTP], wv[NTP];
+#pragma unroll
+      for (int k = 0; k < NTP; ++k) {
+        int w; int64_t g;
+        const bool ok = tile_pos(k, w, g);
+        xv[k] = ok ? a.x_out[g] : 0.0;
+        wv[k] = (ok && a.dot_with) ? __ldg(a.dot_with + g) : 0.0;
+      }
+      double dot = 0.0;
+#pragma unroll
+      for (int k = 0; k < NTP; ++k) {
+        int w; int64_t g;
+        if (!tile_pos(k, w, g)) continue;
+        const double v = xv[k] + D0[w];
+        a.z_out[g] = v;
+        dot += a.dot_with ? v * wv[k] : v;
+      }
+      if (a.dot_out) { double v1[1] = {dot}; reduce_finish<1>(v1, a.site, a.slot, a.dot_out, true); }
+    } else {
+      tile_pass([&](int w, int64_t g) { a.d_out[g] = D0[w]; });
+    }
   }
 #undef CT_STEP
 }
@@ -1937,7 +1960,9 @@ static void launch_cheb_st(const Level& lv, const ChebArgs& c, bool post, double
 // Temporally blocked smoothing pass on an interior-stencil level (degree 3, real interval).
 static void launch_cheb_tile(const Level& lv, bool post, const double* b, const double* x_in, double* x_out,
                              double* r_out, double* d_out, const std::vector<double>& c1,
-                             const std::vector<double>& c2, double theta, const double* done, cudaStream_t st) {
+                             const std::vector<double>& c2, double theta, const double* done, cudaStream_t st,
+                             double* z_out = nullptr, const double* dot_with = nullptr,
+                             const RedSite* site = nullptr, int slot = 0, double* dot_out = nullptr) {
   static bool smem_set = false;
   if (!smem_set) {
     cudaFuncSetAttribute(k_cheb_tile<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM);
@@ -1953,6 +1978,7 @@ static void launch_cheb_tile(const Level& lv, bool post, const double* b, const 
   a.itheta = 1.0 / theta;
   for (int k = 0; k < 3; ++k) { a.c1[k] = c1[k]; a.c2[k] = c2[k]; }
   a.done = done;
+  a.z_out = z_out; a.dot_with = dot_with; a.site = site ? *site : RedSite{}; a.slot = slot; a.dot_out = dot_out;
   dim3 grid(a.tiles_x * a.tiles_x, 2);
   if (post) k_cheb_tile<1><<<grid, CT_THREADS, CT_SMEM, st>>>(a);
   else k_cheb_tile<0><<<grid, CT_THREADS, CT_SMEM, st>>>(a);
@@ -2080,7 +2106,18 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     etq_count_launch();
     const int gs = grid_for(lv.A.nslices * 32, BS, 4096);
     if (tile_ok(H, lv)) {
-      // residual + two steps in one pass; x goes to d1 (tiles read x halos), deferred d2 to d0
+      // residual + two steps in one pass; x goes to d1 (tiles read x halos), deferred d2 to d0.
+      // Finest level: the pass writes z = x + d2 (and its dot partials) itself, unless z aliases
+      // an input the other tiles still read or the reduction grid exceeds the partials buffer
+      const int tx = (lv.g.m + CT_T - 1) / CT_T;
+      const bool fuse = l == 0 && z_u != r_u && z_u != lv.x && z_u != lv.d1 && z_u != lv.d0 &&
+                        2 * tx * tx <= RED_MAXB && (!dot_out || site);
+      if (fuse) {
+        launch_cheb_tile(lv, true, bvec[l], lv.x, lv.d1, nullptr, lv.d0, c1, c2, theta, done, st, z_u, dot_with,
+                         site, slot, dot_out);
+        etq_count_launch();
+        return ETQ_OK;
+      }
       launch_cheb_tile(lv, true, bvec[l], lv.x, lv.d1, nullptr, lv.d0, c1, c2, theta, done, st); etq_count_launch();
       xres[l] = lv.d1;
       pend[l] = lv.d0;
