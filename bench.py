@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-p3", action="store_true", help="skip the P3 (exact M_Q) time-to-solution block")
     ap.add_argument("--clock-ms", type=int, default=1000, help="nvidia-smi sampling period during the timed region")
+    ap.add_argument("--host-loop", action="store_true",
+                    help="MINRES as one graph launch per iteration instead of one graph with a device while node "
+                         "(ncu cannot profile kernels inside graphs with conditional nodes; same iterates)")
     return ap.parse_args()
 
 
@@ -210,6 +213,8 @@ def run_ours(args):
             dist.barrier()
 
     n = args.n
+    if args.host_loop:
+        etq.set_option(3, 0)
     t0 = time.perf_counter()
     P = etq.Problem(n, bc=0)
     torch.cuda.synchronize()
@@ -288,6 +293,13 @@ def run_ours(args):
         kern[names[w]] = {"ms": k_ms, "algorithmic_bytes": k_bytes,
                           "GB_per_s": (k_bytes / (k_ms * 1e-3) / 1e9) if k_bytes > 0 else None,
                           "frac_of_peak": (k_bytes / (k_ms * 1e-3) / 1e9 / peak) if k_bytes > 0 else None}
+    # the saddle apply is matrix-free (class stencils): its algorithmic bytes are x in + y out; the
+    # stored-operator (CSR model) bytes it replaces are reported beside them
+    nnz = 192 * n * n - 336 * n + 186
+    stored = 12.0 * nnz + 4.0 * (P.N + 1) + 16.0 * P.N
+    s0 = kern[names[0]]
+    s0["csr_model_bytes"] = stored
+    s0["csr_equivalent_GB_per_s"] = stored / (s0["ms"] * 1e-3) / 1e9
     # dominant kernel of the step by the committed ncu launch-list share (profiles/r01_launches_summary.txt)
     dom_name = names[10]
     dom = kern[dom_name]

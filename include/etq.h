@@ -237,7 +237,7 @@ etq_status etq_launch_count(int64_t* count);
 
 /* Time `reps` back-to-back launches of one hot kernel with CUDA events on the problem's stream
  * (bench.py's roofline measurement) and report its algorithmic bytes per launch.
- * which: 0 = fused saddle SpMV [A B^T; B 0] x;
+ * which: 0 = fused saddle SpMV [A B^T; B 0] x (matrix-free Stokes apply: bytes = x in + y out);
  *        1 = finest-level fused Chebyshev step of the V-cycle (SpMV + update, both components);
  *        2 = one V-cycle on both velocity components (P2 set up);
  *        3 = one Pi C Pi pressure apply (P2 set up; L2-resident, bytes reported as 0);

@@ -667,7 +667,10 @@ etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* 
   if (gx) cudaGraphExecDestroy(gx);
   const double nnz_all = (double)(P.Lv.nnz + P.BxT1.nnz + P.ByT1.nnz + P.BxT0.nnz + P.ByT0.nnz + P.B.nnz);
   switch (which) {
-    case 0: *bytes = 12.0 * nnz_all - 4.0 * P.Lv.nnz_implicit - 8.0 * P.Lv.nnz_implicit_vals + 4.0 * P.Lv.nslices * SELL_C + 16.0 * P.N; break;
+    case 0:   // matrix-free apply: x in, y out; stored rows: every stored value / index once + x + y
+      *bytes = (P.mf_on && g_saddle_mf) ? 16.0 * P.N
+               : 12.0 * nnz_all - 4.0 * P.Lv.nnz_implicit - 8.0 * P.Lv.nnz_implicit_vals + 4.0 * P.Lv.nslices * SELL_C + 16.0 * P.N;
+      break;
     case 1: *bytes = cheb_step_bytes(P.mg.lv[0]); break;
     case 2: case 4: *bytes = vcycle_bytes(P.mg); break;
     case 5: *bytes = 8.0 * nnz_all + 4.0 * P.Lv.nslices * SELL_C + 8.0 * P.N; break;

@@ -103,13 +103,14 @@ def test_device_minres_loop_matches_host_loop(kind):
     np.testing.assert_array_equal(xs[0], xs[1])
 
 
+@pytest.mark.parametrize("option", [5])
 @pytest.mark.parametrize("n", [32, 64, 256])
-def test_shared_memory_tail_bitwise_equal(n):
-    """The coarse-level tail run in shared memory with the class stencils (option 5) gives the same
+def test_vcycle_fusions_bitwise_equal(n, option):
+    """Option 5: the coarse-level tail run in shared memory with the class stencils gives the same
     V-cycle output, bit for bit, as the tail through the stored rows in global memory."""
     zs = {}
     for opt in (0, 1):
-        etq.set_option(5, opt)
+        etq.set_option(option, opt)
         try:
             P = etq.Problem(n)
             P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.005))
@@ -120,5 +121,5 @@ def test_shared_memory_tail_bitwise_equal(n):
             zs[opt] = z.cpu().numpy()
             P.close()
         finally:
-            etq.set_option(5, 1)
+            etq.set_option(option, 1)
     np.testing.assert_array_equal(zs[0], zs[1])
