@@ -425,7 +425,7 @@ __device__ __forceinline__ void ct_row_t(const ChebTileArgs& a, int i0, int j0, 
     qq[1] = ct_tap_sum<3, 1, RSLOT>(a.so, win);
   }
   const int j = j0 + jj;
-  if (!lok || j < 0 || j >= m) return;
+  if (!lok || (EDGE && (j < 0 || j >= m))) return;   // interior tiles lie inside the domain
   constexpr int C0 = (t & 1) * 2;
   const int base = ii + CT_R * jj;
   const double2 rr = *reinterpret_cast<const double2*>(RS + base);
@@ -439,7 +439,7 @@ __device__ __forceinline__ void ct_row_t(const ChebTileArgs& a, int i0, int j0, 
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int ik = i + k;
-    const bool dir = ik == 0 || j == 0 || ik == m - 1 || j == m - 1;
+    const bool dir = EDGE && (ik == 0 || j == 0 || ik == m - 1 || j == m - 1);   // interior tiles: never
     if (EDGE && dir) qq[k] = fma(1.0, v[base + k], 0.0);   // identity row (unmasked centre)
     const double di = dir ? 1.0 : a.so.dcls[C0 + k];
     ro[k] = ro[k] - qq[k];
