@@ -1259,6 +1259,241 @@ __global__ void k_sell_to_dense(Sell A, int m, double* D) {
 
 static MassGeo mass_geo(const Geo& g) { MassGeo m{g.n, g.nk, g.n0, g.h}; return m; }
 
+// ---------------------------------------------------------------- tiled matrix-free saddle apply
+// y = [A B^T; B 0] x on the Stokes system (reduced: P0 columns / rows dropped) with x staged in
+// shared memory: a CTA owns a 64 x 64 tile of Q2 nodes (both components), the 32 x 32 Q1 vertices
+// and P0 cells at its even origin, and stages the node window with a halo of 2 (the stencil
+// radius), split by column parity (E: even, O: odd columns) so that every warp access, for the
+// node pairs of the velocity rows and for the stride-2 node gathers of the pressure rows, is 32
+// consecutive words; plus the Q1 (34 x 34) and P0 (33 x 33) windows the B^T parts read.  All
+// staging is cp.async (zero-filled outside the domain).  Velocity rows: lanes own a column pair
+// (even i, odd i + 1), a warp walks 8 rows with a 5-row x 6-column register window, one
+// component at a time.  Every row's arithmetic is that of k_saddle_mf in the same order
+// (Dirichlet / outside nodes read as 0 where k_saddle_mf skips them; zero-weight taps skipped),
+// so y is bitwise the same.
+constexpr int ST_T = 64;               // tile side in Q2 nodes (even origin)
+constexpr int ST_W = ST_T + 4;         // staged window (halo 2)
+constexpr int ST_H = ST_W / 2;         // entries per parity row (34)
+constexpr int ST_PW = ST_T / 2 + 2;    // Q1 window (vertices I0/2 - 1 ... I0/2 + 32)
+constexpr int ST_CW = ST_T / 2 + 1;    // P0 window (cells I0/2 - 1 ... I0/2 + 31)
+constexpr int ST_THREADS = 256;
+constexpr int ST_ROWS = ST_T / (ST_THREADS / 32);   // 8 tile rows per warp
+constexpr int ST_SMEM = (4 * ST_W * ST_H + ST_PW * ST_PW + ST_CW * ST_CW) * (int)sizeof(double);
+static_assert(ST_T == 2 * 32 && ST_ROWS % 2 == 0, "lane = column pair, even strips");
+
+struct SaddleTileArgs {
+  StencilOp so; SaddleSt w;
+  int m, n, nq, nk, tiles_x; int64_t n_u; int reduced;
+  const double* x; double* y; const double* inv_scale;
+  RedSite site; int slot; double* dot_out; const double* done;
+};
+
+// shared-memory layout (one dynamic array; every offset a compile-time constant): E0, O0, E1, O1
+// (ST_W rows x ST_H), then the Q1 window (ST_PW x ST_PW), then the P0 window (ST_CW x ST_CW)
+extern __shared__ __align__(16) double st_sm[];
+constexpr int ST_OFF_P1 = 4 * ST_W * ST_H, ST_OFF_P0 = ST_OFF_P1 + ST_PW * ST_PW;
+struct StSmem {
+  __device__ __forceinline__ const double* E(int c) const { return st_sm + 2 * c * ST_W * ST_H; }
+  __device__ __forceinline__ const double* O(int c) const { return st_sm + (2 * c + 1) * ST_W * ST_H; }
+  __device__ __forceinline__ const double* P1() const { return st_sm + ST_OFF_P1; }
+  __device__ __forceinline__ const double* P0() const { return st_sm + ST_OFF_P0; }
+  // node at window (wi, wj) of component c
+  __device__ __forceinline__ double node(int c, int wi, int wj) const {
+    return (wi & 1) ? O(c)[wj * ST_H + (wi >> 1)] : E(c)[wj * ST_H + (wi >> 1)];
+  }
+};
+
+// window row wr of component c for lane L: columns 2L .. 2L + 4 (the pair's taps: the even node
+// at 2L + 2 reads 2L .. 2L + 4, the odd node at 2L + 3 reads 2L + 2 .. 2L + 4), Dirichlet /
+// outside nodes as 0 on edge tiles
+template <bool EDGE>
+__device__ __forceinline__ void st_load_row(const StSmem& S, int c, int wr, int L, int I0, int J0, int m,
+                                            double (&v)[5]) {
+  const double* e = S.E(c) + wr * ST_H + L;
+  const double* o = S.O(c) + wr * ST_H + L;
+  v[0] = e[0]; v[1] = o[0]; v[2] = e[1]; v[3] = o[1]; v[4] = e[2];
+  if (EDGE) {
+    const int gj = J0 - 2 + wr;
+    const bool rowd = gj <= 0 || gj >= m - 1;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const int gi = I0 - 2 + 2 * L + k;
+      if (rowd || gi <= 0 || gi >= m - 1) v[k] = 0.0;
+    }
+  }
+}
+
+// A-part of one velocity row of class CL from the register window (output at window column
+// offset OC within the 6 loaded columns; RSLOT: ring slot of the output row)
+template <int CL, int OC, int RSLOT>
+__device__ __forceinline__ double st_lap(const StencilOp& so, const double (&win)[5][5]) {
+  constexpr int PI = CL & 1, PJ = CL >> 1, RX = PI ? 1 : 2, RY = PJ ? 1 : 2;
+  double a = 0.0;
+#pragma unroll
+  for (int dj = -RY; dj <= RY; ++dj)
+#pragma unroll
+    for (int di = -RX; di <= RX; ++di)
+      a = fma(so.w[CL][(dj + 2) * 5 + di + 2], win[(RSLOT + dj + 5) % 5][OC + di], a);
+  return a;
+}
+
+// one output row t of the warp's strip for component C (compile-time t: ring slots, classes)
+template <int C, bool EDGE, int t>
+__device__ __forceinline__ void st_vel_row(const SaddleTileArgs& a, const StSmem& S, int L, int tj0, int I0, int J0,
+                                           double sc, double (&win)[5][5], double& dot) {
+  const int m = a.m, n = a.n;
+  if (t + 4 < ST_ROWS + 4) st_load_row<EDGE>(S, C, tj0 + t + 4, L, I0, J0, m, win[(t + 4) % 5]);
+  constexpr int RS = (t + 2) % 5;
+  constexpr int PJ = (t & 1);                 // tile rows start even: row parity = t parity
+  const int tj = tj0 + t, j = J0 + tj;
+  const int jc = j >> 1;
+  const int pr = jc - (J0 >> 1) + 1;          // Q1 / P0 window row of jc
+  double q[2];
+  q[0] = st_lap<2 * PJ, 2, RS>(a.so, win);
+  q[1] = st_lap<2 * PJ + 1, 3, RS>(a.so, win);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = I0 + 2 * L + k;
+    if (EDGE && (i >= m || j >= m)) continue;
+    const int cl = 2 * PJ + k;
+    const double raw = S.node(C, 2 * L + 2 + k, tj + 2);
+    double ax;
+    if (EDGE && (i == 0 || j == 0 || i == m - 1 || j == m - 1)) {   // identity row; B^T rows are empty
+      ax = fma(1.0, raw, 0.0) + 0.0;
+      if (!a.reduced) ax += 0.0;
+    } else {
+      double bx = 0.0;
+#pragma unroll
+      for (int dc = -1; dc <= 1; ++dc)
+#pragma unroll
+        for (int da = -1; da <= 1; ++da)
+          bx = fma(a.w.bt1[cl][C][(dc + 1) * 3 + da + 1], S.P1()[(pr + dc) * ST_PW + L + 1 + da], bx);
+      ax = q[k] + bx;
+      if (!a.reduced) {
+        double cx = 0.0;
+#pragma unroll
+        for (int df = -1; df <= 0; ++df)
+#pragma unroll
+          for (int de = -1; de <= 0; ++de)
+            cx = fma(a.w.bt0[cl][C][(df + 1) * 2 + de + 1], S.P0()[(pr + df) * ST_CW + L + 1 + de], cx);
+        ax += cx;
+      }
+    }
+    ax *= sc;
+    a.y[(int64_t)C * a.nq + i + (int64_t)m * j] = ax;
+    if (a.dot_out) dot += ax * (sc * raw);
+  }
+  (void)n;
+}
+
+template <int C, bool EDGE, int... Ts>
+__device__ __forceinline__ void st_vel_rows(const SaddleTileArgs& a, const StSmem& S, int L, int tj0, int I0, int J0,
+                                            double sc, double (&win)[5][5], double& dot, std::integer_sequence<int, Ts...>) {
+  (st_vel_row<C, EDGE, Ts>(a, S, L, tj0, I0, J0, sc, win, dot), ...);
+}
+
+template <int C, bool EDGE>
+__device__ __forceinline__ void st_vel(const SaddleTileArgs& a, const StSmem& S, int I0, int J0, double sc, double& dot) {
+  const int L = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tj0 = ST_ROWS * w;                // first tile row of the strip; window row = tile row + 2
+  double win[5][5];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) st_load_row<EDGE>(S, C, tj0 + r, L, I0, J0, a.m, win[r]);   // rows tj0-2 .. tj0+1
+  st_vel_rows<C, EDGE>(a, S, L, tj0, I0, J0, sc, win, dot, std::make_integer_sequence<int, ST_ROWS>{});
+}
+
+// node value for the pressure rows (Dirichlet / outside -> 0 on edge tiles)
+template <bool EDGE>
+__device__ __forceinline__ double st_pnode(const StSmem& S, int c, int wi, int wj, int I0, int J0, int m) {
+  const double v = S.node(c, wi, wj);
+  if (!EDGE) return v;
+  const int gi = I0 - 2 + wi, gj = J0 - 2 + wj;
+  return (gi <= 0 || gj <= 0 || gi >= m - 1 || gj >= m - 1) ? 0.0 : v;
+}
+
+template <bool EDGE>
+__device__ __forceinline__ void st_body(const SaddleTileArgs& a, const StSmem& S, int I0, int J0, double sc) {
+  double dot = 0.0;
+  st_vel<0, EDGE>(a, S, I0, J0, sc, dot);
+  st_vel<1, EDGE>(a, S, I0, J0, sc, dot);
+  // pressure rows: Q1 vertices (a, c) and P0 cells (e, f) of the tile, lane = column
+  const int L = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int m = a.m, n = a.n, n1 = n + 1;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int cr = w + 8 * r;                      // tile vertex / cell row
+    const int va = (I0 >> 1) + L, vc = (J0 >> 1) + cr;
+    if (!EDGE || (va <= n && vc <= n)) {
+      double acc = 0.0;
+#pragma unroll
+      for (int dj = -2; dj <= 2; ++dj)
+#pragma unroll
+        for (int di = -2; di <= 2; ++di) {
+          const int wi = 2 * L + 2 + di, wj = 2 * cr + 2 + dj;
+          acc = fma(a.w.b1[0][(dj + 2) * 5 + di + 2], st_pnode<EDGE>(S, 0, wi, wj, I0, J0, m), acc);
+          acc = fma(a.w.b1[1][(dj + 2) * 5 + di + 2], st_pnode<EDGE>(S, 1, wi, wj, I0, J0, m), acc);
+        }
+      acc *= sc;
+      const int64_t row = va + (int64_t)n1 * vc;
+      a.y[a.n_u + row] = acc;
+      if (a.dot_out) dot += acc * (sc * S.P1()[(cr + 1) * ST_PW + L + 1]);
+    }
+    if (!EDGE || (va < n && vc < n)) {
+      double acc = 0.0;
+#pragma unroll
+      for (int dj = 0; dj <= 2; ++dj)
+#pragma unroll
+        for (int di = 0; di <= 2; ++di) {
+          const int wi = 2 * L + 2 + di, wj = 2 * cr + 2 + dj;
+          acc = fma(a.w.b0[0][dj * 3 + di], st_pnode<EDGE>(S, 0, wi, wj, I0, J0, m), acc);
+          acc = fma(a.w.b0[1][dj * 3 + di], st_pnode<EDGE>(S, 1, wi, wj, I0, J0, m), acc);
+        }
+      acc *= sc;
+      if (a.reduced) acc = 0.0;
+      const int64_t row = a.nk + va + (int64_t)n * vc;
+      a.y[a.n_u + row] = acc;
+      if (a.dot_out) dot += acc * (sc * S.P0()[(cr + 1) * ST_CW + L + 1]);
+    }
+  }
+  if (a.dot_out) { double v[1] = {dot}; reduce_finish<1>(v, a.site, a.slot, a.dot_out); }
+}
+
+__global__ void __launch_bounds__(ST_THREADS, 2) k_saddle_tile(SaddleTileArgs a) {
+  if (is_done(a.done)) return;
+  const StSmem S;
+  const int m = a.m, n = a.n, n1 = n + 1;
+  const int I0 = (blockIdx.x % a.tiles_x) * ST_T, J0 = (blockIdx.x / a.tiles_x) * ST_T;
+  const double sc = a.inv_scale ? *a.inv_scale : 1.0;
+  const double* xu = a.x;
+  const double* p1 = a.x + a.n_u;
+  const double* p0 = p1 + a.nk;
+  // ---- stage (cp.async, zero-fill outside the domain)
+  for (int idx = threadIdx.x; idx < ST_W * ST_W; idx += ST_THREADS) {
+    const int wi = idx % ST_W, wj = idx / ST_W;
+    const int gi = I0 - 2 + wi, gj = J0 - 2 + wj;
+    const bool in = gi >= 0 && gj >= 0 && gi < m && gj < m;
+    const int64_t g = in ? gi + (int64_t)m * gj : 0;
+    const int s = wj * ST_H + (wi >> 1);
+    cp_async8(st_sm + ((wi & 1) ? ST_W * ST_H : 0) + s, xu + g, in);
+    cp_async8(st_sm + ((wi & 1) ? 3 : 2) * ST_W * ST_H + s, xu + a.nq + g, in);
+  }
+  for (int idx = threadIdx.x; idx < ST_PW * ST_PW; idx += ST_THREADS) {
+    const int pa = (I0 >> 1) - 1 + idx % ST_PW, pc = (J0 >> 1) - 1 + idx / ST_PW;
+    const bool in = pa >= 0 && pc >= 0 && pa <= n && pc <= n;
+    cp_async8(st_sm + ST_OFF_P1 + idx, p1 + (in ? pa + (int64_t)n1 * pc : 0), in);
+  }
+  for (int idx = threadIdx.x; idx < ST_CW * ST_CW; idx += ST_THREADS) {
+    const int ce = (I0 >> 1) - 1 + idx % ST_CW, cf = (J0 >> 1) - 1 + idx / ST_CW;
+    const bool in = !a.reduced && ce >= 0 && cf >= 0 && ce < n && cf < n;
+    cp_async8(st_sm + ST_OFF_P0 + idx, p0 + (in ? ce + (int64_t)n * cf : 0), in);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const bool edge = I0 - 2 < 1 || J0 - 2 < 1 || I0 + ST_T + 1 > m - 2 || J0 + ST_T + 1 > m - 2;
+  if (edge) st_body<true>(a, S, I0, J0, sc);
+  else st_body<false>(a, S, I0, J0, sc);
+}
+
 void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y, const double* inv_scale,
                       const RedSite* site, int slot, double* dot_out, const double* done, cudaStream_t st) {
   SaddleArgs a;
@@ -1271,6 +1506,20 @@ void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y
     b.so = P.so0; b.w = P.sst;
     b.nq = P.g.nq; b.nk = P.g.nk; b.n_u = P.n_u; b.n_p = P.n_p; b.reduced = a.reduced;
     b.x = x; b.y = y; b.inv_scale = inv_scale; b.site = a.site; b.slot = slot; b.dot_out = dot_out; b.done = done;
+    if (g_saddle_tile) {
+      static bool smem_set = false;
+      if (!smem_set) {
+        cudaFuncSetAttribute(k_saddle_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM);
+        smem_set = true;
+      }
+      SaddleTileArgs t;
+      t.so = P.so0; t.w = P.sst;
+      t.m = P.g.m; t.n = P.g.n; t.nq = P.g.nq; t.nk = P.g.nk; t.n_u = P.n_u; t.reduced = a.reduced;
+      t.tiles_x = (P.g.m + ST_T - 1) / ST_T;
+      t.x = x; t.y = y; t.inv_scale = inv_scale; t.site = a.site; t.slot = slot; t.dot_out = dot_out; t.done = done;
+      k_saddle_tile<<<t.tiles_x * t.tiles_x, ST_THREADS, ST_SMEM, st>>>(t); etq_count_launch();
+      return;
+    }
     k_saddle_mf<<<grid_for(P.N, BS, 8 * 148 * 2), BS, 0, st>>>(b); etq_count_launch();
     return;
   }

@@ -57,12 +57,14 @@ def test_set_option_rejects_unknown():
         etq.set_option(1, 0)
 
 
-@pytest.mark.parametrize("n", [16, 64, 256])
-def test_matrix_free_saddle_bitwise_equal(n):
+@pytest.mark.parametrize("tiled", [0, 1])
+@pytest.mark.parametrize("n", [16, 64, 130 // 2 * 2, 256])
+def test_matrix_free_saddle_bitwise_equal(n, tiled):
     """The matrix-free Stokes saddle apply (class stencils of L, B^T and B) equals the stored-row
     apply bitwise, full and reduced."""
     ys = {}
     x = None
+    etq.set_option(6, tiled)
     for opt in (0, 1):
         etq.set_option(2, opt)
         try:
@@ -76,6 +78,7 @@ def test_matrix_free_saddle_bitwise_equal(n):
             P.close()
         finally:
             etq.set_option(2, 1)
+    etq.set_option(6, 1)
     for red in (False, True):
         np.testing.assert_array_equal(ys[(0, red)], ys[(1, red)])
 
