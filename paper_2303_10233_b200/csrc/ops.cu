@@ -962,12 +962,10 @@ constexpr int SGS_HX = 8, SGS_HY = 4;  // left / bottom halo (right / top: 6 / 2
 constexpr int SGS_TTX = 50, SGS_TTY = 58;   // tile
 constexpr int SGS_P = SGS_W / 2;       // plane side (32)
 constexpr int SGS_PL = SGS_P * SGS_P;  // one plane
-constexpr int SGS_I0 = SGS_HX / 2, SGS_NI = SGS_TTX / 2;   // tile in plane entries: i in [4, 29)
-constexpr int SGS_J0 = SGS_HY / 2, SGS_NJ = SGS_TTY / 2;   //                       j in [2, 31)
-constexpr int SGS_QP = SGS_NI * SGS_NJ;    // one Q plane
+constexpr int SGS_TQ = SGS_TTX * SGS_TTY;  // tile entries (Q: vertices, then cells, row-major)
 constexpr int SGS_PAD = 64;            // zeroed words before the vertex planes (edge reads at -33)
 constexpr int SGS_TX = 32, SGS_TY = 16;
-constexpr int SGS_SMEM = (SGS_PAD + 8 * SGS_PL + 8 * SGS_QP) * (int)sizeof(double);
+constexpr int SGS_SMEM = (SGS_PAD + 8 * SGS_PL + 2 * SGS_TQ) * (int)sizeof(double);
 static_assert(SGS_W - SGS_HX - SGS_TTX >= 6 && SGS_W - SGS_HY - SGS_TTY >= 2, "right / top halo");
 static_assert(SGS_HX % 2 == 0 && SGS_HY % 2 == 0 && SGS_TTX % 2 == 0 && SGS_TTY % 2 == 0, "even origins");
 static_assert(SGS_TX == SGS_P && 2 * SGS_TY == SGS_P, "one thread per plane column, two rows");
@@ -1070,8 +1068,28 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
   const bool use_yp = a.mode && a.yp && co_p != 0.0;
   const double* ys = a.y ? a.y : a.r;      // valid source address for the zero-filling copies
   const double* yps = use_yp ? a.yp : a.r;
-  // ---- one staging phase (plane order): y by cp.async (vertices, cells), r into registers,
-  //      y_prev of the tile by cp.async into Q
+  // ---- one staging phase: y (window) and y_prev (tile) by cp.async in row-major order (each
+  //      warp reads 32 consecutive words of a global row; the shared destinations are the parity
+  //      planes / the tile-ordered Q), r into registers in plane order (the thread's own entries)
+  const int tid = i + SGS_TX * ty;
+#pragma unroll
+  for (int q = 0; q < SGS_W * SGS_W / (SGS_TX * SGS_TY); ++q) {
+    const int idx = tid + q * SGS_TX * SGS_TY;
+    const int la = idx % SGS_W, lc = idx / SGS_W, ga = A0 + la, gc = C0 + lc;
+    const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
+    const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
+    const int pl = ((la & 1) + 2 * (lc & 1)) * SGS_PL + (lc >> 1) * SGS_P + (la >> 1);
+    cp_async8(V + pl, ys + (inv ? ga + (int64_t)n1 * gc : 0), inv && a.y);
+    cp_async8(Cc + pl, ys + nk + (inc ? ga + (int64_t)n * gc : 0), inc && a.y);
+  }
+  if (use_yp) {
+    for (int idx = tid; idx < SGS_TTX * SGS_TTY; idx += SGS_TX * SGS_TY) {
+      const int ga = A0 + SGS_HX + idx % SGS_TTX, gc = C0 + SGS_HY + idx / SGS_TTX;
+      const bool okv = IN || (ga <= n && gc <= n), okc = IN || (ga < n && gc < n);
+      cp_async8(Q + idx, yps + (okv ? ga + (int64_t)n1 * gc : 0), okv);
+      cp_async8(Q + SGS_TQ + idx, yps + nk + (okc ? ga + (int64_t)n * gc : 0), okc);
+    }
+  }
   double rv[4][2], rc[4][2];
 #pragma unroll
   for (int c = 0; c < 4; ++c)
@@ -1081,41 +1099,18 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
       const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
       const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
       const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
-      const int64_t gv = inv ? ga + (int64_t)n1 * gc : 0, gq = inc ? ga + (int64_t)n * gc : 0;
-      cp_async8(V + c * SGS_PL + j * SGS_P + i, ys + gv, inv && a.y);
-      cp_async8(Cc + c * SGS_PL + j * SGS_P + i, ys + nk + gq, inc && a.y);
-      rv[c][m] = inv ? __ldg(r1 + gv) - alpha : 0.0;
-      rc[c][m] = inc ? __ldg(r0 + gq) + alpha : 0.0;
+      rv[c][m] = inv ? __ldg(r1 + ga + (int64_t)n1 * gc) - alpha : 0.0;
+      rc[c][m] = inc ? __ldg(r0 + ga + (int64_t)n * gc) + alpha : 0.0;
     }
-  const bool ti = i >= SGS_I0 && i < SGS_I0 + SGS_NI;
-  if (use_yp && ti) {
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const int j = ty + SGS_TY * m;
-        if (j < SGS_J0 || j >= SGS_J0 + SGS_NJ) continue;
-        const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
-        const bool okv = IN || (ga <= n && gc <= n), okc = IN || (ga < n && gc < n);
-        const int qi = (j - SGS_J0) * SGS_NI + (i - SGS_I0);
-        cp_async8(Q + c * SGS_QP + qi, yps + (okv ? ga + (int64_t)n1 * gc : 0), okv);
-        cp_async8(Q + (4 + c) * SGS_QP + qi, yps + nk + (okc ? ga + (int64_t)n * gc : 0), okc);
-      }
-  }
   cp_async_wait_all();
   __syncthreads();
-  // ---- the y / y_prev part of this thread's outputs, before the sweep overwrites y in place
-  if (ti) {
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const int j = ty + SGS_TY * m;
-        if (j < SGS_J0 || j >= SGS_J0 + SGS_NJ) continue;
-        double* q = Q + c * SGS_QP + (j - SGS_J0) * SGS_NI + (i - SGS_I0);
-        const double yv = (c < 4 ? V : Cc)[(c & 3) * SGS_PL + j * SGS_P + i];
-        *q = fma(co_y, yv, use_yp ? co_p * *q : 0.0);
-      }
+  // ---- the y / y_prev part of this thread's outputs (tile row-major), before the sweep
+  //      overwrites y in place; the write phase below uses the same thread -> entry map
+  for (int idx = tid; idx < SGS_TTX * SGS_TTY; idx += SGS_TX * SGS_TY) {
+    const int la = SGS_HX + idx % SGS_TTX, lc = SGS_HY + idx / SGS_TTX;
+    const int pl = ((la & 1) + 2 * (lc & 1)) * SGS_PL + (lc >> 1) * SGS_P + (la >> 1);
+    Q[idx] = fma(co_y, V[pl], use_yp ? co_p * Q[idx] : 0.0);
+    Q[SGS_TQ + idx] = fma(co_y, Cc[pl], use_yp ? co_p * Q[SGS_TQ + idx] : 0.0);
   }
   __syncthreads();
   const SgsK& k = a.k;
@@ -1128,26 +1123,22 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
   __syncthreads();
   SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
 #undef SGS_V
-  // ---- write the tile: out = co_s S(y) + Q (plane order; the two parities of a row land in the
-  //      same L2 sectors from the same warp)
+  // ---- write the tile: out = co_s S(y) + Q, row-major (coalesced global rows)
   const double co_s = a.mode ? a.omega * a.gam : 1.0;
   double kd = 0.0;
-  if (ti) {
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const int j = ty + SGS_TY * m;
-        if (j < SGS_J0 || j >= SGS_J0 + SGS_NJ) continue;
-        const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + ((c & 3) >> 1);
-        const double o = fma(co_s, (c < 4 ? V : Cc)[(c & 3) * SGS_PL + j * SGS_P + i],
-                             Q[c * SGS_QP + (j - SGS_J0) * SGS_NI + (i - SGS_I0)]);
-        if (c < 4) {
-          if (IN || (ga <= n && gc <= n)) { a.out[ga + (int64_t)n1 * gc] = o; kd += o; }
-        } else {
-          if (IN || (ga < n && gc < n)) { a.out[nk + ga + (int64_t)n * gc] = o; kd -= o; }
-        }
-      }
+  for (int idx = tid; idx < SGS_TTX * SGS_TTY; idx += SGS_TX * SGS_TY) {
+    const int la = SGS_HX + idx % SGS_TTX, lc = SGS_HY + idx / SGS_TTX, ga = A0 + la, gc = C0 + lc;
+    const int pl = ((la & 1) + 2 * (lc & 1)) * SGS_PL + (lc >> 1) * SGS_P + (la >> 1);
+    if (IN || (ga <= n && gc <= n)) {
+      const double o = fma(co_s, V[pl], Q[idx]);
+      a.out[ga + (int64_t)n1 * gc] = o;
+      kd += o;
+    }
+    if (IN || (ga < n && gc < n)) {
+      const double o = fma(co_s, Cc[pl], Q[SGS_TQ + idx]);
+      a.out[nk + ga + (int64_t)n * gc] = o;
+      kd -= o;
+    }
   }
   if (a.kout) { double v[1] = {kd}; reduce_finish<1>(v, a.site, a.slot, a.kout); }
 }
@@ -1161,8 +1152,7 @@ __global__ void __launch_bounds__(SGS_TX * SGS_TY, SGS_MINB) k_sgs_tile(SgsTileA
   double* V = sm + SGS_PAD;
   double* Cc = V + 4 * SGS_PL;
   double* Q = Cc + 4 * SGS_PL;
-  const int tid = threadIdx.x + SGS_TX * threadIdx.y;
-  if (tid < SGS_PAD) sm[tid] = 0.0;
+  if (threadIdx.x + SGS_TX * threadIdx.y < SGS_PAD) sm[threadIdx.x + SGS_TX * threadIdx.y] = 0.0;
   const int n = a.g.n;
   const int A0 = (blockIdx.x % a.tiles_x) * SGS_TTX - SGS_HX, C0 = (blockIdx.x / a.tiles_x) * SGS_TTY - SGS_HY;
   const bool interior = A0 >= 1 && A0 + SGS_W - 1 <= n - 1 && C0 >= 1 && C0 + SGS_W - 1 <= n - 1;
