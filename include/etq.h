@@ -261,7 +261,9 @@ etq_status etq_time_kernel(etq_problem* p, int32_t which, int32_t reps, double* 
  *   option 5 = coarse V-cycle levels (n <= 16) in one CTA with every vector in shared memory and
  *              the class stencils (1 [default], Stokes only) or through the stored rows in global memory (0);
  *   option 6 = matrix-free Stokes saddle apply from shared-memory tiles (1 [default]) or by global
- *              gathers (0); only with option 2 = 1.
+ *              gathers (0); only with option 2 = 1;
+ *   option 7 = programmatic dependent launches between the Chebyshev-SGS steps (1 [default]) or plain
+ *              stream order (0).
  * Applies to solves whose CUDA graphs are captured afterwards (re-run etq_precond_setup). */
 etq_status etq_set_option(int32_t option, int32_t value);
 

@@ -988,6 +988,7 @@ struct SgsTileArgs {
   int tiles_x;
   RedSite site; int slot; double* kout;   // optional k^T out
   const double* done;
+  int pdl;                  // launched as a programmatic dependent of the previous SGS step
 };
 
 
@@ -1123,6 +1124,9 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
   __syncthreads();
   SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
 #undef SGS_V
+  // the next step's CTAs may launch once every CTA of this grid is writing its tile (they wait in
+  // griddepcontrol.wait; triggering at the start would park them on SMs the V-cycle needs)
+  asm volatile("griddepcontrol.launch_dependents;");
   // ---- write the tile: out = co_s S(y) + Q, row-major (coalesced global rows)
   const double co_s = a.mode ? a.omega * a.gam : 1.0;
   double kd = 0.0;
@@ -1147,6 +1151,7 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
 #define SGS_MINB 2
 #endif
 __global__ void __launch_bounds__(SGS_TX * SGS_TY, SGS_MINB) k_sgs_tile(SgsTileArgs a) {
+  if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");   // previous step complete and visible
   if (is_done(a.done)) return;
   extern __shared__ double sm[];
   double* V = sm + SGS_PAD;
@@ -2416,7 +2421,7 @@ void mass_apply(const Geo& g, const double* x, double* y, cudaStream_t st) {
   k_mass_apply<<<grid_for((int64_t)g.nk + g.n0, BS, 4096), BS, 0, st>>>(mass_geo(g), x, y); etq_count_launch();
 }
 
-static void launch_sgs_tile(SgsTileArgs a, cudaStream_t st) {
+static void launch_sgs_tile(SgsTileArgs a, cudaStream_t st, bool pdl = false) {
   static bool smem_set = false;
   if (!smem_set) {
     cudaFuncSetAttribute(k_sgs_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, SGS_SMEM);
@@ -2438,10 +2443,15 @@ static void launch_sgs_tile(SgsTileArgs a, cudaStream_t st) {
   if (lo_prio == 1) cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles); cfg.blockDim = dim3(SGS_TX, SGS_TY); cfg.dynamicSmemBytes = SGS_SMEM; cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributePriority;
   attr[0].val.priority = g_sgs_high_prio ? hi_prio : lo_prio;
-  cfg.attrs = attr; cfg.numAttrs = 1;
+  // programmatic dependent launch on the previous SGS step: this grid's CTAs are launched while
+  // the previous step drains and wait in griddepcontrol.wait (kernel-boundary bubble hidden)
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  a.pdl = pdl && g_sgs_pdl ? 1 : 0;
+  cfg.attrs = attr; cfg.numAttrs = a.pdl ? 2 : 1;
   cudaLaunchKernelEx(&cfg, k_sgs_tile, a); etq_count_launch();
 }
 
@@ -2490,7 +2500,7 @@ etq_status mass_pc_apply_ex(const Problem& P, const double* r_p, double* z_p, co
     a.y = cur; a.yp = prev; a.out = out; a.mode = 1;
     a.omega = (k == 0) ? 1.0 : omega; a.gam = gam;
     a.site = rs; a.slot = 4; a.kout = (k == M.m - 1) ? P.dscal + S_KY : nullptr; a.done = done;
-    launch_sgs_tile(a, st);
+    launch_sgs_tile(a, st, k > 0);
     prev = cur; cur = out;
   }
   k_kproject_out<<<gf, BS, 0, st>>>(g.nk, np, cur, P.dscal + S_KY, inv_kk, scale, z_p, dot_with, rs, slot, dot_out,
