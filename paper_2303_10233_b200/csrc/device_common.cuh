@@ -1,6 +1,7 @@
 // device_common.cuh — device helpers shared by the kernel files of libetq: launch sizing,
 // deterministic block/grid reductions, SELL-32 row products.
 #pragma once
+#include <utility>
 #include "etq_internal.cuh"
 
 // ================================================================ launch helpers
@@ -16,6 +17,26 @@ inline int grid_for(int64_t work_items, int per_block, int cap = MAXB) {
 }
 
 __device__ __forceinline__ bool is_done(const double* done) { return done && *done != 0.0; }
+
+// programmatic dependent launch: wait until the preceding grid has completed and its writes are
+// visible (a no-op when the grid was not launched as a programmatic dependent); allow the next
+// grid, if launched as a programmatic dependent, to start launching
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+// launch with the programmatic-stream-serialization attribute when pdl (the kernel must call
+// pdl_wait() before touching anything the preceding kernel wrote)
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid; cfg.blockDim = block; cfg.dynamicSmemBytes = smem; cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at; cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {

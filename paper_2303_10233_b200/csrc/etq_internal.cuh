@@ -42,6 +42,7 @@ extern bool g_sgs_high_prio;              // api.cu; etq_set_option(4)
 extern bool g_tail_sm;                    // api.cu; etq_set_option(5)
 extern bool g_saddle_tile;                // api.cu; etq_set_option(6)
 extern bool g_sgs_pdl;                    // api.cu; etq_set_option(7)
+extern bool g_vc_pdl;                     // api.cu; etq_set_option(8)
 
 constexpr int SELL_C = 32;           // slice height = warp size
 constexpr int RED_BLOCKS = 592;      // 4 x 148 SMs: grid of plain reduction kernels
@@ -350,7 +351,7 @@ void free_hierarchy(Hierarchy& H);
 etq_status dense_inverse_pivot(double* A, int m, cudaStream_t st);
 etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r_u, double* z_u,
                            const RedSite* site, int slot, double* dot_out, const double* dot_with,
-                           const double* done, cudaStream_t st);
+                           const double* done, cudaStream_t st, bool pdl = false);
 void mass_apply(const Geo& g, const double* x, double* y, cudaStream_t st);
 void sgs_sweep_dev(const Geo& g, const double* r, const double* y, double* z, double* t, cudaStream_t st);
 etq_status mass_pc_alloc(Problem& P);

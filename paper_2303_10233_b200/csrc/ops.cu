@@ -317,6 +317,7 @@ __device__ __forceinline__ void cheb_update2(const ChebStArgs& a, int row, doubl
 #define STENCIL_MINB 6
 #endif
 __global__ void __launch_bounds__(BS, STENCIL_MINB) k_cheb_step_st(ChebStArgs a) {
+  pdl_wait();
   if (is_done(a.done)) return;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -482,6 +483,7 @@ __device__ __forceinline__ void ct_step(const ChebTileArgs& a, int i0, int j0, d
 
 template <int POST>
 __global__ void __launch_bounds__(CT_THREADS, 2) k_cheb_tile(ChebTileArgs a) {
+  pdl_wait();
   if (is_done(a.done)) return;
   extern __shared__ __align__(16) double ct_sm[];
   double* D0 = ct_sm;
@@ -575,6 +577,7 @@ __global__ void __launch_bounds__(CT_THREADS, 2) k_cheb_tile(ChebTileArgs a) {
     tile_accum(D0);                                                              // x3 = x2 + d2
     CT_STEP(6, 0, RS, D0, D0, (double*)nullptr, 0.0, 0.0);
     __syncthreads();
+    pdl_trigger();
     tile_pass([&](int w, int64_t g) { a.r_out[g] = RS[w]; });
   } else {
     CT_STEP(2, 1, RS, D1, (const double*)nullptr, D0, 0.0, 0.0);   // r0 = b - A x, d0 = D^-1 r0 / theta
@@ -586,6 +589,7 @@ __global__ void __launch_bounds__(CT_THREADS, 2) k_cheb_tile(ChebTileArgs a) {
     tile_accum(D1);                                                      // x += d1
     CT_STEP(6, 0, RS, D1, D1, D0, a.c1[1], a.c2[1]);                   // d2 (deferred)
     __syncthreads();
+    pdl_trigger();
     if (a.z_out) {   // finest level: the V-cycle's result z = x + d2 (k_final_add fused), <z, w>
       double xv[NTP], wv[NTP];
 #pragma unroll
@@ -779,6 +783,7 @@ __device__ __forceinline__ int restrict_taps(int I, int* off, double* w) {
 // b_c = Z_c P^T r_f (both components) and d0_c = D_c^{-1} b_c / theta
 __global__ void k_restrict(int mf, int mc, int nqf, int nqc, const double* rf, double* bc, double* d0c,
                            const double* dinvc, double itheta, const double* done) {
+  pdl_wait();
   if (is_done(done)) return;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)nqc;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -821,6 +826,7 @@ __device__ __forceinline__ int prolong_taps(int k, int* idx, double* w) {
 // x_f += Z_f P (x_c + d_c)
 __global__ void k_prolong(int mf, int mc, int nqf, int nqc, const double* xc, const double* dc, double* xf,
                           const double* done) {
+  pdl_wait();
   if (is_done(done)) return;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)nqf;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -1841,6 +1847,7 @@ __device__ __forceinline__ void tsm_cheb_step(const StencilOp& so, int m, const 
 }
 
 __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail_sm(TailSmArgs a) {
+  pdl_wait();
   if (is_done(a.done)) return;
   extern __shared__ double tsm[];
   const int tid = threadIdx.x;
@@ -1959,6 +1966,7 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail_sm(TailSmArgs a) {
     pend_c = din;
   }
   // ---- complete level 0 of the tail: x += pending correction, to global (the caller prolongs it)
+  pdl_trigger();
   {
     const int nq = a.m[0] * a.m[0];
     const double* x = base(0) + 2 * nq;
@@ -2192,13 +2200,14 @@ static void cheb_coeffs(double lo, double hi, double bim, int degree, std::vecto
   }
 }
 
-static void launch_cheb_st(const Level& lv, const ChebArgs& c, bool post, double theta, cudaStream_t st) {
+static void launch_cheb_st(const Level& lv, const ChebArgs& c, bool post, double theta, cudaStream_t st,
+                           bool pdl = false) {
   ChebStArgs a;
   a.so = lv.so; a.F = lv.Afr; a.dinv = c.dinv; a.nq = c.nq;
   a.d_in = c.d_in; a.r_in = c.r_in; a.x_in = c.x_in; a.x_out = c.x_out; a.r_out = c.r_out; a.d_out = c.d_out;
   a.c1 = c.c1; a.c2 = c.c2; a.post = post ? 1 : 0; a.itheta = 1.0 / theta; a.done = c.done;
   const int64_t warps = lv.so.nseg + lv.Afr.nslices;
-  k_cheb_step_st<<<grid_for(warps * 32, BS, 4096), BS, 0, st>>>(a);
+  launch_pdl(k_cheb_step_st, dim3(grid_for(warps * 32, BS, 4096)), dim3(BS), 0, st, pdl, a);
 }
 
 // Temporally blocked smoothing pass on an interior-stencil level (degree 3, real interval).
@@ -2206,7 +2215,8 @@ static void launch_cheb_tile(const Level& lv, bool post, const double* b, const 
                              double* r_out, double* d_out, const std::vector<double>& c1,
                              const std::vector<double>& c2, double theta, const double* done, cudaStream_t st,
                              double* z_out = nullptr, const double* dot_with = nullptr,
-                             const RedSite* site = nullptr, int slot = 0, double* dot_out = nullptr) {
+                             const RedSite* site = nullptr, int slot = 0, double* dot_out = nullptr,
+                             bool pdl = false) {
   static bool smem_set = false;
   if (!smem_set) {
     cudaFuncSetAttribute(k_cheb_tile<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM);
@@ -2224,8 +2234,8 @@ static void launch_cheb_tile(const Level& lv, bool post, const double* b, const 
   a.done = done;
   a.z_out = z_out; a.dot_with = dot_with; a.site = site ? *site : RedSite{}; a.slot = slot; a.dot_out = dot_out;
   dim3 grid(a.tiles_x * a.tiles_x, 2);
-  if (post) k_cheb_tile<1><<<grid, CT_THREADS, CT_SMEM, st>>>(a);
-  else k_cheb_tile<0><<<grid, CT_THREADS, CT_SMEM, st>>>(a);
+  if (post) launch_pdl(k_cheb_tile<1>, grid, dim3(CT_THREADS), CT_SMEM, st, pdl, a);
+  else launch_pdl(k_cheb_tile<0>, grid, dim3(CT_THREADS), CT_SMEM, st, pdl, a);
 }
 
 static bool tile_ok(const Hierarchy& H, const Level& lv) {
@@ -2248,7 +2258,7 @@ static void launch_cheb_sk(const Hierarchy& H, const Level& lv, const ChebArgs& 
 
 etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r_u, double* z_u,
                            const RedSite* site, int slot, double* dot_out, const double* dot_with,
-                           const double* done, cudaStream_t st) {
+                           const double* done, cudaStream_t st, bool pdl) {
   const int L = (int)H.lv.size();
   const int nc = H.ncomp;
   const double theta = 0.5 * (H.hi + H.lo);
@@ -2264,6 +2274,10 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
   }
   std::vector<const double*> bvec(L);
   std::vector<const double*> pend(L, nullptr);
+  // programmatic dependent launches between the cycle's kernels: shorter cycle latency, but the
+  // early-launched CTAs compete with a concurrent branch for SM slots; the caller decides (P3: on,
+  // P2: off - measured: P3 solve 94 -> 88 ms, P2 solve 557 -> 564 ms)
+  const bool vpdl = pdl && g_vc_pdl;
   std::vector<double> c1, c2;
   const bool use_tail = H.kind == 0 && nc == 2 && H.tail_start > 0 && H.tail != nullptr;
   const int Ld = use_tail ? H.tail_start + 1 : L;   // levels handled by the per-level kernels (+1)
@@ -2276,7 +2290,9 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     bvec[l] = b;
     const bool tiled = tile_ok(H, lv);
     if (tiled) {
-      launch_cheb_tile(lv, false, b, nullptr, lv.x, lv.r, nullptr, c1, c2, theta, done, st); etq_count_launch();
+      launch_cheb_tile(lv, false, b, nullptr, lv.x, lv.r, nullptr, c1, c2, theta, done, st, nullptr, nullptr, nullptr,
+                       0, nullptr, vpdl && l > 0);
+      etq_count_launch();
     }
     if (l == 0 && !tiled) {
       k_cheb_init<<<grid_for((int64_t)nc * nq, BS, 4096), BS, 0, st>>>(lv.dinv, nq, nc, b, lv.d0, 1.0 / theta, done); etq_count_launch();
@@ -2289,7 +2305,7 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       a.d_in = din; a.r_in = (k == 0) ? b : lv.r; a.x_in = (k == 0) ? nullptr : lv.x;
       a.x_out = lv.x; a.r_out = lv.r; a.d_out = (k == H.degree - 1) ? nullptr : dout;
       a.c1 = c1[k]; a.c2 = c2[k]; a.done = done;
-      if (lv.st_on) launch_cheb_st(lv, a, false, theta, st);
+      if (lv.st_on) launch_cheb_st(lv, a, false, theta, st, vpdl);
       else if (H.op == 1) launch_cheb_sk(H, lv, a, 0, theta, st);
       else if (nc == 2) k_cheb_step<2><<<gs, BS, 0, st>>>(a);
       else k_cheb_step<1><<<gs, BS, 0, st>>>(a);
@@ -2298,8 +2314,8 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     }
     const Level& cv = H.lv[l + 1];
     if (H.kind == 0) {
-      k_restrict<<<grid_for(cv.g.nq, BS, 4096), BS, 0, st>>>(lv.g.m, cv.g.m, nq, cv.g.nq, lv.r, cv.b, cv.d0,
-                                                            cv.dinv, 1.0 / theta, done);
+      launch_pdl(k_restrict, dim3(grid_for(cv.g.nq, BS, 4096)), dim3(BS), 0, st, vpdl, lv.g.m, cv.g.m, nq, cv.g.nq,
+                 (const double*)lv.r, cv.b, cv.d0, (const double*)cv.dinv, 1.0 / theta, done);
     } else {
       k_restrict_q1<<<grid_for(cv.g.nk, BS, 4096), BS, 0, st>>>(lv.g.n + 1, cv.g.n + 1, lv.r, cv.b, cv.d0,
                                                                cv.dinv, 1.0 / theta, done);
@@ -2317,7 +2333,7 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     if (H.tail_sm && g_tail_sm) {
       TailSmArgs ta = H.tsm;
       ta.done = done;
-      k_vcycle_tail_sm<<<1, TAIL_THREADS, ta.smem_bytes, st>>>(ta);
+      launch_pdl(k_vcycle_tail_sm, dim3(1), dim3(TAIL_THREADS), ta.smem_bytes, st, vpdl, ta);
     } else {
       k_vcycle_tail<<<1, TAIL_THREADS, 0, st>>>(H.tail, L - H.tail_start, H.degree, 1.0 / theta, done);
     }
@@ -2337,7 +2353,8 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     const int nq = lv.nrows;
     cheb_coeffs(H.lo, H.hi, lv.bim, H.degree, c1, c2);
     if (H.kind == 0) {
-      k_prolong<<<grid_for(nq, BS, 4096), BS, 0, st>>>(lv.g.m, cv.g.m, nq, cv.g.nq, xres[l + 1], pend[l + 1], lv.x, done);
+      launch_pdl(k_prolong, dim3(grid_for(nq, BS, 4096)), dim3(BS), 0, st, vpdl, lv.g.m, cv.g.m, nq, cv.g.nq,
+                 xres[l + 1], pend[l + 1], lv.x, done);
     } else {
       k_prolong_q1<<<grid_for(lv.g.nk, BS, 4096), BS, 0, st>>>(lv.g.n + 1, cv.g.n + 1, xres[l + 1], pend[l + 1], lv.x, done);
       if (H.op == 2) {
@@ -2358,11 +2375,13 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
                         2 * tx * tx <= RED_MAXB && (!dot_out || site);
       if (fuse) {
         launch_cheb_tile(lv, true, bvec[l], lv.x, lv.d1, nullptr, lv.d0, c1, c2, theta, done, st, z_u, dot_with,
-                         site, slot, dot_out);
+                         site, slot, dot_out, vpdl);
         etq_count_launch();
         return ETQ_OK;
       }
-      launch_cheb_tile(lv, true, bvec[l], lv.x, lv.d1, nullptr, lv.d0, c1, c2, theta, done, st); etq_count_launch();
+      launch_cheb_tile(lv, true, bvec[l], lv.x, lv.d1, nullptr, lv.d0, c1, c2, theta, done, st, nullptr, nullptr,
+                       nullptr, 0, nullptr, vpdl);
+      etq_count_launch();
       xres[l] = lv.d1;
       pend[l] = lv.d0;
       continue;
@@ -2371,7 +2390,7 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       ChebArgs a{};
       a.A = lv.A; a.dinv = lv.dinv; a.nq = nq; a.x_in = lv.x; a.r_in = bvec[l]; a.r_out = lv.r; a.d_out = lv.d0;
       a.done = done;
-      launch_cheb_st(lv, a, true, theta, st);
+      launch_cheb_st(lv, a, true, theta, st, vpdl);
     } else if (H.op == 1) {
       ChebArgs a{};
       a.x_in = lv.x; a.r_in = bvec[l]; a.r_out = lv.r; a.d_out = lv.d0; a.done = done;
@@ -2389,7 +2408,7 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       a.d_in = din; a.r_in = lv.r; a.x_in = lv.x;
       a.x_out = lv.x; a.r_out = (k == H.degree - 2) ? nullptr : lv.r; a.d_out = dout;
       a.c1 = c1[k]; a.c2 = c2[k]; a.done = done;
-      if (lv.st_on) launch_cheb_st(lv, a, false, theta, st);
+      if (lv.st_on) launch_cheb_st(lv, a, false, theta, st, vpdl);
       else if (H.op == 1) launch_cheb_sk(H, lv, a, 0, theta, st);
       else if (nc == 2) k_cheb_step<2><<<gs, BS, 0, st>>>(a);
       else k_cheb_step<1><<<gs, BS, 0, st>>>(a);

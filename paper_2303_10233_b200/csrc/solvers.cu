@@ -148,7 +148,7 @@ etq_status precond_apply_ex(const Problem& P, etq_pc_kind kind, const double* r,
     ETQ_CHECK(cudaEventRecord(P.ev_fork, st));
     ETQ_CHECK(cudaStreamWaitEvent(P.aux, P.ev_fork, 0));
     ETQ_TRY(exact_mass_apply(P, r + nu, z + nu, site, 2, out_p, w ? w + nu : nullptr, done, P.aux));
-    if (kind == ETQ_PC_P3) ETQ_TRY(vcycle_apply_ex(P, P.mg, r, z, site, 1, out_u, w, done, st));
+    if (kind == ETQ_PC_P3) ETQ_TRY(vcycle_apply_ex(P, P.mg, r, z, site, 1, out_u, w, done, st, true));
     else ETQ_TRY(vel_iter_apply(P, r, z, site, 1, out_u, w, done, st));
     ETQ_CHECK(cudaEventRecord(P.ev_join, P.aux));
     ETQ_CHECK(cudaStreamWaitEvent(st, P.ev_join, 0));

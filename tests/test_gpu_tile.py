@@ -52,7 +52,7 @@ def test_tiled_vcycle_matches_oracle():
 
 def test_set_option_rejects_unknown():
     with pytest.raises(etq.EtqError):
-        etq.set_option(7, 1)
+        etq.set_option(99, 1)
     with pytest.raises(etq.EtqError):
         etq.set_option(1, 0)
 
