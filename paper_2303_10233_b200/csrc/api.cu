@@ -706,6 +706,9 @@ void etq_destroy(etq_problem* h) {
   for (int g = 0; g < 2; ++g) if (P.minres_graph[g]) cudaGraphExecDestroy(P.minres_graph[g]);
   if (P.minres_wgraph) cudaGraphExecDestroy(P.minres_wgraph);
   if (P.wcs) cudaStreamDestroy(P.wcs);
+  if (P.wside) cudaStreamDestroy(P.wside);
+  if (P.ev_wfork) cudaEventDestroy(P.ev_wfork);
+  if (P.ev_wjoin) cudaEventDestroy(P.ev_wjoin);
   free_hierarchy(P.mg);
   exact_free(P);
   oseen_free(P);

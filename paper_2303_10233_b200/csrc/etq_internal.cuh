@@ -307,6 +307,8 @@ struct Problem {
   const double* minres_wgraph_x = nullptr;
   int64_t minres_wbody_nodes = 0, minres_wfixed_nodes = 0;
   cudaStream_t wcs = nullptr;                 // capture stream of the loop body
+  cudaStream_t wside = nullptr;               // MINRES w/x update beside the next saddle apply
+  cudaEvent_t ev_wfork = nullptr, ev_wjoin = nullptr;
   double* tk = nullptr;                       // scratch for etq_time_kernel (3 x N)
   float* tkf = nullptr;                       // fp32 scratch (2 x N)
 };

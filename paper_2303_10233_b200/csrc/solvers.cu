@@ -175,6 +175,13 @@ __global__ void k_minres_cond(const double* sc, cudaGraphConditionalHandle h) {
 }
 
 static etq_status minres_alloc(Problem& P) {
+  if (!P.wside) {
+    int lo = 0, hi = 0;
+    ETQ_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    ETQ_CHECK(cudaStreamCreateWithPriority(&P.wside, cudaStreamNonBlocking, hi));
+    ETQ_CHECK(cudaEventCreateWithFlags(&P.ev_wfork, cudaEventDisableTiming));
+    ETQ_CHECK(cudaEventCreateWithFlags(&P.ev_wjoin, cudaEventDisableTiming));
+  }
   if (P.nkv >= 7) return ETQ_OK;
   for (int i = P.nkv; i < 7; ++i) ETQ_TRY(dalloc(&P.kv[i], P.N));
   P.nkv = 7;
@@ -189,16 +196,32 @@ static etq_status minres_iteration(Problem& P, etq_pc_kind kind, int cur, double
   double* sc = P.dscal;
   const int64_t N = P.N;
   const double* done = sc + S_DONE;
+  // lines 16-17 of the PREVIOUS iteration (w, x update; skipped via S_TMP0 when there is none or the
+  // solve had already stopped) on a side stream, beside this iteration's saddle apply: they share
+  // no vector and no scalar (the update reads z_{j-1}, w and x; the apply reads z_j and writes q and
+  // delta), and this iteration's preconditioner, which overwrites z_{j-1}, starts after the join
+  ETQ_CHECK(cudaEventRecord(P.ev_wfork, st));
+  ETQ_CHECK(cudaStreamWaitEvent(P.wside, P.ev_wfork, 0));
+  k_minres_wx<<<grid_for(N), BS, 0, P.wside>>>(Z[1 - cur], W[1 - cur], W[cur], x, sc, N); etq_count_launch();
+  ETQ_CHECK(cudaEventRecord(P.ev_wjoin, P.wside));
   // line 6-7: q = K (z / gamma), delta = <q, z / gamma>
   launch_saddle_ex(P, false, Z[cur], Q, sc + S_INV_GAMMA, &P.red[0], 0, sc + S_DELTA, done, st);
+  ETQ_CHECK(cudaStreamWaitEvent(st, P.ev_wjoin, 0));
   // line 8
   k_minres_v<<<grid_for(N), BS, 0, st>>>(Q, V[cur], V[1 - cur], sc, N); etq_count_launch();
   // line 9-10 (dot products fused into the preconditioner's last kernels)
   ETQ_TRY(precond_apply_ex(P, kind, V[1 - cur], Z[1 - cur], V[1 - cur], sc + S_DOT0, sc + S_DOT1, done, st));
-  // lines 10-19
+  // lines 10-19 (lines 16-17 of this iteration run at the start of the next one, or in minres_wx_tail)
   k_minres_scalars<<<1, 32, 0, st>>>(sc, P.dhist, P.hist_cap); etq_count_launch();
-  // lines 16-17
-  k_minres_wx<<<grid_for(N), BS, 0, st>>>(Z[cur], W[cur], W[1 - cur], x, sc, N); etq_count_launch();
+  ETQ_CHECK(cudaGetLastError());
+  return ETQ_OK;
+}
+
+// lines 16-17 of the last iteration run (parity cur), after the loop
+static etq_status minres_wx_tail(Problem& P, int cur, double* x, cudaStream_t st) {
+  double* Z[2] = {P.kv[2], P.kv[3]};
+  double* W[2] = {P.kv[4], P.kv[5]};
+  k_minres_wx<<<grid_for(P.N), BS, 0, st>>>(Z[cur], W[cur], W[1 - cur], x, P.dscal, P.N); etq_count_launch();
   ETQ_CHECK(cudaGetLastError());
   return ETQ_OK;
 }
@@ -223,6 +246,7 @@ etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, 
   // scalars
   std::vector<double> h(S_COUNT, 0.0);
   h[S_RTOL] = rtol; h[S_MAXIT] = maxit;
+  h[S_TMP0] = 1.0;   // no previous iteration: the first deferred w/x update is skipped
   ETQ_CHECK(cudaMemcpyAsync(sc, h.data(), sizeof(double) * S_COUNT, cudaMemcpyHostToDevice, st));
   // line 1-2: v^(0) = 0, w^(0) = w^(1) = 0, v^(1) = b - K x0
   ETQ_CHECK(cudaMemsetAsync(V[0], 0, N * sizeof(double), st));
@@ -318,6 +342,7 @@ etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, 
   int it = 0;
   if (devloop) {
     ETQ_CHECK(cudaGraphLaunch(P.minres_wgraph, st));
+    ETQ_TRY(minres_wx_tail(P, 0, x, st));   // the body ends with the parity-0 iteration
     ETQ_CHECK(cudaStreamSynchronize(st));
     ETQ_CHECK(cudaMemcpy(P.hscal, sc, sizeof(double) * 20, cudaMemcpyDeviceToHost));
     const int its = (int)P.hscal[S_IT];
@@ -335,6 +360,7 @@ etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, 
     cur = 1 - cur;
     if (++it > maxit + 2) break;   // safety net; the device flag ends the loop
   }
+  if (!devloop) ETQ_TRY(minres_wx_tail(P, 1 - cur, x, st));   // last iteration run: parity 1 - cur
   ETQ_CHECK(cudaEventRecord(P.ev_t1, st));
   ETQ_CHECK(cudaMemcpyAsync(P.hscal, sc, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost, st));
   ETQ_CHECK(cudaStreamSynchronize(st));
