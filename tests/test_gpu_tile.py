@@ -126,3 +126,27 @@ def test_vcycle_fusions_bitwise_equal(n, option):
         finally:
             etq.set_option(option, 1)
     np.testing.assert_array_equal(zs[0], zs[1])
+
+
+@pytest.mark.parametrize("option,kind", [(7, etq.PC_P2_GMG), (8, etq.PC_P3)])
+def test_programmatic_dependent_launches_bitwise_equal(option, kind):
+    """Programmatic dependent launches (option 7: between the Chebyshev-SGS steps; option 8: between
+    the V-cycle kernels, used by P3) change only when the next kernel's CTAs launch: the MINRES
+    iterates are bit for bit the same with them off."""
+    n = 64
+    xs, its = [], []
+    for opt in (0, 1):
+        etq.set_option(option, opt)
+        try:
+            P = etq.Problem(n)
+            P.precond_setup(kind, etq.make_params(cheb_sgs_lo=0.005))
+            b = torch.zeros(P.N, dtype=torch.float64, device="cuda")
+            P.build_rhs(b)
+            x = torch.zeros(P.N, dtype=torch.float64, device="cuda")
+            rep = P.minres_solve(kind, b, x, rtol=1e-8, maxit=500)
+            xs.append(x.cpu().numpy()); its.append(rep["iterations"])
+            P.close()
+        finally:
+            etq.set_option(option, 1)
+    assert its[0] == its[1]
+    np.testing.assert_array_equal(xs[0], xs[1])
