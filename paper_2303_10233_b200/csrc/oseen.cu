@@ -167,15 +167,33 @@ __global__ void k_copy_vj(const double* V, int64_t N, const double* sc, double* 
     T[i] = vj[i];
 }
 
-// h_i = <V_i, W>, i = 0..j (j from device), in chunks of 8 vectors; deterministic.
+// h_i = <V_i, W>, i = 0..j (j from device), in chunks of 8 vectors; deterministic.  Two elements
+// per thread and iteration with all 18 loads issued first (memory-level parallelism: the kernel is
+// bound by DRAM latency, not bandwidth, at one element per iteration); the per-thread summation
+// order is unchanged (element e, then e + stride, ...).
 __global__ void __launch_bounds__(BS) k_multidot(const double* V, int64_t N, const double* W, const double* sc,
                                                  double* h, RedSite site) {
   const int nv = (int)sc[G_J] + 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int c0 = 0; c0 < nv; c0 += 8) {
     double acc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = 0.0;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; e + stride < N; e += 2 * stride) {
+      const double w0 = W[e], w1 = W[e + stride];
+      double v0[8], v1[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const bool ok = c0 + k < nv;
+        v0[k] = ok ? V[(int64_t)(c0 + k) * N + e] : 0.0;
+        v1[k] = ok ? V[(int64_t)(c0 + k) * N + e + stride] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (c0 + k < nv) { acc[k] = fma(v0[k], w0, acc[k]); acc[k] = fma(v1[k], w1, acc[k]); }
+    }
+    if (e < N) {
       const double w = W[e];
 #pragma unroll
       for (int k = 0; k < 8; ++k)
@@ -185,13 +203,22 @@ __global__ void __launch_bounds__(BS) k_multidot(const double* V, int64_t N, con
   }
 }
 
-// W -= sum_{i <= j} coef_i V_i  (coef device array, count j + 1 from device)
+// W -= sum_{i <= j} coef_i V_i  (coef device array, count j + 1 from device); the vector loads of
+// eight terms are issued before their updates (same update order)
 __global__ void k_multiaxpy(double* W, const double* V, int64_t N, const double* coef, const double* sc, int cnt_slot,
                             int cnt_add, double sign) {
   const int nv = (int)sc[cnt_slot] + cnt_add;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
     double w = W[e];
-    for (int i = 0; i < nv; ++i) w -= sign * coef[i] * V[(int64_t)i * N + e];
+    int i = 0;
+    for (; i + 8 <= nv; i += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = V[(int64_t)(i + u) * N + e];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) w -= sign * coef[i + u] * v[u];
+    }
+    for (; i < nv; ++i) w -= sign * coef[i] * V[(int64_t)i * N + e];
     W[e] = w;
   }
 }
