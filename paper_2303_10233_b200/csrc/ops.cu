@@ -893,12 +893,22 @@ __global__ void k_gemv(const double* A, int m, int ncomp, const double* x, int64
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // both components from one pass over the row (the matrix is read once; per component the
+  // summation order is the lane-strided sum + warp_sum as before)
   for (int64_t r = gw; r < m; r += nw) {
-    for (int c = 0; c < ncomp; ++c) {
-      double s = 0.0;
-      for (int j = lane; j < m; j += 32) s = fma(A[r * m + j], x[c * xs + j], s);
-      s = warp_sum(s);
-      if (lane == 0) y[c * ys + r] = s;
+    for (int c0 = 0; c0 < ncomp; c0 += 2) {
+      const bool two = c0 + 1 < ncomp;
+      const double* x0 = x + c0 * xs;
+      const double* x1 = x + (c0 + 1) * xs;
+      double s0 = 0.0, s1 = 0.0;
+      for (int j = lane; j < m; j += 32) {
+        const double a = A[r * m + j];
+        s0 = fma(a, x0[j], s0);
+        if (two) s1 = fma(a, x1[j], s1);
+      }
+      s0 = warp_sum(s0);
+      if (two) s1 = warp_sum(s1);
+      if (lane == 0) { y[c0 * ys + r] = s0; if (two) y[(c0 + 1) * ys + r] = s1; }
     }
   }
 }
