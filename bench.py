@@ -363,7 +363,8 @@ def run_ours(args):
                            "rel_res": last["rel_res"], "cheb_sgs_lo": a,
                            "assemble_s": assemble_s, "precond_setup_s": setup_s,
                            "parallelism": f"{world} independent replica(s), one per GPU",
-                           "l2": "inputs larger than L2 (operators ~1.6 GB, each vector 84 MB) - no flush needed"},
+                           "l2": ("working set larger than L2: each MINRES iteration streams >= 9 N-vectors of 84 MB "
+                                  "(the operators are matrix-free) - no flush needed")},
                 "roofline": roofline, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e, "p3_solve": p3,
                 "gpu_launches": int(L1 - L0), "clocks": clk}
         print(json.dumps(line), flush=True)
