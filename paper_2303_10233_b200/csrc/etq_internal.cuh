@@ -364,7 +364,7 @@ etq_status dense_inverse_spd(double* A, int m, cudaStream_t st);
 etq_status dense_from_sell(const Sell& A, int m, double* D, cudaStream_t st);
 etq_status p1_build_mass_inverse(const Geo& g, double* W, cudaStream_t st);
 void dense_gemv(const double* A, int m, int ncomp, const double* x, int64_t xstride, double* y,
-                int64_t ystride, const double* done, cudaStream_t st);
+                int64_t ystride, const double* done, cudaStream_t st, bool pdl = false);
 etq_status lanczos_sgs_lo(Problem& P, const double* v0, int steps, double* lam);
 int64_t etq_launch_total();
 void cheb_step_level0(const Problem& P, const double* d_in, double* d_out, cudaStream_t st);

@@ -258,7 +258,7 @@ static void pcg_apply_A(const PcgWs& W, const PcgOps& o, cudaStream_t st) {
 }
 
 static etq_status pcg_apply_M(const PcgWs& W, const PcgOps& o, cudaStream_t st) {
-  return vcycle_apply_ex(*o.P, *o.H, W.r, W.z, &W.red, SL_RZ, W.sc + PG_RZ1, W.r, W.sc + PG_DONE, st);
+  return vcycle_apply_ex(*o.P, *o.H, W.r, W.z, &W.red, SL_RZ, W.sc + PG_RZ1, W.r, W.sc + PG_DONE, st, true);
 }
 
 static etq_status pcg_body(const PcgWs& W, const PcgOps& o, double* x, cudaGraphConditionalHandle h, int use_h,

@@ -653,6 +653,7 @@ struct SkChebArgs {
   const double* done;
 };
 __global__ void __launch_bounds__(BS) k_cheb_sk(SkChebArgs a) {
+  pdl_wait();
   if (is_done(a.done)) return;
   const int n1 = a.n + 1;
   const int64_t nk = (int64_t)n1 * n1;
@@ -689,6 +690,7 @@ __global__ void k_cheb_init(const double* dinv, int nq, int nc, const double* b,
 // b_c = P^T r_f and d0_c = D_c^{-1} b_c / theta
 __global__ void k_restrict_q1(int mf, int mc, const double* rf, double* bc, double* d0c, const double* dinvc,
                               double itheta, const double* done) {
+  pdl_wait();
   if (is_done(done)) return;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)mc * mc;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -712,6 +714,7 @@ __global__ void k_restrict_q1(int mf, int mc, const double* rf, double* bc, doub
 }
 // x_f += P (x_c + d_c)
 __global__ void k_prolong_q1(int mf, int mc, const double* xc, const double* dc, double* xf, const double* done) {
+  pdl_wait();
   if (is_done(done)) return;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)mf * mf;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -855,6 +858,7 @@ __global__ void k_prolong(int mf, int mc, int nqf, int nqc, const double* xc, co
 __global__ void __launch_bounds__(BS) k_final_add(const double* x, const double* d, double* z, int64_t n,
                                                   const double* dw, RedSite site, int slot, double* out,
                                                   const double* done) {
+  pdl_wait();
   if (is_done(done)) return;
   double dot = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -889,6 +893,7 @@ __global__ void k_gj_update(double* A, int m, int p, const double* colp) {
 // y_c = A x_c for ncomp components (A dense m x m row-major), warp per row
 __global__ void k_gemv(const double* A, int m, int ncomp, const double* x, int64_t xs, double* y, int64_t ys,
                        const double* done) {
+  pdl_wait();
   if (is_done(done)) return;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1625,8 +1630,10 @@ __global__ void k_aug_extract(const double* Aug, double* A, int m) {
 }
 
 void dense_gemv(const double* A, int m, int ncomp, const double* x, int64_t xstride, double* y, int64_t ystride,
-                const double* done, cudaStream_t st) {
-  k_gemv<<<grid_for((int64_t)m * 32, BS, 4096), BS, 0, st>>>(A, m, ncomp, x, xstride, y, ystride, done); etq_count_launch();
+                const double* done, cudaStream_t st, bool pdl) {
+  launch_pdl(k_gemv, dim3(grid_for((int64_t)m * 32, BS, 4096)), dim3(BS), 0, st, pdl, A, m, ncomp, x, xstride, y, ystride,
+             done);
+  etq_count_launch();
 }
 
 etq_status dense_inverse_pivot(double* A, int m, cudaStream_t st) {
@@ -2256,14 +2263,14 @@ static bool tile_ok(const Hierarchy& H, const Level& lv) {
 // One V-cycle (readings R9/R9'/R13) on H.ncomp components: z = V(r); optional partial
 // <z, dot_with> into (site, slot) -> dot_out.
 static void launch_cheb_sk(const Hierarchy& H, const Level& lv, const ChebArgs& c, int post, double theta,
-                           cudaStream_t st) {
+                           cudaStream_t st, bool pdl = false) {
   SkChebArgs a;
   a.n = lv.g.n; a.w = H.sk_w;
   a.v = post ? c.x_in : c.d_in;
   a.d_in = c.d_in; a.r_in = c.r_in; a.x_in = c.x_in;
   a.x_out = c.x_out; a.r_out = c.r_out; a.d_out = c.d_out;
   a.c1 = c.c1; a.c2 = c.c2; a.itheta = 1.0 / theta; a.post = post; a.done = c.done;
-  k_cheb_sk<<<grid_for((int64_t)lv.g.nk, BS, 8 * 148), BS, 0, st>>>(a);
+  launch_pdl(k_cheb_sk, dim3(grid_for((int64_t)lv.g.nk, BS, 8 * 148)), dim3(BS), 0, st, pdl, a);
 }
 
 etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r_u, double* z_u,
@@ -2316,7 +2323,7 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       a.x_out = lv.x; a.r_out = lv.r; a.d_out = (k == H.degree - 1) ? nullptr : dout;
       a.c1 = c1[k]; a.c2 = c2[k]; a.done = done;
       if (lv.st_on) launch_cheb_st(lv, a, false, theta, st, vpdl);
-      else if (H.op == 1) launch_cheb_sk(H, lv, a, 0, theta, st);
+      else if (H.op == 1) launch_cheb_sk(H, lv, a, 0, theta, st, vpdl);
       else if (nc == 2) k_cheb_step<2><<<gs, BS, 0, st>>>(a);
       else k_cheb_step<1><<<gs, BS, 0, st>>>(a);
       etq_count_launch();
@@ -2327,8 +2334,8 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       launch_pdl(k_restrict, dim3(grid_for(cv.g.nq, BS, 4096)), dim3(BS), 0, st, vpdl, lv.g.m, cv.g.m, nq, cv.g.nq,
                  (const double*)lv.r, cv.b, cv.d0, (const double*)cv.dinv, 1.0 / theta, done);
     } else {
-      k_restrict_q1<<<grid_for(cv.g.nk, BS, 4096), BS, 0, st>>>(lv.g.n + 1, cv.g.n + 1, lv.r, cv.b, cv.d0,
-                                                               cv.dinv, 1.0 / theta, done);
+      launch_pdl(k_restrict_q1, dim3(grid_for(cv.g.nk, BS, 4096)), dim3(BS), 0, st, vpdl && H.op == 1, lv.g.n + 1,
+                 cv.g.n + 1, (const double*)lv.r, cv.b, cv.d0, (const double*)cv.dinv, 1.0 / theta, done);
       if (H.op == 2) {
         etq_count_launch();
         const int nkf = lv.g.nk, nkc = cv.g.nk;
@@ -2351,7 +2358,7 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     pend[Ld - 1] = nullptr;
   } else {
     const Level& C = H.lv[L - 1];
-    dense_gemv(C.coarse_inv, C.nrows, nc, C.b, C.nrows, C.x, C.nrows, done, st);
+    dense_gemv(C.coarse_inv, C.nrows, nc, C.b, C.nrows, C.x, C.nrows, done, st, vpdl);
     pend[L - 1] = nullptr;
   }
   // ---- up
@@ -2366,7 +2373,8 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       launch_pdl(k_prolong, dim3(grid_for(nq, BS, 4096)), dim3(BS), 0, st, vpdl, lv.g.m, cv.g.m, nq, cv.g.nq,
                  xres[l + 1], pend[l + 1], lv.x, done);
     } else {
-      k_prolong_q1<<<grid_for(lv.g.nk, BS, 4096), BS, 0, st>>>(lv.g.n + 1, cv.g.n + 1, xres[l + 1], pend[l + 1], lv.x, done);
+      launch_pdl(k_prolong_q1, dim3(grid_for(lv.g.nk, BS, 4096)), dim3(BS), 0, st, vpdl && H.op == 1, lv.g.n + 1,
+                 cv.g.n + 1, xres[l + 1], pend[l + 1], lv.x, done);
       if (H.op == 2) {
         etq_count_launch();
         const int nkf = lv.g.nk, nkc = cv.g.nk;
@@ -2404,7 +2412,7 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     } else if (H.op == 1) {
       ChebArgs a{};
       a.x_in = lv.x; a.r_in = bvec[l]; a.r_out = lv.r; a.d_out = lv.d0; a.done = done;
-      launch_cheb_sk(H, lv, a, 1, theta, st);
+      launch_cheb_sk(H, lv, a, 1, theta, st, vpdl);
     } else if (nc == 2) {
       k_post_residual<2><<<gs, BS, 0, st>>>(lv.A, lv.dinv, nq, bvec[l], lv.x, lv.r, lv.d0, 1.0 / theta, done);
     } else {
@@ -2419,7 +2427,7 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
       a.x_out = lv.x; a.r_out = (k == H.degree - 2) ? nullptr : lv.r; a.d_out = dout;
       a.c1 = c1[k]; a.c2 = c2[k]; a.done = done;
       if (lv.st_on) launch_cheb_st(lv, a, false, theta, st, vpdl);
-      else if (H.op == 1) launch_cheb_sk(H, lv, a, 0, theta, st);
+      else if (H.op == 1) launch_cheb_sk(H, lv, a, 0, theta, st, vpdl);
       else if (nc == 2) k_cheb_step<2><<<gs, BS, 0, st>>>(a);
       else k_cheb_step<1><<<gs, BS, 0, st>>>(a);
       etq_count_launch();
@@ -2429,8 +2437,8 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
   }
   const Level& F = H.lv[0];
   const int64_t nv = (int64_t)nc * F.nrows;
-  k_final_add<<<grid_for(nv, BS, RED_BLOCKS), BS, 0, st>>>(xres[0], pend[0], z_u, nv, dot_with,
-                                                          site ? *site : dummy, slot, dot_out, done); etq_count_launch();
+launch_pdl(k_final_add, dim3(grid_for(nv, BS, RED_BLOCKS)), dim3(BS), 0, st, vpdl, (const double*)xres[0], pend[0], z_u,
+             nv, dot_with, site ? *site : dummy, slot, dot_out, done); etq_count_launch();
   return ETQ_OK;
 }
 
