@@ -107,7 +107,7 @@ def test_apply_saddle(n):
     assert np.all(yr[nr:] == 0.0)
 
 
-@pytest.mark.parametrize("n", [2, 8, 64])
+@pytest.mark.parametrize("n", [2, 8, 64, 129, 200])     # 129, 200: interior and ragged SGS tiles
 def test_mass_and_sgs(n):
     s = oracle_system(n)
     P = etq.Problem(n)
