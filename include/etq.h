@@ -177,6 +177,10 @@ etq_status etq_export_operator(const etq_problem* p, int32_t which, int32_t leve
                                int64_t* nrows, int64_t* nnz,
                                int64_t* rowptr, int32_t* col, double* val);
 
+/* Largest GMRES restart length m accepted by etq_gmres_solve / etq_two_stage_solve /
+ * etq_picard_solve (the Krylov basis holds m + 1 vectors; larger m returns ETQ_EINVAL). */
+#define ETQ_MAX_RESTART 63
+
 /* Right-preconditioned restarted GMRES(m) with classical Gram-Schmidt applied twice (
  * readings R14, R18) on the Oseen system [F B^T; B 0] (reduced = 0, kind = ETQ_PC_OSEEN_M1) or the
  * reduced Taylor-Hood system [F B1^T; B1 0] (reduced = 1, kind = ETQ_PC_OSEEN_PCD1; the p_0 block of

@@ -444,7 +444,7 @@ etq_status etq_apply_pcd_schur(const etq_problem* h, const double* r_p1, double*
 
 etq_status etq_gmres_solve(etq_problem* h, int32_t reduced, etq_pc_kind kind, const double* b, double* x,
                            double rtol, int32_t restart, int32_t maxit, etq_report* report) {
-  if (!h || !b || !x || !(rtol > 0.0) || restart < 1 || maxit < 1) return ETQ_EINVAL;
+  if (!h || !b || !x || !(rtol > 0.0) || restart < 1 || restart > ETQ_MAX_RESTART || maxit < 1) return ETQ_EINVAL;
   if (kind != ETQ_PC_OSEEN_M1 && kind != ETQ_PC_OSEEN_PCD1 && kind != ETQ_PC_OSEEN_M2 && kind != ETQ_PC_OSEEN_LSC)
     return ETQ_EINVAL;
   if ((kind == ETQ_PC_OSEEN_M2 || kind == ETQ_PC_OSEEN_LSC) && reduced) return ETQ_EINVAL;   // full system only
@@ -464,7 +464,8 @@ etq_status etq_gmres_solve(etq_problem* h, int32_t reduced, etq_pc_kind kind, co
 
 etq_status etq_two_stage_solve(etq_problem* h, const double* b, double* x, double eta, double c, int32_t restart,
                                int32_t maxit, etq_report* st1, etq_report* st2, double bound_out[2]) {
-  if (!h || !b || !x || !(eta > 0.0) || !(c > 0.0) || restart < 1 || maxit < 1) return ETQ_EINVAL;
+  if (!h || !b || !x || !(eta > 0.0) || !(c > 0.0) || restart < 1 || restart > ETQ_MAX_RESTART || maxit < 1)
+    return ETQ_EINVAL;
   Problem& P = h->P;
   StreamScope sc(P);
   return two_stage_run(P, b, x, eta, c, restart, maxit, st1, st2, bound_out);
@@ -479,7 +480,8 @@ etq_status etq_set_wind(etq_problem* h, const double* w) {
 
 etq_status etq_picard_solve(etq_problem* h, int32_t steps, double eta, double c, int32_t restart, int32_t maxit,
                             double* x, int32_t* its, double* res, double* ms_total) {
-  if (!h || !x || steps < 0 || !(eta > 0.0) || !(c > 0.0) || restart < 1 || maxit < 1) return ETQ_EINVAL;
+  if (!h || !x || steps < 0 || !(eta > 0.0) || !(c > 0.0) || restart < 1 || restart > ETQ_MAX_RESTART || maxit < 1)
+    return ETQ_EINVAL;
   Problem& P = h->P;
   StreamScope sc(P);
   return picard_run(P, steps, eta, c, restart, maxit, x, its, res, ms_total);

@@ -167,39 +167,61 @@ __global__ void k_copy_vj(const double* V, int64_t N, const double* sc, double* 
     T[i] = vj[i];
 }
 
-// h_i = <V_i, W>, i = 0..j (j from device), in chunks of 8 vectors; deterministic.  Two elements
-// per thread and iteration with all 18 loads issued first (memory-level parallelism: the kernel is
-// bound by DRAM latency, not bandwidth, at one element per iteration); the per-thread summation
-// order is unchanged (element e, then e + stride, ...).
+// h_i = <V_i, W>, i = 0..j (j from device).  Each warp owns segments of MD_SEG consecutive
+// elements (grid-stride over segments): the segment of W stays in registers, and every basis
+// vector is streamed with MD_KV independent coalesced loads per lane (memory-level parallelism),
+// summed, warp-reduced, and the warp's running total for vector i kept by lane i mod 32.  W and
+// each V_i are read once.  The warps' totals are combined in warp order in shared memory, the
+// blocks' in block order by the last block: deterministic for a fixed grid.
+constexpr int MD_KV = 8, MD_SEG = 32 * MD_KV, MD_MAXV = 64;
 __global__ void __launch_bounds__(BS) k_multidot(const double* V, int64_t N, const double* W, const double* sc,
                                                  double* h, RedSite site) {
-  const int nv = (int)sc[G_J] + 1;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int c0 = 0; c0 < nv; c0 += 8) {
-    double acc[8];
+  const int nv = min((int)sc[G_J] + 1, MD_MAXV);
+  __shared__ double part[BS / 32][MD_MAXV];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nseg = (N + MD_SEG - 1) / MD_SEG;
+  const int64_t nw = (int64_t)gridDim.x * (BS / 32);
+  double t0 = 0.0, t1 = 0.0;   // this lane's running totals of vectors lane and lane + 32
+  for (int64_t sg = (int64_t)blockIdx.x * (BS / 32) + warp; sg < nseg; sg += nw) {
+    const int64_t e0 = sg * MD_SEG + lane;
+    double w[MD_KV];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k] = 0.0;
-    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (; e + stride < N; e += 2 * stride) {
-      const double w0 = W[e], w1 = W[e + stride];
-      double v0[8], v1[8];
+    for (int k = 0; k < MD_KV; ++k) { const int64_t e = e0 + 32 * k; w[k] = e < N ? W[e] : 0.0; }
+#pragma unroll 2
+    for (int i = 0; i < nv; ++i) {
+      const double* vi = V + (int64_t)i * N;
+      double v[MD_KV];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const bool ok = c0 + k < nv;
-        v0[k] = ok ? V[(int64_t)(c0 + k) * N + e] : 0.0;
-        v1[k] = ok ? V[(int64_t)(c0 + k) * N + e + stride] : 0.0;
-      }
+      for (int k = 0; k < MD_KV; ++k) { const int64_t e = e0 + 32 * k; v[k] = e < N ? vi[e] : 0.0; }
+      double sv = 0.0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (c0 + k < nv) { acc[k] = fma(v0[k], w0, acc[k]); acc[k] = fma(v1[k], w1, acc[k]); }
+      for (int k = 0; k < MD_KV; ++k) sv = fma(v[k], w[k], sv);
+      sv = warp_sum(sv);
+      if (lane == (i & 31)) { if (i < 32) t0 += sv; else t1 += sv; }
     }
-    if (e < N) {
-      const double w = W[e];
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (c0 + k < nv) acc[k] = fma(V[(int64_t)(c0 + k) * N + e], w, acc[k]);
+  }
+  if (lane < nv) part[warp][lane] = t0;
+  if (lane + 32 < nv) part[warp][lane + 32] = t1;
+  __syncthreads();
+  for (int i = threadIdx.x; i < nv; i += BS) {
+    double b = 0.0;
+    for (int wi = 0; wi < BS / 32; ++wi) b += part[wi][i];
+    site.partials[(int64_t)i * MAXB + blockIdx.x] = b;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(site.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    for (int i = warp; i < nv; i += BS / 32) {
+      double sv = 0.0;
+      for (int b = lane; b < (int)gridDim.x; b += 32) sv += __ldcg(site.partials + (int64_t)i * MAXB + b);
+      sv = warp_sum(sv);
+      if (lane == 0) h[i] = sv;
     }
-    reduce_finish<8>(acc, site, c0, h + c0);
+    if (threadIdx.x == 0) site.counter[0] = 0u;
   }
 }
 
