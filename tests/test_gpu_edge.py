@@ -128,3 +128,19 @@ def test_c4_full_size_sampled_parity():
     assert out["zstar"] <= out["bound"] * (1 + 1e-9)
     y = zeros(P.N); P.apply_saddle(x, y)
     assert float(torch.linalg.norm(b - y) / torch.linalg.norm(b)) <= 1e-6 * (1 + 1e-6)
+
+
+@pytest.mark.gpu
+def test_gmres_restart_above_limit_rejected():
+    """GMRES restart lengths above ETQ_MAX_RESTART (63) are rejected, not run past the Krylov
+    bookkeeping (include/etq.h)."""
+    P = etq.Problem(4, viscosity=0.01, wind=1)
+    P.precond_setup(etq.PC_OSEEN_M1, etq.make_params(cheb_sgs_lo=0.01, coarse_n=2))
+    b = torch.zeros(P.N, dtype=torch.float64, device="cuda")
+    P.build_rhs(b)
+    x = torch.zeros_like(b)
+    with pytest.raises(etq.EtqError):
+        P.gmres_solve(etq.PC_OSEEN_M1, b, x, rtol=1e-6, restart=64, maxit=10)
+    rep = P.gmres_solve(etq.PC_OSEEN_M1, b, x, rtol=1e-6, restart=63, maxit=10)
+    assert rep["iterations"] >= 1
+    P.close()
