@@ -269,7 +269,8 @@ etq_status etq_time_kernel(etq_problem* p, int32_t which, int32_t reps, double* 
  *   option 7 = programmatic dependent launches between the Chebyshev-SGS steps (1 [default]) or plain
  *              stream order (0);
  *   option 8 = programmatic dependent launches between the kernels of the Q2 V-cycle (1 [default]) or
- *              plain stream order (0).
+ *              plain stream order (0);
+ *   option 9 = nested-Q2 prolongation from shared-memory tiles (1 [default]) or by gathers (0).
  * Applies to solves whose CUDA graphs are captured afterwards (re-run etq_precond_setup). */
 etq_status etq_set_option(int32_t option, int32_t value);
 

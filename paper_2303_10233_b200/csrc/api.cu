@@ -19,6 +19,7 @@ bool g_tail_sm = true;              // etq_set_option(5): shared-memory matrix-f
 bool g_saddle_tile = true;          // etq_set_option(6): shared-memory tiled matrix-free saddle apply
 bool g_sgs_pdl = true;              // etq_set_option(7): programmatic dependent launches in the SGS chain
 bool g_vc_pdl = true;               // etq_set_option(8): programmatic dependent launches in the V-cycle
+bool g_prolong_tile = true;         // etq_set_option(9): tiled nested-Q2 prolongation
 void etq_count_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 int64_t etq_launch_total() { return g_launches.load(std::memory_order_relaxed); }
 
@@ -698,6 +699,7 @@ etq_status etq_set_option(int32_t option, int32_t value) {
   if (option == 6) { g_saddle_tile = value != 0; return ETQ_OK; }
   if (option == 7) { g_sgs_pdl = value != 0; return ETQ_OK; }
   if (option == 8) { g_vc_pdl = value != 0; return ETQ_OK; }
+  if (option == 9) { g_prolong_tile = value != 0; return ETQ_OK; }
   return ETQ_EINVAL;
 }
 

@@ -43,6 +43,7 @@ extern bool g_tail_sm;                    // api.cu; etq_set_option(5)
 extern bool g_saddle_tile;                // api.cu; etq_set_option(6)
 extern bool g_sgs_pdl;                    // api.cu; etq_set_option(7)
 extern bool g_vc_pdl;                     // api.cu; etq_set_option(8)
+extern bool g_prolong_tile;               // api.cu; etq_set_option(9)
 
 constexpr int SELL_C = 32;           // slice height = warp size
 constexpr int RED_BLOCKS = 592;      // 4 x 148 SMs: grid of plain reduction kernels

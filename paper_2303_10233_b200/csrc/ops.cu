@@ -854,6 +854,63 @@ __global__ void k_prolong(int mf, int mc, int nqf, int nqc, const double* xc, co
   }
 }
 
+// Tiled nested-Q2 prolongation xf += P (xc + dc) (same operations and order as k_prolong, so
+// bitwise the same): a CTA owns a PT_X x PT_Y block of fine nodes; the coarse correction of its
+// coarse window is staged in shared memory, each needed coarse row is interpolated along x once
+// (the per-row partial sums t0 of k_prolong), then every fine node combines up to three of them
+// along y.  Replaces up to 36 gathered coarse loads per fine node.
+constexpr int PT_X = 64, PT_Y = 32, PT_THREADS = 256;
+constexpr int PT_CX = PT_X / 2 + 3, PT_CY = PT_Y / 2 + 3;   // coarse window (origin K0/2 - 1, L0/2 - 1)
+__global__ void __launch_bounds__(PT_THREADS) k_prolong_tile(int mf, int mc, int nqf, int nqc, const double* xc,
+                                                            const double* dc, double* xf, const double* done) {
+  pdl_wait();
+  if (is_done(done)) return;
+  __shared__ double ec[2][PT_CY][PT_CX];
+  __shared__ double tx[2][PT_CY][PT_X];
+  const int tilesx = (mf + PT_X - 1) / PT_X;
+  const int K0 = (blockIdx.x % tilesx) * PT_X, L0 = (blockIdx.x / tilesx) * PT_Y;
+  const int I0 = K0 / 2 - 1, J0 = L0 / 2 - 1;
+  for (int idx = threadIdx.x; idx < PT_CY * PT_CX; idx += PT_THREADS) {
+    const int ci = I0 + idx % PT_CX, cj = J0 + idx / PT_CX;
+    const bool in = ci >= 0 && cj >= 0 && ci < mc && cj < mc;
+    const int64_t c = in ? ci + (int64_t)mc * cj : 0;
+#pragma unroll
+    for (int comp = 0; comp < 2; ++comp) {
+      const int64_t cc = c + (int64_t)comp * nqc;
+      ec[comp][idx / PT_CX][idx % PT_CX] = in ? (dc ? xc[cc] + dc[cc] : xc[cc]) : 0.0;
+    }
+  }
+  __syncthreads();
+  // x pass: t0(J, k) for the window's coarse rows and the tile's fine columns
+  for (int idx = threadIdx.x; idx < PT_CY * PT_X; idx += PT_THREADS) {
+    const int jr = idx / PT_X, kk = idx % PT_X, k = K0 + kk;
+    if (k >= mf) continue;
+    int ix[3]; double wx[3];
+    const int nx = prolong_taps(k, ix, wx);
+#pragma unroll
+    for (int comp = 0; comp < 2; ++comp) {
+      double t0 = 0.0;
+      for (int p = 0; p < nx; ++p) t0 = fma(wx[p], ec[comp][jr][ix[p] - I0], t0);
+      tx[comp][jr][kk] = t0;
+    }
+  }
+  __syncthreads();
+  // y pass
+  for (int idx = threadIdx.x; idx < PT_Y * PT_X; idx += PT_THREADS) {
+    const int kk = idx % PT_X, k = K0 + kk, l = L0 + idx / PT_X;
+    if (k >= mf || l >= mf || k == 0 || l == 0 || k == mf - 1 || l == mf - 1) continue;
+    int iy[3]; double wy[3];
+    const int ny = prolong_taps(l, iy, wy);
+    double s0 = 0.0, s1 = 0.0;
+    for (int q = 0; q < ny; ++q) {
+      s0 = fma(wy[q], tx[0][iy[q] - J0][kk], s0);
+      s1 = fma(wy[q], tx[1][iy[q] - J0][kk], s1);
+    }
+    const int64_t t = k + (int64_t)mf * l;
+    xf[t] += s0; xf[nqf + t] += s1;
+  }
+}
+
 // z = x + d (d nullable), optional dot partial <z, w>
 __global__ void __launch_bounds__(BS) k_final_add(const double* x, const double* d, double* z, int64_t n,
                                                   const double* dw, RedSite site, int slot, double* out,
@@ -2370,8 +2427,14 @@ etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r
     const int nq = lv.nrows;
     cheb_coeffs(H.lo, H.hi, lv.bim, H.degree, c1, c2);
     if (H.kind == 0) {
-      launch_pdl(k_prolong, dim3(grid_for(nq, BS, 4096)), dim3(BS), 0, st, vpdl, lv.g.m, cv.g.m, nq, cv.g.nq,
-                 xres[l + 1], pend[l + 1], lv.x, done);
+      if (g_prolong_tile) {
+        const int tx = (lv.g.m + PT_X - 1) / PT_X, ty = (lv.g.m + PT_Y - 1) / PT_Y;
+        launch_pdl(k_prolong_tile, dim3(tx * ty), dim3(PT_THREADS), 0, st, vpdl, lv.g.m, cv.g.m, nq, cv.g.nq,
+                   xres[l + 1], pend[l + 1], lv.x, done);
+      } else {
+        launch_pdl(k_prolong, dim3(grid_for(nq, BS, 4096)), dim3(BS), 0, st, vpdl, lv.g.m, cv.g.m, nq, cv.g.nq,
+                   xres[l + 1], pend[l + 1], lv.x, done);
+      }
     } else {
       launch_pdl(k_prolong_q1, dim3(grid_for(lv.g.nk, BS, 4096)), dim3(BS), 0, st, vpdl && H.op == 1, lv.g.n + 1,
                  cv.g.n + 1, xres[l + 1], pend[l + 1], lv.x, done);

@@ -106,11 +106,12 @@ def test_device_minres_loop_matches_host_loop(kind):
     np.testing.assert_array_equal(xs[0], xs[1])
 
 
-@pytest.mark.parametrize("option", [5])
+@pytest.mark.parametrize("option", [5, 9])
 @pytest.mark.parametrize("n", [32, 64, 256])
 def test_vcycle_fusions_bitwise_equal(n, option):
-    """Option 5: the coarse-level tail run in shared memory with the class stencils gives the same
-    V-cycle output, bit for bit, as the tail through the stored rows in global memory."""
+    """Option 5: the coarse-level tail run in shared memory with the class stencils; option 9: the
+    tiled prolongation.  Either way the V-cycle output is the same, bit for bit, as with the
+    global-memory kernels."""
     zs = {}
     for opt in (0, 1):
         etq.set_option(option, opt)
