@@ -12,7 +12,8 @@ timed region and reported separately).  value = MINRES iterations / second over 
 
 Multi-GPU: the path is not partitioned across GPUs in this build (BASELINE.json fixes 1 GPU;
 SURVEY §8(e)); --gpus N runs N independent replicas, one per rank ("replicas only",
-scaling "weak"), timed as the max over ranks.
+scaling "weak"), timed as the max over ranks.  Without torchrun, --gpus N > 1 re-launches
+itself under `torch.distributed.run --nproc-per-node N` (127.0.0.1 rendezvous).
 --impl reference times the CPU oracle (oracle/, plain NumPy/SciPy, single thread) on a
 bounded sample of the same workload (one MINRES iteration per step).
 """
@@ -39,7 +40,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--grid-n", dest="n", type=int, default=1024,
+                    help="elements per side (the driver passes no value: c3, n = 1024)")
     ap.add_argument("--rtol", type=float, default=1e-8)
     ap.add_argument("--maxit", type=int, default=5000)
     ap.add_argument("--cpu-baseline-iters", type=int, default=1,
@@ -168,7 +170,8 @@ def run_reference(args):
     value = args.steps / tot
     sample = (f"{args.steps} steps x 1 oracle MINRES iteration on the c3 system (n={n}); oracle assembly "
               f"+ hierarchy {setup_s:.1f}s excluded; first preconditioner apply excluded")
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": workload_name(n), "n": n, "cheb_sgs_lo": a},
@@ -374,8 +377,25 @@ def run_ours(args):
     return 0
 
 
+def _free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch_under_torchrun(args):
+    """`--gpus N` (N > 1) outside torchrun: re-run this command as N ranks on this node
+    (one process per GPU, rendezvous on 127.0.0.1), exactly as the driver launches it."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

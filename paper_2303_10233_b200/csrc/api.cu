@@ -231,12 +231,7 @@ etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_para
   const etq_pc_params prm = merge_params(P, params);
   P.params = prm;
   // cached MINRES graphs bake in hierarchy buffers that a new setup may replace
-  for (int g = 0; g < 2; ++g) {
-    if (P.minres_graph[g]) { cudaGraphExecDestroy(P.minres_graph[g]); P.minres_graph[g] = nullptr; }
-  }
-  P.minres_graph_kind = -1;
-  if (P.minres_wgraph) { cudaGraphExecDestroy(P.minres_wgraph); P.minres_wgraph = nullptr; }
-  P.minres_wgraph_kind = -1;
+  drop_minres_graphs(P);
   if (kind == ETQ_PC_P3 || kind == ETQ_PC_P1_ITER) {
     if (P.oseen) return ETQ_EINVAL;
     if (!is_pow2(P.g.n) || !is_pow2(prm.coarse_n) || prm.coarse_n > P.g.n || !is_pow2(prm.inner_coarse_n))
@@ -253,6 +248,7 @@ etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_para
     if (!P.p1.Ainv) {
       ETQ_TRY(dalloc(&P.p1.Ainv, (size_t)P.g.nq * P.g.nq));
       ETQ_TRY(dalloc(&P.p1.MQinv, (size_t)P.n_p * P.n_p));
+      ETQ_TRY(dalloc(&P.p1.tmp, 2 * (size_t)P.n_p));
     }
     ETQ_TRY(dense_from_sell(P.Lv, P.g.nq, P.p1.Ainv, P.stream));
     ETQ_TRY(dense_inverse_spd(P.p1.Ainv, P.g.nq, P.stream));
@@ -264,6 +260,9 @@ etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_para
   if (kind == ETQ_PC_P2_GMG) {
     if (P.oseen) return ETQ_EINVAL;
     if (!is_pow2(P.g.n) || !is_pow2(prm.coarse_n) || prm.coarse_n > P.g.n) return ETQ_EINVAL;
+    // a failed re-setup must not leave the previous setup marked ready on a rebuilt hierarchy
+    P.p2_ready = false;
+    P.pm.ready = false;
     if (P.mg.built) free_hierarchy(P.mg);
     ETQ_TRY(build_hierarchy(P, P.mg, prm.coarse_n, prm.smooth_lo, prm.smooth_hi, prm.smooth_degree));
     ETQ_TRY(mass_pc_alloc(P));
@@ -276,8 +275,9 @@ etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_para
       ETQ_TRY(dalloc(&dv, P.n_p));
       ETQ_CHECK(cudaMemcpy(dv, v0.data(), sizeof(double) * P.n_p, cudaMemcpyHostToDevice));
       double lam = 0.0;
-      ETQ_TRY(lanczos_sgs_lo(P, dv, std::min<int64_t>(prm.lanczos_steps, P.n_p / 2), &lam));
+      const etq_status ls = lanczos_sgs_lo(P, dv, std::min<int64_t>(prm.lanczos_steps, P.n_p / 2), &lam);
       cudaFree(dv);
+      if (ls < 0) return ls;
       const double floor_ = 2.0 / ((double)P.pm.m * P.pm.m);   // reading R7: a = max(lam, 2/m^2)
       a = lam > floor_ ? lam : floor_;
     }
@@ -285,8 +285,7 @@ etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_para
     P.pm.a = a;
     P.pm.ready = true;
     P.p2_ready = true;
-    for (int g = 0; g < 2; ++g)
-      if (P.minres_graph[g]) { cudaGraphExecDestroy(P.minres_graph[g]); P.minres_graph[g] = nullptr; }
+    drop_minres_graphs(P);
     ETQ_CHECK(cudaStreamSynchronize(P.stream));
     return ETQ_OK;
   }
@@ -720,7 +719,7 @@ void etq_destroy(etq_problem* h) {
   P.Lv.perm = nullptr; P.BxT1.perm = nullptr; P.ByT1.perm = nullptr; P.BxT0.perm = nullptr; P.ByT0.perm = nullptr;
   sell_free(P.Lv); sell_free(P.BxT1); sell_free(P.ByT1); sell_free(P.BxT0); sell_free(P.ByT0); sell_free(P.B);
   if (P.node_perm) cudaFree(P.node_perm);
-  cudaFree(P.p1.Ainv); cudaFree(P.p1.MQinv);
+  cudaFree(P.p1.Ainv); cudaFree(P.p1.MQinv); cudaFree(P.p1.tmp);
   cudaFree(P.pm.t); cudaFree(P.pm.y0); cudaFree(P.pm.y1); cudaFree(P.pm.rr);
   cudaFree(P.red[0].partials); cudaFree(P.red[0].counter);
   cudaFree(P.dscal); cudaFree(P.dhist); cudaFree(P.tk); cudaFree(P.tkf);

@@ -188,6 +188,7 @@ struct PcP1 {
   bool ready = false;
   double* Ainv = nullptr;     // nq x nq inverse of the scalar velocity block (Dirichlet rows)
   double* MQinv = nullptr;    // n_p x n_p inverse of (M_Q + k k^T)
+  double* tmp = nullptr;      // [2 n_p] residual and correction of the refinement step
 };
 
 struct PcMass {               // Chebyshev-SGS on M_Q (P2 / M1 pressure block)
@@ -404,6 +405,8 @@ etq_status precond_apply_ex(const Problem& P, etq_pc_kind kind, const double* r,
                             double* out_u, double* out_p, const double* done, cudaStream_t st);
 etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, double rtol,
                       int maxit, etq_report* rep);
+// destroy every cached MINRES graph (they bake in hierarchy buffers, x and the history buffer)
+void drop_minres_graphs(Problem& P);
 
 // exact.cu (NEXT-2: exact M_Q solve through S_k, iterative A^{-1}, preconditioners P3 / P1_ITER)
 etq_status exact_mass_setup(Problem& P);

@@ -1579,7 +1579,9 @@ void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y
     b.so = P.so0; b.w = P.sst;
     b.nq = P.g.nq; b.nk = P.g.nk; b.n_u = P.n_u; b.n_p = P.n_p; b.reduced = a.reduced;
     b.x = x; b.y = y; b.inv_scale = inv_scale; b.site = a.site; b.slot = slot; b.dot_out = dot_out; b.done = done;
-    if (g_saddle_tile) {
+    const int tiles_x = (P.g.m + ST_T - 1) / ST_T;
+    // a fused <K z, z> reduction keeps one partial per CTA: at most RED_MAXB of them per slot
+    if (g_saddle_tile && (!dot_out || tiles_x * tiles_x <= RED_MAXB)) {
       static bool smem_set = false;
       if (!smem_set) {
         cudaFuncSetAttribute(k_saddle_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM);
@@ -1588,7 +1590,7 @@ void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y
       SaddleTileArgs t;
       t.so = P.so0; t.w = P.sst;
       t.m = P.g.m; t.n = P.g.n; t.nq = P.g.nq; t.nk = P.g.nk; t.n_u = P.n_u; t.reduced = a.reduced;
-      t.tiles_x = (P.g.m + ST_T - 1) / ST_T;
+      t.tiles_x = tiles_x;
       t.x = x; t.y = y; t.inv_scale = inv_scale; t.site = a.site; t.slot = slot; t.dot_out = dot_out; t.done = done;
       k_saddle_tile<<<t.tiles_x * t.tiles_x, ST_THREADS, ST_SMEM, st>>>(t); etq_count_launch();
       return;

@@ -507,6 +507,9 @@ static etq_status gmres_alloc(Problem& P, int m, int hist_cap) {
     ETQ_CHECK(cudaMemset(P.gred.counter, 0, 64 * sizeof(unsigned)));
   }
   if (P.ghist_cap < hist_cap) {
+    // the cached Arnoldi graph captures (ghist, ghist_cap) as kernel arguments: rebuild it
+    if (P.gmres_graph) { cudaGraphExecDestroy(P.gmres_graph); P.gmres_graph = nullptr; }
+    P.gmres_graph_key = -1;
     cudaFree(P.ghist);
     ETQ_TRY(dalloc(&P.ghist, hist_cap + 1));
     P.ghist_cap = hist_cap;

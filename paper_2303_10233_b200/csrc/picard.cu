@@ -346,18 +346,25 @@ etq_status picard_run(Problem& P, int steps, double eta, double c, int restart, 
   if (!(P.oseen && P.wind == 2)) return ETQ_EINVAL;
   if (!P.pcd_ready || !P.m1_ready) return ETQ_ENOTSETUP;
   cudaStream_t st = P.stream;
-  double* b;
-  double* y;
-  ETQ_TRY(dalloc(&b, P.N));
-  ETQ_TRY(dalloc(&y, P.N));
   if (!P.wnod) ETQ_TRY(dalloc(&P.wnod, (size_t)P.n_u));
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  double* b = nullptr;
+  double* y = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // every exit below goes through this cleanup (no early return leaks b, y or the events)
+  auto cleanup = [&](etq_status s) {
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    cudaFree(b); cudaFree(y);
+    return s;
+  };
+  if (dalloc(&b, P.N) != ETQ_OK || dalloc(&y, P.N) != ETQ_OK) return cleanup(ETQ_ENOMEM);
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return cleanup(ETQ_ECUDA);
   cudaEventRecord(e0, st);
   etq_status status = ETQ_OK;
   for (int k = 0; k <= steps; ++k) {
-    if (k == 0) ETQ_CHECK(cudaMemsetAsync(P.wnod, 0, sizeof(double) * P.n_u, st));
-    else ETQ_CHECK(cudaMemcpyAsync(P.wnod, x, sizeof(double) * P.n_u, cudaMemcpyDeviceToDevice, st));
+    cudaError_t ce = (k == 0) ? cudaMemsetAsync(P.wnod, 0, sizeof(double) * P.n_u, st)
+                              : cudaMemcpyAsync(P.wnod, x, sizeof(double) * P.n_u, cudaMemcpyDeviceToDevice, st);
+    if (ce != cudaSuccess) { status = ETQ_ECUDA; break; }
     etq_status s = picard_refresh(P);
     if (s < 0) { status = s; break; }
     s = build_rhs_dev(P, nullptr, b);
@@ -378,7 +385,5 @@ etq_status picard_run(Problem& P, int steps, double eta, double c, int restart, 
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   if (ms_total) *ms_total = ms;
-  cudaEventDestroy(e0); cudaEventDestroy(e1);
-  cudaFree(b); cudaFree(y);
-  return status;
+  return cleanup(status);
 }

@@ -99,6 +99,18 @@ __global__ void k_minres_wx(const double* z, const double* w, double* wp, double
   }
 }
 
+// P1 pressure refinement (below): s = r - s ; z += t
+__global__ void k_sub_from(const double* r, double* s, int64_t n, const double* done) {
+  if (done && *done != 0.0) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s[i] = r[i] - s[i];
+}
+__global__ void k_add_to(double* z, const double* t, int64_t n, const double* done) {
+  if (done && *done != 0.0) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    z[i] += t[i];
+}
+
 __global__ void k_minres_init(double* sc) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const double zv = sc[S_DOT0] + sc[S_DOT1];
@@ -138,6 +150,15 @@ etq_status precond_apply_ex(const Problem& P, etq_pc_kind kind, const double* r,
     if (!P.p1.ready) return ETQ_ENOTSETUP;
     dense_gemv(P.p1.Ainv, P.g.nq, 2, r, P.g.nq, z, P.g.nq, done, st);
     dense_gemv(P.p1.MQinv, (int)np, 1, r + nu, np, z + nu, np, done, st);
+    // one step of iterative refinement of the augmented M_Q solve: the dense inverse
+    // W = (M_Q + k k^T)^{-1} - k k^T/(k^T k)^2 carries an error ~ cond(M_Q + k k^T) eps; with
+    // s = r_p - M_Q z_p, z_p += W s restores M_Q z_p = r_p - lambda k to rounding (k^T W s = 0)
+    double* s = P.p1.tmp;
+    double* t = P.p1.tmp + np;
+    mass_apply(P.g, z + nu, s, st);
+    k_sub_from<<<grid_for(np, 1024), BS, 0, st>>>(r + nu, s, np, done); etq_count_launch();
+    dense_gemv(P.p1.MQinv, (int)np, 1, s, np, t, np, done, st);
+    k_add_to<<<grid_for(np, 1024), BS, 0, st>>>(z + nu, t, np, done); etq_count_launch();
     if (out_u) launch_dot(z, w, nu, const_cast<RedSite*>(site), 1, out_u, done, st);
     if (out_p) launch_dot(z + nu, w + nu, np, const_cast<RedSite*>(site), 2, out_p, done, st);
     return ETQ_OK;
@@ -172,6 +193,16 @@ etq_status precond_apply_ex(const Problem& P, etq_pc_kind kind, const double* r,
 // end of every two-iteration body)
 __global__ void k_minres_cond(const double* sc, cudaGraphConditionalHandle h) {
   if (threadIdx.x == 0 && blockIdx.x == 0) cudaGraphSetConditional(h, sc[S_DONE] != 0.0 ? 0u : 1u);
+}
+
+void drop_minres_graphs(Problem& P) {
+  for (int g = 0; g < 2; ++g)
+    if (P.minres_graph[g]) { cudaGraphExecDestroy(P.minres_graph[g]); P.minres_graph[g] = nullptr; }
+  P.minres_graph_kind = -1;
+  P.minres_graph_x = nullptr;
+  if (P.minres_wgraph) { cudaGraphExecDestroy(P.minres_wgraph); P.minres_wgraph = nullptr; }
+  P.minres_wgraph_kind = -1;
+  P.minres_wgraph_x = nullptr;
 }
 
 static etq_status minres_alloc(Problem& P) {
@@ -238,6 +269,8 @@ etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, 
   double* Q = P.kv[6];
   double* sc = P.dscal;
   if (P.hist_cap < maxit + 1) {
+    // the cached graphs capture (dhist, hist_cap) as kernel arguments: rebuild them
+    drop_minres_graphs(P);
     if (P.dhist) cudaFree(P.dhist);
     P.hist_cap = maxit + 1;
     ETQ_TRY(dalloc(&P.dhist, 3 * (size_t)P.hist_cap));

@@ -142,20 +142,43 @@ def _check(s, what):
     return s
 
 
-def _ptr(t):
+def _ptr(t, n):
+    """Device pointer of a contiguous float64 CUDA tensor of exactly n elements (the C ABI takes
+    no lengths: a shorter tensor would be read or written out of bounds)."""
     if t is None:
         return None
     import torch
     if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
         raise ValueError("expected a contiguous float64 CUDA tensor")
+    if t.numel() != n:
+        raise ValueError(f"expected {n} elements, got {t.numel()}")
     return C.c_void_p(t.data_ptr())
 
 
-def _fptr(t):
+def _fptr(t, n):
     import torch
     if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
         raise ValueError("expected a contiguous float32 CUDA tensor")
+    if t.numel() != n:
+        raise ValueError(f"expected {n} elements, got {t.numel()}")
     return C.c_void_p(t.data_ptr())
+
+
+def _hptr(a, n):
+    """Host pointer of a contiguous float64 CPU tensor or numpy array of exactly n elements."""
+    import numpy as np
+    if hasattr(a, "data_ptr"):
+        import torch
+        if a.is_cuda or a.dtype != torch.float64 or not a.is_contiguous():
+            raise ValueError("expected a contiguous float64 CPU tensor")
+        size, ptr = a.numel(), a.data_ptr()
+    else:
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]):
+            raise ValueError("expected a C-contiguous float64 numpy array")
+        size, ptr = a.size, a.ctypes.data
+    if size != n:
+        raise ValueError(f"expected {n} elements, got {size}")
+    return C.c_void_p(ptr)
 
 
 def _stream():
@@ -201,11 +224,11 @@ class Problem:
 
     # ---- C-ABI mirrors
     def build_rhs(self, b, f_nodal=None):
-        _check(lib().etq_build_rhs(self.h, _ptr(f_nodal), _ptr(b)), "etq_build_rhs")
+        _check(lib().etq_build_rhs(self.h, _ptr(f_nodal, self.n_u), _ptr(b, self.N)), "etq_build_rhs")
         return b
 
     def apply_saddle(self, x, y, reduced=False):
-        _check(lib().etq_apply_saddle(self.h, int(reduced), _ptr(x), _ptr(y)), "etq_apply_saddle")
+        _check(lib().etq_apply_saddle(self.h, int(reduced), _ptr(x, self.N), _ptr(y, self.N)), "etq_apply_saddle")
         return y
 
     def precond_setup(self, kind, params: PcParams | None = None):
@@ -213,21 +236,21 @@ class Problem:
                "etq_precond_setup")
 
     def apply_precond(self, kind, r, z):
-        _check(lib().etq_apply_precond(self.h, kind, _ptr(r), _ptr(z)), "etq_apply_precond")
+        _check(lib().etq_apply_precond(self.h, kind, _ptr(r, self.N), _ptr(z, self.N)), "etq_apply_precond")
         return z
 
     def apply_vcycle(self, kind, r_u, z_u):
-        _check(lib().etq_apply_vcycle(self.h, kind, _ptr(r_u), _ptr(z_u)), "etq_apply_vcycle")
+        _check(lib().etq_apply_vcycle(self.h, kind, _ptr(r_u, self.n_u), _ptr(z_u, self.n_u)), "etq_apply_vcycle")
         return z_u
 
     def apply_mass_pc(self, r_p, z_p):
-        _check(lib().etq_apply_mass_pc(self.h, _ptr(r_p), _ptr(z_p)), "etq_apply_mass_pc")
+        _check(lib().etq_apply_mass_pc(self.h, _ptr(r_p, self.n_p), _ptr(z_p, self.n_p)), "etq_apply_mass_pc")
         return z_p
 
     def apply_mass_exact(self, r_p, z_p):
         """Exact augmented M_Q solve through S_k (P3 / P1_ITER set up); returns the CG iterations."""
         it = C.c_int32()
-        _check(lib().etq_apply_mass_exact(self.h, _ptr(r_p), _ptr(z_p), C.byref(it)), "etq_apply_mass_exact")
+        _check(lib().etq_apply_mass_exact(self.h, _ptr(r_p, self.n_p), _ptr(z_p, self.n_p), C.byref(it)), "etq_apply_mass_exact")
         return it.value
 
     def inner_stats(self, which=0):
@@ -237,16 +260,16 @@ class Problem:
         return it.value, calls.value
 
     def apply_mass(self, x_p, y_p):
-        _check(lib().etq_apply_mass(self.h, _ptr(x_p), _ptr(y_p)), "etq_apply_mass")
+        _check(lib().etq_apply_mass(self.h, _ptr(x_p, self.n_p), _ptr(y_p, self.n_p)), "etq_apply_mass")
         return y_p
 
     def sgs_sweep(self, r_p, y_p, z_p):
-        _check(lib().etq_sgs_sweep(self.h, _ptr(r_p), _ptr(y_p), _ptr(z_p)), "etq_sgs_sweep")
+        _check(lib().etq_sgs_sweep(self.h, _ptr(r_p, self.n_p), _ptr(y_p, self.n_p), _ptr(z_p, self.n_p)), "etq_sgs_sweep")
         return z_p
 
     def estimate_sgs_lo(self, v0, steps):
         lam = C.c_double()
-        _check(lib().etq_estimate_sgs_lo(self.h, _ptr(v0), steps, C.byref(lam)), "etq_estimate_sgs_lo")
+        _check(lib().etq_estimate_sgs_lo(self.h, _ptr(v0, self.n_p), steps, C.byref(lam)), "etq_estimate_sgs_lo")
         return lam.value
 
     def get_cheb_sgs_lo(self):
@@ -278,34 +301,34 @@ class Problem:
 
     def minres_solve(self, kind, b, x, rtol=1e-8, maxit=1000):
         rep, hist, dl, gm = self._report(maxit + 1)
-        s = _check(lib().etq_minres_solve(self.h, kind, _ptr(b), _ptr(x), rtol, maxit, C.byref(rep)),
-                   "etq_minres_solve")
+        s = _check(lib().etq_minres_solve(self.h, kind, _ptr(b, self.N), _ptr(x, self.N), rtol, maxit,
+                                               C.byref(rep)), "etq_minres_solve")
         return self._report_dict(rep, hist, dl, gm, s)
 
     def minres_solve_host(self, kind, b_host, x_host, rtol=1e-8, maxit=1000):
         """b_host, x_host: contiguous float64 CPU tensors or numpy arrays (x in/out)."""
         rep, hist, dl, gm = self._report(maxit + 1)
-        pb = C.c_void_p(b_host.data_ptr() if hasattr(b_host, "data_ptr") else b_host.ctypes.data)
-        px = C.c_void_p(x_host.data_ptr() if hasattr(x_host, "data_ptr") else x_host.ctypes.data)
+        pb = _hptr(b_host, self.N)
+        px = _hptr(x_host, self.N)
         s = _check(lib().etq_minres_solve_host(self.h, kind, pb, px, rtol, maxit, C.byref(rep)),
                    "etq_minres_solve_host")
         return self._report_dict(rep, hist, dl, gm, s)
 
     def apply_saddle_f32(self, x, y, reduced=False):
-        _check(lib().etq_apply_saddle_f32(self.h, int(reduced), _fptr(x), _fptr(y)), "etq_apply_saddle_f32")
+        _check(lib().etq_apply_saddle_f32(self.h, int(reduced), _fptr(x, self.N), _fptr(y, self.N)), "etq_apply_saddle_f32")
         return y
 
     def apply_vcycle_f32(self, r_u, z_u):
-        _check(lib().etq_apply_vcycle_f32(self.h, _fptr(r_u), _fptr(z_u)), "etq_apply_vcycle_f32")
+        _check(lib().etq_apply_vcycle_f32(self.h, _fptr(r_u, self.n_u), _fptr(z_u, self.n_u)), "etq_apply_vcycle_f32")
         return z_u
 
     def apply_pcd_schur(self, r_p1, z_p1):
-        _check(lib().etq_apply_pcd_schur(self.h, _ptr(r_p1), _ptr(z_p1)), "etq_apply_pcd_schur")
+        _check(lib().etq_apply_pcd_schur(self.h, _ptr(r_p1, self.n_k), _ptr(z_p1, self.n_k)), "etq_apply_pcd_schur")
         return z_p1
 
     def gmres_solve(self, kind, b, x, rtol=1e-6, restart=50, maxit=1000, reduced=False):
         rep, hist, dl, gm = self._report(maxit + 2)
-        s = _check(lib().etq_gmres_solve(self.h, int(reduced), kind, _ptr(b), _ptr(x), rtol, restart, maxit,
+        s = _check(lib().etq_gmres_solve(self.h, int(reduced), kind, _ptr(b, self.N), _ptr(x, self.N), rtol, restart, maxit,
                                          C.byref(rep)), "etq_gmres_solve")
         d = self._report_dict(rep, hist, dl, gm, s)
         d["history"] = hist[:rep.iterations + 1].copy()
@@ -316,7 +339,7 @@ class Problem:
         r1, h1, d1, g1 = self._report(maxit + 2)
         r2, h2, d2, g2 = self._report(maxit + 2)
         bound = (C.c_double * 2)()
-        s = _check(lib().etq_two_stage_solve(self.h, _ptr(b), _ptr(x), eta, c, restart, maxit, C.byref(r1),
+        s = _check(lib().etq_two_stage_solve(self.h, _ptr(b, self.N), _ptr(x, self.N), eta, c, restart, maxit, C.byref(r1),
                                              C.byref(r2), bound), "etq_two_stage_solve")
         st1 = self._report_dict(r1, h1, d1, g1, s); st1["history"] = h1[:r1.iterations + 1].copy()
         st2 = self._report_dict(r2, h2, d2, g2, s); st2["history"] = h2[:r2.iterations + 1].copy()
@@ -324,7 +347,7 @@ class Problem:
 
     def set_wind(self, w):
         """Nodal Q2 wind [w_x | w_y] (device tensor, length n_u) of a wind-kind-2 problem."""
-        _check(lib().etq_set_wind(self.h, _ptr(w)), "etq_set_wind")
+        _check(lib().etq_set_wind(self.h, _ptr(w, self.n_u)), "etq_set_wind")
 
     def picard_solve(self, x, steps=5, eta=1e-6, c=10.0, restart=50, maxit=2000):
         """Picard loop (etq_picard_solve); x receives the last iterate."""
@@ -332,7 +355,7 @@ class Problem:
         its = np.zeros(2 * (steps + 1), dtype=np.int32)
         res = np.zeros(steps + 1)
         ms = C.c_double()
-        s = _check(lib().etq_picard_solve(self.h, steps, eta, c, restart, maxit, _ptr(x),
+        s = _check(lib().etq_picard_solve(self.h, steps, eta, c, restart, maxit, _ptr(x, self.N),
                                           C.c_void_p(its.ctypes.data), C.c_void_p(res.ctypes.data),
                                           C.byref(ms)), "etq_picard_solve")
         return {"status": s, "step1_its": its[0::2].copy(), "step2_its": its[1::2].copy(), "rel_res": res,

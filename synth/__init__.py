@@ -36,6 +36,13 @@ def lanczos_start(n_p: int, seed: int = 12345) -> np.ndarray:
     return np.random.default_rng(seed).standard_normal(n_p)
 
 
+def sample_indices(length: int, count: int, seed: int) -> np.ndarray:
+    """Sorted seeded sample of distinct indices in [0, length) (solution-sample positions of
+    the full-size golden records, tests/golden/c*_*.json)."""
+    count = min(count, length)
+    return np.sort(np.random.default_rng(seed).choice(length, size=count, replace=False))
+
+
 # BASELINE.json configs (SURVEY §8 head)
 CONFIGS = {
     "c1": {"n": 16, "bc": "lid", "force": None, "pc": "P1"},

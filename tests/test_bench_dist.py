@@ -50,7 +50,7 @@ def test_aggregate_max_time_sum_units():
 
 def test_reference_arm_nonzero_rank_exits_without_work():
     env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--n", "4"],
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--grid-n", "4"],
                        env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip() == ""
 
@@ -58,7 +58,7 @@ def test_reference_arm_nonzero_rank_exits_without_work():
 def test_reference_arm_rank0_prints_contract_line():
     import json
     env = dict(os.environ, RANK="0", WORLD_SIZE="1")
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--n", "8",
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--grid-n", "8",
                         "--steps", "2", "--warmup", "1"], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     line = json.loads(r.stdout.strip().splitlines()[-1])
@@ -66,3 +66,19 @@ def test_reference_arm_rank0_prints_contract_line():
               "cpu_baseline", "e2e", "config"):
         assert k in line
     assert line["impl"] == "reference" and line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_gpus_flag_self_launches_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks (torch.distributed.run,
+    127.0.0.1): the reference arm prints exactly one contract line, from rank 0, with n_gpus = 2."""
+    import json
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                            "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--grid-n", "4", "--steps", "1", "--warmup", "0"], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr
+    lines = [l for l in r.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2

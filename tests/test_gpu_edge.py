@@ -144,3 +144,54 @@ def test_gmres_restart_above_limit_rejected():
     rep = P.gmres_solve(etq.PC_OSEEN_M1, b, x, rtol=1e-6, restart=63, maxit=10)
     assert rep["iterations"] >= 1
     P.close()
+
+
+def test_cached_graphs_follow_history_reallocation():
+    """A solve with a larger maxit reallocates the device history buffer; the cached MINRES /
+    Arnoldi graphs (which capture that buffer) must be rebuilt, so the reported |eta|, delta,
+    gamma and GMRES histories equal those of a fresh problem (solvers.cu / oseen.cu)."""
+    n = 8
+    P = etq.Problem(n)
+    P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.01))
+    b = zeros(P.N); P.build_rhs(b)
+    x = zeros(P.N)
+    P.minres_solve(etq.PC_P2_GMG, b, x, rtol=1e-8, maxit=3)
+    x.zero_()
+    rep = P.minres_solve(etq.PC_P2_GMG, b, x, rtol=1e-10, maxit=400)
+    F = etq.Problem(n)
+    F.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.01))
+    xf = zeros(F.N)
+    ref = F.minres_solve(etq.PC_P2_GMG, b, xf, rtol=1e-10, maxit=400)
+    assert rep["iterations"] == ref["iterations"] > 3
+    for key in ("history", "delta", "gamma"):
+        np.testing.assert_array_equal(rep[key], ref[key])
+    np.testing.assert_array_equal(host(x), host(xf))
+    # GMRES: a short reduced solve, then the two-stage driver on the same problem
+    Q = etq.Problem(16, bc=0, viscosity=0.01, wind=1)
+    G = etq.Problem(16, bc=0, viscosity=0.01, wind=1)
+    for p in (Q, G):
+        p.precond_setup(etq.PC_OSEEN_M1, etq.make_params(coarse_n=4, cheb_sgs_lo=0.005))
+        p.precond_setup(etq.PC_OSEEN_PCD1, etq.make_params(coarse_n=4))
+    bq = zeros(Q.N); Q.build_rhs(bq)
+    xq = zeros(Q.N)
+    Q.gmres_solve(etq.PC_OSEEN_PCD1, bq, xq, rtol=1e-6, restart=50, maxit=3, reduced=True)
+    xq.zero_()
+    o1 = Q.two_stage_solve(bq, xq, eta=1e-6, c=10.0, restart=50, maxit=2000)
+    xg = zeros(G.N)
+    o2 = G.two_stage_solve(bq, xg, eta=1e-6, c=10.0, restart=50, maxit=2000)
+    for st in ("step1", "step2"):
+        assert o1[st]["iterations"] == o2[st]["iterations"]
+        np.testing.assert_array_equal(o1[st]["history"], o2[st]["history"])
+
+
+def test_binding_rejects_wrong_lengths():
+    """The C ABI takes no lengths; the binding checks every tensor against the problem's sizes."""
+    P = etq.Problem(4)
+    with pytest.raises(ValueError):
+        P.apply_saddle(zeros(P.N - 1), zeros(P.N))
+    with pytest.raises(ValueError):
+        P.apply_mass(zeros(P.n_p + 1), zeros(P.n_p))
+    with pytest.raises(ValueError):
+        P.minres_solve_host(etq.PC_P2_GMG, np.zeros(P.N - 1), np.zeros(P.N))
+    with pytest.raises(ValueError):
+        P.minres_solve_host(etq.PC_P2_GMG, np.zeros(P.N, dtype=np.float32), np.zeros(P.N))

@@ -80,7 +80,9 @@ def test_exact_mass_solve_matches_bordered_lu(n):
         its = P.apply_mass_exact(dev(r), z)
         zg = host(z)
         zr = ref.solve(r)
-        assert rel_err(zg, zr) < 1e-9, (n, seed)
+        # floor: the oracle's own sparse LU of the bordered matrix is accurate to ~cond * eps
+        # (measured GPU-oracle difference 1.6e-12 at n = 128 for every inner tolerance <= 1e-10)
+        assert rel_err(zg, zr) < 1e-11, (n, seed)
         assert 1 <= its <= 40
         assert abs(k @ zg) <= 1e-10 * np.abs(zg).sum()
         lam = (k @ r) / (g.n_k + g.n_0)   # lambda = k^T r / 1^T a (reading R21)
@@ -150,7 +152,7 @@ def test_minres_p3_parity(n):
     assert abs(rep["iterations"] - ro.iterations) <= 2
     assert rel_err(xg, xr) < 1e-8
     m = min(len(rep["delta"]), len(ro.delta))
-    np.testing.assert_allclose(rep["delta"][:m], ro.delta[:m], rtol=1e-7, atol=1e-12)
+    np.testing.assert_allclose(rep["delta"][:m], ro.delta[:m], rtol=1e-9, atol=1e-12)
 
 
 @pytest.mark.parametrize("n", [16, 32])
@@ -162,7 +164,7 @@ def test_minres_p1_iter_matches_exact_p1(n):
     assert abs(rep["iterations"] - ro.iterations) <= 1
     assert rel_err(xg, xr) < 1e-8
     m = min(len(rep["delta"]), len(ro.delta))
-    np.testing.assert_allclose(rep["delta"][:m], ro.delta[:m], rtol=1e-7, atol=1e-12)
+    np.testing.assert_allclose(rep["delta"][:m], ro.delta[:m], rtol=1e-9, atol=1e-12)
 
 
 def test_minres_p1_iter_c2_force():
@@ -171,7 +173,7 @@ def test_minres_p1_iter_c2_force():
                                         force=True)
     assert rep["converged"] and ro.converged
     assert abs(rep["iterations"] - ro.iterations) <= 2
-    assert rel_err(xg, xr) < 1e-7
+    assert rel_err(xg, xr) < 1e-8
 
 
 def test_p3_iterations_mesh_independent():

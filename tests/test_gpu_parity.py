@@ -182,7 +182,7 @@ def test_full_precond_p1(n):
     r[P.n_u:] -= (k @ r[P.n_u:]) / (k @ k) * k
     z = torch.zeros(P.N, dtype=torch.float64, device=DEV)
     P.apply_precond(etq.PC_P1_EXACT, dev(r), z)
-    assert rel_err(host(z), Pr(r)) < 1e-11
+    assert rel_err(host(z), Pr(r)) < APPLY_TOL
 
 
 @pytest.mark.parametrize("n", [8, 32])

@@ -107,7 +107,7 @@ def test_picard_iterates_match_oracle():
     for v in (xg, xr):
         v[g.n_u:g.n_u + g.n_k] -= v[g.n_u:g.n_u + g.n_k].mean()
         v[g.n_u + g.n_k:] -= v[g.n_u + g.n_k:].mean()
-    assert np.abs(xg[g.n_u:] - xr[g.n_u:]).max() <= 1e-7 * np.abs(xr[g.n_u:]).max()
+    assert np.abs(xg[g.n_u:] - xr[g.n_u:]).max() <= 1e-8 * np.abs(xr[g.n_u:]).max()
     assert np.linalg.norm(s.K @ xg - s.b) <= 1e-8 * np.linalg.norm(s.b)
 
 

@@ -11,7 +11,7 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-from oracle import fem, krylov, oseen, schur2  # noqa: E402
+from oracle import fem, krylov, normalize, oseen, schur2  # noqa: E402
 from paper_2303_10233_b200 import etq  # noqa: E402
 import synth  # noqa: E402
 
@@ -70,8 +70,9 @@ def test_block_triangular_apply_matches_oracle(kind, n):
     z = torch.zeros(g.N, dtype=torch.float64, device=DEV)
     P.apply_precond(kind, dev(r), z)
     zg, zr = host(z), Mo(r)
-    np.testing.assert_allclose(zg[g.n_u:], zr[g.n_u:], rtol=0, atol=1e-9 * np.abs(zr[g.n_u:]).max())
-    np.testing.assert_allclose(zg, zr, rtol=0, atol=1e-9 * np.abs(zr).max())
+    # inner CG at 1e-13 makes the inexact Lp^+ solves exact to rounding (measured <= 3e-13)
+    np.testing.assert_allclose(zg[g.n_u:], zr[g.n_u:], rtol=0, atol=1e-12 * np.abs(zr[g.n_u:]).max())
+    np.testing.assert_allclose(zg, zr, rtol=0, atol=1e-12 * np.abs(zr).max())
 
 
 def test_gmres_m2_stagnates_and_lsc_converges_like_the_oracle():
@@ -86,16 +87,24 @@ def test_gmres_m2_stagnates_and_lsc_converges_like_the_oracle():
     nb = np.linalg.norm(s.b)
     for kind, S in ((etq.PC_OSEEN_M2, schur2.TwoFieldPCD(s, NU, fem.pcd_f1(g, NU), schur2.f0_jump(g, NU, wx, wy))),
                     (etq.PC_OSEEN_LSC, schur2.LSCSchur(s))):
-        _, ro = krylov.gmres(lambda v: s.K @ v, s.b, schur2.OseenBlockTriangular(s, hF, S), tol_abs=1e-6 * nb,
-                             restart=50, maxit=120)
+        xo, ro = krylov.gmres(lambda v: s.K @ v, s.b, schur2.OseenBlockTriangular(s, hF, S), tol_abs=1e-6 * nb,
+                              restart=50, maxit=120)
         P = _problem(n, kind, inner_rtol=1e-13)
         b = torch.zeros(P.N, dtype=torch.float64, device=DEV)
         P.build_rhs(b)
         xg = torch.zeros(P.N, dtype=torch.float64, device=DEV)
         rep = P.gmres_solve(kind, b, xg, rtol=1e-6, restart=50, maxit=120)
         hg = rep["history"]
-        k = min(40, len(hg), len(ro.history))
+        k = min(len(hg), len(ro.history))
+        # residual path: the first 40 estimates to 1e-9; over the whole 120-iteration path (M2 restarts
+        # twice while stagnating) the inexact inner Lp^+ solves (CG to 1e-13) drift it by up to ~3e-8
+        np.testing.assert_allclose(hg[:40], ro.history[:40], rtol=1e-9)
         np.testing.assert_allclose(hg[:k], ro.history[:k], rtol=1e-6)
+        # solution level (O12 normalisation): M2 after the same 120 iterations, LSC at convergence
+        kv = fem.null_vector_k(g)
+        xgn = normalize.normalise_solution(host(xg), g.n_u, s.MQ, kv)
+        xon = normalize.normalise_solution(xo, g.n_u, s.MQ, kv)
+        assert np.abs(xgn - xon).max() <= 1e-8 * np.abs(xon).max()
         if kind == etq.PC_OSEEN_M2:
             assert not rep["converged"] and hg[-1] > 1e-3 * hg[0] and hg[10] < 1e-2 * hg[0]
         else:
