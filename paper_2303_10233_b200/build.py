@@ -9,9 +9,9 @@ SOURCES = ["assemble.cu", "ops.cu", "solvers.cu", "oseen.cu", "sweep32.cu", "exa
 OUT = os.path.join(HERE, "libetq.so")
 
 
-def nvcc_cmd(out=OUT):
+def nvcc_cmd(out=OUT, extra=()):
     return ["nvcc", "-shared", "-Xcompiler", "-fPIC", "-gencode", "arch=compute_100a,code=sm_100a",
-            "-lineinfo", "-O3", "-std=c++17", "-o", out] + [os.path.join(HERE, "csrc", s) for s in SOURCES]
+            "-lineinfo", "-O3", "-std=c++17", *extra, "-o", out] + [os.path.join(HERE, "csrc", s) for s in SOURCES]
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
@@ -26,5 +26,16 @@ def build(force: bool = False, verbose: bool = True) -> str:
     return OUT
 
 
+def build_variant(out, defines):
+    """A/B variant of the library with extra -D flags (experiments; ETQ_LIB=<out> selects it)."""
+    cmd = nvcc_cmd(out, ["-D" + d for d in defines])
+    subprocess.run(cmd, check=True)
+    return out
+
+
 if __name__ == "__main__":
-    build(force=True)
+    import sys
+    if len(sys.argv) > 2:          # python build.py <out.so> DEF1=.. DEF2=..
+        build_variant(sys.argv[1], sys.argv[2:])
+    else:
+        build(force=True)

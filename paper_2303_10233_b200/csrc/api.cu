@@ -18,6 +18,7 @@ bool g_sgs_high_prio = false;       // etq_set_option(4): Chebyshev-SGS kernels 
 bool g_tail_sm = true;              // etq_set_option(5): shared-memory matrix-free coarse-level tail
 bool g_saddle_tile = true;          // etq_set_option(6): shared-memory tiled matrix-free saddle apply
 bool g_sgs_pdl = true;              // etq_set_option(7): programmatic dependent launches in the SGS chain
+bool g_sgs_planar = false;          // etq_set_option(10): Chebyshev-SGS on parity planes with TMA windows
 bool g_vc_pdl = true;               // etq_set_option(8): programmatic dependent launches in the V-cycle
 bool g_prolong_tile = true;         // etq_set_option(9): tiled nested-Q2 prolongation
 void etq_count_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
@@ -699,6 +700,7 @@ etq_status etq_set_option(int32_t option, int32_t value) {
   if (option == 7) { g_sgs_pdl = value != 0; return ETQ_OK; }
   if (option == 8) { g_vc_pdl = value != 0; return ETQ_OK; }
   if (option == 9) { g_prolong_tile = value != 0; return ETQ_OK; }
+  if (option == 10) { g_sgs_planar = value != 0; return ETQ_OK; }
   return ETQ_EINVAL;
 }
 
@@ -721,6 +723,7 @@ void etq_destroy(etq_problem* h) {
   if (P.node_perm) cudaFree(P.node_perm);
   cudaFree(P.p1.Ainv); cudaFree(P.p1.MQinv); cudaFree(P.p1.tmp);
   cudaFree(P.pm.t); cudaFree(P.pm.y0); cudaFree(P.pm.y1); cudaFree(P.pm.rr);
+  cudaFree(P.pm.rp); cudaFree(P.pm.yp[0]); cudaFree(P.pm.yp[1]);
   cudaFree(P.red[0].partials); cudaFree(P.red[0].counter);
   cudaFree(P.dscal); cudaFree(P.dhist); cudaFree(P.tk); cudaFree(P.tkf);
   if (P.hscal) cudaFreeHost(P.hscal);

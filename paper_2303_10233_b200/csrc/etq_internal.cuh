@@ -42,6 +42,7 @@ extern bool g_sgs_high_prio;              // api.cu; etq_set_option(4)
 extern bool g_tail_sm;                    // api.cu; etq_set_option(5)
 extern bool g_saddle_tile;                // api.cu; etq_set_option(6)
 extern bool g_sgs_pdl;                    // api.cu; etq_set_option(7)
+extern bool g_sgs_planar;                 // api.cu; etq_set_option(10)
 extern bool g_vc_pdl;                     // api.cu; etq_set_option(8)
 extern bool g_prolong_tile;               // api.cu; etq_set_option(9)
 
@@ -196,6 +197,12 @@ struct PcMass {               // Chebyshev-SGS on M_Q (P2 / M1 pressure block)
   double a = 0.0;             // lower end of the SGS-preconditioned spectrum
   int m = 20;
   double *t = nullptr, *y0 = nullptr, *y1 = nullptr, *rr = nullptr;   // n_p work vectors
+  // parity-plane ("planar") copies of r and of the Chebyshev iterates (ops.cu, k_sgs_plane): 8 planes
+  // (4 vertex, 4 cell parities) of ph x pw entries, zero outside the domain; TMA descriptors of y
+  int pw = 0, ph = 0;
+  double *rp = nullptr, *yp[2] = {nullptr, nullptr};
+  alignas(64) unsigned char tmap[2][128];   // CUtensorMap of yp[0], yp[1] (opaque, 64-byte aligned)
+  bool planar = false;
 };
 
 // ---------------------------------------------------------------- PCG inner solves (exact.cu)

@@ -9,6 +9,8 @@
 //   * deterministic reductions (block partials + last-block fixed-order sum), dense
 //     Gauss-Jordan inverse and GEMV for the exact (P1) and coarse solves.
 #include "etq_internal.cuh"
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cmath>
 #include <cstdio>
 #include <vector>
@@ -1243,6 +1245,214 @@ __global__ void __launch_bounds__(SGS_TX * SGS_TY, SGS_MINB) k_sgs_tile(SgsTileA
   else sgs_tile_body<false>(a, V, Cc, Q, A0, C0);
 }
 
+// ---------------------------------------------------------------- SGS on parity planes (TMA)
+// The same Chebyshev-SGS step as k_sgs_tile (same colour updates sgs_colour / sgs_cells, same
+// arithmetic, same outputs) on an internal "planar" copy of the pressure vectors: 8 planes (vertex
+// parities q = px + 2 py, then cell parities) of ph x pw entries, plane q entry (i, j) = vertex
+// (2i + px, 2j + py) (cell (2i + px, 2j + py)), zero outside the domain.  A window's 8 parity
+// planes are then one dense 3D box {32, 32, 8} of the planar tensor: ONE TMA load
+// (cp.async.bulk.tensor, hardware zero fill outside the tensor) replaces the 32 per-thread
+// stride-2 cp.async gathers and their index arithmetic, and every global row access of the step
+// (r, y, y_prev, out) is a contiguous plane row.  y (window) arrives by TMA; r is read into
+// registers (coalesced) while the TMA is in flight; y and y_prev at the thread's own tile entries
+// are read at write time (L2: y was just fetched, y_prev is prefetched to L2 by a TMA prefetch at
+// the start), so the Q pass and its 46 KB of shared memory are gone (64 KB per CTA).
+// The last step of a chain writes the ABI (lexicographic) layout directly.
+struct SgsPlaneArgs {
+  MassGeo g;
+  SgsK k;
+  int pw, ph; int64_t pl;        // planar geometry: plane row length, rows, plane size
+  const double* rp;              // planar r (Pi applied on the fly: r - (kproj / k^T k) k)
+  const double* kproj;
+  double inv_kk;
+  const double* yg;              // planar y (nullable = 0: first step); the TMA map describes it
+  const double* ypg;             // planar y_prev (nullable)
+  double* outp;                  // planar output (or null when out_abi is set)
+  double* out_abi;               // ABI-layout output of the chain's last step
+  double omega, gam;
+  int tiles_x;
+  RedSite site; int slot; double* kout;
+  const double* done;
+  int pdl;
+};
+constexpr int SGSP_PAD = 128;                                      // zero words before V (edge reads at -33)
+// TMA box origins must be 16-byte aligned in the innermost dimension: the window's first plane
+// column A0 / 2 must be even, so the tile is 48 wide (halo 8 / 8, the right one >= 6 as required)
+// instead of k_sgs_tile's 50; vertically (dimension 1, no alignment rule) it stays 58.
+constexpr int SGSP_TTX = 48;
+static_assert(SGS_W - SGS_HX - SGSP_TTX >= 6 && (SGSP_TTX / 2) % 2 == 0 && (SGS_HX / 2) % 2 == 0, "TMA-aligned tile");
+constexpr int SGSP_BYTES = 8 * SGS_PL * (int)sizeof(double);       // one TMA box (8 planes x 32 x 32)
+constexpr int SGSP_SMEM = (SGSP_PAD + 8 * SGS_PL) * (int)sizeof(double) + 1024 + 64;   // + alignment slack, mbarrier
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+template <bool IN>
+__device__ __forceinline__ void sgsp_body(const SgsPlaneArgs& a, double* V, double* Cc, unsigned bar, bool tma,
+                                          int A0, int C0) {
+  const int i = threadIdx.x, ty = threadIdx.y;
+  const int n = a.g.n;
+  const int pw = a.pw, ph = a.ph;
+  const int64_t pl = a.pl;
+  const int X0 = A0 >> 1, Y0 = C0 >> 1;                      // window origin in plane coordinates
+  const double alpha = a.kproj ? (*a.kproj * a.inv_kk) : 0.0;
+  // ---- r (own entries of every plane, coalesced plane rows) while the TMA is in flight
+  double rv[4][2], rc[4][2];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int j = ty + SGS_TY * m;
+      const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
+      const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
+      const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
+      const int64_t o = (int64_t)(Y0 + j) * pw + (X0 + i);
+      rv[c][m] = inv ? __ldg(a.rp + c * pl + o) - alpha : 0.0;
+      rc[c][m] = inc ? __ldg(a.rp + (4 + c) * pl + o) + alpha : 0.0;
+    }
+  if (tma) {
+    // wait for the window (phase 0 of the single-use barrier)
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}\n" ::"r"(bar)
+        : "memory");
+  }
+  __syncthreads();
+  const SgsK& k = a.k;
+#define SGS_V(PX, PY) do { sgs_colour<PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
+  SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
+  sgs_cells<0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);             // P0 (once; see k_sgs_tile)
+  sgs_cells<1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);
+  sgs_cells<0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
+  sgs_cells<1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
+  __syncthreads();
+  SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0);
+  sgs_colour<0, 0, IN>(V, Cc, rv[0], A0, C0, n, k);            // backward colour 0: each thread reads back
+  __syncwarp();                                                 // only its own entries below
+#undef SGS_V
+  asm volatile("griddepcontrol.launch_dependents;");
+  // ---- write the own tile entries: out = co_s S(y) + (co_y y + co_p y_prev), as k_sgs_tile
+  const double co_s = a.omega * a.gam;
+  const double co_y = a.omega * (1.0 - a.gam);
+  const double co_p = 1.0 - a.omega;
+  const bool use_yp = a.ypg && co_p != 0.0;
+  const int n1 = n + 1, nk = a.g.nk;
+  double kd = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int j = ty + SGS_TY * m;
+      if (i < SGS_HX / 2 || i >= SGS_HX / 2 + SGSP_TTX / 2 || j < SGS_HY / 2 || j >= SGS_HY / 2 + SGS_TTY / 2) continue;
+      const int px = q & 1, py = (q >> 1) & 1;
+      const int ga = A0 + 2 * i + px, gc = C0 + 2 * j + py;
+      const bool vert = q < 4;
+      if (!IN && !(vert ? (ga <= n && gc <= n) : (ga < n && gc < n))) continue;
+      const int64_t po = q * pl + (int64_t)(Y0 + j) * pw + (X0 + i);
+      const double yv = a.yg ? __ldg(a.yg + po) : 0.0;
+      const double Q = fma(co_y, yv, use_yp ? co_p * __ldg(a.ypg + po) : 0.0);
+      const double o = fma(co_s, (vert ? V : Cc)[(q & 3) * SGS_PL + j * SGS_P + i], Q);
+      if (a.out_abi) {
+        if (vert) a.out_abi[ga + (int64_t)n1 * gc] = o;
+        else a.out_abi[nk + ga + (int64_t)n * gc] = o;
+      } else {
+        a.outp[po] = o;
+      }
+      kd += vert ? o : -o;
+    }
+  (void)ph;
+  if (a.kout) { double v[1] = {kd}; reduce_finish<1>(v, a.site, a.slot, a.kout); }
+}
+
+#ifndef SGSP_MINB
+#define SGSP_MINB SGS_MINB
+#endif
+__global__ void __launch_bounds__(SGS_TX * SGS_TY, SGSP_MINB) k_sgs_plane(const __grid_constant__ SgsPlaneArgs a,
+                                                                        const __grid_constant__ CUtensorMap tm_y,
+                                                                        const __grid_constant__ CUtensorMap tm_yp) {
+  extern __shared__ unsigned char sgsp_raw[];
+  // 1024-byte aligned window: [pad | V (4 planes) | Cc (4 planes)], mbarrier after it
+  const unsigned base = smem_u32(sgsp_raw);
+  const unsigned off = ((base + SGSP_PAD * 8 + 1023u) & ~1023u) - base;
+  double* V = reinterpret_cast<double*>(sgsp_raw + off);
+  double* Cc = V + 4 * SGS_PL;
+  double* pad = V - SGSP_PAD;
+  unsigned long long* barp = reinterpret_cast<unsigned long long*>(Cc + 4 * SGS_PL);
+  const unsigned bar = smem_u32(barp);
+  const int tid = threadIdx.x + SGS_TX * threadIdx.y;
+  const int n = a.g.n;
+  const int A0 = (blockIdx.x % a.tiles_x) * SGSP_TTX - SGS_HX, C0 = (blockIdx.x / a.tiles_x) * SGS_TTY - SGS_HY;
+  const bool tma = a.yg != nullptr;
+  if (tid == 0) {
+    if (a.ypg) {   // y_prev is only read at write time: start pulling its window into L2 now
+      asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(&tm_yp), "r"(A0 >> 1),
+                   "r"(C0 >> 1), "r"(0) : "memory");
+    }
+    if (tma) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
+  __syncthreads();                                                  // barrier initialised before any wait
+  if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");   // previous step complete and visible
+  if (is_done(a.done)) return;
+  if (tid < SGSP_PAD) pad[tid] = 0.0;
+  if (tma) {
+#if defined(SGSP_NOTMA)
+    {
+      const int X0 = A0 >> 1, Y0 = C0 >> 1;
+      for (int t = tid; t < 8 * SGS_PL; t += SGS_TX * SGS_TY) {
+        const int q = t >> 10, jj = (t >> 5) & 31, ii = t & 31;
+        const int x = X0 + ii, y = Y0 + jj;
+        V[t] = (x >= 0 && y >= 0 && x < a.pw && y < a.ph) ? a.yg[q * a.pl + (int64_t)y * a.pw + x] : 0.0;
+      }
+      __syncthreads();
+      if (tid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+    }
+#elif defined(SGSP_SPLIT)
+    if (tid == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(SGSP_BYTES) : "memory");
+      for (int q = 0; q < 8; ++q)
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+            ::"r"(smem_u32(V + q * SGS_PL)), "l"(&tm_y), "r"(A0 >> 1), "r"(C0 >> 1), "r"(q), "r"(bar)
+            : "memory");
+    }
+#else
+    if (tid == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(SGSP_BYTES) : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+          ::"r"(smem_u32(V)), "l"(&tm_y), "r"(A0 >> 1), "r"(C0 >> 1), "r"(0), "r"(bar)
+          : "memory");
+    }
+#endif
+  } else {   // first step: y = 0
+    for (int t = tid; t < 8 * SGS_PL; t += SGS_TX * SGS_TY) V[t] = 0.0;
+  }
+  const bool interior = A0 >= 1 && A0 + SGS_W - 1 <= n - 1 && C0 >= 1 && C0 + SGS_W - 1 <= n - 1;
+  if (interior) sgsp_body<true>(a, V, Cc, bar, tma, A0, C0);
+  else sgsp_body<false>(a, V, Cc, bar, tma, A0, C0);
+}
+
+// planar copy of r (rp) fused with k^T r (the Pi projection coefficient of Pi C Pi, reading R6)
+__global__ void __launch_bounds__(BS) k_kdot_planar(int n, int64_t np, int pw, int64_t pl, const double* x,
+                                                    double* xp, RedSite site, int slot, double* out,
+                                                    const double* done) {
+  if (is_done(done)) return;
+  const int n1 = n + 1;
+  const int64_t nk = (int64_t)n1 * n1;
+  double s = 0.0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < np; t += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[t];
+    int a, c, q;
+    if (t < nk) { a = (int)(t % n1); c = (int)(t / n1); q = (a & 1) + 2 * (c & 1); s += v; }
+    else { const int64_t e = t - nk; a = (int)(e % n); c = (int)(e / n); q = 4 + (a & 1) + 2 * (c & 1); s -= v; }
+    xp[q * pl + (int64_t)(c >> 1) * pw + (a >> 1)] = v;
+  }
+  double v[1] = {s};
+  reduce_finish<1>(v, site, slot, out);
+}
+
 // k^T x
 __global__ void __launch_bounds__(BS) k_kdot(int nk, int64_t np, const double* x, RedSite site, int slot,
                                              double* out, const double* done) {
@@ -1531,7 +1741,10 @@ __device__ __forceinline__ void st_body(const SaddleTileArgs& a, const StSmem& S
   if (a.dot_out) { double v[1] = {dot}; reduce_finish<1>(v, a.site, a.slot, a.dot_out); }
 }
 
-__global__ void __launch_bounds__(ST_THREADS, 2) k_saddle_tile(SaddleTileArgs a) {
+#ifndef ST_MINB
+#define ST_MINB 2
+#endif
+__global__ void __launch_bounds__(ST_THREADS, ST_MINB) k_saddle_tile(SaddleTileArgs a) {
   if (is_done(a.done)) return;
   const StSmem S;
   const int m = a.m, n = a.n, n1 = n + 1;
@@ -2575,6 +2788,78 @@ void sgs_sweep_dev(const Geo& g, const double* r, const double* y, double* z, do
 }
 
 // z_p = Pi C Pi r_p (reading R6) with C = m-step Chebyshev semi-iteration on SGS (reading R7)
+// Pi C Pi on the planar copies: k^T r fused with the planar copy of r, m steps of k_sgs_plane (TMA
+// windows), the last one writing the lexicographic layout, then the k-projection of the output.
+// Same operations and arithmetic as the lexicographic chain below (k^T out summed in another order).
+static etq_status mass_pc_apply_planar(const Problem& P, const double* r_p, double* z_p, RedSite rs, int slot,
+                                       double* dot_out, const double* dot_with, const double* done, cudaStream_t st,
+                                       double scale) {
+  const PcMass& M = P.pm;
+  const Geo& g = P.g;
+  const int64_t np = (int64_t)g.nk + g.n0;
+  const int64_t pl = (int64_t)M.pw * M.ph;
+  const double inv_kk = 1.0 / (double)np;
+  const int gf = grid_for(np, BS, RED_BLOCKS);
+  k_kdot_planar<<<gf, BS, 0, st>>>(g.n, np, M.pw, pl, r_p, M.rp, rs, 3, P.dscal + S_KR, done); etq_count_launch();
+  static bool smem_set = false;
+  if (!smem_set) {
+    cudaFuncSetAttribute(k_sgs_plane, cudaFuncAttributeMaxDynamicSharedMemorySize, SGSP_SMEM);
+    smem_set = true;
+  }
+  static int lo_prio = 1, hi_prio = 0;
+  if (lo_prio == 1) cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+  const double rho = 1.0 - M.a;
+  const double gam = 2.0 / (2.0 - rho), rh = rho / (2.0 - rho);
+  double omega = 1.0;
+  int cur = -1, prev = -1;                  // planar buffer indices of y and y_prev
+  SgsPlaneArgs a{};
+  a.g = mass_geo(g);
+  {
+    SgsK& k = a.k;
+    const double h = g.h;
+    k.w_in = 4.0 * h / 6.0; k.w_bd = 2.0 * h / 6.0; k.w_off = h / 6.0; k.rq = 0.25 * h * h;
+    k.c_dd = k.w_off * k.w_off; k.c_ed = k.w_off * k.w_in;
+    k.inv_in2 = 1.0 / (k.w_in * k.w_in); k.inv_inbd = 1.0 / (k.w_in * k.w_bd); k.inv_bd2 = 1.0 / (k.w_bd * k.w_bd);
+    k.inv_q0 = 1.0 / (h * h);
+  }
+  a.pw = M.pw; a.ph = M.ph; a.pl = pl;
+  a.rp = M.rp; a.kproj = P.dscal + S_KR; a.inv_kk = inv_kk;
+  a.gam = gam;
+  a.tiles_x = (g.n + 1 + SGSP_TTX - 1) / SGSP_TTX;
+  const int tiles = a.tiles_x * ((g.n + 1 + SGS_TTY - 1) / SGS_TTY);
+  a.site = rs; a.slot = 4; a.done = done;
+  for (int k = 0; k < M.m; ++k) {
+    if (k == 1) omega = 1.0 / (1.0 - 0.5 * rh * rh);
+    else if (k > 1) omega = 1.0 / (1.0 - 0.25 * rh * rh * omega);
+    const bool last = k == M.m - 1;
+    const int outb = (cur == 0) ? 1 : 0;    // never the buffer read as y (y_prev is overwritten in place)
+    a.yg = cur >= 0 ? M.yp[cur] : nullptr;
+    a.ypg = prev >= 0 ? M.yp[prev] : nullptr;
+    a.outp = last ? nullptr : M.yp[outb];
+    a.out_abi = last ? M.y0 : nullptr;
+    a.omega = (k == 0) ? 1.0 : omega;
+    a.kout = last ? P.dscal + S_KY : nullptr;
+    a.pdl = (k > 0 && g_sgs_pdl) ? 1 : 0;
+    const void* tm_y = M.tmap[cur >= 0 ? cur : 0];
+    const void* tm_yp = M.tmap[prev >= 0 ? prev : 0];
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(tiles); cfg.blockDim = dim3(SGS_TX, SGS_TY); cfg.dynamicSmemBytes = SGSP_SMEM; cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributePriority;
+    attr[0].val.priority = g_sgs_high_prio ? hi_prio : lo_prio;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr; cfg.numAttrs = a.pdl ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, k_sgs_plane, a, *reinterpret_cast<const CUtensorMap*>(tm_y),
+                       *reinterpret_cast<const CUtensorMap*>(tm_yp));
+    etq_count_launch();
+    prev = cur; cur = outb;
+  }
+  k_kproject_out<<<gf, BS, 0, st>>>(g.nk, np, M.y0, P.dscal + S_KY, inv_kk, scale, z_p, dot_with, rs, slot, dot_out,
+                                    done); etq_count_launch();
+  return ETQ_OK;
+}
+
 etq_status mass_pc_apply_ex(const Problem& P, const double* r_p, double* z_p, const RedSite* site, int slot,
                             double* dot_out, const double* dot_with, const double* done, cudaStream_t st,
                             double scale) {
@@ -2585,6 +2870,8 @@ etq_status mass_pc_apply_ex(const Problem& P, const double* r_p, double* z_p, co
   const double inv_kk = 1.0 / (double)np;
   const int gf = grid_for(np, BS, RED_BLOCKS);
   RedSite rs = *site;
+  if (M.planar && g_sgs_planar && M.m >= 1) return mass_pc_apply_planar(P, r_p, z_p, rs, slot, dot_out, dot_with, done,
+                                                                        st, scale);
   // k^T r (Pi applied on the fly inside the sweeps)
   k_kdot<<<gf, BS, 0, st>>>(g.nk, np, r_p, rs, 3, P.dscal + S_KR, done); etq_count_launch();
   const double rho = 1.0 - M.a;
@@ -2636,11 +2923,48 @@ etq_status cheb_tile_bench(const Problem& P, bool post, const double* in_b, cons
   return ETQ_OK;
 }
 
+// TMA descriptor of a planar pressure vector: 3D tensor {pw, ph, 8 planes}, box {32, 32, 8} (one SGS
+// window), zero fill outside (the domain edges of every window)
+static etq_status encode_planar_map(void* tmap, double* base, int pw, int ph) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return ETQ_ECUDA;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)pw, (cuuint64_t)ph, 8};
+  const cuuint64_t strides[2] = {(cuuint64_t)pw * sizeof(double), (cuuint64_t)pw * ph * sizeof(double)};
+#if defined(SGSP_SPLIT)
+  const cuuint32_t box[3] = {SGS_P, SGS_P, 1};
+#else
+  const cuuint32_t box[3] = {SGS_P, SGS_P, 8};
+#endif
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides,
+                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? ETQ_OK : ETQ_ECUDA;
+}
+
 etq_status mass_pc_alloc(Problem& P) {
   const int64_t np = P.n_p;
   PcMass& M = P.pm;
   if (!M.t) {
     ETQ_TRY(dalloc(&M.t, np)); ETQ_TRY(dalloc(&M.y0, np)); ETQ_TRY(dalloc(&M.y1, np)); ETQ_TRY(dalloc(&M.rr, np));
+  }
+  if (!M.rp && P.g.n >= 2 && P.g.n % 2 == 0) {
+    // planar copies (k_sgs_plane): pw even so that plane rows are 16-byte multiples (TMA strides)
+    M.pw = ((P.g.n / 2 + 1) + 1) & ~1;
+    M.ph = P.g.n / 2 + 1;
+    const size_t sz = (size_t)8 * M.pw * M.ph;
+    ETQ_TRY(dalloc(&M.rp, sz)); ETQ_TRY(dalloc(&M.yp[0], sz)); ETQ_TRY(dalloc(&M.yp[1], sz));
+    // entries outside the domain stay zero forever (only in-domain entries are ever written)
+    for (double* b : {M.rp, M.yp[0], M.yp[1]}) ETQ_CHECK(cudaMemset(b, 0, sz * sizeof(double)));
+    for (int k = 0; k < 2; ++k) ETQ_TRY(encode_planar_map(M.tmap[k], M.yp[k], M.pw, M.ph));
+    M.planar = true;
   }
   return ETQ_OK;
 }
