@@ -18,6 +18,7 @@ bool g_sgs_high_prio = false;       // etq_set_option(4): Chebyshev-SGS kernels 
 bool g_tail_sm = true;              // etq_set_option(5): shared-memory matrix-free coarse-level tail
 bool g_saddle_tile = true;          // etq_set_option(6): shared-memory tiled matrix-free saddle apply
 bool g_sgs_pdl = true;              // etq_set_option(7): programmatic dependent launches in the SGS chain
+bool g_cheb_tile2 = true;           // etq_set_option(11): leaner temporally blocked smoother (k_cheb_tile2)
 bool g_sgs_planar = false;          // etq_set_option(10): Chebyshev-SGS on parity planes with TMA windows
 bool g_vc_pdl = true;               // etq_set_option(8): programmatic dependent launches in the V-cycle
 bool g_prolong_tile = true;         // etq_set_option(9): tiled nested-Q2 prolongation
@@ -701,6 +702,7 @@ etq_status etq_set_option(int32_t option, int32_t value) {
   if (option == 8) { g_vc_pdl = value != 0; return ETQ_OK; }
   if (option == 9) { g_prolong_tile = value != 0; return ETQ_OK; }
   if (option == 10) { g_sgs_planar = value != 0; return ETQ_OK; }
+  if (option == 11) { g_cheb_tile2 = value != 0; return ETQ_OK; }
   return ETQ_EINVAL;
 }
 

@@ -43,6 +43,7 @@ extern bool g_tail_sm;                    // api.cu; etq_set_option(5)
 extern bool g_saddle_tile;                // api.cu; etq_set_option(6)
 extern bool g_sgs_pdl;                    // api.cu; etq_set_option(7)
 extern bool g_sgs_planar;                 // api.cu; etq_set_option(10)
+extern bool g_cheb_tile2;                 // api.cu; etq_set_option(11)
 extern bool g_vc_pdl;                     // api.cu; etq_set_option(8)
 extern bool g_prolong_tile;               // api.cu; etq_set_option(9)
 
@@ -126,6 +127,7 @@ struct Level {
   int nrows = 0;              // nq (Q2 velocity) or nk (Q1 pressure)
   double bim = 0.0;           // imaginary semi-axis of the smoother ellipse (0: real interval)
   bool st_on = false;         // interior stencil + frame SELL (Afr) instead of A for the smoother
+  bool ct2 = false;           // its stencils equal the constant-bank table of k_cheb_tile2
   StencilOp so;
   Sell Afr;                   // rows outside the interior rectangle (own permutation)
   // two-component work vectors, each [2*nq]

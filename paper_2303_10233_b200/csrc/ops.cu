@@ -12,6 +12,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <cstdio>
 #include <vector>
 #include <utility>
@@ -375,15 +377,76 @@ struct ChebTileArgs {
 // class stencil of one output from the register window: win[slot][col], rows jj-2..jj+2 in
 // slots (R0 + dj) % 5 (R0: slot of the output row, compile-time), cols ii-2..ii+3 with the
 // output at column offset OC
+// class stencils in the constant bank for k_cheb_tile2 (the Stokes Q2 Laplacian stencils are
+// h-independent: every Stokes level's StencilOp equals this table bitwise, checked at launch)
+__constant__ double c_ct_w[4][25];
+__constant__ double c_ct_dcls[4];
+// symmetric groups of the class stencils (reflections in x and y; classes 0 and 3 also the
+// transpose): class 0 weights of |offset| (0,0) (1,0) (1,1) (2,0) (2,1) (2,2); class 1 (i odd,
+// j even) (0,0) (1,0) (0,1) (1,1) (1,2); class 2 = class 1 transposed; class 3 (0,0) (1,0) (1,1)
+__constant__ double c_ct_g0[6], c_ct_g1[5], c_ct_g3[3];
+
+// grouped evaluation: sums of the mirrored taps first (independent adds), then one multiply-add
+// per distinct weight.  Not the stored-row summation order (rounding-level differences).
 template <int C, int OC, int R0>
+__device__ __forceinline__ double ct_group_sum(const double (&win)[5][6]) {
+#define W_(di, dj) win[(R0 + (dj) + 5) % 5][OC + (di) + 2]
+  if (C == 0) {
+    const double g10 = (W_(-1, 0) + W_(1, 0)) + (W_(0, -1) + W_(0, 1));
+    const double g11 = (W_(-1, -1) + W_(1, -1)) + (W_(-1, 1) + W_(1, 1));
+    const double g20 = (W_(-2, 0) + W_(2, 0)) + (W_(0, -2) + W_(0, 2));
+    const double g21 = ((W_(-2, -1) + W_(2, -1)) + (W_(-2, 1) + W_(2, 1))) +
+                       ((W_(-1, -2) + W_(1, -2)) + (W_(-1, 2) + W_(1, 2)));
+    const double g22 = (W_(-2, -2) + W_(2, -2)) + (W_(-2, 2) + W_(2, 2));
+    double a = c_ct_g0[0] * W_(0, 0);
+    a = fma(c_ct_g0[1], g10, a);
+    a = fma(c_ct_g0[2], g11, a);
+    a = fma(c_ct_g0[3], g20, a);
+    a = fma(c_ct_g0[4], g21, a);
+    return fma(c_ct_g0[5], g22, a);
+  } else if (C == 1 || C == 2) {
+    // class 1 groups (|di|, |dj|); class 2 is its transpose (swap di and dj)
+    constexpr bool T = C == 2;
+#define V_(u, v) (T ? W_(v, u) : W_(u, v))
+    const double g10 = V_(-1, 0) + V_(1, 0);
+    const double g01 = V_(0, -1) + V_(0, 1);
+    const double g11 = (V_(-1, -1) + V_(1, -1)) + (V_(-1, 1) + V_(1, 1));
+    const double g12 = (V_(-1, -2) + V_(1, -2)) + (V_(-1, 2) + V_(1, 2));
+#undef V_
+    double a = c_ct_g1[0] * W_(0, 0);
+    a = fma(c_ct_g1[1], g10, a);
+    a = fma(c_ct_g1[2], g01, a);
+    a = fma(c_ct_g1[3], g11, a);
+    return fma(c_ct_g1[4], g12, a);
+  } else {
+    const double g10 = (W_(-1, 0) + W_(1, 0)) + (W_(0, -1) + W_(0, 1));
+    const double g11 = (W_(-1, -1) + W_(1, -1)) + (W_(-1, 1) + W_(1, 1));
+    double a = c_ct_g3[0] * W_(0, 0);
+    a = fma(c_ct_g3[1], g10, a);
+    return fma(c_ct_g3[2], g11, a);
+  }
+#undef W_
+}
+
+template <int C, int OC, int R0, bool CW = false>
 __device__ __forceinline__ double ct_tap_sum(const StencilOp& so, const double (&win)[5][6]) {
+  if (CW) return ct_group_sum<C, OC, R0>(win);
   constexpr int PI = C & 1, PJ = C >> 1, RX = PI ? 1 : 2, RY = PJ ? 1 : 2;
   double a = 0.0;
 #pragma unroll
   for (int dj = -RY; dj <= RY; ++dj) {
 #pragma unroll
-    for (int di = -RX; di <= RX; ++di)
-      a = fma(so.w[C][(dj + 2) * 5 + di + 2], win[(R0 + dj + 5) % 5][OC + di + 2], a);
+    for (int di = -RX; di <= RX; ++di) {
+      if (CW) {
+        // taps the Stokes enumeration drops (exact Kronecker cancellations: weight 0, and
+        // fma(0, v, a) == a for the finite window values) are skipped at compile time
+        if ((di == 2 || di == -2) && dj == 0 && PJ) continue;
+        if ((dj == 2 || dj == -2) && di == 0 && PI) continue;
+        a = fma(c_ct_w[C][(dj + 2) * 5 + di + 2], win[(R0 + dj + 5) % 5][OC + di + 2], a);
+      } else {
+        a = fma(so.w[C][(dj + 2) * 5 + di + 2], win[(R0 + dj + 5) % 5][OC + di + 2], a);
+      }
+    }
   }
   return a;
 }
@@ -410,7 +473,7 @@ __device__ __forceinline__ void ct_load_row(const double* __restrict__ v, int ii
 }
 
 // row t of a warp's strip (compile-time t: window slots and stencil classes are constants)
-template <int S, int MODE, bool EDGE, int t>
+template <int S, int MODE, bool EDGE, int t, bool CW = false>
 __device__ __forceinline__ void ct_row_t(const ChebTileArgs& a, int i0, int j0, double* RS, const double* v,
                                          const double* din, double* dout, double c1, double c2, int jb, int ii,
                                          int i, bool lok, double (&win)[5][6]) {
@@ -421,11 +484,11 @@ __device__ __forceinline__ void ct_row_t(const ChebTileArgs& a, int i0, int j0, 
   constexpr int RSLOT = (t + 2) % 5;
   double qq[2];
   if ((t & 1) == 0) {                                  // jj even (jb even): classes 0 (i even), 1 (i odd)
-    qq[0] = ct_tap_sum<0, 0, RSLOT>(a.so, win);
-    qq[1] = ct_tap_sum<1, 1, RSLOT>(a.so, win);
+    qq[0] = ct_tap_sum<0, 0, RSLOT, CW>(a.so, win);
+    qq[1] = ct_tap_sum<1, 1, RSLOT, CW>(a.so, win);
   } else {
-    qq[0] = ct_tap_sum<2, 0, RSLOT>(a.so, win);
-    qq[1] = ct_tap_sum<3, 1, RSLOT>(a.so, win);
+    qq[0] = ct_tap_sum<2, 0, RSLOT, CW>(a.so, win);
+    qq[1] = ct_tap_sum<3, 1, RSLOT, CW>(a.so, win);
   }
   const int j = j0 + jj;
   if (!lok || (EDGE && (j < 0 || j >= m))) return;   // interior tiles lie inside the domain
@@ -444,7 +507,7 @@ __device__ __forceinline__ void ct_row_t(const ChebTileArgs& a, int i0, int j0, 
     const int ik = i + k;
     const bool dir = EDGE && (ik == 0 || j == 0 || ik == m - 1 || j == m - 1);   // interior tiles: never
     if (EDGE && dir) qq[k] = fma(1.0, v[base + k], 0.0);   // identity row (unmasked centre)
-    const double di = dir ? 1.0 : a.so.dcls[C0 + k];
+    const double di = dir ? 1.0 : (CW ? c_ct_dcls[C0 + k] : a.so.dcls[C0 + k]);
     ro[k] = ro[k] - qq[k];
     if (MODE == 1) outd[k] = di * ro[k] * a.itheta;
     else outd[k] = c1 * dd[k] + c2 * (di * ro[k]);
@@ -454,17 +517,17 @@ __device__ __forceinline__ void ct_row_t(const ChebTileArgs& a, int i0, int j0, 
   if (MODE == 1 || dout) *reinterpret_cast<double2*>(dout + base) = make_double2(outd[0], outd[1]);
 }
 
-template <int S, int MODE, bool EDGE, int... Ts>
+template <int S, int MODE, bool EDGE, bool CW, int... Ts>
 __device__ __forceinline__ void ct_rows(const ChebTileArgs& a, int i0, int j0, double* RS, const double* v,
                                         const double* din, double* dout, double c1, double c2, int jb, int ii,
                                         int i, bool lok, double (&win)[5][6], std::integer_sequence<int, Ts...>) {
-  (ct_row_t<S, MODE, EDGE, Ts>(a, i0, j0, RS, v, din, dout, c1, c2, jb, ii, i, lok, win), ...);
+  (ct_row_t<S, MODE, EDGE, Ts, CW>(a, i0, j0, RS, v, din, dout, c1, c2, jb, ii, i, lok, win), ...);
 }
 
 // One Chebyshev update over the square [S, CT_R - S)^2 of the window.  MODE 0: r <- r - A v,
 // dout <- c1 din + c2 D^-1 r (dout null: r only); MODE 1 (post-smoothing start, v = x):
 // r <- b - A x (r holds b), dout <- D^-1 r / theta.
-template <int S, int MODE, bool EDGE>
+template <int S, int MODE, bool EDGE, bool CW = false>
 __device__ __forceinline__ void ct_step(const ChebTileArgs& a, int i0, int j0, double* RS, const double* v,
                                         const double* din, double* dout, double c1, double c2) {
   constexpr int W = CT_R - 2 * S;
@@ -479,8 +542,8 @@ __device__ __forceinline__ void ct_step(const ChebTileArgs& a, int i0, int j0, d
   // rows jb-2 .. jb+1 into slots 0..3 (slot of row jj = (jj - jb + 2) % 5)
 #pragma unroll
   for (int r = 0; r < 4; ++r) ct_load_row<EDGE>(v, ii, jb - 2 + r, i, j0 + jb - 2 + r, m, win[r]);
-  ct_rows<S, MODE, EDGE>(a, i0, j0, RS, v, din, dout, c1, c2, jb, ii, i, lok, win,
-                         std::make_integer_sequence<int, CT_STRIP>{});
+  ct_rows<S, MODE, EDGE, CW>(a, i0, j0, RS, v, din, dout, c1, c2, jb, ii, i, lok, win,
+                             std::make_integer_sequence<int, CT_STRIP>{});
 }
 
 template <int POST>
@@ -616,6 +679,174 @@ __global__ void __launch_bounds__(CT_THREADS, 2) k_cheb_tile(ChebTileArgs a) {
     }
   }
 #undef CT_STEP
+}
+
+// k_cheb_tile with fewer instructions per output (the smoother was issue-bound: 29 k warp
+// instructions per CTA, a quarter of them in the staging loop's index arithmetic and a fifth in the
+// tile passes): the class weights and D^-1 are constant-bank operands with the structurally zero
+// taps skipped (no uniform-register reloads), the window is staged by row strips of column pairs
+// (one 128-bit shared store per pair, no division), and the tile passes use the same pair layout.
+// Same per-row arithmetic and summation order as k_cheb_tile: bitwise-identical outputs.
+constexpr int CT2_TP = CT_T / 2;                       // tile column pairs (28) = active lanes in tile passes
+constexpr int CT2_TR = CT_T / (CT_THREADS / 32);       // tile rows per warp (7)
+static_assert(CT2_TP <= 32 && CT_T % (CT_THREADS / 32) == 0, "tile pass layout");
+
+template <int POST, bool EDGE>
+__device__ __forceinline__ void ct2_body(const ChebTileArgs& a, double* D0, double* D1, double* RS, int i0, int j0,
+                                         int64_t off) {
+  const int m = a.so.m;
+  const double* __restrict__ b = a.b + off;
+  const double* __restrict__ xin = POST ? a.x_in + off : nullptr;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // ---- staging: column pairs in window order, pair p = tid + 256 k (row p / 34); all loads of a
+  //      group are issued before its stores; interior tiles need no bounds tests
+  constexpr int PR = CT_R / 2, NP = PR * CT_R, NK = (NP + CT_THREADS - 1) / CT_THREADS, G = 5;
+#pragma unroll
+  for (int k0 = 0; k0 < NK; k0 += G) {
+    double lb[G][2], lx[G][2];
+#pragma unroll
+    for (int kk = 0; kk < G; ++kk) {
+      const int p = tid + CT_THREADS * (k0 + kk);
+      const int jj = p / PR, pp = p - PR * jj;
+      const int j = j0 + jj, i = i0 + 2 * pp;
+      const int64_t g = (int64_t)m * j + i;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const bool in = (k0 + kk < NK) && p < NP && (!EDGE || (j >= 0 && j < m && i + e >= 0 && i + e < m));
+        lb[kk][e] = in ? __ldg(b + g + e) : 0.0;
+        if (POST) lx[kk][e] = in ? __ldg(xin + g + e) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < G; ++kk) {
+      const int p = tid + CT_THREADS * (k0 + kk);
+      if (k0 + kk >= NK || p >= NP) continue;
+      const int jj = p / PR, pp = p - PR * jj;
+      const int idx = 2 * pp + CT_R * jj;
+      *reinterpret_cast<double2*>(RS + idx) = make_double2(lb[kk][0], lb[kk][1]);
+      if (POST) {
+        *reinterpret_cast<double2*>(D1 + idx) = make_double2(lx[kk][0], lx[kk][1]);
+        *reinterpret_cast<double2*>(D0 + idx) = make_double2(0.0, 0.0);
+      } else {
+        const int odd = jj & 1;                            // j0 even: the row parity of j
+        double dv[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double di = c_ct_dcls[e + 2 * odd];
+          if (EDGE) {
+            const int j = j0 + jj, ie = i0 + 2 * pp + e;
+            if (ie == 0 || j == 0 || ie == m - 1 || j == m - 1) di = 1.0;
+            const bool in = ie >= 0 && j >= 0 && ie < m && j < m;
+            dv[e] = in ? di * lb[kk][e] * a.itheta : 0.0;
+          } else {
+            dv[e] = di * lb[kk][e] * a.itheta;             // k_cheb_init
+          }
+        }
+        *reinterpret_cast<double2*>(D0 + idx) = make_double2(dv[0], dv[1]);
+        *reinterpret_cast<double2*>(D1 + idx) = make_double2(0.0, 0.0);
+      }
+    }
+  }
+  __syncthreads();
+  // ---- tile passes: lane L < 28 owns the column pair (CT_H + 2L, +1) of the warp's 7 tile rows
+  const bool tl = lane < CT2_TP;
+  const int tii = CT_H + 2 * (tl ? lane : 0);
+  const int ti = i0 + tii;
+  auto tile_pass = [&](auto&& f) {
+    if (!tl) return;
+#pragma unroll
+    for (int r = 0; r < CT2_TR; ++r) {
+      const int tjj = CT_H + warp * CT2_TR + r;
+      const int j = j0 + tjj;
+      if (EDGE && j >= m) continue;
+      const int w = tii + CT_R * tjj;
+      const int64_t g = off + ti + (int64_t)m * j;
+      f(w, g, !EDGE || ti + 1 < m, !EDGE || ti < m, r);
+    }
+  };
+  // the tile's x accumulates in registers (pair r of the warp's rows): no global round trips
+  double xs[CT2_TR][2];
+  auto tile_acc = [&](const double* D, bool init, const double* D2) {
+    if (!tl) return;
+#pragma unroll
+    for (int r = 0; r < CT2_TR; ++r) {
+      const int w = tii + CT_R * (CT_H + warp * CT2_TR + r);
+      const double2 p = *reinterpret_cast<const double2*>(D + w);
+      if (init) {   // x = v0 + d (v0 from D2: POST x, pre 0 + d0)
+        const double2 q = *reinterpret_cast<const double2*>(D2 + w);
+        xs[r][0] = POST ? q.x + p.x : (0.0 + q.x) + p.x;
+        xs[r][1] = POST ? q.y + p.y : (0.0 + q.y) + p.y;
+      } else {
+        xs[r][0] = xs[r][0] + p.x;
+        xs[r][1] = xs[r][1] + p.y;
+      }
+    }
+  };
+  if (!POST) {
+    ct_step<2, 0, EDGE, true>(a, i0, j0, RS, D0, D0, D1, a.c1[0], a.c2[0]);
+    __syncthreads();
+    tile_acc(D1, true, D0);                                  // x2 = (0 + d0) + d1
+    __syncthreads();
+    ct_step<4, 0, EDGE, true>(a, i0, j0, RS, D1, D1, D0, a.c1[1], a.c2[1]);
+    __syncthreads();
+    tile_acc(D0, false, nullptr);                            // x3 = x2 + d2
+    ct_step<6, 0, EDGE, true>(a, i0, j0, RS, D0, D0, (double*)nullptr, 0.0, 0.0);
+    __syncthreads();
+    pdl_trigger();
+    tile_pass([&](int w, int64_t g, bool ok1, bool ok0, int r) {
+      const double2 p = *reinterpret_cast<const double2*>(RS + w);
+      if (ok0) { a.r_out[g] = p.x; a.x_out[g] = xs[r][0]; }
+      if (ok1) { a.r_out[g + 1] = p.y; a.x_out[g + 1] = xs[r][1]; }
+    });
+  } else {
+    ct_step<2, 1, EDGE, true>(a, i0, j0, RS, D1, (const double*)nullptr, D0, 0.0, 0.0);   // r0 = b - A x, d0
+    __syncthreads();
+    tile_acc(D0, true, D1);                                  // x += d0
+    __syncthreads();                                         // x (in D1) no longer read
+    ct_step<4, 0, EDGE, true>(a, i0, j0, RS, D0, D0, D1, a.c1[0], a.c2[0]);
+    __syncthreads();
+    tile_acc(D1, false, nullptr);                            // x += d1
+    ct_step<6, 0, EDGE, true>(a, i0, j0, RS, D1, D1, D0, a.c1[1], a.c2[1]);   // d2 (deferred)
+    __syncthreads();
+    pdl_trigger();
+    if (a.z_out) {   // finest level: z = x + d2, <z, w>
+      double dot = 0.0;
+      tile_pass([&](int w, int64_t g, bool ok1, bool ok0, int r) {
+        const double2 p = *reinterpret_cast<const double2*>(D0 + w);
+        if (ok0) {
+          const double v = xs[r][0] + p.x;
+          a.z_out[g] = v;
+          dot += a.dot_with ? v * __ldg(a.dot_with + g) : v;
+        }
+        if (ok1) {
+          const double v = xs[r][1] + p.y;
+          a.z_out[g + 1] = v;
+          dot += a.dot_with ? v * __ldg(a.dot_with + g + 1) : v;
+        }
+      });
+      if (a.dot_out) { double v1[1] = {dot}; reduce_finish<1>(v1, a.site, a.slot, a.dot_out, true); }
+    } else {
+      tile_pass([&](int w, int64_t g, bool ok1, bool ok0, int r) {
+        const double2 p = *reinterpret_cast<const double2*>(D0 + w);
+        if (ok0) { a.d_out[g] = p.x; a.x_out[g] = xs[r][0]; }
+        if (ok1) { a.d_out[g + 1] = p.y; a.x_out[g + 1] = xs[r][1]; }
+      });
+    }
+  }
+}
+
+template <int POST>
+__global__ void __launch_bounds__(CT_THREADS, 2) k_cheb_tile2(ChebTileArgs a) {
+  pdl_wait();
+  if (is_done(a.done)) return;
+  extern __shared__ __align__(16) double ct_sm[];
+  const int m = a.so.m;
+  const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
+  const int i0 = tx * CT_T - CT_H, j0 = ty * CT_T - CT_H;
+  const int64_t off = (int64_t)blockIdx.y * a.nq;
+  const bool edge = i0 < 3 || j0 < 3 || i0 + CT_R > m - 3 || j0 + CT_R > m - 3;   // block-uniform
+  if (edge) ct2_body<POST, true>(a, ct_sm, ct_sm + CT_ARR, ct_sm + 2 * CT_ARR, i0, j0, off);
+  else ct2_body<POST, false>(a, ct_sm, ct_sm + CT_ARR, ct_sm + 2 * CT_ARR, i0, j0, off);
 }
 
 // r = b - A x ; d = D^{-1} r / theta  (start of post-smoothing), NC components
@@ -2292,6 +2523,56 @@ static etq_status level_sizes(int n, int coarse_n, std::vector<int>& ns) {
 // Velocity-block hierarchy (reading R9/R9'): rediscretised scalar operator L or F_s per level,
 // Dirichlet identity rows, smoother ellipse per level (Oseen: imaginary semi-axis = Gershgorin
 // radius of D^{-1}N), dense coarse inverse (Gauss-Jordan; pivoted for the nonsymmetric F).
+// Constant-bank stencil table of k_cheb_tile2: uploaded once (setup time, never during capture);
+// a level may use k_cheb_tile2 only if its class stencils and D^-1 equal the table bitwise.
+// the grouped weights of ct_group_sum and the symmetry they rely on: every tap equals its group's
+// representative (the + offsets) to within a few ulp (the assembled mirrored taps may differ in the
+// last bit: different element-contribution order); the taps the Stokes enumeration drops are zero
+static bool ct2_groups(const StencilOp& so, double g0[6], double g1[5], double g3[3]) {
+  auto w = [&](int c, int di, int dj) { return so.w[c][(dj + 2) * 5 + di + 2]; };
+  g0[0] = w(0, 0, 0); g0[1] = w(0, 1, 0); g0[2] = w(0, 1, 1); g0[3] = w(0, 2, 0); g0[4] = w(0, 2, 1); g0[5] = w(0, 2, 2);
+  g1[0] = w(1, 0, 0); g1[1] = w(1, 1, 0); g1[2] = w(1, 0, 1); g1[3] = w(1, 1, 1); g1[4] = w(1, 1, 2);
+  g3[0] = w(3, 0, 0); g3[1] = w(3, 1, 0); g3[2] = w(3, 1, 1);
+  for (int dj = -2; dj <= 2; ++dj)
+    for (int di = -2; di <= 2; ++di) {
+      const int u = std::abs(di), v = std::abs(dj);
+      const int lo = std::min(u, v), hi = std::max(u, v);
+      const double e0 = (hi == 0) ? g0[0] : (hi == 1) ? (lo == 0 ? g0[1] : g0[2]) : (lo == 0 ? g0[3] : lo == 1 ? g0[4] : g0[5]);
+      auto near = [](double x, double y) { return std::fabs(x - y) <= 8e-16 * std::fabs(y); };
+      if (!near(w(0, di, dj), e0)) return false;
+      if (u <= 1) {   // class 1 (i odd: |di| <= 1), class 2 = its transpose
+        const double e1 = (u == 0 && v == 0) ? g1[0] : (u == 1 && v == 0) ? g1[1] : (u == 0 && v == 1) ? g1[2]
+                        : (u == 1 && v == 1) ? g1[3] : (u == 1 && v == 2) ? g1[4] : 0.0;
+        if (!near(w(1, di, dj), e1) || !near(w(2, dj, di), e1)) return false;
+      }
+      if (u <= 1 && v <= 1) {
+        const double e3 = (u + v == 0) ? g3[0] : (u + v == 1) ? g3[1] : g3[2];
+        if (!near(w(3, di, dj), e3)) return false;
+      }
+    }
+  return true;
+}
+
+static bool ct2_register(const StencilOp& so) {
+  static bool have = false;
+  static double w[4][25], d[4];
+  if (!have) {
+    double g0[6], g1[5], g3[3];
+    if (!ct2_groups(so, g0, g1, g3)) return false;
+    if (cudaMemcpyToSymbol(c_ct_w, so.w, sizeof(w)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_ct_dcls, so.dcls, sizeof(d)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_ct_g0, g0, sizeof(g0)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_ct_g1, g1, sizeof(g1)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_ct_g3, g3, sizeof(g3)) != cudaSuccess)
+      return false;
+    std::memcpy(w, so.w, sizeof(w));
+    std::memcpy(d, so.dcls, sizeof(d));
+    have = true;
+    return true;
+  }
+  return std::memcmp(w, so.w, sizeof(w)) == 0 && std::memcmp(d, so.dcls, sizeof(d)) == 0;
+}
+
 etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, double hi, int degree) {
   std::vector<int> ns;
   ETQ_TRY(level_sizes(P.g.n, coarse_n, ns));
@@ -2334,6 +2615,8 @@ etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, do
       }
       ETQ_CHECK(cudaStreamSynchronize(P.stream));
       lv.st_on = true;
+      lv.ct2 = ct2_register(lv.so);
+      if (std::getenv("ETQ_DEBUG")) std::fprintf(stderr, "[etq] level n=%d k_cheb_tile2 %s\n", lv.g.n, lv.ct2 ? "on" : "off");
     }
   }
   // coarse-level tail: first level l >= 1 with n <= TAIL_N (degree <= 4)
@@ -2523,6 +2806,17 @@ static void launch_cheb_tile(const Level& lv, bool post, const double* b, const 
   a.done = done;
   a.z_out = z_out; a.dot_with = dot_with; a.site = site ? *site : RedSite{}; a.slot = slot; a.dot_out = dot_out;
   dim3 grid(a.tiles_x * a.tiles_x, 2);
+  if (lv.ct2 && g_cheb_tile2) {
+    static bool smem2 = false;
+    if (!smem2) {
+      cudaFuncSetAttribute(k_cheb_tile2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM);
+      cudaFuncSetAttribute(k_cheb_tile2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM);
+      smem2 = true;
+    }
+    if (post) launch_pdl(k_cheb_tile2<1>, grid, dim3(CT_THREADS), CT_SMEM, st, pdl, a);
+    else launch_pdl(k_cheb_tile2<0>, grid, dim3(CT_THREADS), CT_SMEM, st, pdl, a);
+    return;
+  }
   if (post) launch_pdl(k_cheb_tile<1>, grid, dim3(CT_THREADS), CT_SMEM, st, pdl, a);
   else launch_pdl(k_cheb_tile<0>, grid, dim3(CT_THREADS), CT_SMEM, st, pdl, a);
 }

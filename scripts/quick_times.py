@@ -22,10 +22,14 @@ def main():
     ap.add_argument("--n", type=int, default=1024)
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--opt", action="append", default=[], help="etq_set_option k=v before setup (repeatable)")
     args = ap.parse_args()
+    for kv in args.opt:
+        k, v = kv.split("=")
+        etq.set_option(int(k), int(v))
     P = etq.Problem(args.n)
     P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.005))
-    row = {"n": args.n}
+    row = {"n": args.n, "opts": args.opt}
     for w, name in NAMES.items():
         try:
             row[name + "_us"] = round(P.time_kernel(w, args.reps)[0] * 1e3, 2)
