@@ -47,8 +47,14 @@ enum {
  * storage (velocity operators; results are bitwise identical in all modes):
  *   0 = compressed: interior SELL slices keep neither column indices (col = row + per-class
  *       offset) nor values when these equal the per-class stencil bitwise;
- *   1 = implicit column indices only;  2 = explicit SELL (indices and values stored). */
-typedef struct { int32_t n; int32_t bc; int32_t storage; } etq_grid;
+ *   1 = implicit column indices only;  2 = explicit SELL (indices and values stored).
+ * enriched = 1: the paper's Q2-Q1* (pressure space Q1 + P0); enriched = 0: plain
+ *   Taylor-Hood Q2-Q1 on the same mesh (Stokes only; for the local-conservation contrast of
+ *   P:198-202).  The vector layout is the same; in plain mode the p_0 block is inert: the saddle
+ *   apply is the reduced [A B1^T; B1 0] (p_0 rows 0), the right-hand side's p_0 block is 0, and
+ *   ETQ_PC_P2_GMG becomes diag(one V-cycle, m_p-step Chebyshev-Jacobi on the Q1 mass Q_k)
+ *   (the standard Taylor-Hood Stokes preconditioner; m_p = mass_cheb_steps). */
+typedef struct { int32_t n; int32_t bc; int32_t storage; int32_t enriched; } etq_grid;
 
 /* Convection field of the Oseen problem.
  * kind = 0: none (Stokes, viscosity ignored);
@@ -254,25 +260,8 @@ etq_status etq_launch_count(int64_t* count);
  * Host outputs: *ms = average device time per launch, *bytes = algorithmic bytes per launch. */
 etq_status etq_time_kernel(etq_problem* p, int32_t which, int32_t reps, double* ms, double* bytes);
 
-/* Process-wide implementation switches (A/B tests; results are bitwise identical either way):
- *   option 0 = temporally blocked Chebyshev smoothing on the Stokes interior-stencil levels
- *              (value 1 = on [default], 0 = one kernel per Chebyshev step);
- *   option 1 = coarsest level n that uses it [64] (smaller grids are launch-latency bound);
- *   option 2 = matrix-free Stokes saddle apply (1 [default]) or the stored SELL rows (0);
- *   option 3 = MINRES loop as one CUDA graph with a device-side while node (1 [default]) or one
- *              graph launch and one flag read-back per iteration (0);
- *   option 4 = launch priority of the Chebyshev-SGS pressure kernels (0 = lowest [default], 1 = highest);
- *   option 5 = coarse V-cycle levels (n <= 16) in one CTA with every vector in shared memory and
- *              the class stencils (1 [default], Stokes only) or through the stored rows in global memory (0);
- *   option 6 = matrix-free Stokes saddle apply from shared-memory tiles (1 [default]) or by global
- *              gathers (0); only with option 2 = 1;
- *   option 7 = programmatic dependent launches between the Chebyshev-SGS steps (1 [default]) or plain
- *              stream order (0);
- *   option 8 = programmatic dependent launches between the kernels of the Q2 V-cycle (1 [default]) or
- *              plain stream order (0);
- *   option 9 = nested-Q2 prolongation from shared-memory tiles (1 [default]) or by gathers (0).
- * Applies to solves whose CUDA graphs are captured afterwards (re-run etq_precond_setup). */
-etq_status etq_set_option(int32_t option, int32_t value);
+/* Implementation A/B switches are not part of this ABI: see include/etq_debug.h (test and
+ * measurement builds only). */
 
 const char* etq_status_string(etq_status s);
 void etq_destroy(etq_problem* p);

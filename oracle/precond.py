@@ -7,6 +7,9 @@ Stokes, block diagonal P = diag(M, M_S) (Eq. stokes_pre):
        system [[M_Q, k], [k^T, 0]] (P:409-427, P:515-516)            -> StokesP1
   P2 = diag(one V-cycle, 20 Chebyshev-SGS steps) (AMG -> GMG per
        BASELINE.json, reading R9; k-constraint by Pi C Pi, reading R6) -> StokesP2
+Plain Taylor-Hood Q2-Q1 on the same mesh (the local-conservation contrast):
+  diag(one V-cycle, m_p Chebyshev-Jacobi steps on the Q1 mass Q_k over [1/4, 9/4]) on the
+  reduced system [A B1^T; B1 0] (reading R13)                -> StokesP2Plain
 """
 from __future__ import annotations
 
@@ -49,6 +52,27 @@ class StokesP2:
 
     def __call__(self, r):
         return np.concatenate([self.velocity(r[:self.n_u]), self.pressure(r[self.n_u:])])
+
+
+class StokesP2Plain:
+    """Plain Q2-Q1 Stokes preconditioner on [u; p_1]: z_u = one V-cycle per component,
+    z_p = m_p-step Chebyshev-Jacobi approximation of Q_k^{-1} (interval [1/4, 9/4], reading R13)."""
+
+    def __init__(self, s: fem.SaddleSystem, mp_steps: int = 10, hierarchy=None):
+        self.n_u = s.g.n_u
+        self.h = hierarchy if hierarchy is not None else mg.Hierarchy(s.g.n)
+        self.Qk = s.Qk
+        self.dinv = 1.0 / s.Qk.diagonal()
+        self.mp_steps = mp_steps
+
+    def __call__(self, r):
+        zp, _ = mg.chebyshev_smooth(self.Qk, self.dinv, r[self.n_u:], None, 0.25, 2.25, self.mp_steps)
+        return np.concatenate([self.h.apply_velocity(r[:self.n_u]), zp])
+
+
+def plain_system(s: fem.SaddleSystem):
+    """Plain Taylor-Hood operator [A B1^T; B1 0] and right-hand side [f; g1] (P0 dropped)."""
+    return fem.reduced_operator(s), s.b[:s.g.n_u + s.g.n_k].copy()
 
 
 class StokesP3:

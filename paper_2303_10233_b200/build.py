@@ -16,7 +16,7 @@ def nvcc_cmd(out=OUT, extra=()):
 
 def build(force: bool = False, verbose: bool = True) -> str:
     srcs = [os.path.join(HERE, "csrc", s) for s in SOURCES] + \
-        [os.path.join(HERE, "csrc", "etq_internal.cuh"), os.path.join(HERE, "csrc", "device_common.cuh"), os.path.join(os.path.dirname(HERE), "include", "etq.h")]
+        [os.path.join(HERE, "csrc", "etq_internal.cuh"), os.path.join(HERE, "csrc", "device_common.cuh"), os.path.join(os.path.dirname(HERE), "include", "etq.h"), os.path.join(os.path.dirname(HERE), "include", "etq_debug.h")]
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(s) for s in srcs):
         return OUT
     cmd = nvcc_cmd()

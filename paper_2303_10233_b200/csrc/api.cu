@@ -1,5 +1,6 @@
 // api.cu — the extern "C" boundary of libetq (declared and documented in include/etq.h).
 #include "etq_internal.cuh"
+#include "../../include/etq_debug.h"
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -137,10 +138,13 @@ const char* etq_status_string(etq_status s) {
 
 etq_status etq_assemble(const etq_grid* grid, double viscosity, const etq_wind* wind, void* cuda_stream,
                         etq_problem** out) {
+  NvtxRange nvtx_("etq_assemble");
   if (!grid || !out) return ETQ_EINVAL;
   if (grid->n < 2 || grid->n > 4096 || (grid->bc != 0 && grid->bc != 1)) return ETQ_EINVAL;
   if (grid->storage < 0 || grid->storage > 2) return ETQ_EINVAL;
+  if (grid->enriched != 0 && grid->enriched != 1) return ETQ_EINVAL;
   const bool oseen = wind && wind->kind != 0;
+  if (!grid->enriched && oseen) return ETQ_EINVAL;      // plain Q2-Q1: Stokes only
   if (oseen && !(viscosity > 0.0)) return ETQ_EINVAL;
   if (wind && (wind->kind < 0 || wind->kind > 2)) return ETQ_EINVAL;
   etq_problem* h = new (std::nothrow) etq_problem();
@@ -150,6 +154,7 @@ etq_status etq_assemble(const etq_grid* grid, double viscosity, const etq_wind* 
   P.bc = grid->bc;
   P.storage = (oseen && wind->kind == 2) ? 2 : grid->storage;   // nodal winds refill explicit values
   P.oseen = oseen;
+  P.plain = grid->enriched == 0;
   P.wind = oseen ? wind->kind : 0;
   P.nu = oseen ? viscosity : 1.0;
   P.n_u = 2LL * P.g.nq;
@@ -214,19 +219,24 @@ etq_status etq_sizes(const etq_problem* h, int64_t* n_u, int64_t* n_k, int64_t* 
 etq_status etq_build_rhs(const etq_problem* h, const double* f_nodal, double* b) {
   if (!h || !b) return ETQ_EINVAL;
   StreamScope sc(h->P);
-  return build_rhs_dev(h->P, f_nodal, b);
+  ETQ_TRY(build_rhs_dev(h->P, f_nodal, b));
+  const Problem& P = h->P;
+  if (P.plain)   // plain Q2-Q1: no P0 rows (the reduced right-hand side [f; g1])
+    ETQ_CHECK(cudaMemsetAsync(b + P.n_u + P.g.nk, 0, sizeof(double) * P.g.n0, P.stream));
+  return ETQ_OK;
 }
 
 etq_status etq_apply_saddle(const etq_problem* h, int32_t reduced, const double* x, double* y) {
   if (!h || !x || !y || x == y) return ETQ_EINVAL;
   const Problem& P = h->P;
   StreamScope sc(P);
-  launch_saddle_ex(P, reduced != 0, x, y, nullptr, nullptr, 0, nullptr, nullptr, P.stream);
+  launch_saddle_ex(P, reduced != 0 || P.plain, x, y, nullptr, nullptr, 0, nullptr, nullptr, P.stream);
   ETQ_CHECK(cudaGetLastError());
   return ETQ_OK;
 }
 
 etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_params* params) {
+  NvtxRange nvtx_("etq_precond_setup");
   if (!h) return ETQ_EINVAL;
   Problem& P = h->P;
   StreamScope sc(P);
@@ -234,6 +244,7 @@ etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_para
   P.params = prm;
   // cached MINRES graphs bake in hierarchy buffers that a new setup may replace
   drop_minres_graphs(P);
+  if (P.plain && kind != ETQ_PC_P2_GMG) return ETQ_EINVAL;   // plain Q2-Q1: only the Taylor-Hood P2
   if (kind == ETQ_PC_P3 || kind == ETQ_PC_P1_ITER) {
     if (P.oseen) return ETQ_EINVAL;
     if (!is_pow2(P.g.n) || !is_pow2(prm.coarse_n) || prm.coarse_n > P.g.n || !is_pow2(prm.inner_coarse_n))
@@ -267,6 +278,14 @@ etq_status etq_precond_setup(etq_problem* h, etq_pc_kind kind, const etq_pc_para
     P.pm.ready = false;
     if (P.mg.built) free_hierarchy(P.mg);
     ETQ_TRY(build_hierarchy(P, P.mg, prm.coarse_n, prm.smooth_lo, prm.smooth_hi, prm.smooth_degree));
+    if (P.plain) {   // plain Q2-Q1: the pressure block is Chebyshev-Jacobi on Q_k (no M_Q, no k)
+      if (prm.mass_cheb_steps < 1) return ETQ_EINVAL;
+      if (!P.plain_w) ETQ_TRY(dalloc(&P.plain_w, 3 * (size_t)P.g.nk));
+      P.p2_ready = true;
+      drop_minres_graphs(P);
+      ETQ_CHECK(cudaStreamSynchronize(P.stream));
+      return ETQ_OK;
+    }
     ETQ_TRY(mass_pc_alloc(P));
     P.pm.m = prm.cheb_sgs_steps;
     double a = prm.cheb_sgs_lo;
@@ -690,7 +709,7 @@ etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* 
   return ETQ_OK;
 }
 
-etq_status etq_set_option(int32_t option, int32_t value) {
+etq_status etq_debug_set_option(int32_t option, int32_t value) {
   if (option == 0) { g_cheb_tile_enabled = value != 0; return ETQ_OK; }
   if (option == 1) { if (value < 2) return ETQ_EINVAL; g_cheb_tile_min_n = value; return ETQ_OK; }
   if (option == 2) { g_saddle_mf = value != 0; return ETQ_OK; }
@@ -726,6 +745,7 @@ void etq_destroy(etq_problem* h) {
   cudaFree(P.p1.Ainv); cudaFree(P.p1.MQinv); cudaFree(P.p1.tmp);
   cudaFree(P.pm.t); cudaFree(P.pm.y0); cudaFree(P.pm.y1); cudaFree(P.pm.rr);
   cudaFree(P.pm.rp); cudaFree(P.pm.yp[0]); cudaFree(P.pm.yp[1]);
+  cudaFree(P.plain_w);
   cudaFree(P.red[0].partials); cudaFree(P.red[0].counter);
   cudaFree(P.dscal); cudaFree(P.dhist); cudaFree(P.tk); cudaFree(P.tkf);
   if (P.hscal) cudaFreeHost(P.hscal);

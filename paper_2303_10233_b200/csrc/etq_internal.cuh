@@ -16,6 +16,17 @@
 #include <vector>
 #include <string>
 #include "../../include/etq.h"
+#include <nvtx3/nvToolsExt.h>
+
+// NVTX range for a solver phase / kernel family (header-only NVTX v3: no link dependency; a
+// profiler such as Nsight Systems picks the ranges up through its injection library).  The
+// ranges cover host time: eager launches, graph captures and graph launches.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 #define ETQ_CHECK(call)                                                        \
   do {                                                                         \
@@ -248,6 +259,8 @@ struct Problem {
   int bc = 0;
   int storage = 0;                            // etq_grid.storage
   int wind = 0;
+  bool plain = false;                         // etq_grid.enriched == 0: plain Q2-Q1 (p_0 block inert)
+  double* plain_w = nullptr;                  // [3 n_k] scratch of the plain P2 pressure block
   double nu = 1.0;
   bool oseen = false;
   int64_t n_u = 0, n_p = 0, N = 0;
@@ -393,6 +406,9 @@ etq_status gmres_run(Problem& P, bool reduced, etq_pc_kind kind, const double* b
                      int restart, int maxit, etq_report* rep, double* p0_res_norm);
 void oseen_free(Problem& P);
 etq_status pcd_schur_apply(const Problem& P, const double* r, double* z, cudaStream_t st);
+// out = m_p-step Chebyshev-Jacobi approximation of Q_k^{-1} r on [1/4, 9/4] (reading R13); ws: 3 n_k scratch
+void qk_cheb_ws(const Problem& P, const double* r, double* out, int steps, double* ws, const double* done,
+                cudaStream_t st);
 etq_status make_reduced_rhs(Problem& P, const double* b, double** bred);
 double host_norm(Problem& P, const double* v, int64_t n);
 etq_status two_stage_run(Problem& P, const double* b, double* x, double eta, double c, int restart, int maxit,

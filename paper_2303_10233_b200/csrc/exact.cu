@@ -449,6 +449,7 @@ void exact_free(Problem& P) {
 
 etq_status exact_mass_apply(const Problem& P, const double* r_p, double* z_p, const RedSite* site, int slot,
                             double* dot_out, const double* dot_with, const double* done, cudaStream_t st) {
+  NvtxRange nvtx_("exact M_Q solve");
   if (!P.mx.ready) return ETQ_ENOTSETUP;
   PcExactMass& X = const_cast<PcExactMass&>(P.mx);
   return run_graphed(P, st, [&](cudaStream_t s) {

@@ -2013,6 +2013,7 @@ __global__ void __launch_bounds__(ST_THREADS, ST_MINB) k_saddle_tile(SaddleTileA
 
 void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y, const double* inv_scale,
                       const RedSite* site, int slot, double* dot_out, const double* done, cudaStream_t st) {
+  NvtxRange nvtx_("saddle apply");
   SaddleArgs a;
   a.L = P.Lv; a.BxT1 = P.BxT1; a.ByT1 = P.ByT1; a.BxT0 = P.BxT0; a.ByT0 = P.ByT0; a.B = P.B;
   a.nq = P.g.nq; a.nk = P.g.nk; a.n_u = P.n_u; a.n_p = P.n_p; a.reduced = reduced ? 1 : 0;
@@ -2842,6 +2843,7 @@ static void launch_cheb_sk(const Hierarchy& H, const Level& lv, const ChebArgs& 
 etq_status vcycle_apply_ex(const Problem& P, const Hierarchy& H, const double* r_u, double* z_u,
                            const RedSite* site, int slot, double* dot_out, const double* dot_with,
                            const double* done, cudaStream_t st, bool pdl) {
+  NvtxRange nvtx_("V-cycle");
   const int L = (int)H.lv.size();
   const int nc = H.ncomp;
   const double theta = 0.5 * (H.hi + H.lo);
@@ -3157,6 +3159,7 @@ static etq_status mass_pc_apply_planar(const Problem& P, const double* r_p, doub
 etq_status mass_pc_apply_ex(const Problem& P, const double* r_p, double* z_p, const RedSite* site, int slot,
                             double* dot_out, const double* dot_with, const double* done, cudaStream_t st,
                             double scale) {
+  NvtxRange nvtx_("Pi C Pi (Chebyshev-SGS)");
   const PcMass& M = P.pm;
   if (!M.ready) return ETQ_ENOTSETUP;
   const Geo& g = P.g;

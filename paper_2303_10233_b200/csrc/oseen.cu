@@ -353,11 +353,11 @@ __global__ void __launch_bounds__(BS) k_dot2(const double* a, const double* b, i
 static double theta_of(double lo, double hi) { return 0.5 * (hi + lo); }
 
 // Mp^{-1} r: m_p-step Chebyshev-Jacobi on Qk over [1/4, 9/4] from zero (reading R13); x -> out
-static void qk_cheb(const Problem& P, const double* r, double* out, int steps, const double* done, cudaStream_t st) {
+static void qk_cheb_impl(const Problem& P, const double* r, double* out, int steps, double* rr, double* d0, double* d1,
+                         const double* done, cudaStream_t st) {
   const int n = P.g.n; const double h = P.g.h;
   const int64_t nk = P.g.nk;
   const double lo = 0.25, hi = 2.25, theta = theta_of(lo, hi), delta = 0.5 * (hi - lo), sigma = theta / delta;
-  double* rr = P.pw[1]; double* d0 = P.pw[2]; double* d1 = P.tu;   // scratch (tu is free at this point)
   const int gsz = grid_for(nk, BS, 4096);
   k_qk_cheb_init<<<gsz, BS, 0, st>>>(n, h, r, rr, d0, theta, done); etq_count_launch();
   double rho = 1.0 / sigma;
@@ -370,6 +370,15 @@ static void qk_cheb(const Problem& P, const double* r, double* out, int steps, c
     rho = rn;
     std::swap(din, dout);
   }
+}
+
+static void qk_cheb(const Problem& P, const double* r, double* out, int steps, const double* done, cudaStream_t st) {
+  qk_cheb_impl(P, r, out, steps, P.pw[1], P.pw[2], P.tu, done, st);   // scratch (tu is free at this point)
+}
+
+void qk_cheb_ws(const Problem& P, const double* r, double* out, int steps, double* ws, const double* done,
+                cudaStream_t st) {
+  qk_cheb_impl(P, r, out, steps, ws, ws + P.g.nk, ws + 2 * P.g.nk, done, st);
 }
 
 // z_p = -M_S^+ r_p for the two-field PCD (M2) or LSC (M3) approximation (NEXT-4, oracle.schur2)
@@ -407,6 +416,7 @@ etq_status schur2_apply(const Problem& P, etq_pc_kind kind, const double* r_p, d
 }
 
 etq_status oseen_precond_apply(const Problem& P, etq_pc_kind kind, const double* r, double* z, cudaStream_t st) {
+  NvtxRange nvtx_("Oseen block-triangular apply");
   const int64_t nu = P.n_u;
   const double* done = nullptr;
   if (kind == ETQ_PC_OSEEN_PCD1) {
@@ -540,6 +550,7 @@ static etq_status arnoldi_step(Problem& P, bool reduced, etq_pc_kind kind, cudaS
 
 etq_status gmres_run(Problem& P, bool reduced, etq_pc_kind kind, const double* b, double* x, double tol_abs,
                      int restart, int maxit, etq_report* rep, double* p0_res_norm) {
+  NvtxRange nvtx_("gmres (CGS2)");
   if (restart < 1 || maxit < 1) return ETQ_EINVAL;
   ETQ_TRY(gmres_alloc(P, restart, maxit + 1));
   cudaStream_t st = P.stream;
@@ -653,6 +664,7 @@ etq_status gmres_run(Problem& P, bool reduced, etq_pc_kind kind, const double* b
 
 // z = M_S1^{-1} r = Ap^{-1} F1 Mp^{-1} r on the Q1 block (test hook; no sign change)
 etq_status pcd_schur_apply(const Problem& P, const double* r, double* z, cudaStream_t st) {
+  NvtxRange nvtx_("PCD Schur apply");
   if (!P.pcd_ready) return ETQ_ENOTSETUP;
   qk_cheb(P, r, P.pw[0], P.params.mass_cheb_steps, nullptr, st);
   k_spmv1<<<grid_for(P.F1.nslices * 32, BS, 4096), BS, 0, st>>>(P.F1, P.pw[0], P.pw[1], 1.0, nullptr); etq_count_launch();
@@ -689,6 +701,7 @@ double host_norm(Problem& P, const double* v, int64_t n) {
 // bound[1] = sqrt(c^2 eta^2 ||b_red||^2 + ||g0 - B0 u1*||^2) (Prop 3.3, reading R16).
 etq_status two_stage_run(Problem& P, const double* b, double* x, double eta, double c, int restart, int maxit,
                          etq_report* r1, etq_report* r2, double* bound) {
+  NvtxRange nvtx_("two-stage PCD");
   if (!P.pcd_ready || !P.m1_ready) return ETQ_ENOTSETUP;
   cudaStream_t st = P.stream;
   double* bred;

@@ -343,6 +343,7 @@ etq_status picard_rhs_convection(const Problem& P, double* b) {
 // res[k] its true residual ||b_k - K_k x^k|| / ||b_k|| (host arrays, may be NULL).
 etq_status picard_run(Problem& P, int steps, double eta, double c, int restart, int maxit, double* x,
                       int* its, double* res, double* ms_total) {
+  NvtxRange nvtx_("Picard loop");
   if (!(P.oseen && P.wind == 2)) return ETQ_EINVAL;
   if (!P.pcd_ready || !P.m1_ready) return ETQ_ENOTSETUP;
   cudaStream_t st = P.stream;

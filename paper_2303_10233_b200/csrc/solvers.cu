@@ -142,6 +142,7 @@ void vec_lincomb3(double* w, const double* a, double ca, const double* b, double
 // <z_u, w_u> -> out_u and <z_p, w_p> -> out_p.
 etq_status precond_apply_ex(const Problem& P, etq_pc_kind kind, const double* r, double* z, const double* w,
                             double* out_u, double* out_p, const double* done, cudaStream_t st) {
+  NvtxRange nvtx_("preconditioner apply");
   const RedSite* site = &P.red[0];
   const int64_t nu = P.n_u, np = P.n_p;
   if (kind == ETQ_PC_OSEEN_M1 || kind == ETQ_PC_OSEEN_PCD1 || kind == ETQ_PC_OSEEN_M2 || kind == ETQ_PC_OSEEN_LSC)
@@ -180,7 +181,14 @@ etq_status precond_apply_ex(const Problem& P, etq_pc_kind kind, const double* r,
     // pressure branch on the aux stream, velocity V-cycle on the main stream
     ETQ_CHECK(cudaEventRecord(P.ev_fork, st));
     ETQ_CHECK(cudaStreamWaitEvent(P.aux, P.ev_fork, 0));
-    ETQ_TRY(mass_pc_apply_ex(P, r + nu, z + nu, site, 2, out_p, w ? w + nu : nullptr, done, P.aux));
+    if (P.plain) {   // plain Q2-Q1: z_p1 = Chebyshev-Jacobi(Q_k) r_p1, z_p0 = 0 (etq.h, etq_grid.enriched)
+      const int64_t nk = P.g.nk;
+      qk_cheb_ws(P, r + nu, z + nu, P.params.mass_cheb_steps, P.plain_w, done, P.aux);
+      ETQ_CHECK(cudaMemsetAsync(z + nu + nk, 0, sizeof(double) * (np - nk), P.aux));
+      if (out_p) launch_dot(z + nu, w + nu, np, const_cast<RedSite*>(site), 2, out_p, done, P.aux);
+    } else {
+      ETQ_TRY(mass_pc_apply_ex(P, r + nu, z + nu, site, 2, out_p, w ? w + nu : nullptr, done, P.aux));
+    }
     ETQ_TRY(vcycle_apply_ex(P, P.mg, r, z, site, 1, out_u, w, done, st));
     ETQ_CHECK(cudaEventRecord(P.ev_join, P.aux));
     ETQ_CHECK(cudaStreamWaitEvent(st, P.ev_join, 0));
@@ -236,7 +244,7 @@ static etq_status minres_iteration(Problem& P, etq_pc_kind kind, int cur, double
   k_minres_wx<<<grid_for(N), BS, 0, P.wside>>>(Z[1 - cur], W[1 - cur], W[cur], x, sc, N); etq_count_launch();
   ETQ_CHECK(cudaEventRecord(P.ev_wjoin, P.wside));
   // line 6-7: q = K (z / gamma), delta = <q, z / gamma>
-  launch_saddle_ex(P, false, Z[cur], Q, sc + S_INV_GAMMA, &P.red[0], 0, sc + S_DELTA, done, st);
+  launch_saddle_ex(P, P.plain, Z[cur], Q, sc + S_INV_GAMMA, &P.red[0], 0, sc + S_DELTA, done, st);
   ETQ_CHECK(cudaStreamWaitEvent(st, P.ev_wjoin, 0));
   // line 8
   k_minres_v<<<grid_for(N), BS, 0, st>>>(Q, V[cur], V[1 - cur], sc, N); etq_count_launch();
@@ -259,6 +267,7 @@ static etq_status minres_wx_tail(Problem& P, int cur, double* x, cudaStream_t st
 
 etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, double rtol, int maxit,
                       etq_report* rep) {
+  NvtxRange nvtx_("minres (Algorithm 1)");
   if (maxit < 1) return ETQ_EINVAL;
   ETQ_TRY(minres_alloc(P));
   cudaStream_t st = P.stream;
@@ -285,7 +294,7 @@ etq_status minres_run(Problem& P, etq_pc_kind kind, const double* b, double* x, 
   ETQ_CHECK(cudaMemsetAsync(V[0], 0, N * sizeof(double), st));
   ETQ_CHECK(cudaMemsetAsync(W[0], 0, N * sizeof(double), st));
   ETQ_CHECK(cudaMemsetAsync(W[1], 0, N * sizeof(double), st));
-  launch_saddle_ex(P, false, x, Q, nullptr, nullptr, 0, nullptr, nullptr, st);
+  launch_saddle_ex(P, P.plain, x, Q, nullptr, nullptr, 0, nullptr, nullptr, st);
   k_sub<<<grid_for(N), BS, 0, st>>>(V[1], b, Q, N); etq_count_launch();
   // line 3
   ETQ_TRY(precond_apply_ex(P, kind, V[1], Z[1], V[1], sc + S_DOT0, sc + S_DOT1, nullptr, st));

@@ -14,6 +14,7 @@ import re
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ETQ_LIB", os.path.join(_HERE, "libetq.so"))
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "etq.h")
+DEBUG_HEADER = os.path.join(os.path.dirname(_HERE), "include", "etq_debug.h")
 
 ETQ_OK, ETQ_NOT_CONVERGED = 0, 1
 PC_P1_EXACT, PC_P2_GMG, PC_OSEEN_M1, PC_OSEEN_PCD1, PC_P1_ITER, PC_P3, PC_OSEEN_M2, PC_OSEEN_LSC = 0, 1, 2, 3, 4, 5, 6, 7
@@ -26,7 +27,7 @@ class EtqError(RuntimeError):
 
 
 class Grid(C.Structure):
-    _fields_ = [("n", C.c_int32), ("bc", C.c_int32), ("storage", C.c_int32)]
+    _fields_ = [("n", C.c_int32), ("bc", C.c_int32), ("storage", C.c_int32), ("enriched", C.c_int32)]
 
 
 class Wind(C.Structure):
@@ -82,7 +83,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "etq_apply_saddle_f32": ([P, I32, VP, VP], I32),
         "etq_apply_vcycle_f32": ([P, VP, VP], I32),
         "etq_time_kernel": ([P, I32, I32, C.POINTER(D), C.POINTER(D)], I32),
-        "etq_set_option": ([I32, I32], I32),
+        "etq_debug_set_option": ([I32, I32], I32),
         "etq_status_string": ([I32], C.c_char_p),
         "etq_destroy": ([P], None),
     }
@@ -128,8 +129,8 @@ def est_minres(delta, gamma):
 
 
 def set_option(option: int, value: int):
-    """Process-wide implementation switch (etq_set_option); 0 = temporally blocked smoothing."""
-    _check(lib().etq_set_option(option, value), "etq_set_option")
+    """Process-wide A/B switch for tests and measurements (etq_debug_set_option, include/etq_debug.h)."""
+    _check(lib().etq_debug_set_option(option, value), "etq_debug_set_option")
 
 
 def status_string(s: int) -> str:
@@ -197,9 +198,11 @@ def make_params(**kw) -> PcParams:
 class Problem:
     """Owns an etq_problem (device matrices and workspaces)."""
 
-    def __init__(self, n: int, bc: int = 0, viscosity: float = 1.0, wind: int = 0, storage: int = 0):
+    def __init__(self, n: int, bc: int = 0, viscosity: float = 1.0, wind: int = 0, storage: int = 0,
+                 enriched: bool = True):
+        """enriched=False: plain Taylor-Hood Q2-Q1 on the same mesh (etq_grid.enriched = 0)."""
         h = C.c_void_p()
-        g = Grid(n, bc, storage)
+        g = Grid(n, bc, storage, 1 if enriched else 0)
         w = Wind(wind)
         _check(lib().etq_assemble(C.byref(g), viscosity, C.byref(w), _stream(), C.byref(h)), "etq_assemble")
         self.h = h

@@ -9,10 +9,15 @@ from paper_2303_10233_b200 import etq
 
 def test_library_exports_every_header_symbol():
     lib = etq.lib()
-    names = etq.header_functions()
+    names = etq.header_functions() + etq.header_functions(etq.DEBUG_HEADER)
     assert len(names) >= 15
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
+
+
+def test_ab_switches_are_not_in_the_product_header():
+    assert "etq_set_option" not in etq.header_functions()
+    assert etq.header_functions(etq.DEBUG_HEADER) == ["etq_debug_set_option"]
 
 
 def test_binding_mirrors_header_names():
@@ -53,3 +58,11 @@ def test_est_minres_host_matches_oracle():
             assert np.isnan(got)
         else:
             assert abs(got - ref) <= 1e-10 * max(1.0, abs(ref))
+
+
+def test_nvtx_ranges_compiled_in():
+    """Solver phases and kernel families carry NVTX ranges (SURVEY §5 tracing)."""
+    blob = open(etq.LIB_PATH, "rb").read()
+    for name in (b"minres (Algorithm 1)", b"V-cycle", b"Pi C Pi (Chebyshev-SGS)", b"saddle apply", b"gmres (CGS2)",
+                 b"two-stage PCD", b"exact M_Q solve", b"etq_precond_setup"):
+        assert name in blob, name

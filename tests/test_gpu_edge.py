@@ -195,3 +195,24 @@ def test_binding_rejects_wrong_lengths():
         P.minres_solve_host(etq.PC_P2_GMG, np.zeros(P.N - 1), np.zeros(P.N))
     with pytest.raises(ValueError):
         P.minres_solve_host(etq.PC_P2_GMG, np.zeros(P.N, dtype=np.float32), np.zeros(P.N))
+
+
+def test_nan_input_reports_enan():
+    """A NaN in the right-hand side reaches the scalar recurrences: MINRES (Algorithm 1 line 3) and
+    GMRES return ETQ_ENAN (-7) instead of iterating on garbage."""
+    P = etq.Problem(8)
+    P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.01))
+    b = zeros(P.N); P.build_rhs(b)
+    b[5] = float("nan")
+    x = zeros(P.N)
+    with pytest.raises(etq.EtqError) as e:
+        P.minres_solve(etq.PC_P2_GMG, b, x, rtol=1e-8, maxit=50)
+    assert e.value.status == -7
+    Q = etq.Problem(8, bc=0, viscosity=0.01, wind=1)
+    Q.precond_setup(etq.PC_OSEEN_M1, etq.make_params(coarse_n=2, cheb_sgs_lo=0.01))
+    bq = zeros(Q.N); Q.build_rhs(bq)
+    bq[Q.n_u + 3] = float("nan")
+    xq = zeros(Q.N)
+    with pytest.raises(etq.EtqError) as e:
+        Q.gmres_solve(etq.PC_OSEEN_M1, bq, xq, rtol=1e-6, restart=20, maxit=40)
+    assert e.value.status == -7

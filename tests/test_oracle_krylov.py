@@ -168,3 +168,22 @@ def test_gmres_matches_brute_force_and_monotone():
     Ainv = np.linalg.inv(A)
     x, rep = krylov.gmres(lambda v: A @ v, b, lambda v: Ainv @ v, tol_abs=1e-10, restart=10, maxit=10)
     assert rep.iterations == 1
+
+
+def test_plain_q2q1_minres_matches_dense_solution():
+    """Plain Taylor-Hood (the conservation contrast): MINRES with the oracle's
+    diag(V-cycle, Chebyshev-Jacobi(Q_k)) preconditioner reaches the least-squares solution of the
+    reduced system [A B1^T; B1 0] (unique up to the constant Q1 pressure, compared mean-free)."""
+    n = 8
+    s = fem.assemble_system(n)
+    g = s.g
+    K, b = precond.plain_system(s)
+    x, rep = krylov.minres(lambda v: K @ v, b, precond.StokesP2Plain(s), rtol=1e-12, maxit=500)
+    assert rep.converged
+    xd = np.linalg.lstsq(K.toarray(), b, rcond=None)[0]
+    for v in (x, xd):
+        v[g.n_u:] -= v[g.n_u:].mean()
+    assert np.abs(x - xd).max() <= 1e-8 * np.abs(xd).max()
+    # and the plain solution violates element-wise mass conservation (S:606)
+    g0 = s.b[g.n_u + g.n_k:]
+    assert np.abs(s.B0 @ x[:g.n_u] - g0).max() > 1e-4
