@@ -296,6 +296,15 @@ def run_ours(args):
         kern[names[w]] = {"ms": k_ms, "algorithmic_bytes": k_bytes,
                           "GB_per_s": (k_bytes / (k_ms * 1e-3) / 1e9) if k_bytes > 0 else None,
                           "frac_of_peak": (k_bytes / (k_ms * 1e-3) / 1e9 / peak) if k_bytes > 0 else None}
+    # one whole MINRES iteration (the step / its iteration count): saddle apply (16 N), P2 apply (both
+    # branches), the <z, v> dot inputs read by the P2 epilogues (8 N), lines 8 and 16-17 of Algorithm 1
+    # (k_minres_v: q, v, v_prev in, v_prev out = 32 N; k_minres_wx: z, w, w_prev, x in, w_prev, x out
+    # = 48 N).  Algorithmic bytes (each kernel's vectors once); the pressure vectors are L2-sized
+    it_bytes = 16.0 * P.N + kern[names[4]]["algorithmic_bytes"] + 8.0 * P.N + 80.0 * P.N
+    it_ms = ms / its if its else float("nan")
+    kern["whole MINRES iteration (solve time / iterations)"] = {
+        "ms": it_ms, "algorithmic_bytes": it_bytes, "GB_per_s": it_bytes / (it_ms * 1e-3) / 1e9,
+        "frac_of_peak": it_bytes / (it_ms * 1e-3) / 1e9 / peak}
     # the saddle apply is matrix-free (class stencils): its algorithmic bytes are x in + y out; the
     # stored-operator (CSR model) bytes it replaces are reported beside them
     nnz = 192 * n * n - 336 * n + 186

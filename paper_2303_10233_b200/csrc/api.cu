@@ -19,6 +19,7 @@ bool g_sgs_high_prio = false;       // etq_set_option(4): Chebyshev-SGS kernels 
 bool g_tail_sm = true;              // etq_set_option(5): shared-memory matrix-free coarse-level tail
 bool g_saddle_tile = true;          // etq_set_option(6): shared-memory tiled matrix-free saddle apply
 bool g_sgs_pdl = true;              // etq_set_option(7): programmatic dependent launches in the SGS chain
+bool g_cheb_tile3 = true;           // etq_debug_set_option(12): smoother with the residual in registers (k_cheb_tile3)
 bool g_cheb_tile2 = true;           // etq_set_option(11): leaner temporally blocked smoother (k_cheb_tile2)
 bool g_sgs_planar = false;          // etq_set_option(10): Chebyshev-SGS on parity planes with TMA windows
 bool g_vc_pdl = true;               // etq_set_option(8): programmatic dependent launches in the V-cycle
@@ -698,7 +699,9 @@ etq_status etq_time_kernel(etq_problem* h, int32_t which, int32_t reps, double* 
                : 12.0 * nnz_all - 4.0 * P.Lv.nnz_implicit - 8.0 * P.Lv.nnz_implicit_vals + 4.0 * P.Lv.nslices * SELL_C + 16.0 * P.N;
       break;
     case 1: *bytes = cheb_step_bytes(P.mg.lv[0]); break;
-    case 2: case 4: *bytes = vcycle_bytes(P.mg); break;
+    case 2: *bytes = vcycle_bytes(P.mg); break;
+    case 3: *bytes = mass_pc_bytes(P); break;
+    case 4: *bytes = vcycle_bytes(P.mg) + mass_pc_bytes(P); break;   // both branches
     case 5: *bytes = 8.0 * nnz_all + 4.0 * P.Lv.nslices * SELL_C + 8.0 * P.N; break;
     case 6: *bytes = vcycle_bytes_f32(P.mg); break;
     case 10: *bytes = 32.0 * (double)P.n_p; break;            // r, y, yp in; out
@@ -722,6 +725,7 @@ etq_status etq_debug_set_option(int32_t option, int32_t value) {
   if (option == 9) { g_prolong_tile = value != 0; return ETQ_OK; }
   if (option == 10) { g_sgs_planar = value != 0; return ETQ_OK; }
   if (option == 11) { g_cheb_tile2 = value != 0; return ETQ_OK; }
+  if (option == 12) { g_cheb_tile3 = value != 0; return ETQ_OK; }
   return ETQ_EINVAL;
 }
 

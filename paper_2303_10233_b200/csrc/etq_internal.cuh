@@ -54,6 +54,7 @@ extern bool g_tail_sm;                    // api.cu; etq_set_option(5)
 extern bool g_saddle_tile;                // api.cu; etq_set_option(6)
 extern bool g_sgs_pdl;                    // api.cu; etq_set_option(7)
 extern bool g_sgs_planar;                 // api.cu; etq_set_option(10)
+extern bool g_cheb_tile3;                 // api.cu; etq_debug_set_option(12)
 extern bool g_cheb_tile2;                 // api.cu; etq_set_option(11)
 extern bool g_vc_pdl;                     // api.cu; etq_set_option(8)
 extern bool g_prolong_tile;               // api.cu; etq_set_option(9)
@@ -298,7 +299,8 @@ struct Problem {
   double* pw[3] = {nullptr, nullptr, nullptr};   // n_k work vectors of the PCD chain
   double* tu = nullptr;                       // [n_u] r_u - B^T z_p
   // GMRES workspace
-  double* gV = nullptr; int gm = 0;           // (m+1) x N Arnoldi basis
+  double* gV = nullptr; int gm = 0;           // (m+1) x N Arnoldi basis (stride gld)
+  int64_t gld = 0;                            // basis stride: N rounded up to 32 elements
   double* gH = nullptr;                       // (m+1) x m Hessenberg (column-major)
   double* gsm = nullptr;                      // cs[m], sn[m], g[m+1], y[m], hh[m+1]
   double* gW = nullptr; double* gZ = nullptr; double* gT = nullptr; double* gU = nullptr;
@@ -393,6 +395,7 @@ etq_status lanczos_sgs_lo(Problem& P, const double* v0, int steps, double* lam);
 int64_t etq_launch_total();
 void cheb_step_level0(const Problem& P, const double* d_in, double* d_out, cudaStream_t st);
 double vcycle_bytes(const Hierarchy& H);
+double mass_pc_bytes(const Problem& P);
 double cheb_step_bytes(const Level& L);
 void sgs_step_bench(const Problem& P, const double* r, const double* y, const double* yp, double* out,
                     cudaStream_t st);

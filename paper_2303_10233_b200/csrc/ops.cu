@@ -849,6 +849,218 @@ __global__ void __launch_bounds__(CT_THREADS, 2) k_cheb_tile2(ChebTileArgs a) {
   else ct2_body<POST, false>(a, ct_sm, ct_sm + CT_ARR, ct_sm + 2 * CT_ARR, i0, j0, off);
 }
 
+// k_cheb_tile2 with the residual in registers (k_cheb_tile3).  ncu on k_cheb_tile2: the shared-memory
+// pipe is the bound (20.9 M wavefronts per finest pass ~ 72 us at one wavefront per clock per SM;
+// short-scoreboard and MIO-throttle stalls lead), not the fp64 pipe (~30 us).  Here every thread
+// keeps ONE output map for all three steps - lane L owns window columns 2 + 2L, 3 + 2L, warp w the
+// rows 2 + 8w .. 9 + 8w (the widest step region [2, 66)^2) - so:
+//   * r lives in registers (no shared r array, no r load / store per row),
+//   * the step's own d_k is the centre of the register window (no din load),
+//   * the tile's outputs are written straight from the last step's row loop (no trailing tile
+//     passes and their barriers); x = d0 + d1 + d2 (resp. x + d0 + d1) is summed there from the
+//     two earlier d arrays in the same order as k_cheb_tile2 (bitwise-identical outputs).
+// Per row and lane: 3 window loads + 1 d store (step 3: + 2 loads on tile rows) instead of 7.
+// Lanes / rows outside a step's region compute finite garbage from unused window entries that no
+// valid output reads (each region lies inside the previous one shrunk by the stencil radius 2).
+template <int S, int MODE, bool EDGE, int FIN, int t>
+__device__ __forceinline__ void ct3_row(const ChebTileArgs& a, int i0, int j0, const double* __restrict__ v,
+                                        double* __restrict__ dout, const double* __restrict__ e0,
+                                        const double* __restrict__ e1, double c1, double c2, int jb, int ii,
+                                        int lane, double (&win)[5][6], double (&rr)[CT_STRIP][2], double& dot) {
+  const int m = a.so.m;
+  const int jj = jb + t;
+  if (jj + 2 < CT_R) ct_load_row<EDGE>(v, ii, jj + 2, i0 + ii, j0 + jj + 2, m, win[(t + 4) % 5]);
+  if (jj < S || jj >= CT_R - S) return;               // warp-uniform
+  const int j = j0 + jj;
+  if (EDGE && (j < 0 || j >= m)) return;
+  constexpr int RSLOT = (t + 2) % 5;
+  double qq[2];
+  if ((t & 1) == 0) {                                  // jj even (jb even): classes 0 (i even), 1 (i odd)
+    qq[0] = ct_tap_sum<0, 0, RSLOT, true>(a.so, win);
+    qq[1] = ct_tap_sum<1, 1, RSLOT, true>(a.so, win);
+  } else {
+    qq[0] = ct_tap_sum<2, 0, RSLOT, true>(a.so, win);
+    qq[1] = ct_tap_sum<3, 1, RSLOT, true>(a.so, win);
+  }
+  constexpr int C0 = (t & 1) * 2;
+  const int i = i0 + ii;
+  const int base = ii + CT_R * jj;
+  double outd[2], dd[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int ik = i + k;
+    const bool dir = EDGE && (ik == 0 || j == 0 || ik == m - 1 || j == m - 1);
+    dd[k] = win[RSLOT][2 + k];                         // d_k at the output (interior: unmasked)
+    if (EDGE && dir) {
+      dd[k] = v[base + k];                             // Dirichlet centre: the unmasked value
+      qq[k] = fma(1.0, dd[k], 0.0);                    // identity row
+    }
+    const double di = dir ? 1.0 : c_ct_dcls[C0 + k];
+    rr[t][k] = rr[t][k] - qq[k];
+    if (MODE == 1) outd[k] = di * rr[t][k] * a.itheta;
+    else outd[k] = c1 * dd[k] + c2 * (di * rr[t][k]);
+  }
+  if (FIN == 0) {
+    *reinterpret_cast<double2*>(dout + base) = make_double2(outd[0], outd[1]);
+    return;
+  }
+  // last step: the tile's outputs (tile rows / columns [CT_H, CT_H + CT_T) only)
+  if (jj < CT_H || jj >= CT_H + CT_T || ii < CT_H || ii >= CT_H + CT_T) return;
+  const double2 p0 = *reinterpret_cast<const double2*>(e0 + base);
+  const double2 p1 = *reinterpret_cast<const double2*>(e1 + base);
+  const double q0[2] = {p0.x, p0.y}, q1[2] = {p1.x, p1.y};
+  const int64_t g = (int64_t)blockIdx.y * a.nq + i + (int64_t)m * j;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (EDGE && i + k >= m) continue;
+    if (FIN == 1) {                                    // pre: r out, x3 = ((0 + d0) + d1) + d2
+      a.r_out[g + k] = rr[t][k];
+      a.x_out[g + k] = ((0.0 + q0[k]) + q1[k]) + dd[k];
+    } else {                                           // post: x = (x + d0) + d1, d2 = MODE-0 output
+      const double x = (q0[k] + q1[k]) + dd[k];
+      if (FIN == 3) {                                  // finest: z = x + d2, <z, w>
+        const double z = x + outd[k];
+        a.z_out[g + k] = z;
+        dot += a.dot_with ? z * __ldg(a.dot_with + g + k) : z;
+      } else {
+        a.d_out[g + k] = outd[k];
+        a.x_out[g + k] = x;
+      }
+    }
+  }
+}
+
+template <int S, int MODE, bool EDGE, int FIN, int... Ts>
+__device__ __forceinline__ void ct3_rows(const ChebTileArgs& a, int i0, int j0, const double* v, double* dout,
+                                         const double* e0, const double* e1, double c1, double c2, int jb, int ii,
+                                         int lane, double (&win)[5][6], double (&rr)[CT_STRIP][2], double& dot,
+                                         std::integer_sequence<int, Ts...>) {
+  (ct3_row<S, MODE, EDGE, FIN, Ts>(a, i0, j0, v, dout, e0, e1, c1, c2, jb, ii, lane, win, rr, dot), ...);
+}
+
+// FIN: 0 = intermediate step (d out to shared memory), 1 = last pre step, 2 = last post step
+// (x, d out), 3 = last post step of the finest level (z out + dot)
+template <int S, int MODE, bool EDGE, int FIN>
+__device__ __forceinline__ void ct3_step(const ChebTileArgs& a, int i0, int j0, const double* v, double* dout,
+                                         const double* e0, const double* e1, double c1, double c2,
+                                         double (&rr)[CT_STRIP][2], double& dot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int jb = 2 + CT_STRIP * warp;
+  const int ii = 2 + 2 * lane;
+  double win[5][6];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) ct_load_row<EDGE>(v, ii, jb - 2 + r, i0 + ii, j0 + jb - 2 + r, a.so.m, win[r]);
+  ct3_rows<S, MODE, EDGE, FIN>(a, i0, j0, v, dout, e0, e1, c1, c2, jb, ii, lane, win, rr, dot,
+                               std::make_integer_sequence<int, CT_STRIP>{});
+}
+
+static_assert(2 + 2 * 31 + 3 < CT_R && 2 + CT_STRIP * (CT_THREADS / 32) == CT_R - 2, "tile3 output map");
+
+template <int POST, bool EDGE>
+__device__ __forceinline__ void ct3_body(const ChebTileArgs& a, double* A0, double* A1, double* A2, int i0, int j0,
+                                         int64_t off) {
+  const int m = a.so.m;
+  const double* __restrict__ b = a.b + off;
+  const double* __restrict__ xin = POST ? a.x_in + off : nullptr;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // ---- r = b at the thread's own outputs (registers; 16-byte coalesced rows), issued first
+  double rr[CT_STRIP][2];
+  {
+    const int i = i0 + 2 + 2 * lane;
+#pragma unroll
+    for (int t = 0; t < CT_STRIP; ++t) {
+      const int j = j0 + 2 + CT_STRIP * warp + t;
+      const int64_t g = (int64_t)m * j + i;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const bool in = !EDGE || (j >= 0 && j < m && i + e >= 0 && i + e < m);
+        rr[t][e] = in ? __ldg(b + g + e) : 0.0;
+      }
+    }
+  }
+  // ---- staging of the first step's window: pre d0 = D^-1 b / theta (k_cheb_init) into A0; post x
+  //      into A0.  Column pairs in window order, all loads of a group before its stores
+  constexpr int PR = CT_R / 2, NP = PR * CT_R, NK = (NP + CT_THREADS - 1) / CT_THREADS, G = 5;
+#pragma unroll
+  for (int k0 = 0; k0 < NK; k0 += G) {
+    double lv[G][2];
+#pragma unroll
+    for (int kk = 0; kk < G; ++kk) {
+      const int p = tid + CT_THREADS * (k0 + kk);
+      const int jj = p / PR, pp = p - PR * jj;
+      const int j = j0 + jj, i = i0 + 2 * pp;
+      const int64_t g = (int64_t)m * j + i;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const bool in = (k0 + kk < NK) && p < NP && (!EDGE || (j >= 0 && j < m && i + e >= 0 && i + e < m));
+        lv[kk][e] = in ? __ldg((POST ? xin : b) + g + e) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < G; ++kk) {
+      const int p = tid + CT_THREADS * (k0 + kk);
+      if (k0 + kk >= NK || p >= NP) continue;
+      const int jj = p / PR, pp = p - PR * jj;
+      const int idx = 2 * pp + CT_R * jj;
+      if (POST) {
+        *reinterpret_cast<double2*>(A0 + idx) = make_double2(lv[kk][0], lv[kk][1]);
+      } else {
+        const int odd = jj & 1;
+        double dv[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double di = c_ct_dcls[e + 2 * odd];
+          if (EDGE) {
+            const int j = j0 + jj, ie = i0 + 2 * pp + e;
+            if (ie == 0 || j == 0 || ie == m - 1 || j == m - 1) di = 1.0;
+            const bool in = ie >= 0 && j >= 0 && ie < m && j < m;
+            dv[e] = in ? di * lv[kk][e] * a.itheta : 0.0;
+          } else {
+            dv[e] = di * lv[kk][e] * a.itheta;
+          }
+        }
+        *reinterpret_cast<double2*>(A0 + idx) = make_double2(dv[0], dv[1]);
+      }
+    }
+  }
+  __syncthreads();
+  double dot = 0.0;
+  if (!POST) {
+    ct3_step<2, 0, EDGE, 0>(a, i0, j0, A0, A1, nullptr, nullptr, a.c1[0], a.c2[0], rr, dot);   // d1
+    __syncthreads();
+    ct3_step<4, 0, EDGE, 0>(a, i0, j0, A1, A2, nullptr, nullptr, a.c1[1], a.c2[1], rr, dot);   // d2
+    __syncthreads();
+    pdl_trigger();
+    ct3_step<6, 0, EDGE, 1>(a, i0, j0, A2, nullptr, A0, A1, 0.0, 0.0, rr, dot);               // r, x3
+  } else {
+    ct3_step<2, 1, EDGE, 0>(a, i0, j0, A0, A1, nullptr, nullptr, 0.0, 0.0, rr, dot);          // r0, d0
+    __syncthreads();
+    ct3_step<4, 0, EDGE, 0>(a, i0, j0, A1, A2, nullptr, nullptr, a.c1[0], a.c2[0], rr, dot);   // d1
+    __syncthreads();
+    pdl_trigger();
+    if (a.z_out) {
+      ct3_step<6, 0, EDGE, 3>(a, i0, j0, A2, nullptr, A0, A1, a.c1[1], a.c2[1], rr, dot);      // z = x + d2
+      if (a.dot_out) { double v1[1] = {dot}; reduce_finish<1>(v1, a.site, a.slot, a.dot_out, true); }
+    } else {
+      ct3_step<6, 0, EDGE, 2>(a, i0, j0, A2, nullptr, A0, A1, a.c1[1], a.c2[1], rr, dot);      // x, d2
+    }
+  }
+}
+
+template <int POST>
+__global__ void __launch_bounds__(CT_THREADS, 2) k_cheb_tile3(ChebTileArgs a) {
+  pdl_wait();
+  if (is_done(a.done)) return;
+  extern __shared__ __align__(16) double ct_sm[];
+  const int m = a.so.m;
+  const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
+  const int i0 = tx * CT_T - CT_H, j0 = ty * CT_T - CT_H;
+  const int64_t off = (int64_t)blockIdx.y * a.nq;
+  const bool edge = i0 < 3 || j0 < 3 || i0 + CT_R > m - 3 || j0 + CT_R > m - 3;   // block-uniform
+  if (edge) ct3_body<POST, true>(a, ct_sm, ct_sm + CT_ARR, ct_sm + 2 * CT_ARR, i0, j0, off);
+  else ct3_body<POST, false>(a, ct_sm, ct_sm + CT_ARR, ct_sm + 2 * CT_ARR, i0, j0, off);
+}
+
 // r = b - A x ; d = D^{-1} r / theta  (start of post-smoothing), NC components
 template <int NC>
 __global__ void __launch_bounds__(BS, SPMV_MINB) k_post_residual(Sell A, const double* dinv, int nq, const double* b,
@@ -1382,17 +1594,30 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
   const double* yps = use_yp ? a.yp : a.r;
   // ---- one staging phase: y (window) and y_prev (tile) by cp.async in row-major order (each
   //      warp reads 32 consecutive words of a global row; the shared destinations are the parity
-  //      planes / the tile-ordered Q), r into registers in plane order (the thread's own entries)
+  //      planes / the tile-ordered Q), r into registers in plane order (the thread's own entries).
+  //      Window: thread t stages column t mod 64 of rows t / 64 + 8q (plane and parity fixed per
+  //      thread, addresses incremented)
   const int tid = i + SGS_TX * ty;
-#pragma unroll
-  for (int q = 0; q < SGS_W * SGS_W / (SGS_TX * SGS_TY); ++q) {
-    const int idx = tid + q * SGS_TX * SGS_TY;
-    const int la = idx % SGS_W, lc = idx / SGS_W, ga = A0 + la, gc = C0 + lc;
-    const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
-    const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
-    const int pl = ((la & 1) + 2 * (lc & 1)) * SGS_PL + (lc >> 1) * SGS_P + (la >> 1);
-    cp_async8(V + pl, ys + (inv ? ga + (int64_t)n1 * gc : 0), inv && a.y);
-    cp_async8(Cc + pl, ys + nk + (inc ? ga + (int64_t)n * gc : 0), inc && a.y);
+  {
+    constexpr int RSTEP = SGS_TX * SGS_TY / SGS_W;           // 8 window rows per pass
+    static_assert(SGS_TX * SGS_TY % SGS_W == 0 && RSTEP % 2 == 0, "fixed parity per thread");
+    const int la = tid & (SGS_W - 1), lc0 = tid / SGS_W;
+    const int ga = A0 + la;
+    double* vdst = V + ((la & 1) + 2 * (lc0 & 1)) * SGS_PL + (lc0 >> 1) * SGS_P + (la >> 1);
+    double* cdst = Cc + (vdst - V);
+    const double* vsrc = ys + ga + (int64_t)n1 * (C0 + lc0);
+    const double* csrc = ys + nk + ga + (int64_t)n * (C0 + lc0);
+    const int64_t dv = (int64_t)RSTEP * n1, dc = (int64_t)RSTEP * n;
+    const bool xin_v = IN || (ga >= 0 && ga <= n), xin_c = IN || (ga >= 0 && ga < n);
+#pragma unroll 4
+    for (int q = 0; q < SGS_W / RSTEP; ++q) {
+      const int gc = C0 + lc0 + RSTEP * q;
+      const bool inv = IN || (xin_v && gc >= 0 && gc <= n);
+      const bool inc = IN || (xin_c && gc >= 0 && gc < n);
+      cp_async8(vdst, inv ? vsrc : ys, inv && a.y);
+      cp_async8(cdst, inc ? csrc : ys, inc && a.y);
+      vdst += (RSTEP / 2) * SGS_P; cdst += (RSTEP / 2) * SGS_P; vsrc += dv; csrc += dc;
+    }
   }
   if (use_yp) {
     for (int idx = tid; idx < SGS_TTX * SGS_TTY; idx += SGS_TX * SGS_TY) {
@@ -1865,6 +2090,7 @@ __device__ __forceinline__ void st_vel_row(const SaddleTileArgs& a, const StSmem
   double q[2];
   q[0] = st_lap<2 * PJ, 2, RS>(a.so, win);
   q[1] = st_lap<2 * PJ + 1, 3, RS>(a.so, win);
+  double out[2] = {0.0, 0.0};
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int i = I0 + 2 * L + k;
@@ -1894,8 +2120,23 @@ __device__ __forceinline__ void st_vel_row(const SaddleTileArgs& a, const StSmem
       }
     }
     ax *= sc;
-    a.y[(int64_t)C * a.nq + i + (int64_t)m * j] = ax;
+    if (EDGE) a.y[(int64_t)C * a.nq + i + (int64_t)m * j] = ax;
+    out[k] = ax;
     if (a.dot_out) dot += ax * (sc * raw);
+  }
+  if (!EDGE) {
+    // 16-byte stores of aligned pairs (a warp row = 512 contiguous bytes, no half-written
+    // sectors); rows whose pair addresses are only 8-byte aligned (warp-uniform: lanes are 16 B
+    // apart) pair lane L's odd column with lane L + 1's even one
+    double* yr = a.y + (int64_t)C * a.nq + I0 + (int64_t)m * j + 2 * L;
+    if ((reinterpret_cast<uintptr_t>(yr) & 15) == 0) {
+      *reinterpret_cast<double2*>(yr) = make_double2(out[0], out[1]);
+    } else {
+      const double nx = __shfl_down_sync(0xffffffffu, out[0], 1);
+      if (L == 0) yr[0] = out[0];
+      if (L < 31) *reinterpret_cast<double2*>(yr + 1) = make_double2(out[1], nx);
+      else yr[1] = out[1];
+    }
   }
   (void)n;
 }
@@ -2807,6 +3048,17 @@ static void launch_cheb_tile(const Level& lv, bool post, const double* b, const 
   a.done = done;
   a.z_out = z_out; a.dot_with = dot_with; a.site = site ? *site : RedSite{}; a.slot = slot; a.dot_out = dot_out;
   dim3 grid(a.tiles_x * a.tiles_x, 2);
+  if (lv.ct2 && g_cheb_tile3) {
+    static bool smem3 = false;
+    if (!smem3) {
+      cudaFuncSetAttribute(k_cheb_tile3<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM);
+      cudaFuncSetAttribute(k_cheb_tile3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, CT_SMEM);
+      smem3 = true;
+    }
+    if (post) launch_pdl(k_cheb_tile3<1>, grid, dim3(CT_THREADS), CT_SMEM, st, pdl, a);
+    else launch_pdl(k_cheb_tile3<0>, grid, dim3(CT_THREADS), CT_SMEM, st, pdl, a);
+    return;
+  }
   if (lv.ct2 && g_cheb_tile2) {
     static bool smem2 = false;
     if (!smem2) {
@@ -3379,11 +3631,23 @@ double vcycle_bytes(const Hierarchy& H) {
       for (int k = 0; k < deg - 1; ++k)                      // post steps
         b += mat + v * (3 + (k == deg - 2 ? 2 : 3));
     }
-    if (l == 0) b += 2 * v + v;                              // final: x + d -> z
+    if (l == 0) b -= tiled ? v : 0.0;                        // tiled finest post pass: z out, no x / d
+    if (l == 0 && !tiled) b += 2 * v + v;                    // final: x + d -> z
   }
   const Level& C = H.lv[L - 1];
   b += 8.0 * (double)C.g.nq * C.g.nq + 4.0 * 8.0 * C.g.nq;  // dense coarse solve
   return b;
+}
+
+// Pi C Pi (mass_pc_apply_ex): k^T r (r in), step 0 (r in, out), step 1 (r, y in, out), steps
+// 2..m-1 (r, y, y_prev in, out), projection (y in, z out); 640 n_p bytes at m = 20
+double mass_pc_bytes(const Problem& P) {
+  const double np = (double)P.g.nk + P.g.n0;
+  const int m = P.pm.m;
+  if (m < 1) return 0.0;
+  double b = 8.0 * np + 16.0 * np;
+  if (m >= 2) b += 24.0 * np + 32.0 * np * (m - 2);
+  return b + 16.0 * np;
 }
 
 // fp32 V-cycle algorithmic bytes: 8 B per stored entry + 4 B index... i.e. values 4 B + index 4 B,

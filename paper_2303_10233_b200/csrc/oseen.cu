@@ -160,47 +160,44 @@ __global__ void k_fill(double* x, int64_t n, double v, const double* done) {
 }
 
 // ---------------------------------------------------------------- GMRES kernels
-__global__ void k_copy_vj(const double* V, int64_t N, const double* sc, double* T) {
+__global__ void k_copy_vj(const double* V, int64_t N, int64_t ld, const double* sc, double* T) {
   const int64_t j = (int64_t)sc[G_J];
-  const double* vj = V + j * N;
+  const double* vj = V + j * ld;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
     T[i] = vj[i];
 }
 
-// h_i = <V_i, W>, i = 0..j (j from device).  Each warp owns segments of MD_SEG consecutive
-// elements (grid-stride over segments): the segment of W stays in registers, and every basis
-// vector is streamed with MD_KV independent coalesced loads per lane (memory-level parallelism),
-// summed, warp-reduced, and the warp's running total for vector i kept by lane i mod 32.  W and
-// each V_i are read once.  The warps' totals are combined in warp order in shared memory, the
-// blocks' in block order by the last block: deterministic for a fixed grid.
-constexpr int MD_KV = 8, MD_SEG = 32 * MD_KV, MD_MAXV = 64;
-__global__ void __launch_bounds__(BS) k_multidot(const double* V, int64_t N, const double* W, const double* sc,
-                                                 double* h, RedSite site) {
-  const int nv = min((int)sc[G_J] + 1, MD_MAXV);
+// CGS2 (reading R18) in three passes over the basis instead of four:
+//   A  h = V^T w                                   (k_multidot)
+//   B  w <- w - V h, then h' = V^T w               (k_cgs_mid: the segment of every V_i is read
+//                                                   twice by the same warp, the second time from L2)
+//   C  w <- w - V h', ||w||^2                      (k_cgs_last)
+// The basis vectors are stored with a stride ld (N rounded up to 32 elements) so that every V_i is
+// 256-byte aligned and is streamed with 128-bit loads.  Dot products: each warp owns segments of
+// CG_SEG consecutive elements (grid-stride over segments), lane l the pairs 2l + 64k; per segment
+// and vector the lane sums its CG_K pairs, the warp sums its lanes (shuffles) and lane (i mod 32)
+// keeps the warp's running total of vector i; warps are combined in warp order in shared memory,
+// blocks in block order by the last block: deterministic for a fixed grid.
+constexpr int CG_K = 4, CG_SEG = 64 * CG_K, MD_MAXV = 64;
+
+__device__ __forceinline__ void cg_ld(const double* __restrict__ p, int64_t e, int64_t N, double& a, double& b) {
+  if (e + 1 < N) { const double2 t = __ldg(reinterpret_cast<const double2*>(p + e)); a = t.x; b = t.y; }
+  else { a = e < N ? __ldg(p + e) : 0.0; b = 0.0; }
+}
+__device__ __forceinline__ void cg_ldw(const double* p, int64_t e, int64_t N, double& a, double& b) {
+  if (e + 1 < N) { const double2 t = *reinterpret_cast<const double2*>(p + e); a = t.x; b = t.y; }
+  else { a = e < N ? p[e] : 0.0; b = 0.0; }
+}
+__device__ __forceinline__ void cg_st(double* p, int64_t e, int64_t N, double a, double b) {
+  if (e + 1 < N) *reinterpret_cast<double2*>(p + e) = make_double2(a, b);
+  else if (e < N) p[e] = a;
+}
+
+// running totals of a warp (lane i mod 32 holds vector i's) -> h[0..nv) through the grid reduction
+__device__ __forceinline__ void md_finish(double t0, double t1, int nv, double* h, RedSite site) {
   __shared__ double part[BS / 32][MD_MAXV];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t nseg = (N + MD_SEG - 1) / MD_SEG;
-  const int64_t nw = (int64_t)gridDim.x * (BS / 32);
-  double t0 = 0.0, t1 = 0.0;   // this lane's running totals of vectors lane and lane + 32
-  for (int64_t sg = (int64_t)blockIdx.x * (BS / 32) + warp; sg < nseg; sg += nw) {
-    const int64_t e0 = sg * MD_SEG + lane;
-    double w[MD_KV];
-#pragma unroll
-    for (int k = 0; k < MD_KV; ++k) { const int64_t e = e0 + 32 * k; w[k] = e < N ? W[e] : 0.0; }
-#pragma unroll 2
-    for (int i = 0; i < nv; ++i) {
-      const double* vi = V + (int64_t)i * N;
-      double v[MD_KV];
-#pragma unroll
-      for (int k = 0; k < MD_KV; ++k) { const int64_t e = e0 + 32 * k; v[k] = e < N ? vi[e] : 0.0; }
-      double sv = 0.0;
-#pragma unroll
-      for (int k = 0; k < MD_KV; ++k) sv = fma(v[k], w[k], sv);
-      sv = warp_sum(sv);
-      if (lane == (i & 31)) { if (i < 32) t0 += sv; else t1 += sv; }
-    }
-  }
   if (lane < nv) part[warp][lane] = t0;
   if (lane + 32 < nv) part[warp][lane + 32] = t1;
   __syncthreads();
@@ -225,10 +222,110 @@ __global__ void __launch_bounds__(BS) k_multidot(const double* V, int64_t N, con
   }
 }
 
+// pass A: h_i = <V_i, W>, i = 0..j (j from device)
+__global__ void __launch_bounds__(BS) k_multidot(const double* V, int64_t N, int64_t ld, const double* W,
+                                                 const double* sc, double* h, RedSite site) {
+  const int nv = min((int)sc[G_J] + 1, MD_MAXV);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nseg = (N + CG_SEG - 1) / CG_SEG;
+  const int64_t nw = (int64_t)gridDim.x * (BS / 32);
+  double t0 = 0.0, t1 = 0.0;
+  for (int64_t sg = (int64_t)blockIdx.x * (BS / 32) + warp; sg < nseg; sg += nw) {
+    const int64_t e0 = sg * CG_SEG + 2 * lane;
+    double w[2 * CG_K];
+#pragma unroll
+    for (int k = 0; k < CG_K; ++k) cg_ldw(W, e0 + 64 * k, N, w[2 * k], w[2 * k + 1]);
+#pragma unroll 2
+    for (int i = 0; i < nv; ++i) {
+      const double* vi = V + (int64_t)i * ld;
+      double v[2 * CG_K];
+#pragma unroll
+      for (int k = 0; k < CG_K; ++k) cg_ld(vi, e0 + 64 * k, N, v[2 * k], v[2 * k + 1]);
+      double sv = 0.0;
+#pragma unroll
+      for (int k = 0; k < 2 * CG_K; ++k) sv = fma(v[k], w[k], sv);
+      sv = warp_sum(sv);
+      if (lane == (i & 31)) { if (i < 32) t0 += sv; else t1 += sv; }
+    }
+  }
+  md_finish(t0, t1, nv, h, site);
+}
+
+// pass B: W <- W - sum_i h_i V_i (in i order), then h'_i = <V_i, W> on the updated segment
+__global__ void __launch_bounds__(BS) k_cgs_mid(const double* V, int64_t N, int64_t ld, double* W, const double* h,
+                                                const double* sc, double* h2, RedSite site) {
+  const int nv = min((int)sc[G_J] + 1, MD_MAXV);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nseg = (N + CG_SEG - 1) / CG_SEG;
+  const int64_t nw = (int64_t)gridDim.x * (BS / 32);
+  double t0 = 0.0, t1 = 0.0;
+  for (int64_t sg = (int64_t)blockIdx.x * (BS / 32) + warp; sg < nseg; sg += nw) {
+    const int64_t e0 = sg * CG_SEG + 2 * lane;
+    double w[2 * CG_K];
+#pragma unroll
+    for (int k = 0; k < CG_K; ++k) cg_ldw(W, e0 + 64 * k, N, w[2 * k], w[2 * k + 1]);
+#pragma unroll 2
+    for (int i = 0; i < nv; ++i) {
+      const double* vi = V + (int64_t)i * ld;
+      const double hi = __ldg(h + i);
+      double v[2 * CG_K];
+#pragma unroll
+      for (int k = 0; k < CG_K; ++k) cg_ld(vi, e0 + 64 * k, N, v[2 * k], v[2 * k + 1]);
+#pragma unroll
+      for (int k = 0; k < 2 * CG_K; ++k) w[k] -= hi * v[k];
+    }
+#pragma unroll
+    for (int k = 0; k < CG_K; ++k) cg_st(W, e0 + 64 * k, N, w[2 * k], w[2 * k + 1]);
+#pragma unroll 2
+    for (int i = 0; i < nv; ++i) {
+      const double* vi = V + (int64_t)i * ld;
+      double v[2 * CG_K];
+#pragma unroll
+      for (int k = 0; k < CG_K; ++k) cg_ld(vi, e0 + 64 * k, N, v[2 * k], v[2 * k + 1]);
+      double sv = 0.0;
+#pragma unroll
+      for (int k = 0; k < 2 * CG_K; ++k) sv = fma(v[k], w[k], sv);
+      sv = warp_sum(sv);
+      if (lane == (i & 31)) { if (i < 32) t0 += sv; else t1 += sv; }
+    }
+  }
+  md_finish(t0, t1, nv, h2, site);
+}
+
+// pass C: W <- W - sum_i h'_i V_i, out = ||W||^2 (deterministic grid reduction)
+__global__ void __launch_bounds__(BS) k_cgs_last(const double* V, int64_t N, int64_t ld, double* W, const double* h,
+                                                 const double* sc, RedSite site, int slot, double* out) {
+  const int nv = (int)sc[G_J] + 1;
+  double s = 0.0;
+  for (int64_t e = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); e < N; e += 2 * (int64_t)gridDim.x * blockDim.x) {
+    double w0, w1;
+    cg_ldw(W, e, N, w0, w1);
+    int i = 0;
+    for (; i + 4 <= nv; i += 4) {
+      double v[4][2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cg_ld(V + (int64_t)(i + u) * ld, e, N, v[u][0], v[u][1]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { const double c = __ldg(h + i + u); w0 -= c * v[u][0]; w1 -= c * v[u][1]; }
+    }
+    for (; i < nv; ++i) {
+      double v0, v1;
+      cg_ld(V + (int64_t)i * ld, e, N, v0, v1);
+      const double c = __ldg(h + i);
+      w0 -= c * v0; w1 -= c * v1;
+    }
+    cg_st(W, e, N, w0, w1);
+    s = fma(w0, w0, s);
+    if (e + 1 < N) s = fma(w1, w1, s);
+  }
+  double v1[1] = {s};
+  reduce_finish<1>(v1, site, slot, out);
+}
+
 // W -= sum_{i <= j} coef_i V_i  (coef device array, count j + 1 from device); the vector loads of
 // eight terms are issued before their updates (same update order)
-__global__ void k_multiaxpy(double* W, const double* V, int64_t N, const double* coef, const double* sc, int cnt_slot,
-                            int cnt_add, double sign) {
+__global__ void k_multiaxpy(double* W, const double* V, int64_t N, int64_t ld, const double* coef, const double* sc,
+                            int cnt_slot, int cnt_add, double sign) {
   const int nv = (int)sc[cnt_slot] + cnt_add;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (int64_t)gridDim.x * blockDim.x) {
     double w = W[e];
@@ -236,11 +333,11 @@ __global__ void k_multiaxpy(double* W, const double* V, int64_t N, const double*
     for (; i + 8 <= nv; i += 8) {
       double v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = V[(int64_t)(i + u) * N + e];
+      for (int u = 0; u < 8; ++u) v[u] = V[(int64_t)(i + u) * ld + e];
 #pragma unroll
       for (int u = 0; u < 8; ++u) w -= sign * coef[i + u] * v[u];
     }
-    for (; i < nv; ++i) w -= sign * coef[i] * V[(int64_t)i * N + e];
+    for (; i < nv; ++i) w -= sign * coef[i] * V[(int64_t)i * ld + e];
     W[e] = w;
   }
 }
@@ -288,11 +385,11 @@ __global__ void k_store_hcol(double* H, const double* h, const double* sc, int m
 }
 
 // V_{j+1} = W / ||W||
-__global__ void k_set_vnext(double* V, int64_t N, const double* W, const double* sc) {
+__global__ void k_set_vnext(double* V, int64_t N, int64_t ld, const double* W, const double* sc) {
   const double hn = sc[G_HN];
   if (hn == 0.0) return;
   const int64_t jw = (int64_t)sc[G_JW];
-  double* vn = V + (jw + 1) * N;
+  double* vn = V + (jw + 1) * ld;
   const double inv = 1.0 / hn;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
     vn[i] = W[i] * inv;
@@ -503,7 +600,8 @@ void oseen_free(Problem& P) {
 static etq_status gmres_alloc(Problem& P, int m, int hist_cap) {
   if (P.gm != m) {
     cudaFree(P.gV); cudaFree(P.gH); cudaFree(P.gsm);
-    ETQ_TRY(dalloc(&P.gV, (size_t)(m + 1) * P.N));
+    P.gld = (P.N + 31) / 32 * 32;   // 256-byte aligned basis vectors (128-bit loads in CGS2)
+    ETQ_TRY(dalloc(&P.gV, (size_t)(m + 1) * P.gld));
     ETQ_TRY(dalloc(&P.gH, (size_t)(m + 1) * m));
     ETQ_TRY(dalloc(&P.gsm, (size_t)gseg(m, 6)));
     P.gm = m;
@@ -535,15 +633,17 @@ static etq_status arnoldi_step(Problem& P, bool reduced, etq_pc_kind kind, cudaS
   double* hh = P.gsm + gseg(m, 4);
   double* Hcol = P.gsm + gseg(m, 5);
   const int gN = grid_for(N, BS, RED_BLOCKS);
-  k_copy_vj<<<grid_for(N, BS, 4096), BS, 0, st>>>(P.gV, N, sc, P.gT); etq_count_launch();
+  const int64_t ld = P.gld;
+  k_copy_vj<<<grid_for(N, BS, 4096), BS, 0, st>>>(P.gV, N, ld, sc, P.gT); etq_count_launch();
   ETQ_TRY(oseen_precond_apply(P, kind, P.gT, P.gZ, st));
   launch_saddle_ex(P, reduced, P.gZ, P.gW, nullptr, nullptr, 0, nullptr, nullptr, st);
-  // CGS2: h = V^T w ; w -= V h ; h' = V^T w ; w -= V h' ; h += h'
-  k_multidot<<<gN, BS, 0, st>>>(P.gV, N, P.gW, sc, Hcol, P.gred); etq_count_launch();
-  k_multiaxpy<<<grid_for(N, BS, 4096), BS, 0, st>>>(P.gW, P.gV, N, Hcol, sc, G_J, 1, 1.0); etq_count_launch();
-  k_multidot<<<gN, BS, 0, st>>>(P.gV, N, P.gW, sc, hh, P.gred); etq_count_launch();
-  k_multiaxpy<<<grid_for(N, BS, 4096), BS, 0, st>>>(P.gW, P.gV, N, hh, sc, G_J, 1, 1.0); etq_count_launch();
-  k_dot2<<<gN, BS, 0, st>>>(P.gW, P.gW, N, P.red[0], 7, sc + G_HN); etq_count_launch();
+  // CGS2: h = V^T w ; w -= V h ; h' = V^T w ; w -= V h' ; h += h' (k_gmres_scalar), in three passes
+  const int gs = grid_for((N + CG_SEG - 1) / CG_SEG, BS / 32, RED_BLOCKS);
+  k_multidot<<<gs, BS, 0, st>>>(P.gV, N, ld, P.gW, sc, Hcol, P.gred); etq_count_launch();
+  k_cgs_mid<<<gs, BS, 0, st>>>(P.gV, N, ld, P.gW, Hcol, sc, hh, P.gred); etq_count_launch();
+  k_cgs_last<<<grid_for((N + 1) / 2, BS, RED_BLOCKS), BS, 0, st>>>(P.gV, N, ld, P.gW, hh, sc, P.red[0], 7, sc + G_HN);
+  etq_count_launch();
+  (void)gN;
   return ETQ_OK;
 }
 
@@ -597,7 +697,7 @@ etq_status gmres_run(Problem& P, bool reduced, etq_pc_kind kind, const double* b
     etq_status s = arnoldi_step(P, reduced, kind, st);
     k_store_hcol<<<1, 64, 0, st>>>(P.gH, P.gsm + gseg(m, 5), sc, m); etq_count_launch();
     k_gmres_scalar<<<1, 32, 0, st>>>(sc, P.gH, P.gsm, m, P.ghist, P.ghist_cap); etq_count_launch();
-    k_set_vnext<<<grid_for(N, BS, 4096), BS, 0, st>>>(P.gV, N, P.gW, sc); etq_count_launch();
+    k_set_vnext<<<grid_for(N, BS, 4096), BS, 0, st>>>(P.gV, N, P.gld, P.gW, sc); etq_count_launch();
     cudaError_t e = cudaStreamEndCapture(st, &graph);
     P.gmres_graph_nodes = etq_launch_total() - before;
     etq_count_launch(-P.gmres_graph_nodes);
@@ -622,7 +722,7 @@ etq_status gmres_run(Problem& P, bool reduced, etq_pc_kind kind, const double* b
         ETQ_TRY(arnoldi_step(P, reduced, kind, st));
         k_store_hcol<<<1, 64, 0, st>>>(P.gH, P.gsm + gseg(m, 5), sc, m); etq_count_launch();
         k_gmres_scalar<<<1, 32, 0, st>>>(sc, P.gH, P.gsm, m, P.ghist, P.ghist_cap); etq_count_launch();
-        k_set_vnext<<<grid_for(N, BS, 4096), BS, 0, st>>>(P.gV, N, P.gW, sc); etq_count_launch();
+        k_set_vnext<<<grid_for(N, BS, 4096), BS, 0, st>>>(P.gV, N, P.gld, P.gW, sc); etq_count_launch();
       }
       ETQ_TRY(read_sc());
       if (P.hscal[G_DONE] != 0.0 || P.hscal[G_BREAK] != 0.0 || (int)P.hscal[G_TOT] >= maxit) break;
@@ -631,7 +731,7 @@ etq_status gmres_run(Problem& P, bool reduced, etq_pc_kind kind, const double* b
     // x += M^{-1} (V_k y)
     k_trisolve<<<1, 32, 0, st>>>(P.gH, P.gsm, sc, m); etq_count_launch();
     ETQ_CHECK(cudaMemsetAsync(P.gU, 0, sizeof(double) * N, st));
-    k_multiaxpy<<<grid_for(N, BS, 4096), BS, 0, st>>>(P.gU, P.gV, N, P.gsm + gseg(m, 3), sc, G_J, 0, -1.0);
+    k_multiaxpy<<<grid_for(N, BS, 4096), BS, 0, st>>>(P.gU, P.gV, N, P.gld, P.gsm + gseg(m, 3), sc, G_J, 0, -1.0);
     etq_count_launch();
     ETQ_TRY(oseen_precond_apply(P, kind, P.gU, P.gZ, st));
     k_axpy<<<grid_for(N, BS, 4096), BS, 0, st>>>(x, P.gZ, N); etq_count_launch();

@@ -16,10 +16,11 @@ from paper_2303_10233_b200 import etq  # noqa: E402
 import synth  # noqa: E402
 
 
-def _vcycle(n, tile, bc=0, min_n=32, tile2=1):
+def _vcycle(n, tile, bc=0, min_n=32, tile2=1, tile3=0):
     etq.set_option(0, 1 if tile else 0)
     etq.set_option(1, min_n)
     etq.set_option(11, tile2)
+    etq.set_option(12, tile3)
     try:
         P = etq.Problem(n, bc=bc)
         P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.005))
@@ -34,6 +35,7 @@ def _vcycle(n, tile, bc=0, min_n=32, tile2=1):
         etq.set_option(0, 1)
         etq.set_option(1, 64)
         etq.set_option(11, 1)
+        etq.set_option(12, 1)
 
 
 @pytest.mark.parametrize("n,bc", [(32, 0), (64, 1), (128, 0), (512, 0)])
@@ -45,6 +47,43 @@ def test_tiled_smoother_bitwise_equal(n, bc):
     np.testing.assert_array_equal(a, b)
     c = _vcycle(n, True, bc, tile2=1)
     assert np.abs(c - b).max() <= 1e-14 * np.abs(b).max()
+
+
+@pytest.mark.parametrize("n,bc", [(32, 0), (64, 1), (128, 0), (256, 1), (512, 0), (1024, 1)])
+def test_tile3_smoother_bitwise_equal_tile2(n, bc):
+    """k_cheb_tile3 (residual in registers, one output map for the three steps, outputs written from
+    the last step) performs k_cheb_tile2's arithmetic in the same order: bitwise-identical V-cycles
+    (ragged last tiles at every n; n = 1024: the c3 finest level)."""
+    a = _vcycle(n, True, bc, tile2=1, tile3=0)
+    b = _vcycle(n, True, bc, tile2=1, tile3=1)
+    np.testing.assert_array_equal(a, b)
+
+
+def _minres_tile3(n, tile3):
+    etq.set_option(12, tile3)
+    try:
+        P = etq.Problem(n)
+        P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.005))
+        b = torch.zeros(P.N, dtype=torch.float64, device="cuda")
+        P.build_rhs(b)
+        x = torch.zeros_like(b)
+        rep = P.minres_solve(etq.PC_P2_GMG, b, x, rtol=1e-8, maxit=500)
+        out = x.cpu().numpy(), rep["iterations"]
+        P.close()
+        return out
+    finally:
+        etq.set_option(12, 1)
+
+
+def test_tile3_minres_bitwise_equal_tile2():
+    """The finest post pass of k_cheb_tile3 also writes z = x + d2 and the <z, v> partials inside the
+    MINRES graph.  z is bitwise k_cheb_tile2's (test above); the <z, v> partials are summed per thread
+    over a different set of outputs (one output map for all steps), so gamma_j differs in the last
+    bits (deterministic either way): same iterations, solutions equal to rounding."""
+    x0, i0 = _minres_tile3(256, 0)
+    x1, i1 = _minres_tile3(256, 1)
+    assert i0 == i1
+    assert np.abs(x1 - x0).max() <= 1e-12 * np.abs(x0).max()
 
 
 def test_tiled_vcycle_matches_oracle():
@@ -87,6 +126,25 @@ def test_matrix_free_saddle_bitwise_equal(n, tiled):
     etq.set_option(6, 1)
     for red in (False, True):
         np.testing.assert_array_equal(ys[(0, red)], ys[(1, red)])
+
+
+@pytest.mark.parametrize("n", [64, 256])
+def test_saddle_apply_any_output_alignment(n):
+    """The tiled saddle apply stores aligned 16-byte pairs; an output vector that is only 8-byte
+    aligned (a view at element offset 1) and one at offset 2 get bitwise the same values."""
+    P = etq.Problem(n)
+    x = torch.as_tensor(synth.random_vector(P.N, seed=8), device="cuda")
+    buf = torch.zeros(P.N + 2, dtype=torch.float64, device="cuda")
+    outs = []
+    for off in (1, 2):
+        buf.zero_()
+        y = buf[off:off + P.N]
+        P.apply_saddle(x, y)
+        torch.cuda.synchronize()
+        outs.append(y.cpu().numpy().copy())
+        assert buf[:off].abs().sum().item() == 0.0 and buf[off + P.N:].abs().sum().item() == 0.0
+    P.close()
+    np.testing.assert_array_equal(outs[0], outs[1])
 
 
 @pytest.mark.parametrize("kind", [etq.PC_P2_GMG, etq.PC_P3])
