@@ -32,7 +32,10 @@ extern "C" {
  *   option 10 = Chebyshev-SGS on parity planes with TMA windows (1) or the lexicographic tiles (0 [default]);
  *               outputs agree to rounding (the k^T y sum order differs);
  *   option 11 = the leaner temporally blocked smoother k_cheb_tile2 (1 [default], grouped symmetric
- *               stencil sums: agrees to rounding) or k_cheb_tile (0, bitwise the per-step path).
+ *               stencil sums: agrees to rounding) or k_cheb_tile (0, bitwise the per-step path);
+ *   option 12 = k_cheb_tile3, the smoother with the residual in registers (1 [default], bitwise the
+ *               k_cheb_tile2 V-cycle) or k_cheb_tile2 (0);
+ *   option 13 = programmatic dependent launches inside the V-cycle of P2 (0 [default]) - bitwise the same.
  * Applies to solves whose CUDA graphs are captured afterwards (re-run etq_precond_setup). */
 etq_status etq_debug_set_option(int32_t option, int32_t value);
 

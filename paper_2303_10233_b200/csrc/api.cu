@@ -19,7 +19,9 @@ bool g_sgs_high_prio = false;       // etq_set_option(4): Chebyshev-SGS kernels 
 bool g_tail_sm = true;              // etq_set_option(5): shared-memory matrix-free coarse-level tail
 bool g_saddle_tile = true;          // etq_set_option(6): shared-memory tiled matrix-free saddle apply
 bool g_sgs_pdl = true;              // etq_set_option(7): programmatic dependent launches in the SGS chain
-bool g_cheb_tile3 = true;           // etq_debug_set_option(12): smoother with the residual in registers (k_cheb_tile3)
+bool g_cheb_tile3 = true;
+bool g_p2_vc_pdl = false;
+bool g_oseen_mf = true;             // etq_debug_set_option(14): matrix-free interior rows of the cavity-wind F levels           // etq_debug_set_option(13): programmatic dependent launches inside P2's V-cycle           // etq_debug_set_option(12): smoother with the residual in registers (k_cheb_tile3)
 bool g_cheb_tile2 = true;           // etq_set_option(11): leaner temporally blocked smoother (k_cheb_tile2)
 bool g_sgs_planar = false;          // etq_set_option(10): Chebyshev-SGS on parity planes with TMA windows
 bool g_vc_pdl = true;               // etq_set_option(8): programmatic dependent launches in the V-cycle
@@ -726,6 +728,8 @@ etq_status etq_debug_set_option(int32_t option, int32_t value) {
   if (option == 10) { g_sgs_planar = value != 0; return ETQ_OK; }
   if (option == 11) { g_cheb_tile2 = value != 0; return ETQ_OK; }
   if (option == 12) { g_cheb_tile3 = value != 0; return ETQ_OK; }
+  if (option == 13) { g_p2_vc_pdl = value != 0; return ETQ_OK; }
+  if (option == 14) { g_oseen_mf = value != 0; return ETQ_OK; }
   return ETQ_EINVAL;
 }
 

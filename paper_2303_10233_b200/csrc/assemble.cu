@@ -896,6 +896,62 @@ etq_status class_weights(const Geo& g, const Sell& A, StencilOp* so) {
   return ETQ_OK;
 }
 
+// Oseen levels with the separable cavity wind (oseen == 1, reading R9'): F_s = nu L + N with
+// N((i,j),(i',j')) = A1(i,i') T2(j,j') - T2(i,i') A1(j,j') (the 1D tables of the file header).  The
+// interior rows are applied matrix-free: nu times the (h-independent) Stokes class stencil plus the
+// convection weights formed from two 1D tables per node index, tab[0][5 i + d] = A1(i, i + d - 2)
+// and tab[1][5 i + d] = T2(i, i + d - 2); frame rows keep stored SELL rows.
+namespace {
+__global__ void k_oseen_tabs(Geo g, double nu, double* w, double* tab) {
+  const int n = g.n, m = g.m;
+  const double h = g.h;
+  const int tot = 100 + 5 * m;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
+    if (t < 100) {   // nu L class stencil at an interior reference node of class c
+      const int c = t / 25, k = t % 25, dj = k / 5 - 2, di = k % 5 - 2;
+      const int i = 4 + (c & 1), j = 4 + (c >> 1);
+      w[t] = nu * (m1(n, h, j, j + dj) * k1(n, h, i, i + di) + k1(n, h, j, j + dj) * m1(n, h, i, i + di));
+    } else {
+      const int q = t - 100, i = q / 5, ii = i + q % 5 - 2;
+      const bool ok = ii >= 0 && ii < m;
+      tab[q] = ok ? osn1(0, n, h, i, ii) : 0.0;
+      tab[5 * m + q] = ok ? osn1(1, n, h, i, ii) : 0.0;
+    }
+  }
+}
+}  // namespace
+
+etq_status build_oseen_stencil_level(const Geo& g, double nu, StencilOp* so, Sell* frame, double** tab,
+                                     cudaStream_t st) {
+  if (g.n < 16) return ETQ_EINVAL;
+  StencilOp o;
+  o.m = g.m; o.lo = 4; o.hi = g.m - 5;
+  o.nseg_x = (o.hi - o.lo + 1 + 31) / 32;
+  o.nseg = (int64_t)o.nseg_x * (o.hi - o.lo + 1);
+  double* dw;
+  ETQ_TRY(dalloc(&dw, 100));
+  ETQ_TRY(dalloc(tab, (size_t)10 * g.m));
+  k_oseen_tabs<<<(100 + 5 * g.m + 255) / 256, 256, 0, st>>>(g, nu, dw, *tab); etq_count_launch();
+  ETQ_CHECK(cudaMemcpyAsync(&o.w[0][0], dw, sizeof(double) * 100, cudaMemcpyDeviceToHost, st));
+  ETQ_CHECK(cudaStreamSynchronize(st));
+  cudaFree(dw);
+  std::vector<int> rows;
+  for (int c = 0; c < 4; ++c)
+    for (int j = (c >> 1); j < g.m; j += 2)
+      for (int i = (c & 1); i < g.m; i += 2)
+        if (i < o.lo || i > o.hi || j < o.lo || j > o.hi) rows.push_back(i + g.m * j);
+  const int64_t ns = ((int64_t)rows.size() + SELL_C - 1) / SELL_C;
+  rows.resize(ns * SELL_C, -1);
+  int* perm;
+  ETQ_TRY(dalloc(&perm, rows.size()));
+  ETQ_CHECK(cudaMemcpy(perm, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
+  VelFn fn{VelParams{g, 1, nu}};
+  ETQ_TRY(build_sell(fn, perm, g.nq, ns, frame, st));
+  frame->own_perm = true;
+  *so = o;
+  return ETQ_OK;
+}
+
 etq_status build_stencil_level(const Geo& g, const Sell& A, StencilOp* so, Sell* frame, cudaStream_t st) {
   if (!A.stval || !A.stoff || g.n < 16) return ETQ_EINVAL;
   std::vector<double> sv(4 * 32);

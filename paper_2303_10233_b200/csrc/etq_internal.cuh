@@ -54,6 +54,8 @@ extern bool g_tail_sm;                    // api.cu; etq_set_option(5)
 extern bool g_saddle_tile;                // api.cu; etq_set_option(6)
 extern bool g_sgs_pdl;                    // api.cu; etq_set_option(7)
 extern bool g_sgs_planar;                 // api.cu; etq_set_option(10)
+extern bool g_oseen_mf;                   // api.cu; etq_debug_set_option(14)
+extern bool g_p2_vc_pdl;                  // api.cu; etq_debug_set_option(13)
 extern bool g_cheb_tile3;                 // api.cu; etq_debug_set_option(12)
 extern bool g_cheb_tile2;                 // api.cu; etq_set_option(11)
 extern bool g_vc_pdl;                     // api.cu; etq_set_option(8)
@@ -142,6 +144,7 @@ struct Level {
   bool ct2 = false;           // its stencils equal the constant-bank table of k_cheb_tile2
   StencilOp so;
   Sell Afr;                   // rows outside the interior rectangle (own permutation)
+  double* os_tab = nullptr;   // Oseen cavity-wind levels: 1D convection tables A1, T2 [2][m][5] (matrix-free interior)
   // two-component work vectors, each [2*nq]
   double *b = nullptr, *x = nullptr, *r = nullptr, *d0 = nullptr, *d1 = nullptr;
   double* coarse_inv = nullptr;   // dense inverse (coarsest level only), nq x nq row-major
@@ -364,6 +367,8 @@ etq_status sell_diag_inv(const Sell& A, double* dinv, cudaStream_t st);
 etq_status build_rhs_dev(const Problem& P, const double* f_nodal, double* b);
 etq_status mark_implicit(const Geo& g, bool oseen, double nu, int wind, Sell& S, cudaStream_t st, bool values);
 etq_status build_stencil_level(const Geo& g, const Sell& A, StencilOp* so, Sell* frame, cudaStream_t st);
+etq_status build_oseen_stencil_level(const Geo& g, double nu, StencilOp* so, Sell* frame, double** tab,
+                                     cudaStream_t st);
 etq_status saddle_weights(const Geo& g, SaddleSt* out, cudaStream_t st);
 etq_status class_weights(const Geo& g, const Sell& A, StencilOp* so);
 

@@ -345,6 +345,60 @@ __global__ void __launch_bounds__(BS, STENCIL_MINB) k_cheb_step_st(ChebStArgs a)
   }
 }
 
+// Oseen levels with the cavity wind (reading R9'): interior row (i, j) of F_s = nu L + N, both
+// components from one set of weights w = nu L_class(di, dj) + A1_i(di) T2_j(dj) - T2_i(di) A1_j(dj)
+// (tab: A1 then T2, [m][5] each; the tables hold 0 outside the 1D supports, so the full 5 x 5
+// (odd j: 5 x 3) loop needs no per-lane branches).  Not the stored-row summation order.
+__device__ __forceinline__ void oseen_row2(const StencilOp& so, const double* __restrict__ tab, int i, int j,
+                                           const double* __restrict__ x0, const double* __restrict__ x1, double& a0,
+                                           double& a1) {
+  const int cl = (j & 1) * 2 + (i & 1);
+  const int node = i + so.m * j;
+  const double* __restrict__ tA = tab;
+  const double* __restrict__ tT = tab + 5 * so.m;
+  double ai[5], ti[5];
+#pragma unroll
+  for (int d = 0; d < 5; ++d) { ai[d] = __ldg(tA + 5 * i + d); ti[d] = __ldg(tT + 5 * i + d); }
+  a0 = 0.0; a1 = 0.0;
+#pragma unroll
+  for (int dj = -2; dj <= 2; ++dj) {
+    if ((j & 1) && (dj == 2 || dj == -2)) continue;   // warp-uniform
+    const double aj = __ldg(tA + 5 * j + dj + 2), tj = __ldg(tT + 5 * j + dj + 2);
+    const int rb = node + dj * so.m;
+#pragma unroll
+    for (int di = -2; di <= 2; ++di) {
+      const double w = fma(ai[di + 2], tj, fma(-ti[di + 2], aj, so.w[cl][(dj + 2) * 5 + (di + 2)]));
+      a0 = fma(w, __ldg(x0 + rb + di), a0);
+      a1 = fma(w, __ldg(x1 + rb + di), a1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(BS, 3) k_cheb_step_os(ChebStArgs a, const double* __restrict__ tab) {
+  pdl_wait();
+  if (is_done(a.done)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const double* g = a.post ? a.x_in : a.d_in;
+  for (int64_t s = gw; s < a.so.nseg + a.F.nslices; s += nw) {
+    if (s < a.so.nseg) {
+      const int j = a.so.lo + (int)(s / a.so.nseg_x);
+      const int i = a.so.lo + (int)(s % a.so.nseg_x) * 32 + lane;
+      if (i > a.so.hi) continue;
+      double q0, q1;
+      oseen_row2(a.so, tab, i, j, g, g + a.nq, q0, q1);
+      cheb_update2(a, i + a.so.m * j, q0, q1);
+    } else {
+      const int64_t sf = s - a.so.nseg;
+      const int row = a.F.perm[sf * SELL_C + lane];
+      double q0 = 0.0, q1 = 0.0;
+      sell_row2(a.F, sf, lane, row, g, g + a.nq, q0, q1);
+      if (row >= 0) cheb_update2(a, row, q0, q1);
+    }
+  }
+}
+
 // ---- temporally blocked Chebyshev smoothing (Stokes levels, storage 0): all three steps of a
 // pre- or post-smoothing pass in one kernel.  A CTA owns a CT_T x CT_T tile of one velocity
 // component and stages a CT_R x CT_R window (halo CT_H = 3 steps x stencil radius 2) of each
@@ -2859,6 +2913,10 @@ etq_status build_hierarchy(Problem& P, Hierarchy& H, int coarse_n, double lo, do
       lv.st_on = true;
       lv.ct2 = ct2_register(lv.so);
       if (std::getenv("ETQ_DEBUG")) std::fprintf(stderr, "[etq] level n=%d k_cheb_tile2 %s\n", lv.g.n, lv.ct2 ? "on" : "off");
+    } else if (P.oseen && P.wind == 1 && P.storage == 0 && g_oseen_mf && lv.g.n >= 16 && l + 1 < H.lv.size()) {
+      // cavity-wind F levels: matrix-free interior rows (k_cheb_step_os), stored frame rows
+      ETQ_TRY(build_oseen_stencil_level(lv.g, P.nu, &lv.so, &lv.Afr, &lv.os_tab, P.stream));
+      lv.st_on = true;
     }
   }
   // coarse-level tail: first level l >= 1 with n <= TAIL_N (degree <= 4)
@@ -2981,6 +3039,7 @@ void free_hierarchy(Hierarchy& H) {
     cudaFree(L.f_coarse);
     if (H.kind == 1 || l > 0) sell_free(L.A);
     sell_free(L.Afr);
+    cudaFree(L.os_tab);
     cudaFree(L.dinv); cudaFree(L.b); cudaFree(L.x); cudaFree(L.r); cudaFree(L.d0); cudaFree(L.d1);
     cudaFree(L.coarse_inv);
     cudaFree(L.wind); cudaFree(L.lapval);
@@ -3021,7 +3080,9 @@ static void launch_cheb_st(const Level& lv, const ChebArgs& c, bool post, double
   a.d_in = c.d_in; a.r_in = c.r_in; a.x_in = c.x_in; a.x_out = c.x_out; a.r_out = c.r_out; a.d_out = c.d_out;
   a.c1 = c.c1; a.c2 = c.c2; a.post = post ? 1 : 0; a.itheta = 1.0 / theta; a.done = c.done;
   const int64_t warps = lv.so.nseg + lv.Afr.nslices;
-  launch_pdl(k_cheb_step_st, dim3(grid_for(warps * 32, BS, 4096)), dim3(BS), 0, st, pdl, a);
+  if (lv.os_tab) launch_pdl(k_cheb_step_os, dim3(grid_for(warps * 32, BS, 4096)), dim3(BS), 0, st, pdl, a,
+                            (const double*)lv.os_tab);
+  else launch_pdl(k_cheb_step_st, dim3(grid_for(warps * 32, BS, 4096)), dim3(BS), 0, st, pdl, a);
 }
 
 // Temporally blocked smoothing pass on an interior-stencil level (degree 3, real interval).

@@ -189,7 +189,7 @@ etq_status precond_apply_ex(const Problem& P, etq_pc_kind kind, const double* r,
     } else {
       ETQ_TRY(mass_pc_apply_ex(P, r + nu, z + nu, site, 2, out_p, w ? w + nu : nullptr, done, P.aux));
     }
-    ETQ_TRY(vcycle_apply_ex(P, P.mg, r, z, site, 1, out_u, w, done, st));
+    ETQ_TRY(vcycle_apply_ex(P, P.mg, r, z, site, 1, out_u, w, done, st, g_p2_vc_pdl));
     ETQ_CHECK(cudaEventRecord(P.ev_join, P.aux));
     ETQ_CHECK(cudaStreamWaitEvent(st, P.ev_join, 0));
     return ETQ_OK;
