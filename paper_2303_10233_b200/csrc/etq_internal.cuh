@@ -54,6 +54,8 @@ extern bool g_tail_sm;                    // api.cu; etq_set_option(5)
 extern bool g_saddle_tile;                // api.cu; etq_set_option(6)
 extern bool g_sgs_pdl;                    // api.cu; etq_set_option(7)
 extern bool g_sgs_planar;                 // api.cu; etq_set_option(10)
+extern int g_sgs_window;                  // api.cu; etq_debug_set_option(16)
+extern bool g_sgs_yp_ldg;                 // api.cu; etq_debug_set_option(15)
 extern bool g_oseen_mf;                   // api.cu; etq_debug_set_option(14)
 extern bool g_p2_vc_pdl;                  // api.cu; etq_debug_set_option(13)
 extern bool g_cheb_tile3;                 // api.cu; etq_debug_set_option(12)

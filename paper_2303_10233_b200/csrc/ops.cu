@@ -1546,6 +1546,14 @@ constexpr int SGS_SMEM = (SGS_PAD + 8 * SGS_PL + 2 * SGS_TQ) * (int)sizeof(doubl
 static_assert(SGS_W - SGS_HX - SGS_TTX >= 6 && SGS_W - SGS_HY - SGS_TTY >= 2, "right / top halo");
 static_assert(SGS_HX % 2 == 0 && SGS_HY % 2 == 0 && SGS_TTX % 2 == 0 && SGS_TTY % 2 == 0, "even origins");
 static_assert(SGS_TX == SGS_P && 2 * SGS_TY == SGS_P, "one thread per plane column, two rows");
+// window geometry by height WY (64: a 64 x 64 window of 512 threads; 32: a 64 x 32 window of 256
+// threads, the default); the halos are unchanged
+#define SGS_GEO(WY_)                                                                              \
+  constexpr int TY_ = (WY_) / 4, PL_ = SGS_P * ((WY_) / 2), TTY_ = (WY_) - 6, TQ_ = SGS_TTX * TTY_; \
+  static_assert(2 * TY_ == (WY_) / 2 && TTY_ % 2 == 0, "two plane rows per thread");             \
+  (void)TQ_
+template <int WY>
+constexpr int sgs_smem() { return (SGS_PAD + 8 * SGS_P * (WY / 2) + 2 * SGS_TTX * (WY - 6)) * (int)sizeof(double); }
 
 struct SgsK {                 // M_Q coefficients (Qk = Mlin x Mlin, R = h^2/4, Q0 = h^2)
   double w_in, w_bd, w_off, rq, c_dd, c_ed, inv_in2, inv_inbd, inv_bd2, inv_q0;
@@ -1566,6 +1574,7 @@ struct SgsTileArgs {
   RedSite site; int slot; double* kout;   // optional k^T out
   const double* done;
   int pdl;                  // launched as a programmatic dependent of the previous SGS step
+  int yp_ldg;               // y_prev read from global in the Q pass (1) or staged by cp.async (0)
 };
 
 
@@ -1578,25 +1587,26 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 // update of colour (PX, PY): plane entries (i, j), j = ty + 16 m; vertex (2i + PX, 2j + PY)
-template <int PX, int PY, bool IN>
+template <int WY, int PX, int PY, bool IN>
 __device__ __forceinline__ void sgs_colour(double* __restrict__ V, const double* __restrict__ Cc,
                                            const double (&rr)[2], int A0, int C0, int n, const SgsK& k) {
+  SGS_GEO(WY);
   constexpr int c = PX + 2 * PY, cx = (1 - PX) + 2 * PY, cy = PX + 2 * (1 - PY), cxy = (1 - PX) + 2 * (1 - PY);
   constexpr int OW = PX - 1, OE = PX, OS = (PY - 1) * SGS_P, ON = PY * SGS_P;   // neighbour offsets
   const int i = threadIdx.x;
 #pragma unroll
   for (int m = 0; m < 2; ++m) {
-    const int j = threadIdx.y + SGS_TY * m;
+    const int j = threadIdx.y + TY_ * m;
     const int B = j * SGS_P + i;
-    const double* vd = V + cxy * SGS_PL + B;
-    const double* vx = V + cx * SGS_PL + B;
-    const double* vy = V + cy * SGS_PL + B;
+    const double* vd = V + cxy * PL_ + B;
+    const double* vx = V + cx * PL_ + B;
+    const double* vy = V + cy * PL_ + B;
     const double sd = (vd[OS + OW] + vd[OS + OE]) + (vd[ON + OW] + vd[ON + OE]);
     const double sx = vx[OW] + vx[OE];
     const double sy = vy[OS] + vy[ON];
     // cells (la-1, lc-1), (la, lc-1), (la-1, lc), (la, lc)
-    const double sc = (Cc[cxy * SGS_PL + B + OS + OW] + Cc[cy * SGS_PL + B + OS]) +
-                      (Cc[cx * SGS_PL + B + OW] + Cc[c * SGS_PL + B]);
+    const double sc = (Cc[cxy * PL_ + B + OS + OW] + Cc[cy * PL_ + B + OS]) +
+                      (Cc[cx * PL_ + B + OW] + Cc[c * PL_ + B]);
     double wx = k.c_ed, wy = k.c_ed, inv = k.inv_in2;
     bool in = true;
     if (!IN) {
@@ -1608,34 +1618,36 @@ __device__ __forceinline__ void sgs_colour(double* __restrict__ V, const double*
       inv = bx ? (by ? k.inv_bd2 : k.inv_inbd) : (by ? k.inv_inbd : k.inv_in2);
     }
     const double s = rr[m] - k.c_dd * sd - wx * sx - wy * sy - k.rq * sc;
-    V[c * SGS_PL + B] = in ? s * inv : 0.0;
+    V[c * PL_ + B] = in ? s * inv : 0.0;
   }
 }
 
 // P0 cells of parity plane (PE, PF): cell (2i + PE, 2j + PF) from its four vertices
-template <int PE, int PF, bool IN>
+template <int WY, int PE, int PF, bool IN>
 __device__ __forceinline__ void sgs_cells(const double* __restrict__ V, double* __restrict__ Cc,
                                           const double (&rc)[2], int A0, int C0, int n, const SgsK& k) {
+  SGS_GEO(WY);
   constexpr int p00 = PE + 2 * PF, p10 = (1 - PE) + 2 * PF, p01 = PE + 2 * (1 - PF), p11 = (1 - PE) + 2 * (1 - PF);
   const int i = threadIdx.x;
 #pragma unroll
   for (int m = 0; m < 2; ++m) {
-    const int j = threadIdx.y + SGS_TY * m;
+    const int j = threadIdx.y + TY_ * m;
     const int B = j * SGS_P + i;
-    const double sv = (V[p00 * SGS_PL + B] + V[p10 * SGS_PL + B + PE]) +
-                      (V[p01 * SGS_PL + B + PF * SGS_P] + V[p11 * SGS_PL + B + PF * SGS_P + PE]);
+    const double sv = (V[p00 * PL_ + B] + V[p10 * PL_ + B + PE]) +
+                      (V[p01 * PL_ + B + PF * SGS_P] + V[p11 * PL_ + B + PF * SGS_P + PE]);
     const double z = (rc[m] - k.rq * sv) * k.inv_q0;
     bool in = true;
     if (!IN) {
       const int e = A0 + 2 * i + PE, f = C0 + 2 * j + PF;
       in = e >= 0 && e < n && f >= 0 && f < n;
     }
-    Cc[p00 * SGS_PL + B] = in ? z : 0.0;
+    Cc[p00 * PL_ + B] = in ? z : 0.0;
   }
 }
 
-template <bool IN>
+template <int WY, bool IN>
 __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, double* Cc, double* Q, int A0, int C0) {
+  SGS_GEO(WY);
   const int i = threadIdx.x, ty = threadIdx.y;
   const int n = a.g.n, n1 = n + 1, nk = a.g.nk;
   const double alpha = a.kproj ? (*a.kproj * a.inv_kk) : 0.0;
@@ -1653,18 +1665,18 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
   //      thread, addresses incremented)
   const int tid = i + SGS_TX * ty;
   {
-    constexpr int RSTEP = SGS_TX * SGS_TY / SGS_W;           // 8 window rows per pass
-    static_assert(SGS_TX * SGS_TY % SGS_W == 0 && RSTEP % 2 == 0, "fixed parity per thread");
+    constexpr int RSTEP = SGS_TX * TY_ / SGS_W;              // window rows per pass (64 columns)
+    static_assert(SGS_TX * TY_ % SGS_W == 0 && RSTEP % 2 == 0 && WY % RSTEP == 0, "fixed parity per thread");
     const int la = tid & (SGS_W - 1), lc0 = tid / SGS_W;
     const int ga = A0 + la;
-    double* vdst = V + ((la & 1) + 2 * (lc0 & 1)) * SGS_PL + (lc0 >> 1) * SGS_P + (la >> 1);
+    double* vdst = V + ((la & 1) + 2 * (lc0 & 1)) * PL_ + (lc0 >> 1) * SGS_P + (la >> 1);
     double* cdst = Cc + (vdst - V);
     const double* vsrc = ys + ga + (int64_t)n1 * (C0 + lc0);
     const double* csrc = ys + nk + ga + (int64_t)n * (C0 + lc0);
     const int64_t dv = (int64_t)RSTEP * n1, dc = (int64_t)RSTEP * n;
     const bool xin_v = IN || (ga >= 0 && ga <= n), xin_c = IN || (ga >= 0 && ga < n);
 #pragma unroll 4
-    for (int q = 0; q < SGS_W / RSTEP; ++q) {
+    for (int q = 0; q < WY / RSTEP; ++q) {
       const int gc = C0 + lc0 + RSTEP * q;
       const bool inv = IN || (xin_v && gc >= 0 && gc <= n);
       const bool inc = IN || (xin_c && gc >= 0 && gc < n);
@@ -1673,12 +1685,12 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
       vdst += (RSTEP / 2) * SGS_P; cdst += (RSTEP / 2) * SGS_P; vsrc += dv; csrc += dc;
     }
   }
-  if (use_yp) {
-    for (int idx = tid; idx < SGS_TTX * SGS_TTY; idx += SGS_TX * SGS_TY) {
+  if (use_yp && !a.yp_ldg) {
+    for (int idx = tid; idx < SGS_TTX * TTY_; idx += SGS_TX * TY_) {
       const int ga = A0 + SGS_HX + idx % SGS_TTX, gc = C0 + SGS_HY + idx / SGS_TTX;
       const bool okv = IN || (ga <= n && gc <= n), okc = IN || (ga < n && gc < n);
       cp_async8(Q + idx, yps + (okv ? ga + (int64_t)n1 * gc : 0), okv);
-      cp_async8(Q + SGS_TQ + idx, yps + nk + (okc ? ga + (int64_t)n * gc : 0), okc);
+      cp_async8(Q + TQ_ + idx, yps + nk + (okc ? ga + (int64_t)n * gc : 0), okc);
     }
   }
   double rv[4][2], rc[4][2];
@@ -1686,7 +1698,7 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
   for (int c = 0; c < 4; ++c)
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
-      const int j = ty + SGS_TY * m;
+      const int j = ty + TY_ * m;
       const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
       const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
       const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
@@ -1697,20 +1709,45 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
   __syncthreads();
   // ---- the y / y_prev part of this thread's outputs (tile row-major), before the sweep
   //      overwrites y in place; the write phase below uses the same thread -> entry map
-  for (int idx = tid; idx < SGS_TTX * SGS_TTY; idx += SGS_TX * SGS_TY) {
-    const int la = SGS_HX + idx % SGS_TTX, lc = SGS_HY + idx / SGS_TTX;
-    const int pl = ((la & 1) + 2 * (lc & 1)) * SGS_PL + (lc >> 1) * SGS_P + (la >> 1);
-    Q[idx] = fma(co_y, V[pl], use_yp ? co_p * Q[idx] : 0.0);
-    Q[SGS_TQ + idx] = fma(co_y, Cc[pl], use_yp ? co_p * Q[SGS_TQ + idx] : 0.0);
+  if (use_yp && a.yp_ldg) {
+    // y_prev read from global (L2) here instead of staged by cp.async (the default): fewer MIO
+    // operations; all loads of the thread issued before their use (same values, same arithmetic)
+    constexpr int NQ = (SGS_TTX * TTY_ + SGS_TX * TY_ - 1) / (SGS_TX * TY_);
+    double pv[NQ], pc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int idx = tid + q * SGS_TX * TY_;
+      const int ga = A0 + SGS_HX + idx % SGS_TTX, gc = C0 + SGS_HY + idx / SGS_TTX;
+      const bool ok = idx < SGS_TTX * TTY_;
+      const bool okv = ok && (IN || (ga <= n && gc <= n)), okc = ok && (IN || (ga < n && gc < n));
+      pv[q] = okv ? __ldg(yps + ga + (int64_t)n1 * gc) : 0.0;
+      pc[q] = okc ? __ldg(yps + nk + ga + (int64_t)n * gc) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int idx = tid + q * SGS_TX * TY_;
+      if (idx >= SGS_TTX * TTY_) break;
+      const int la = SGS_HX + idx % SGS_TTX, lc = SGS_HY + idx / SGS_TTX;
+      const int pl = ((la & 1) + 2 * (lc & 1)) * PL_ + (lc >> 1) * SGS_P + (la >> 1);
+      Q[idx] = fma(co_y, V[pl], co_p * pv[q]);
+      Q[TQ_ + idx] = fma(co_y, Cc[pl], co_p * pc[q]);
+    }
+  } else {
+    for (int idx = tid; idx < SGS_TTX * TTY_; idx += SGS_TX * TY_) {
+      const int la = SGS_HX + idx % SGS_TTX, lc = SGS_HY + idx / SGS_TTX;
+      const int pl = ((la & 1) + 2 * (lc & 1)) * PL_ + (lc >> 1) * SGS_P + (la >> 1);
+      Q[idx] = fma(co_y, V[pl], use_yp ? co_p * Q[idx] : 0.0);
+      Q[TQ_ + idx] = fma(co_y, Cc[pl], use_yp ? co_p * Q[TQ_ + idx] : 0.0);
+    }
   }
   __syncthreads();
   const SgsK& k = a.k;
-#define SGS_V(PX, PY) do { sgs_colour<PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
+#define SGS_V(PX, PY) do { sgs_colour<WY, PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
   SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
-  sgs_cells<0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);             // P0 (once: the backward sweep's
-  sgs_cells<1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);             // P0 update would repeat it exactly)
-  sgs_cells<0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
-  sgs_cells<1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
+  sgs_cells<WY, 0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);             // P0 (once: the backward sweep's
+  sgs_cells<WY, 1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);             // P0 update would repeat it exactly)
+  sgs_cells<WY, 0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
+  sgs_cells<WY, 1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
   __syncthreads();
   SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
 #undef SGS_V
@@ -1720,16 +1757,16 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
   // ---- write the tile: out = co_s S(y) + Q, row-major (coalesced global rows)
   const double co_s = a.mode ? a.omega * a.gam : 1.0;
   double kd = 0.0;
-  for (int idx = tid; idx < SGS_TTX * SGS_TTY; idx += SGS_TX * SGS_TY) {
+  for (int idx = tid; idx < SGS_TTX * TTY_; idx += SGS_TX * TY_) {
     const int la = SGS_HX + idx % SGS_TTX, lc = SGS_HY + idx / SGS_TTX, ga = A0 + la, gc = C0 + lc;
-    const int pl = ((la & 1) + 2 * (lc & 1)) * SGS_PL + (lc >> 1) * SGS_P + (la >> 1);
+    const int pl = ((la & 1) + 2 * (lc & 1)) * PL_ + (lc >> 1) * SGS_P + (la >> 1);
     if (IN || (ga <= n && gc <= n)) {
       const double o = fma(co_s, V[pl], Q[idx]);
       a.out[ga + (int64_t)n1 * gc] = o;
       kd += o;
     }
     if (IN || (ga < n && gc < n)) {
-      const double o = fma(co_s, Cc[pl], Q[SGS_TQ + idx]);
+      const double o = fma(co_s, Cc[pl], Q[TQ_ + idx]);
       a.out[nk + ga + (int64_t)n * gc] = o;
       kd -= o;
     }
@@ -1740,19 +1777,21 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
 #ifndef SGS_MINB
 #define SGS_MINB 2
 #endif
-__global__ void __launch_bounds__(SGS_TX * SGS_TY, SGS_MINB) k_sgs_tile(SgsTileArgs a) {
+template <int WY>
+__global__ void __launch_bounds__(SGS_TX * (WY / 4), WY == 64 ? SGS_MINB : 4) k_sgs_tile(SgsTileArgs a) {
+  SGS_GEO(WY);
   if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");   // previous step complete and visible
   if (is_done(a.done)) return;
   extern __shared__ double sm[];
   double* V = sm + SGS_PAD;
-  double* Cc = V + 4 * SGS_PL;
-  double* Q = Cc + 4 * SGS_PL;
+  double* Cc = V + 4 * PL_;
+  double* Q = Cc + 4 * PL_;
   if (threadIdx.x + SGS_TX * threadIdx.y < SGS_PAD) sm[threadIdx.x + SGS_TX * threadIdx.y] = 0.0;
   const int n = a.g.n;
-  const int A0 = (blockIdx.x % a.tiles_x) * SGS_TTX - SGS_HX, C0 = (blockIdx.x / a.tiles_x) * SGS_TTY - SGS_HY;
-  const bool interior = A0 >= 1 && A0 + SGS_W - 1 <= n - 1 && C0 >= 1 && C0 + SGS_W - 1 <= n - 1;
-  if (interior) sgs_tile_body<true>(a, V, Cc, Q, A0, C0);
-  else sgs_tile_body<false>(a, V, Cc, Q, A0, C0);
+  const int A0 = (blockIdx.x % a.tiles_x) * SGS_TTX - SGS_HX, C0 = (blockIdx.x / a.tiles_x) * TTY_ - SGS_HY;
+  const bool interior = A0 >= 1 && A0 + SGS_W - 1 <= n - 1 && C0 >= 1 && C0 + WY - 1 <= n - 1;
+  if (interior) sgs_tile_body<WY, true>(a, V, Cc, Q, A0, C0);
+  else sgs_tile_body<WY, false>(a, V, Cc, Q, A0, C0);
 }
 
 // ---------------------------------------------------------------- SGS on parity planes (TMA)
@@ -1828,15 +1867,15 @@ __device__ __forceinline__ void sgsp_body(const SgsPlaneArgs& a, double* V, doub
   }
   __syncthreads();
   const SgsK& k = a.k;
-#define SGS_V(PX, PY) do { sgs_colour<PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
+#define SGS_V(PX, PY) do { sgs_colour<SGS_W, PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
   SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
-  sgs_cells<0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);             // P0 (once; see k_sgs_tile)
-  sgs_cells<1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);
-  sgs_cells<0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
-  sgs_cells<1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
+  sgs_cells<SGS_W, 0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);             // P0 (once; see k_sgs_tile)
+  sgs_cells<SGS_W, 1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);
+  sgs_cells<SGS_W, 0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
+  sgs_cells<SGS_W, 1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
   __syncthreads();
   SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0);
-  sgs_colour<0, 0, IN>(V, Cc, rv[0], A0, C0, n, k);            // backward colour 0: each thread reads back
+  sgs_colour<SGS_W, 0, 0, IN>(V, Cc, rv[0], A0, C0, n, k);            // backward colour 0: each thread reads back
   __syncwarp();                                                 // only its own entries below
 #undef SGS_V
   asm volatile("griddepcontrol.launch_dependents;");
@@ -3348,11 +3387,16 @@ void mass_apply(const Geo& g, const double* x, double* y, cudaStream_t st) {
 static void launch_sgs_tile(SgsTileArgs a, cudaStream_t st, bool pdl = false) {
   static bool smem_set = false;
   if (!smem_set) {
-    cudaFuncSetAttribute(k_sgs_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, SGS_SMEM);
+    cudaFuncSetAttribute(k_sgs_tile<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, sgs_smem<64>());
+    cudaFuncSetAttribute(k_sgs_tile<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sgs_smem<32>());
     smem_set = true;
   }
   a.tiles_x = (a.g.n + 1 + SGS_TTX - 1) / SGS_TTX;
-  const int tiles = a.tiles_x * ((a.g.n + 1 + SGS_TTY - 1) / SGS_TTY);
+  // 64 x 32 windows (256 threads, four CTAs per SM) by default: 12 % more redundant sweep work than
+  // 64 x 64 windows (two per SM), but smaller CTAs fill the SMs left by the concurrent V-cycle
+  // better (measured, n = 1024, interleaved: Pi C Pi 600 -> 574 us, c3 814 -> 825 it/s; n = 512: equal)
+  const int wy = g_sgs_window == 1 ? 64 : 32;
+  const int tiles = a.tiles_x * ((a.g.n + 1 + (wy - 6) - 1) / (wy - 6));
   {
     SgsK& k = a.k;
     const double h = a.g.h;
@@ -3366,7 +3410,8 @@ static void launch_sgs_tile(SgsTileArgs a, cudaStream_t st, bool pdl = false) {
   static int lo_prio = 1, hi_prio = 0;
   if (lo_prio == 1) cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(tiles); cfg.blockDim = dim3(SGS_TX, SGS_TY); cfg.dynamicSmemBytes = SGS_SMEM; cfg.stream = st;
+  cfg.gridDim = dim3(tiles); cfg.blockDim = dim3(SGS_TX, wy / 4);
+  cfg.dynamicSmemBytes = wy == 64 ? sgs_smem<64>() : sgs_smem<32>(); cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributePriority;
   attr[0].val.priority = g_sgs_high_prio ? hi_prio : lo_prio;
@@ -3375,8 +3420,11 @@ static void launch_sgs_tile(SgsTileArgs a, cudaStream_t st, bool pdl = false) {
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   a.pdl = pdl && g_sgs_pdl ? 1 : 0;
+  a.yp_ldg = g_sgs_yp_ldg ? 1 : 0;
   cfg.attrs = attr; cfg.numAttrs = a.pdl ? 2 : 1;
-  cudaLaunchKernelEx(&cfg, k_sgs_tile, a); etq_count_launch();
+  if (wy == 64) cudaLaunchKernelEx(&cfg, k_sgs_tile<64>, a);
+  else cudaLaunchKernelEx(&cfg, k_sgs_tile<32>, a);
+  etq_count_launch();
 }
 
 // z = S(y) (one symmetric sweep from y; y nullable = 0); t is scratch for the in-place case

@@ -251,42 +251,61 @@ __global__ void __launch_bounds__(BS) k_multidot(const double* V, int64_t N, int
   md_finish(t0, t1, nv, h, site);
 }
 
-// pass B: W <- W - sum_i h_i V_i (in i order), then h'_i = <V_i, W> on the updated segment
+// pass B: W <- W - sum_i h_i V_i (in i order), then h'_i = <V_i, W> on the updated segment.  The
+// second sweep re-reads the segment of every V_i: with one 16-byte pair per lane (512-byte
+// segments) and 2 CTAs per SM the grid's working set between the two reads is about
+// 2 x 148 x 8 warps x 512 B x (j + 1) (~50 MB at j = 40), so the re-read is served by L2.
+constexpr int CGM_U = 8;   // loads in flight per lane
 __global__ void __launch_bounds__(BS) k_cgs_mid(const double* V, int64_t N, int64_t ld, double* W, const double* h,
                                                 const double* sc, double* h2, RedSite site) {
   const int nv = min((int)sc[G_J] + 1, MD_MAXV);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t nseg = (N + CG_SEG - 1) / CG_SEG;
+  const int64_t nseg = (N + 63) / 64;
   const int64_t nw = (int64_t)gridDim.x * (BS / 32);
   double t0 = 0.0, t1 = 0.0;
   for (int64_t sg = (int64_t)blockIdx.x * (BS / 32) + warp; sg < nseg; sg += nw) {
-    const int64_t e0 = sg * CG_SEG + 2 * lane;
-    double w[2 * CG_K];
+    const int64_t e = sg * 64 + 2 * lane;
+    double w0, w1;
+    cg_ldw(W, e, N, w0, w1);
+    int i = 0;
+    for (; i + CGM_U <= nv; i += CGM_U) {
+      double v[CGM_U][2];
 #pragma unroll
-    for (int k = 0; k < CG_K; ++k) cg_ldw(W, e0 + 64 * k, N, w[2 * k], w[2 * k + 1]);
-#pragma unroll 2
-    for (int i = 0; i < nv; ++i) {
-      const double* vi = V + (int64_t)i * ld;
-      const double hi = __ldg(h + i);
-      double v[2 * CG_K];
+      for (int u = 0; u < CGM_U; ++u) cg_ld(V + (int64_t)(i + u) * ld, e, N, v[u][0], v[u][1]);
 #pragma unroll
-      for (int k = 0; k < CG_K; ++k) cg_ld(vi, e0 + 64 * k, N, v[2 * k], v[2 * k + 1]);
-#pragma unroll
-      for (int k = 0; k < 2 * CG_K; ++k) w[k] -= hi * v[k];
+      for (int u = 0; u < CGM_U; ++u) { const double hi = __ldg(h + i + u); w0 -= hi * v[u][0]; w1 -= hi * v[u][1]; }
     }
+    for (; i < nv; ++i) {
+      double v0, v1;
+      cg_ld(V + (int64_t)i * ld, e, N, v0, v1);
+      const double hi = __ldg(h + i);
+      w0 -= hi * v0; w1 -= hi * v1;
+    }
+    cg_st(W, e, N, w0, w1);
+    // h'_i partials of this segment for 32 vectors at a time, reduced across the warp by recursive
+    // halving (31 shuffles per 32 sums instead of 5 per sum): lane l ends with vector (32 c + l)
 #pragma unroll
-    for (int k = 0; k < CG_K; ++k) cg_st(W, e0 + 64 * k, N, w[2 * k], w[2 * k + 1]);
-#pragma unroll 2
-    for (int i = 0; i < nv; ++i) {
-      const double* vi = V + (int64_t)i * ld;
-      double v[2 * CG_K];
+    for (int c = 0; c < 2; ++c) {
+      const int base = 32 * c;
+      if (base >= nv) break;
+      double pp[32];
 #pragma unroll
-      for (int k = 0; k < CG_K; ++k) cg_ld(vi, e0 + 64 * k, N, v[2 * k], v[2 * k + 1]);
-      double sv = 0.0;
+      for (int k = 0; k < 32; ++k) {
+        double v0 = 0.0, v1 = 0.0;
+        if (base + k < nv) cg_ld(V + (int64_t)(base + k) * ld, e, N, v0, v1);
+        pp[k] = fma(v1, w1, v0 * w0);
+      }
 #pragma unroll
-      for (int k = 0; k < 2 * CG_K; ++k) sv = fma(v[k], w[k], sv);
-      sv = warp_sum(sv);
-      if (lane == (i & 31)) { if (i < 32) t0 += sv; else t1 += sv; }
+      for (int o = 16; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < o; ++k) {
+          const double keep = up ? pp[k + o] : pp[k];
+          const double send = up ? pp[k] : pp[k + o];
+          pp[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (c == 0) t0 += pp[0]; else t1 += pp[0];
     }
   }
   md_finish(t0, t1, nv, h2, site);
@@ -640,7 +659,7 @@ static etq_status arnoldi_step(Problem& P, bool reduced, etq_pc_kind kind, cudaS
   // CGS2: h = V^T w ; w -= V h ; h' = V^T w ; w -= V h' ; h += h' (k_gmres_scalar), in three passes
   const int gs = grid_for((N + CG_SEG - 1) / CG_SEG, BS / 32, RED_BLOCKS);
   k_multidot<<<gs, BS, 0, st>>>(P.gV, N, ld, P.gW, sc, Hcol, P.gred); etq_count_launch();
-  k_cgs_mid<<<gs, BS, 0, st>>>(P.gV, N, ld, P.gW, Hcol, sc, hh, P.gred); etq_count_launch();
+  k_cgs_mid<<<2 * 148, BS, 0, st>>>(P.gV, N, ld, P.gW, Hcol, sc, hh, P.gred); etq_count_launch();
   k_cgs_last<<<grid_for((N + 1) / 2, BS, RED_BLOCKS), BS, 0, st>>>(P.gV, N, ld, P.gW, hh, sc, P.red[0], 7, sc + G_HN);
   etq_count_launch();
   (void)gN;

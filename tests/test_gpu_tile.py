@@ -147,6 +147,33 @@ def test_saddle_apply_any_output_alignment(n):
     np.testing.assert_array_equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("n", [64, 512, 1024])
+def test_sgs_window_heights_agree(n):
+    """Chebyshev-SGS with 64 x 64 windows (512 threads) and 64 x 32 windows (256 threads, chosen
+    automatically when the large tiles would leave SMs idle, e.g. n = 512): both halos are the exact
+    dependency cone, so one symmetric sweep is bitwise the same; the Pi C Pi apply agrees to
+    rounding (its k^T y reduction runs over a different tile grid)."""
+    P = etq.Problem(n)
+    P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.005))
+    r = torch.as_tensor(synth.random_vector(P.n_p, seed=31), device="cuda")
+    y = torch.as_tensor(synth.random_vector(P.n_p, seed=32), device="cuda")
+    outs = {}
+    try:
+        for win in (1, 2):
+            etq.set_option(16, win)
+            z = torch.zeros(P.n_p, dtype=torch.float64, device="cuda")
+            P.sgs_sweep(r, y, z)
+            w = torch.zeros(P.n_p, dtype=torch.float64, device="cuda")
+            P.apply_mass_pc(r, w)
+            torch.cuda.synchronize()
+            outs[win] = (z.cpu().numpy(), w.cpu().numpy())
+    finally:
+        etq.set_option(16, 0)
+    P.close()
+    np.testing.assert_array_equal(outs[1][0], outs[2][0])
+    assert np.abs(outs[1][1] - outs[2][1]).max() <= 1e-14 * np.abs(outs[1][1]).max()
+
+
 @pytest.mark.parametrize("kind", [etq.PC_P2_GMG, etq.PC_P3])
 def test_device_minres_loop_matches_host_loop(kind):
     """MINRES as one CUDA graph with a while node (no host round trip per iteration) gives the same
