@@ -38,7 +38,8 @@ extern "C" {
  *   option 13 = programmatic dependent launches inside the V-cycle of P2 (0 [default]) - bitwise the same;
  *   option 14 = matrix-free interior rows of the cavity-wind F levels (1 [default]) or stored SELL rows (0);
  *   option 15 = Chebyshev-SGS y_prev read in the Q pass (1 [default]) or staged by cp.async (0) - bitwise;
- *   option 16 = Chebyshev-SGS window: 0 or 2 = 64 x 32 [default], 1 = 64 x 64 - bitwise sweeps.
+ *   option 16 = Chebyshev-SGS window: 0 = automatic [default: 64 x 32, with 512 threads when the tiles
+ *               fit one wave], 1 = 64 x 64, 2 = 64 x 32 / 256 threads, 3 = 64 x 32 / 512 threads - bitwise sweeps.
  * Applies to solves whose CUDA graphs are captured afterwards (re-run etq_precond_setup). */
 etq_status etq_debug_set_option(int32_t option, int32_t value);
 

@@ -23,7 +23,7 @@ bool g_cheb_tile3 = true;
 bool g_p2_vc_pdl = false;
 bool g_oseen_mf = true;
 bool g_sgs_yp_ldg = true; 
-int g_sgs_window = 0;               // etq_debug_set_option(16): Chebyshev-SGS window 0 auto, 1 64 x 64, 2 64 x 32          // etq_debug_set_option(15): Chebyshev-SGS y_prev loaded in the Q pass             // etq_debug_set_option(14): matrix-free interior rows of the cavity-wind F levels           // etq_debug_set_option(13): programmatic dependent launches inside P2's V-cycle           // etq_debug_set_option(12): smoother with the residual in registers (k_cheb_tile3)
+int g_sgs_window = 0;               // etq_debug_set_option(16): Chebyshev-SGS window 0 auto, 1 64x64, 2 64x32, 3 64x32 / 512 threads          // etq_debug_set_option(15): Chebyshev-SGS y_prev loaded in the Q pass             // etq_debug_set_option(14): matrix-free interior rows of the cavity-wind F levels           // etq_debug_set_option(13): programmatic dependent launches inside P2's V-cycle           // etq_debug_set_option(12): smoother with the residual in registers (k_cheb_tile3)
 bool g_cheb_tile2 = true;           // etq_set_option(11): leaner temporally blocked smoother (k_cheb_tile2)
 bool g_sgs_planar = false;          // etq_set_option(10): Chebyshev-SGS on parity planes with TMA windows
 bool g_vc_pdl = true;               // etq_set_option(8): programmatic dependent launches in the V-cycle
@@ -733,7 +733,7 @@ etq_status etq_debug_set_option(int32_t option, int32_t value) {
   if (option == 13) { g_p2_vc_pdl = value != 0; return ETQ_OK; }
   if (option == 14) { g_oseen_mf = value != 0; return ETQ_OK; }
   if (option == 15) { g_sgs_yp_ldg = value != 0; return ETQ_OK; }
-  if (option == 16) { if (value < 0 || value > 2) return ETQ_EINVAL; g_sgs_window = value; return ETQ_OK; }
+  if (option == 16) { if (value < 0 || value > 3) return ETQ_EINVAL; g_sgs_window = value; return ETQ_OK; }
   return ETQ_EINVAL;
 }
 

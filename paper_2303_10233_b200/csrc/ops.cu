@@ -1546,11 +1546,11 @@ constexpr int SGS_SMEM = (SGS_PAD + 8 * SGS_PL + 2 * SGS_TQ) * (int)sizeof(doubl
 static_assert(SGS_W - SGS_HX - SGS_TTX >= 6 && SGS_W - SGS_HY - SGS_TTY >= 2, "right / top halo");
 static_assert(SGS_HX % 2 == 0 && SGS_HY % 2 == 0 && SGS_TTX % 2 == 0 && SGS_TTY % 2 == 0, "even origins");
 static_assert(SGS_TX == SGS_P && 2 * SGS_TY == SGS_P, "one thread per plane column, two rows");
-// window geometry by height WY (64: a 64 x 64 window of 512 threads; 32: a 64 x 32 window of 256
-// threads, the default); the halos are unchanged
-#define SGS_GEO(WY_)                                                                              \
-  constexpr int TY_ = (WY_) / 4, PL_ = SGS_P * ((WY_) / 2), TTY_ = (WY_) - 6, TQ_ = SGS_TTX * TTY_; \
-  static_assert(2 * TY_ == (WY_) / 2 && TTY_ % 2 == 0, "two plane rows per thread");             \
+// window geometry by height WY (64 or 32 rows; 64 columns) and plane rows per thread MR (2: 512 / 256
+// threads, 1: 1024 / 512 threads); the halos are unchanged
+#define SGS_GEO(WY_, MR_)                                                                         \
+  constexpr int TY_ = (WY_) / 2 / (MR_), PL_ = SGS_P * ((WY_) / 2), TTY_ = (WY_) - 6, TQ_ = SGS_TTX * TTY_; \
+  static_assert((MR_) * TY_ == (WY_) / 2 && TTY_ % 2 == 0, "MR plane rows per thread");          \
   (void)TQ_
 template <int WY>
 constexpr int sgs_smem() { return (SGS_PAD + 8 * SGS_P * (WY / 2) + 2 * SGS_TTX * (WY - 6)) * (int)sizeof(double); }
@@ -1587,15 +1587,15 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 // update of colour (PX, PY): plane entries (i, j), j = ty + 16 m; vertex (2i + PX, 2j + PY)
-template <int WY, int PX, int PY, bool IN>
+template <int WY, int MR, int PX, int PY, bool IN>
 __device__ __forceinline__ void sgs_colour(double* __restrict__ V, const double* __restrict__ Cc,
-                                           const double (&rr)[2], int A0, int C0, int n, const SgsK& k) {
-  SGS_GEO(WY);
+                                           const double (&rr)[MR], int A0, int C0, int n, const SgsK& k) {
+  SGS_GEO(WY, MR);
   constexpr int c = PX + 2 * PY, cx = (1 - PX) + 2 * PY, cy = PX + 2 * (1 - PY), cxy = (1 - PX) + 2 * (1 - PY);
   constexpr int OW = PX - 1, OE = PX, OS = (PY - 1) * SGS_P, ON = PY * SGS_P;   // neighbour offsets
   const int i = threadIdx.x;
 #pragma unroll
-  for (int m = 0; m < 2; ++m) {
+  for (int m = 0; m < MR; ++m) {
     const int j = threadIdx.y + TY_ * m;
     const int B = j * SGS_P + i;
     const double* vd = V + cxy * PL_ + B;
@@ -1623,14 +1623,14 @@ __device__ __forceinline__ void sgs_colour(double* __restrict__ V, const double*
 }
 
 // P0 cells of parity plane (PE, PF): cell (2i + PE, 2j + PF) from its four vertices
-template <int WY, int PE, int PF, bool IN>
+template <int WY, int MR, int PE, int PF, bool IN>
 __device__ __forceinline__ void sgs_cells(const double* __restrict__ V, double* __restrict__ Cc,
-                                          const double (&rc)[2], int A0, int C0, int n, const SgsK& k) {
-  SGS_GEO(WY);
+                                          const double (&rc)[MR], int A0, int C0, int n, const SgsK& k) {
+  SGS_GEO(WY, MR);
   constexpr int p00 = PE + 2 * PF, p10 = (1 - PE) + 2 * PF, p01 = PE + 2 * (1 - PF), p11 = (1 - PE) + 2 * (1 - PF);
   const int i = threadIdx.x;
 #pragma unroll
-  for (int m = 0; m < 2; ++m) {
+  for (int m = 0; m < MR; ++m) {
     const int j = threadIdx.y + TY_ * m;
     const int B = j * SGS_P + i;
     const double sv = (V[p00 * PL_ + B] + V[p10 * PL_ + B + PE]) +
@@ -1645,9 +1645,9 @@ __device__ __forceinline__ void sgs_cells(const double* __restrict__ V, double* 
   }
 }
 
-template <int WY, bool IN>
+template <int WY, int MR, bool IN>
 __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, double* Cc, double* Q, int A0, int C0) {
-  SGS_GEO(WY);
+  SGS_GEO(WY, MR);
   const int i = threadIdx.x, ty = threadIdx.y;
   const int n = a.g.n, n1 = n + 1, nk = a.g.nk;
   const double alpha = a.kproj ? (*a.kproj * a.inv_kk) : 0.0;
@@ -1693,11 +1693,11 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
       cp_async8(Q + TQ_ + idx, yps + nk + (okc ? ga + (int64_t)n * gc : 0), okc);
     }
   }
-  double rv[4][2], rc[4][2];
+  double rv[4][MR], rc[4][MR];
 #pragma unroll
   for (int c = 0; c < 4; ++c)
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
+    for (int m = 0; m < MR; ++m) {
       const int j = ty + TY_ * m;
       const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
       const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
@@ -1742,12 +1742,12 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
   }
   __syncthreads();
   const SgsK& k = a.k;
-#define SGS_V(PX, PY) do { sgs_colour<WY, PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
+#define SGS_V(PX, PY) do { sgs_colour<WY, MR, PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
   SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
-  sgs_cells<WY, 0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);             // P0 (once: the backward sweep's
-  sgs_cells<WY, 1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);             // P0 update would repeat it exactly)
-  sgs_cells<WY, 0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
-  sgs_cells<WY, 1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
+  sgs_cells<WY, MR, 0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);             // P0 (once: the backward sweep's
+  sgs_cells<WY, MR, 1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);             // P0 update would repeat it exactly)
+  sgs_cells<WY, MR, 0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
+  sgs_cells<WY, MR, 1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
   __syncthreads();
   SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
 #undef SGS_V
@@ -1777,9 +1777,10 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
 #ifndef SGS_MINB
 #define SGS_MINB 2
 #endif
-template <int WY>
-__global__ void __launch_bounds__(SGS_TX * (WY / 4), WY == 64 ? SGS_MINB : 4) k_sgs_tile(SgsTileArgs a) {
-  SGS_GEO(WY);
+template <int WY, int MR>
+__global__ void __launch_bounds__(SGS_TX * (WY / 2 / MR), SGS_TX * (WY / 2 / MR) <= 256 ? 4 : (SGS_TX * (WY / 2 / MR) <= 512 ? SGS_MINB : 1))
+    k_sgs_tile(SgsTileArgs a) {
+  SGS_GEO(WY, MR);
   if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");   // previous step complete and visible
   if (is_done(a.done)) return;
   extern __shared__ double sm[];
@@ -1790,8 +1791,8 @@ __global__ void __launch_bounds__(SGS_TX * (WY / 4), WY == 64 ? SGS_MINB : 4) k_
   const int n = a.g.n;
   const int A0 = (blockIdx.x % a.tiles_x) * SGS_TTX - SGS_HX, C0 = (blockIdx.x / a.tiles_x) * TTY_ - SGS_HY;
   const bool interior = A0 >= 1 && A0 + SGS_W - 1 <= n - 1 && C0 >= 1 && C0 + WY - 1 <= n - 1;
-  if (interior) sgs_tile_body<WY, true>(a, V, Cc, Q, A0, C0);
-  else sgs_tile_body<WY, false>(a, V, Cc, Q, A0, C0);
+  if (interior) sgs_tile_body<WY, MR, true>(a, V, Cc, Q, A0, C0);
+  else sgs_tile_body<WY, MR, false>(a, V, Cc, Q, A0, C0);
 }
 
 // ---------------------------------------------------------------- SGS on parity planes (TMA)
@@ -1867,15 +1868,15 @@ __device__ __forceinline__ void sgsp_body(const SgsPlaneArgs& a, double* V, doub
   }
   __syncthreads();
   const SgsK& k = a.k;
-#define SGS_V(PX, PY) do { sgs_colour<SGS_W, PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
+#define SGS_V(PX, PY) do { sgs_colour<SGS_W, 2, PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
   SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
-  sgs_cells<SGS_W, 0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);             // P0 (once; see k_sgs_tile)
-  sgs_cells<SGS_W, 1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);
-  sgs_cells<SGS_W, 0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
-  sgs_cells<SGS_W, 1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
+  sgs_cells<SGS_W, 2, 0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);             // P0 (once; see k_sgs_tile)
+  sgs_cells<SGS_W, 2, 1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);
+  sgs_cells<SGS_W, 2, 0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
+  sgs_cells<SGS_W, 2, 1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
   __syncthreads();
   SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0);
-  sgs_colour<SGS_W, 0, 0, IN>(V, Cc, rv[0], A0, C0, n, k);            // backward colour 0: each thread reads back
+  sgs_colour<SGS_W, 2, 0, 0, IN>(V, Cc, rv[0], A0, C0, n, k);            // backward colour 0: each thread reads back
   __syncwarp();                                                 // only its own entries below
 #undef SGS_V
   asm volatile("griddepcontrol.launch_dependents;");
@@ -3385,17 +3386,25 @@ void mass_apply(const Geo& g, const double* x, double* y, cudaStream_t st) {
 }
 
 static void launch_sgs_tile(SgsTileArgs a, cudaStream_t st, bool pdl = false) {
-  static bool smem_set = false;
-  if (!smem_set) {
-    cudaFuncSetAttribute(k_sgs_tile<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, sgs_smem<64>());
-    cudaFuncSetAttribute(k_sgs_tile<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, sgs_smem<32>());
-    smem_set = true;
+  static int sms = 0;
+  if (!sms) {
+    cudaFuncSetAttribute(k_sgs_tile<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sgs_smem<64>());
+    cudaFuncSetAttribute(k_sgs_tile<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sgs_smem<32>());
+    cudaFuncSetAttribute(k_sgs_tile<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sgs_smem<32>());
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
   }
   a.tiles_x = (a.g.n + 1 + SGS_TTX - 1) / SGS_TTX;
   // 64 x 32 windows (256 threads, four CTAs per SM) by default: 12 % more redundant sweep work than
   // 64 x 64 windows (two per SM), but smaller CTAs fill the SMs left by the concurrent V-cycle
-  // better (measured, n = 1024, interleaved: Pi C Pi 600 -> 574 us, c3 814 -> 825 it/s; n = 512: equal)
-  const int wy = g_sgs_window == 1 ? 64 : 32;
+  // better (measured, n = 1024, interleaved: Pi C Pi 600 -> 574 us, c3 814 -> 825 it/s).  When the
+  // tiles fit in one wave of 512-thread CTAs (n <= 512), one plane row per thread (512 threads):
+  // the step is then the latency of one CTA, which this halves in the sweep
+  const int tiles32 = a.tiles_x * ((a.g.n + 1 + (32 - 6) - 1) / (32 - 6));
+  const int geo = g_sgs_window ? g_sgs_window : (tiles32 <= 2 * sms ? 3 : 2);
+  const int wy = geo == 1 ? 64 : 32, mr = geo == 3 ? 1 : 2;
   const int tiles = a.tiles_x * ((a.g.n + 1 + (wy - 6) - 1) / (wy - 6));
   {
     SgsK& k = a.k;
@@ -3410,7 +3419,7 @@ static void launch_sgs_tile(SgsTileArgs a, cudaStream_t st, bool pdl = false) {
   static int lo_prio = 1, hi_prio = 0;
   if (lo_prio == 1) cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(tiles); cfg.blockDim = dim3(SGS_TX, wy / 4);
+  cfg.gridDim = dim3(tiles); cfg.blockDim = dim3(SGS_TX, wy / 2 / mr);
   cfg.dynamicSmemBytes = wy == 64 ? sgs_smem<64>() : sgs_smem<32>(); cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributePriority;
@@ -3422,8 +3431,9 @@ static void launch_sgs_tile(SgsTileArgs a, cudaStream_t st, bool pdl = false) {
   a.pdl = pdl && g_sgs_pdl ? 1 : 0;
   a.yp_ldg = g_sgs_yp_ldg ? 1 : 0;
   cfg.attrs = attr; cfg.numAttrs = a.pdl ? 2 : 1;
-  if (wy == 64) cudaLaunchKernelEx(&cfg, k_sgs_tile<64>, a);
-  else cudaLaunchKernelEx(&cfg, k_sgs_tile<32>, a);
+  if (geo == 1) cudaLaunchKernelEx(&cfg, k_sgs_tile<64, 2>, a);
+  else if (geo == 3) cudaLaunchKernelEx(&cfg, k_sgs_tile<32, 1>, a);
+  else cudaLaunchKernelEx(&cfg, k_sgs_tile<32, 2>, a);
   etq_count_launch();
 }
 

@@ -149,17 +149,17 @@ def test_saddle_apply_any_output_alignment(n):
 
 @pytest.mark.parametrize("n", [64, 512, 1024])
 def test_sgs_window_heights_agree(n):
-    """Chebyshev-SGS with 64 x 64 windows (512 threads) and 64 x 32 windows (256 threads, chosen
-    automatically when the large tiles would leave SMs idle, e.g. n = 512): both halos are the exact
-    dependency cone, so one symmetric sweep is bitwise the same; the Pi C Pi apply agrees to
-    rounding (its k^T y reduction runs over a different tile grid)."""
+    """Chebyshev-SGS with 64 x 64 windows (512 threads), 64 x 32 windows with 256 threads (two plane
+    rows per thread) and with 512 threads (one row): every halo is the exact dependency cone, so one
+    symmetric sweep is bitwise the same; the Pi C Pi apply agrees to rounding (its k^T y reduction
+    runs over a different tile grid)."""
     P = etq.Problem(n)
     P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.005))
     r = torch.as_tensor(synth.random_vector(P.n_p, seed=31), device="cuda")
     y = torch.as_tensor(synth.random_vector(P.n_p, seed=32), device="cuda")
     outs = {}
     try:
-        for win in (1, 2):
+        for win in (1, 2, 3):
             etq.set_option(16, win)
             z = torch.zeros(P.n_p, dtype=torch.float64, device="cuda")
             P.sgs_sweep(r, y, z)
@@ -170,8 +170,9 @@ def test_sgs_window_heights_agree(n):
     finally:
         etq.set_option(16, 0)
     P.close()
-    np.testing.assert_array_equal(outs[1][0], outs[2][0])
-    assert np.abs(outs[1][1] - outs[2][1]).max() <= 1e-14 * np.abs(outs[1][1]).max()
+    for win in (2, 3):
+        np.testing.assert_array_equal(outs[1][0], outs[win][0])
+        assert np.abs(outs[1][1] - outs[win][1]).max() <= 1e-14 * np.abs(outs[1][1]).max()
 
 
 @pytest.mark.parametrize("kind", [etq.PC_P2_GMG, etq.PC_P3])
