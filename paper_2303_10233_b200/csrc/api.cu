@@ -192,6 +192,13 @@ etq_status etq_assemble(const etq_grid* grid, double viscosity, const etq_wind* 
     A_TRY(class_weights(P.g, P.Lv, &P.so0));
     A_TRY(saddle_weights(P.g, &P.sst, P.stream));
     P.mf_on = true;
+    P.bt_mf = true;
+  } else if (P.oseen && P.storage == 0 && P.g.n >= 16) {
+    // B / B^T do not depend on the wind: their class weights serve the matrix-free B^T of M1; the
+    // cavity wind's F is applied matrix-free from nu L class stencils and 1D tables (k_saddle_mf<1>)
+    A_TRY(saddle_weights(P.g, &P.sst, P.stream));
+    P.bt_mf = true;
+    if (P.wind == 1) A_TRY(oseen_tables(P.g, P.nu, &P.so_os, &P.os_tab0, P.stream));
   }
   A_TRY(assemble_bt(P.g, 0, 0, P.node_perm, nsl, &P.BxT1, P.stream));
   A_TRY(assemble_bt(P.g, 1, 0, P.node_perm, nsl, &P.ByT1, P.stream));
@@ -750,7 +757,7 @@ void etq_destroy(etq_problem* h) {
   free_hierarchy(P.mg);
   exact_free(P);
   oseen_free(P);
-  cudaFree(P.wnod); cudaFree(P.lv_lap); cudaFree(P.f1_lap);
+  cudaFree(P.wnod); cudaFree(P.lv_lap); cudaFree(P.f1_lap); cudaFree(P.os_tab0);
   P.Lv.perm = nullptr; P.BxT1.perm = nullptr; P.ByT1.perm = nullptr; P.BxT0.perm = nullptr; P.ByT0.perm = nullptr;
   sell_free(P.Lv); sell_free(P.BxT1); sell_free(P.ByT1); sell_free(P.BxT0); sell_free(P.ByT0); sell_free(P.B);
   if (P.node_perm) cudaFree(P.node_perm);

@@ -921,9 +921,8 @@ __global__ void k_oseen_tabs(Geo g, double nu, double* w, double* tab) {
 }
 }  // namespace
 
-etq_status build_oseen_stencil_level(const Geo& g, double nu, StencilOp* so, Sell* frame, double** tab,
-                                     cudaStream_t st) {
-  if (g.n < 16) return ETQ_EINVAL;
+// nu L class stencils (so->w) and the 1D convection tables of the cavity wind on grid g
+etq_status oseen_tables(const Geo& g, double nu, StencilOp* so, double** tab, cudaStream_t st) {
   StencilOp o;
   o.m = g.m; o.lo = 4; o.hi = g.m - 5;
   o.nseg_x = (o.hi - o.lo + 1 + 31) / 32;
@@ -935,6 +934,15 @@ etq_status build_oseen_stencil_level(const Geo& g, double nu, StencilOp* so, Sel
   ETQ_CHECK(cudaMemcpyAsync(&o.w[0][0], dw, sizeof(double) * 100, cudaMemcpyDeviceToHost, st));
   ETQ_CHECK(cudaStreamSynchronize(st));
   cudaFree(dw);
+  *so = o;
+  return ETQ_OK;
+}
+
+etq_status build_oseen_stencil_level(const Geo& g, double nu, StencilOp* so, Sell* frame, double** tab,
+                                     cudaStream_t st) {
+  if (g.n < 16) return ETQ_EINVAL;
+  StencilOp o;
+  ETQ_TRY(oseen_tables(g, nu, &o, tab, st));
   std::vector<int> rows;
   for (int c = 0; c < 4; ++c)
     for (int j = (c >> 1); j < g.m; j += 2)

@@ -280,6 +280,9 @@ struct Problem {
   Sell BxT1, ByT1, BxT0, ByT0;                // B^T split by component and pressure part
   Sell B;                                     // pressure rows (Q1 then P0) over [u_x; u_y]
   bool mf_on = false;                         // Stokes storage 0: matrix-free saddle apply (k_saddle_mf)
+  bool bt_mf = false;                         // storage 0: sst holds the B / B^T class weights (any wind)
+  double* os_tab0 = nullptr;                  // Oseen cavity wind, storage 0: 1D convection tables of level 0
+  StencilOp so_os;                            // ... and the nu L class stencils (matrix-free Oseen saddle apply)
   StencilOp so0;                              // class stencil of L (level 0)
   SaddleSt sst;                               // B / B^T weights
   int* node_perm = nullptr;                   // shared by Lv and the B^T blocks
@@ -371,6 +374,7 @@ etq_status mark_implicit(const Geo& g, bool oseen, double nu, int wind, Sell& S,
 etq_status build_stencil_level(const Geo& g, const Sell& A, StencilOp* so, Sell* frame, cudaStream_t st);
 etq_status build_oseen_stencil_level(const Geo& g, double nu, StencilOp* so, Sell* frame, double** tab,
                                      cudaStream_t st);
+etq_status oseen_tables(const Geo& g, double nu, StencilOp* so, double** tab, cudaStream_t st);
 etq_status saddle_weights(const Geo& g, SaddleSt* out, cudaStream_t st);
 etq_status class_weights(const Geo& g, const Sell& A, StencilOp* so);
 

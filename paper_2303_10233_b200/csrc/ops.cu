@@ -97,7 +97,11 @@ struct SaddleMfArgs {
   int nq, nk; int64_t n_u, n_p; int reduced;
   const double* x; double* y; const double* inv_scale;
   RedSite site; int slot; double* dot_out; const double* done;
+  const double* tab;          // OS: 1D convection tables A1, T2 [2][m][5] of the cavity wind
 };
+// OS = 1: the Oseen operator [F B^T; B 0] of the cavity wind, F = nu L + N with the interior weights
+// nu L_class(di, dj) + A1_i(di) T2_j(dj) - T2_i(di) A1_j(dj) (reading R9'; not the stored-row order)
+template <int OS>
 __global__ void __launch_bounds__(BS) k_saddle_mf(SaddleMfArgs a) {
   if (is_done(a.done)) return;
   const double sc = a.inv_scale ? *a.inv_scale : 1.0;
@@ -121,15 +125,23 @@ __global__ void __launch_bounds__(BS) k_saddle_mf(SaddleMfArgs a) {
         const double* w = a.so.w[cl];
         const bool near = i < 3 || j < 3 || i > m - 4 || j > m - 4;
         double a0 = 0.0, a1 = 0.0;
+        double ai[5], ti[5];
+        if (OS) {
+#pragma unroll
+          for (int d = 0; d < 5; ++d) { ai[d] = __ldg(a.tab + 5 * i + d); ti[d] = __ldg(a.tab + 5 * (m + i) + d); }
+        }
         for (int dj = -2; dj <= 2; ++dj) {
           if ((j & 1) && (dj == 2 || dj == -2)) continue;
           const int jt = j + dj;
           if (near && (jt <= 0 || jt >= m - 1)) continue;
           const int rb = node + dj * m;
+          double aj = 0.0, tj = 0.0;
+          if (OS) { aj = __ldg(a.tab + 5 * j + dj + 2); tj = __ldg(a.tab + 5 * (m + j) + dj + 2); }
 #pragma unroll
           for (int di = -2; di <= 2; ++di) {
             if (near && (i + di <= 0 || i + di >= m - 1)) continue;
-            const double wv = w[(dj + 2) * 5 + (di + 2)];
+            double wv = w[(dj + 2) * 5 + (di + 2)];
+            if (OS) wv = fma(ai[di + 2], tj, fma(-ti[di + 2], aj, wv));
             a0 = fma(wv, __ldg(xu + rb + di), a0);
             a1 = fma(wv, __ldg(xv + rb + di), a1);
           }
@@ -2369,6 +2381,15 @@ void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y
   a.nq = P.g.nq; a.nk = P.g.nk; a.n_u = P.n_u; a.n_p = P.n_p; a.reduced = reduced ? 1 : 0;
   a.x = x; a.y = y; a.inv_scale = inv_scale;
   a.site = site ? *site : RedSite{}; a.slot = slot; a.dot_out = dot_out; a.done = done;
+  if (P.os_tab0 && g_oseen_mf) {   // Oseen cavity wind, storage 0: matrix-free F, B^T, B
+    SaddleMfArgs b;
+    b.so = P.so_os; b.w = P.sst;
+    b.nq = P.g.nq; b.nk = P.g.nk; b.n_u = P.n_u; b.n_p = P.n_p; b.reduced = a.reduced;
+    b.x = x; b.y = y; b.inv_scale = inv_scale; b.site = a.site; b.slot = slot; b.dot_out = dot_out; b.done = done;
+    b.tab = P.os_tab0;
+    k_saddle_mf<1><<<grid_for(P.N, BS, 8 * 148 * 2), BS, 0, st>>>(b); etq_count_launch();
+    return;
+  }
   if (P.mf_on && g_saddle_mf) {
     SaddleMfArgs b;
     b.so = P.so0; b.w = P.sst;
@@ -2390,7 +2411,8 @@ void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y
       k_saddle_tile<<<t.tiles_x * t.tiles_x, ST_THREADS, ST_SMEM, st>>>(t); etq_count_launch();
       return;
     }
-    k_saddle_mf<<<grid_for(P.N, BS, 8 * 148 * 2), BS, 0, st>>>(b); etq_count_launch();
+    b.tab = nullptr;
+    k_saddle_mf<0><<<grid_for(P.N, BS, 8 * 148 * 2), BS, 0, st>>>(b); etq_count_launch();
     return;
   }
   const int64_t warps = P.Lv.nslices + P.B.nslices;

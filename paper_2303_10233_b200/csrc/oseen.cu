@@ -102,6 +102,60 @@ __global__ void __launch_bounds__(BS) k_bt_sub(BtSubArgs a) {
   }
 }
 
+// t_u = r_u - B^T z_p matrix-free (storage 0): every non-Dirichlet velocity row of B^T is its class
+// stencil over the 3 x 3 Q1 vertices and 2 x 2 P0 cells around it (SaddleSt, wind-independent);
+// Dirichlet rows of B^T are empty.  One thread per node, both components.
+struct BtMfArgs {
+  SaddleSt w; int m, n, nq, nk, reduced;
+  const double* r_u; const double* z_p; double* t_u; const double* done;
+};
+__global__ void __launch_bounds__(BS) k_bt_sub_mf(BtMfArgs a) {
+  if (is_done(a.done)) return;
+  const int m = a.m, n = a.n, n1 = n + 1;
+  const double* __restrict__ p1 = a.z_p;
+  const double* __restrict__ p0 = a.z_p + a.nk;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < a.nq; t += (int64_t)gridDim.x * blockDim.x) {
+    const int node = (int)t, i = node % m, j = node / m;
+    double bx = 0.0, by = 0.0;
+    if (!(i == 0 || j == 0 || i == m - 1 || j == m - 1)) {
+      const int cl = (j & 1) * 2 + (i & 1);
+      const int ia = i / 2, jc = j / 2;
+#pragma unroll
+      for (int dc = -1; dc <= 1; ++dc) {
+        const int c = jc + dc;
+        if (c < 0 || c > n) continue;
+#pragma unroll
+        for (int da = -1; da <= 1; ++da) {
+          const int aa = ia + da;
+          if (aa < 0 || aa > n) continue;
+          const double pv = __ldg(p1 + aa + (int64_t)n1 * c);
+          bx = fma(a.w.bt1[cl][0][(dc + 1) * 3 + da + 1], pv, bx);
+          by = fma(a.w.bt1[cl][1][(dc + 1) * 3 + da + 1], pv, by);
+        }
+      }
+      if (!a.reduced) {
+        double cx = 0.0, cy = 0.0;
+#pragma unroll
+        for (int df = -1; df <= 0; ++df) {
+          const int f = jc + df;
+          if (f < 0 || f >= n) continue;
+#pragma unroll
+          for (int de = -1; de <= 0; ++de) {
+            const int e = ia + de;
+            if (e < 0 || e >= n) continue;
+            const double pv = __ldg(p0 + e + (int64_t)n * f);
+            cx = fma(a.w.bt0[cl][0][(df + 1) * 2 + de + 1], pv, cx);
+            cy = fma(a.w.bt0[cl][1][(df + 1) * 2 + de + 1], pv, cy);
+          }
+        }
+        bx += cx; by += cy;
+      }
+    }
+    a.t_u[node] = __ldg(a.r_u + node) - bx;
+    a.t_u[a.nq + node] = __ldg(a.r_u + a.nq + node) - by;
+  }
+}
+
 // t_u = minv o (B^T z_p) (both parts; minv = 1 / Mdiag, zero on Dirichlet nodes)
 __global__ void __launch_bounds__(BS) k_bt_minv(BtSubArgs a, const double* minv) {
   if (is_done(a.done)) return;
@@ -555,11 +609,19 @@ etq_status oseen_precond_apply(const Problem& P, etq_pc_kind kind, const double*
   } else {
     return ETQ_EINVAL;
   }
+  if (P.bt_mf && g_oseen_mf) {
+    BtMfArgs b;
+    b.w = P.sst; b.m = P.g.m; b.n = P.g.n; b.nq = P.g.nq; b.nk = P.g.nk;
+    b.reduced = kind == ETQ_PC_OSEEN_PCD1 ? 1 : 0;
+    b.r_u = r; b.z_p = z + nu; b.t_u = P.tu; b.done = done;
+    k_bt_sub_mf<<<grid_for(P.g.nq, BS, 8 * 148), BS, 0, st>>>(b); etq_count_launch();
+  } else {
   BtSubArgs a;
   a.BxT1 = P.BxT1; a.ByT1 = P.ByT1; a.BxT0 = P.BxT0; a.ByT0 = P.ByT0; a.nq = P.g.nq; a.nk = P.g.nk;
   a.reduced = kind == ETQ_PC_OSEEN_PCD1 ? 1 : 0;
   a.r_u = r; a.z_p = z + nu; a.t_u = P.tu; a.done = done;
   k_bt_sub<<<grid_for(P.BxT1.nslices * 32, BS, 4096), BS, 0, st>>>(a); etq_count_launch();
+  }
   return vcycle_apply_ex(P, P.mg, P.tu, z, nullptr, 0, nullptr, nullptr, done, st);
 }
 

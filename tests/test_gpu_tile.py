@@ -175,6 +175,36 @@ def test_sgs_window_heights_agree(n):
         assert np.abs(outs[1][1] - outs[win][1]).max() <= 1e-14 * np.abs(outs[1][1]).max()
 
 
+@pytest.mark.parametrize("n", [16, 64, 256])
+def test_oseen_matrix_free_rows_match_stored_rows(n):
+    """Cavity-wind Oseen problem (storage 0): the matrix-free F (nu L class stencils + 1D convection
+    tables), B^T and B of the saddle apply (full and reduced), the matrix-free B^T of M1 and the
+    matrix-free interior rows of the F V-cycle levels agree with the stored SELL rows to rounding
+    (debug option 14 switches all of them)."""
+    out = {}
+    try:
+        for opt in (0, 1):
+            etq.set_option(14, opt)
+            P = etq.Problem(n, bc=0, viscosity=0.01, wind=1)
+            P.precond_setup(etq.PC_OSEEN_M1, etq.make_params(cheb_sgs_lo=0.005, coarse_n=8))
+            x = torch.as_tensor(synth.random_vector(P.N, seed=41), device="cuda")
+            res = []
+            for red in (False, True):
+                y = torch.zeros(P.N, dtype=torch.float64, device="cuda")
+                P.apply_saddle(x, y, reduced=red)
+                res.append(y.cpu().numpy())
+            z = torch.zeros(P.N, dtype=torch.float64, device="cuda")
+            P.apply_precond(etq.PC_OSEEN_M1, x, z)
+            torch.cuda.synchronize()
+            res.append(z.cpu().numpy())
+            out[opt] = res
+            P.close()
+    finally:
+        etq.set_option(14, 1)
+    for a, b in zip(out[0], out[1]):
+        assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
+
+
 @pytest.mark.parametrize("kind", [etq.PC_P2_GMG, etq.PC_P3])
 def test_device_minres_loop_matches_host_loop(kind):
     """MINRES as one CUDA graph with a while node (no host round trip per iteration) gives the same
