@@ -1650,7 +1650,7 @@ __device__ __forceinline__ void sgs_colour(double* __restrict__ V, const double*
 }
 
 // P0 cells of parity plane (PE, PF): cell (2i + PE, 2j + PF) from its four vertices
-template <int WY, int MR, int PE, int PF, bool IN>
+template <int WY, int MR, int PE, int PF, bool IN, bool ADJ = false>
 __device__ __forceinline__ void sgs_cells(const double* __restrict__ V, double* __restrict__ Cc,
                                           const double (&rc)[MR], int A0, int C0, int n, const SgsK& k) {
   SGS_GEO(WY, MR);
@@ -1658,7 +1658,7 @@ __device__ __forceinline__ void sgs_cells(const double* __restrict__ V, double* 
   const int i = threadIdx.x;
 #pragma unroll
   for (int m = 0; m < MR; ++m) {
-    const int j = threadIdx.y + TY_ * m;
+    const int j = ADJ ? 2 * (int)threadIdx.y + m : threadIdx.y + TY_ * m;
     const int B = j * SGS_P + i;
     const double sv = (V[p00 * PL_ + B] + V[p10 * PL_ + B + PE]) +
                       (V[p01 * PL_ + B + PF * SGS_P] + V[p11 * PL_ + B + PF * SGS_P + PE]);
@@ -1669,6 +1669,75 @@ __device__ __forceinline__ void sgs_cells(const double* __restrict__ V, double* 
       in = e >= 0 && e < n && f >= 0 && f < n;
     }
     Cc[p00 * PL_ + B] = in ? z : 0.0;
+  }
+}
+
+// Two ADJACENT plane rows per thread (j0 = 2 ty, j1 = j0 + 1; MR = 2 in k_sgs_tile): the rows
+// j0 + PY - 1 .. j0 + PY + 1 of the diagonal and y-neighbour planes serve both updates (9 loads
+// instead of 12), and the four cells of each vertex enter through sums formed once per sweep
+// direction (the cells only change in the P0 phase between the two directions): 13 shared loads per
+// colour and thread instead of 24.  Same expressions in the same order as sgs_colour (bitwise).
+template <int WY>
+__device__ __forceinline__ void sgs_cellsums(const double* __restrict__ Cc, double (&S)[4][2]) {
+  SGS_GEO(WY, 2);
+  const int i = threadIdx.x, j0 = 2 * threadIdx.y;
+  const double* c00 = Cc;
+  const double* c10 = Cc + PL_;
+  const double* c01 = Cc + 2 * PL_;
+  const double* c11 = Cc + 3 * PL_;
+  double a11m[3], a11[3], a01[3], a10m[2], a10[2], a00[2];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {          // rows j0 - 1, j0, j1
+    const int B = (j0 - 1 + r) * SGS_P + i;
+    a11m[r] = c11[B - 1]; a11[r] = c11[B]; a01[r] = c01[B];
+  }
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {          // rows j0, j1
+    const int B = (j0 + m) * SGS_P + i;
+    a10m[m] = c10[B - 1]; a10[m] = c10[B]; a00[m] = c00[B];
+  }
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    S[0][m] = (a11m[m] + a01[m]) + (a10m[m] + a00[m]);            // colour (0, 0)
+    S[1][m] = (a01[m] + a11[m]) + (a00[m] + a10[m]);              // colour (1, 0)
+    S[2][m] = (a10m[m] + a00[m]) + (a11m[m + 1] + a01[m + 1]);    // colour (0, 1)
+    S[3][m] = (a00[m] + a10[m]) + (a01[m + 1] + a11[m + 1]);      // colour (1, 1)
+  }
+}
+
+template <int WY, int PX, int PY, bool IN>
+__device__ __forceinline__ void sgs_colour_adj(double* __restrict__ V, const double (&sc)[2], const double (&rr)[2],
+                                               int A0, int C0, int n, const SgsK& k) {
+  SGS_GEO(WY, 2);
+  constexpr int c = PX + 2 * PY, cx = (1 - PX) + 2 * PY, cy = PX + 2 * (1 - PY), cxy = (1 - PX) + 2 * (1 - PY);
+  constexpr int OW = PX - 1, OE = PX;
+  const int i = threadIdx.x, j0 = 2 * threadIdx.y;
+  double D[3][2], Y[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {          // rows j0 + PY - 1 + r
+    const int B = (j0 + PY - 1 + r) * SGS_P + i;
+    D[r][0] = V[cxy * PL_ + B + OW]; D[r][1] = V[cxy * PL_ + B + OE];
+    Y[r] = V[cy * PL_ + B];
+  }
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    const int j = j0 + m;
+    const int B = j * SGS_P + i;
+    const double sd = (D[m][0] + D[m][1]) + (D[m + 1][0] + D[m + 1][1]);
+    const double sx = V[cx * PL_ + B + OW] + V[cx * PL_ + B + OE];
+    const double sy = Y[m] + Y[m + 1];
+    double wx = k.c_ed, wy = k.c_ed, inv = k.inv_in2;
+    bool in = true;
+    if (!IN) {
+      const int ga = A0 + 2 * i + PX, gc = C0 + 2 * j + PY;
+      in = ga >= 0 && ga <= n && gc >= 0 && gc <= n;
+      const bool bx = ga == 0 || ga == n, by = gc == 0 || gc == n;
+      wx = by ? k.w_off * k.w_bd : k.c_ed;
+      wy = bx ? k.w_bd * k.w_off : k.c_ed;
+      inv = bx ? (by ? k.inv_bd2 : k.inv_inbd) : (by ? k.inv_inbd : k.inv_in2);
+    }
+    const double s = rr[m] - k.c_dd * sd - wx * sx - wy * sy - k.rq * sc[m];
+    V[c * PL_ + B] = in ? s * inv : 0.0;
   }
 }
 
@@ -1725,12 +1794,13 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
   for (int c = 0; c < 4; ++c)
 #pragma unroll
     for (int m = 0; m < MR; ++m) {
-      const int j = ty + TY_ * m;
+      const int j = MR == 2 ? 2 * ty + m : ty + TY_ * m;   // MR = 2: adjacent rows (sgs_colour_adj)
       const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
       const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
       const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
       rv[c][m] = inv ? __ldg(r1 + ga + (int64_t)n1 * gc) - alpha : 0.0;
-      rc[c][m] = inc ? __ldg(r0 + ga + (int64_t)n * gc) + alpha : 0.0;
+      if (MR != 2) rc[c][m] = inc ? __ldg(r0 + ga + (int64_t)n * gc) + alpha : 0.0;
+      (void)inc;
     }
   cp_async_wait_all();
   __syncthreads();
@@ -1769,15 +1839,41 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
   }
   __syncthreads();
   const SgsK& k = a.k;
-#define SGS_V(PX, PY) do { sgs_colour<WY, MR, PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
-  SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
-  sgs_cells<WY, MR, 0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);             // P0 (once: the backward sweep's
-  sgs_cells<WY, MR, 1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);             // P0 update would repeat it exactly)
-  sgs_cells<WY, MR, 0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
-  sgs_cells<WY, MR, 1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
-  __syncthreads();
-  SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
+  if constexpr (MR == 2) {
+    double S[4][2];
+    sgs_cellsums<WY>(Cc, S);                                       // cells of the forward sweep
+#define SGS_V(PX, PY) do { sgs_colour_adj<WY, PX, PY, IN>(V, S[PX + 2 * PY], rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
+    SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
+    // the cells' right-hand side read only now (L1 / L2): not held in registers through the
+    // forward sweep, where the cell sums S are live
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int m = 0; m < MR; ++m) {
+        const int j = 2 * ty + m;
+        const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
+        const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
+        rc[c][m] = inc ? __ldg(r0 + ga + (int64_t)n * gc) + alpha : 0.0;
+      }
+    sgs_cells<WY, MR, 0, 0, IN, true>(V, Cc, rc[0], A0, C0, n, k);   // P0 (once: the backward sweep's
+    sgs_cells<WY, MR, 1, 0, IN, true>(V, Cc, rc[1], A0, C0, n, k);   // P0 update would repeat it exactly)
+    sgs_cells<WY, MR, 0, 1, IN, true>(V, Cc, rc[2], A0, C0, n, k);
+    sgs_cells<WY, MR, 1, 1, IN, true>(V, Cc, rc[3], A0, C0, n, k);
+    __syncthreads();
+    sgs_cellsums<WY>(Cc, S);                                       // cells after the P0 update
+    SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
 #undef SGS_V
+  } else {
+#define SGS_V(PX, PY) do { sgs_colour<WY, MR, PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
+    SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
+    sgs_cells<WY, MR, 0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);
+    sgs_cells<WY, MR, 1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);
+    sgs_cells<WY, MR, 0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
+    sgs_cells<WY, MR, 1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
+    __syncthreads();
+    SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
+#undef SGS_V
+  }
   // the next step's CTAs may launch once every CTA of this grid is writing its tile (they wait in
   // griddepcontrol.wait; triggering at the start would park them on SMs the V-cycle needs)
   asm volatile("griddepcontrol.launch_dependents;");
