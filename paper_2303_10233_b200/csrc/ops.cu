@@ -1741,6 +1741,84 @@ __device__ __forceinline__ void sgs_colour_adj(double* __restrict__ V, const dou
   }
 }
 
+// The thread's own vertex values own[plane][m] (plane entries (i, j0 + m) of the four vertex planes)
+// are kept in registers through the whole sweep: the thread is their only writer, so every read of
+// column i on rows j0 / j1 comes from registers (7 shared loads per colour instead of 13, the P0
+// phase's own-column vertices likewise).  Same values, same expressions, same order (bitwise).
+template <int WY, int PX, int PY, bool IN>
+__device__ __forceinline__ void sgs_colour_own(double* __restrict__ V, double (&own)[4][2], const double (&sc)[2],
+                                               const double (&rr)[2], int A0, int C0, int n, const SgsK& k) {
+  SGS_GEO(WY, 2);
+  constexpr int c = PX + 2 * PY, cx = (1 - PX) + 2 * PY, cy = PX + 2 * (1 - PY), cxy = (1 - PX) + 2 * (1 - PY);
+  constexpr int OW = PX - 1, OE = PX;
+  constexpr int RL = PY == 0 ? 0 : 2;     // the one row of j0 + PY - 1 .. j0 + PY + 1 that is not own
+  const int i = threadIdx.x, j0 = 2 * threadIdx.y;
+  double D[3][2], Y[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {          // rows j0 + PY - 1 + r; own rows: r - PY + 1 in {0, 1}
+    const int B = (j0 + PY - 1 + r) * SGS_P + i;
+    if (r == RL) {
+      D[r][0] = V[cxy * PL_ + B + OW]; D[r][1] = V[cxy * PL_ + B + OE];
+      Y[r] = V[cy * PL_ + B];
+    } else {
+      const int m = r + PY - 1;
+      if (PX == 0) { D[r][0] = V[cxy * PL_ + B + OW]; D[r][1] = own[cxy][m]; }   // OE = 0: own column
+      else { D[r][0] = own[cxy][m]; D[r][1] = V[cxy * PL_ + B + OE]; }           // OW = 0: own column
+      Y[r] = own[cy][m];
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    const int j = j0 + m;
+    const int B = j * SGS_P + i;
+    const double sd = (D[m][0] + D[m][1]) + (D[m + 1][0] + D[m + 1][1]);
+    const double sx = PX == 0 ? V[cx * PL_ + B + OW] + own[cx][m] : own[cx][m] + V[cx * PL_ + B + OE];
+    const double sy = Y[m] + Y[m + 1];
+    double wx = k.c_ed, wy = k.c_ed, inv = k.inv_in2;
+    bool in = true;
+    if (!IN) {
+      const int ga = A0 + 2 * i + PX, gc = C0 + 2 * j + PY;
+      in = ga >= 0 && ga <= n && gc >= 0 && gc <= n;
+      const bool bx = ga == 0 || ga == n, by = gc == 0 || gc == n;
+      wx = by ? k.w_off * k.w_bd : k.c_ed;
+      wy = bx ? k.w_bd * k.w_off : k.c_ed;
+      inv = bx ? (by ? k.inv_bd2 : k.inv_inbd) : (by ? k.inv_inbd : k.inv_in2);
+    }
+    const double s = rr[m] - k.c_dd * sd - wx * sx - wy * sy - k.rq * sc[m];
+    const double v = in ? s * inv : 0.0;
+    V[c * PL_ + B] = v;
+    own[c][m] = v;
+  }
+}
+
+// P0 cells of parity plane (PE, PF) on the rows j0, j1, own-column vertices from registers
+template <int WY, int PE, int PF, bool IN>
+__device__ __forceinline__ void sgs_cells_own(const double* __restrict__ V, const double (&own)[4][2],
+                                              double* __restrict__ Cc, const double (&rc)[2], int A0, int C0, int n,
+                                              const SgsK& k) {
+  SGS_GEO(WY, 2);
+  constexpr int p00 = PE + 2 * PF, p10 = (1 - PE) + 2 * PF, p01 = PE + 2 * (1 - PF), p11 = (1 - PE) + 2 * (1 - PF);
+  const int i = threadIdx.x, j0 = 2 * threadIdx.y;
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    const int j = j0 + m;
+    const int B = j * SGS_P + i;
+    const bool up_own = PF == 0 || m == 0;          // row j + PF is own
+    const double v00 = own[p00][m];
+    const double v10 = PE == 0 ? own[p10][m] : V[p10 * PL_ + B + PE];
+    const double v01 = up_own ? own[p01][m + PF] : V[p01 * PL_ + B + PF * SGS_P];
+    const double v11 = (PE == 0 && up_own) ? own[p11][m + PF] : V[p11 * PL_ + B + PF * SGS_P + PE];
+    const double sv = (v00 + v10) + (v01 + v11);
+    const double z = (rc[m] - k.rq * sv) * k.inv_q0;
+    bool in = true;
+    if (!IN) {
+      const int e = A0 + 2 * i + PE, f = C0 + 2 * j + PF;
+      in = e >= 0 && e < n && f >= 0 && f < n;
+    }
+    Cc[p00 * PL_ + B] = in ? z : 0.0;
+  }
+}
+
 template <int WY, int MR, bool IN>
 __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, double* Cc, double* Q, int A0, int C0) {
   SGS_GEO(WY, MR);
@@ -1798,9 +1876,11 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
       const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
       const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
       const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
-      rv[c][m] = inv ? __ldg(r1 + ga + (int64_t)n1 * gc) - alpha : 0.0;
-      if (MR != 2) rc[c][m] = inc ? __ldg(r0 + ga + (int64_t)n * gc) + alpha : 0.0;
-      (void)inc;
+      if (MR != 2) {
+        rv[c][m] = inv ? __ldg(r1 + ga + (int64_t)n1 * gc) - alpha : 0.0;
+        rc[c][m] = inc ? __ldg(r0 + ga + (int64_t)n * gc) + alpha : 0.0;
+      }
+      (void)inc; (void)inv;
     }
   cp_async_wait_all();
   __syncthreads();
@@ -1841,8 +1921,27 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
   const SgsK& k = a.k;
   if constexpr (MR == 2) {
     double S[4][2];
+    double own[4][2];
+    {
+      const int j0 = 2 * ty;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int m = 0; m < 2; ++m) own[c][m] = V[c * PL_ + (j0 + m) * SGS_P + i];
+    }
     sgs_cellsums<WY>(Cc, S);                                       // cells of the forward sweep
-#define SGS_V(PX, PY) do { sgs_colour_adj<WY, PX, PY, IN>(V, S[PX + 2 * PY], rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
+    // the vertices' right-hand side read per colour (L1 / L2) instead of held in registers
+    auto rv_of = [&](int c, double (&rr)[2]) {
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int j = 2 * ty + m;
+        const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
+        const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
+        rr[m] = inv ? __ldg(r1 + ga + (int64_t)n1 * gc) - alpha : 0.0;
+      }
+    };
+#define SGS_V(PX, PY) do { double rr_[2]; rv_of(PX + 2 * PY, rr_); \
+      sgs_colour_own<WY, PX, PY, IN>(V, own, S[PX + 2 * PY], rr_, A0, C0, n, k); __syncthreads(); } while (0)
     SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
     // the cells' right-hand side read only now (L1 / L2): not held in registers through the
     // forward sweep, where the cell sums S are live
@@ -1855,10 +1954,10 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
         const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
         rc[c][m] = inc ? __ldg(r0 + ga + (int64_t)n * gc) + alpha : 0.0;
       }
-    sgs_cells<WY, MR, 0, 0, IN, true>(V, Cc, rc[0], A0, C0, n, k);   // P0 (once: the backward sweep's
-    sgs_cells<WY, MR, 1, 0, IN, true>(V, Cc, rc[1], A0, C0, n, k);   // P0 update would repeat it exactly)
-    sgs_cells<WY, MR, 0, 1, IN, true>(V, Cc, rc[2], A0, C0, n, k);
-    sgs_cells<WY, MR, 1, 1, IN, true>(V, Cc, rc[3], A0, C0, n, k);
+    sgs_cells_own<WY, 0, 0, IN>(V, own, Cc, rc[0], A0, C0, n, k);   // P0 (once: the backward sweep's
+    sgs_cells_own<WY, 1, 0, IN>(V, own, Cc, rc[1], A0, C0, n, k);   // P0 update would repeat it exactly)
+    sgs_cells_own<WY, 0, 1, IN>(V, own, Cc, rc[2], A0, C0, n, k);
+    sgs_cells_own<WY, 1, 1, IN>(V, own, Cc, rc[3], A0, C0, n, k);
     __syncthreads();
     sgs_cellsums<WY>(Cc, S);                                       // cells after the P0 update
     SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
