@@ -1979,19 +1979,28 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
   // ---- write the tile: out = co_s S(y) + Q, row-major (coalesced global rows)
   const double co_s = a.mode ? a.omega * a.gam : 1.0;
   double kd = 0.0;
-  for (int idx = tid; idx < SGS_TTX * TTY_; idx += SGS_TX * TY_) {
-    const int la = SGS_HX + idx % SGS_TTX, lc = SGS_HY + idx / SGS_TTX, ga = A0 + la, gc = C0 + lc;
+  // tile entries idx = tid + q NT walked without divisions: (column, row) and the two output
+  // pointers advance by NT = 5 x 50 + 6 (256 threads) resp. 10 x 50 + 12 (512), with a wrap
+  constexpr int NT = SGS_TX * TY_, DC = NT % SGS_TTX, DR = NT / SGS_TTX;
+  int tc = tid % SGS_TTX, tr = tid / SGS_TTX;
+  double* ov = a.out + (A0 + SGS_HX + tc) + (int64_t)n1 * (C0 + SGS_HY + tr);
+  double* oc = a.out + nk + (A0 + SGS_HX + tc) + (int64_t)n * (C0 + SGS_HY + tr);
+  const int64_t sv = DC + (int64_t)DR * n1, sc = DC + (int64_t)DR * n;
+  for (int idx = tid; idx < SGS_TTX * TTY_; idx += NT) {
+    const int la = SGS_HX + tc, lc = SGS_HY + tr, ga = A0 + la, gc = C0 + lc;
     const int pl = ((la & 1) + 2 * (lc & 1)) * PL_ + (lc >> 1) * SGS_P + (la >> 1);
     if (IN || (ga <= n && gc <= n)) {
       const double o = fma(co_s, V[pl], Q[idx]);
-      a.out[ga + (int64_t)n1 * gc] = o;
+      *ov = o;
       kd += o;
     }
     if (IN || (ga < n && gc < n)) {
       const double o = fma(co_s, Cc[pl], Q[TQ_ + idx]);
-      a.out[nk + ga + (int64_t)n * gc] = o;
+      *oc = o;
       kd -= o;
     }
+    tc += DC; tr += DR; ov += sv; oc += sc;
+    if (tc >= SGS_TTX) { tc -= SGS_TTX; ++tr; ov += n1 - SGS_TTX; oc += n - SGS_TTX; }
   }
   if (a.kout) { double v[1] = {kd}; reduce_finish<1>(v, a.site, a.slot, a.kout); }
 }
