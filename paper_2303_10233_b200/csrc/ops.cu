@@ -1819,6 +1819,93 @@ __device__ __forceinline__ void sgs_cells_own(const double* __restrict__ V, cons
   }
 }
 
+// The same register forwarding with ONE plane row per thread (MR = 1, 512-thread 64 x 32 windows):
+// own[plane] = the thread's entry (i, j); 5 shared loads per colour instead of 12 (cells by sums)
+template <int WY>
+__device__ __forceinline__ void sgs_cellsums1(const double* __restrict__ Cc, double (&S)[4]) {
+  SGS_GEO(WY, 1);
+  const int i = threadIdx.x, j = threadIdx.y;
+  const double* c00 = Cc;
+  const double* c10 = Cc + PL_;
+  const double* c01 = Cc + 2 * PL_;
+  const double* c11 = Cc + 3 * PL_;
+  double a11m[2], a11[2], a01[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {          // rows j - 1, j
+    const int B = (j - 1 + r) * SGS_P + i;
+    a11m[r] = c11[B - 1]; a11[r] = c11[B]; a01[r] = c01[B];
+  }
+  const int B = j * SGS_P + i;
+  const double a10m = c10[B - 1], a10 = c10[B], a00 = c00[B];
+  S[0] = (a11m[0] + a01[0]) + (a10m + a00);
+  S[1] = (a01[0] + a11[0]) + (a00 + a10);
+  S[2] = (a10m + a00) + (a11m[1] + a01[1]);
+  S[3] = (a00 + a10) + (a01[1] + a11[1]);
+}
+
+template <int WY, int PX, int PY, bool IN>
+__device__ __forceinline__ void sgs_colour_own1(double* __restrict__ V, double (&own)[4], double sc, double rr,
+                                                int A0, int C0, int n, const SgsK& k) {
+  SGS_GEO(WY, 1);
+  constexpr int c = PX + 2 * PY, cx = (1 - PX) + 2 * PY, cy = PX + 2 * (1 - PY), cxy = (1 - PX) + 2 * (1 - PY);
+  constexpr int OW = PX - 1, OE = PX;
+  const int i = threadIdx.x, j = threadIdx.y;
+  const int B = j * SGS_P + i;
+  constexpr int OS = (PY - 1) * SGS_P, ON = PY * SGS_P;
+  // diagonal rows j + PY - 1 (S) and j + PY (N): the own row is N for PY = 0, S for PY = 1
+  double dSW, dSE, dNW, dNE, ys, yn, sx;
+  if (PY == 0) {
+    dSW = V[cxy * PL_ + B + OS + OW]; dSE = V[cxy * PL_ + B + OS + OE];
+    dNW = PX == 0 ? V[cxy * PL_ + B + OW] : own[cxy];
+    dNE = PX == 0 ? own[cxy] : V[cxy * PL_ + B + OE];
+    ys = V[cy * PL_ + B + OS]; yn = own[cy];
+  } else {
+    dSW = PX == 0 ? V[cxy * PL_ + B + OW] : own[cxy];
+    dSE = PX == 0 ? own[cxy] : V[cxy * PL_ + B + OE];
+    dNW = V[cxy * PL_ + B + ON + OW]; dNE = V[cxy * PL_ + B + ON + OE];
+    ys = own[cy]; yn = V[cy * PL_ + B + ON];
+  }
+  sx = PX == 0 ? V[cx * PL_ + B + OW] + own[cx] : own[cx] + V[cx * PL_ + B + OE];
+  const double sd = (dSW + dSE) + (dNW + dNE);
+  const double sy = ys + yn;
+  double wx = k.c_ed, wy = k.c_ed, inv = k.inv_in2;
+  bool in = true;
+  if (!IN) {
+    const int ga = A0 + 2 * i + PX, gc = C0 + 2 * j + PY;
+    in = ga >= 0 && ga <= n && gc >= 0 && gc <= n;
+    const bool bx = ga == 0 || ga == n, by = gc == 0 || gc == n;
+    wx = by ? k.w_off * k.w_bd : k.c_ed;
+    wy = bx ? k.w_bd * k.w_off : k.c_ed;
+    inv = bx ? (by ? k.inv_bd2 : k.inv_inbd) : (by ? k.inv_inbd : k.inv_in2);
+  }
+  const double s = rr - k.c_dd * sd - wx * sx - wy * sy - k.rq * sc;
+  const double v = in ? s * inv : 0.0;
+  V[c * PL_ + B] = v;
+  own[c] = v;
+}
+
+template <int WY, int PE, int PF, bool IN>
+__device__ __forceinline__ void sgs_cells_own1(const double* __restrict__ V, const double (&own)[4],
+                                               double* __restrict__ Cc, double rc, int A0, int C0, int n,
+                                               const SgsK& k) {
+  SGS_GEO(WY, 1);
+  constexpr int p00 = PE + 2 * PF, p10 = (1 - PE) + 2 * PF, p01 = PE + 2 * (1 - PF), p11 = (1 - PE) + 2 * (1 - PF);
+  const int i = threadIdx.x, j = threadIdx.y;
+  const int B = j * SGS_P + i;
+  const double v00 = own[p00];
+  const double v10 = PE == 0 ? own[p10] : V[p10 * PL_ + B + PE];
+  const double v01 = PF == 0 ? own[p01] : V[p01 * PL_ + B + PF * SGS_P];
+  const double v11 = (PE == 0 && PF == 0) ? own[p11] : V[p11 * PL_ + B + PF * SGS_P + PE];
+  const double sv = (v00 + v10) + (v01 + v11);
+  const double z = (rc - k.rq * sv) * k.inv_q0;
+  bool in = true;
+  if (!IN) {
+    const int e = A0 + 2 * i + PE, f = C0 + 2 * j + PF;
+    in = e >= 0 && e < n && f >= 0 && f < n;
+  }
+  Cc[p00 * PL_ + B] = in ? z : 0.0;
+}
+
 template <int WY, int MR, bool IN>
 __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, double* Cc, double* Q, int A0, int C0) {
   SGS_GEO(WY, MR);
@@ -1876,11 +1963,7 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
       const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
       const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
       const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
-      if (MR != 2) {
-        rv[c][m] = inv ? __ldg(r1 + ga + (int64_t)n1 * gc) - alpha : 0.0;
-        rc[c][m] = inc ? __ldg(r0 + ga + (int64_t)n * gc) + alpha : 0.0;
-      }
-      (void)inc; (void)inv;
+      (void)inc; (void)inv; (void)rv; (void)rc;
     }
   cp_async_wait_all();
   __syncthreads();
@@ -1891,23 +1974,32 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
     // operations; all loads of the thread issued before their use (same values, same arithmetic)
     constexpr int NQ = (SGS_TTX * TTY_ + SGS_TX * TY_ - 1) / (SGS_TX * TY_);
     double pv[NQ], pc[NQ];
+    // tile entries walked without divisions (see the write phase)
+    constexpr int NT = SGS_TX * TY_, DC = NT % SGS_TTX, DR = NT / SGS_TTX;
+    {
+      int tc = tid % SGS_TTX, tr = tid / SGS_TTX;
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const int idx = tid + q * SGS_TX * TY_;
-      const int ga = A0 + SGS_HX + idx % SGS_TTX, gc = C0 + SGS_HY + idx / SGS_TTX;
-      const bool ok = idx < SGS_TTX * TTY_;
-      const bool okv = ok && (IN || (ga <= n && gc <= n)), okc = ok && (IN || (ga < n && gc < n));
-      pv[q] = okv ? __ldg(yps + ga + (int64_t)n1 * gc) : 0.0;
-      pc[q] = okc ? __ldg(yps + nk + ga + (int64_t)n * gc) : 0.0;
+      for (int q = 0; q < NQ; ++q) {
+        const int ga = A0 + SGS_HX + tc, gc = C0 + SGS_HY + tr;
+        const bool ok = tr < TTY_;
+        const bool okv = ok && (IN || (ga <= n && gc <= n)), okc = ok && (IN || (ga < n && gc < n));
+        pv[q] = okv ? __ldg(yps + ga + (int64_t)n1 * gc) : 0.0;
+        pc[q] = okc ? __ldg(yps + nk + ga + (int64_t)n * gc) : 0.0;
+        tc += DC; tr += DR;
+        if (tc >= SGS_TTX) { tc -= SGS_TTX; ++tr; }
+      }
     }
+    int tc = tid % SGS_TTX, tr = tid / SGS_TTX;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      const int idx = tid + q * SGS_TX * TY_;
-      if (idx >= SGS_TTX * TTY_) break;
-      const int la = SGS_HX + idx % SGS_TTX, lc = SGS_HY + idx / SGS_TTX;
+      if (tr >= TTY_) break;
+      const int idx = tid + q * NT;
+      const int la = SGS_HX + tc, lc = SGS_HY + tr;
       const int pl = ((la & 1) + 2 * (lc & 1)) * PL_ + (lc >> 1) * SGS_P + (la >> 1);
       Q[idx] = fma(co_y, V[pl], co_p * pv[q]);
       Q[TQ_ + idx] = fma(co_y, Cc[pl], co_p * pc[q]);
+      tc += DC; tr += DR;
+      if (tc >= SGS_TTX) { tc -= SGS_TTX; ++tr; }
     }
   } else {
     for (int idx = tid; idx < SGS_TTX * TTY_; idx += SGS_TX * TY_) {
@@ -1963,13 +2055,33 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
     SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
 #undef SGS_V
   } else {
-#define SGS_V(PX, PY) do { sgs_colour<WY, MR, PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
+    static_assert(MR == 1, "one or two rows per thread");
+    double S[4];
+    double own[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) own[c] = V[c * PL_ + ty * SGS_P + i];
+    sgs_cellsums1<WY>(Cc, S);
+    auto rv1 = [&](int c) {
+      const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * ty + (c >> 1);
+      const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
+      return inv ? __ldg(r1 + ga + (int64_t)n1 * gc) - alpha : 0.0;
+    };
+#define SGS_V(PX, PY) do { const double rr_ = rv1(PX + 2 * PY); \
+      sgs_colour_own1<WY, PX, PY, IN>(V, own, S[PX + 2 * PY], rr_, A0, C0, n, k); __syncthreads(); } while (0)
     SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
-    sgs_cells<WY, MR, 0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);
-    sgs_cells<WY, MR, 1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);
-    sgs_cells<WY, MR, 0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
-    sgs_cells<WY, MR, 1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
+    double rc1[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * ty + (c >> 1);
+      const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
+      rc1[c] = inc ? __ldg(r0 + ga + (int64_t)n * gc) + alpha : 0.0;
+    }
+    sgs_cells_own1<WY, 0, 0, IN>(V, own, Cc, rc1[0], A0, C0, n, k);
+    sgs_cells_own1<WY, 1, 0, IN>(V, own, Cc, rc1[1], A0, C0, n, k);
+    sgs_cells_own1<WY, 0, 1, IN>(V, own, Cc, rc1[2], A0, C0, n, k);
+    sgs_cells_own1<WY, 1, 1, IN>(V, own, Cc, rc1[3], A0, C0, n, k);
     __syncthreads();
+    sgs_cellsums1<WY>(Cc, S);
     SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
 #undef SGS_V
   }
