@@ -198,7 +198,7 @@ enum ScalarIdx {
   S_GAMMA = 0, S_GAMMA_PREV, S_DELTA, S_ETA, S_C, S_C_PREV, S_S, S_S_PREV, S_GAMMA1,
   S_A2, S_A3, S_A1, S_CNEW_ETA, S_DONE, S_STATUS, S_IT, S_RTOL, S_MAXIT,
   S_DOT0, S_DOT1, S_DOT2, S_DOT3, S_DOT4, S_DOT5, S_KR, S_KY, S_INV_GAMMA, S_TMP0, S_TMP1,
-  S_APSUM,
+  S_APSUM, S_CE_PREV,
   // GMRES (solvers in oseen.cu)
   G_J = 32, G_JW, G_HN, G_RES, G_TOL, G_DONE, G_BREAK, G_TOT, G_BETA, G_MAXIT, G_NRM_P0, G_CAP,
   S_COUNT = 64

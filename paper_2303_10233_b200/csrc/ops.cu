@@ -2454,8 +2454,55 @@ constexpr int ST_PW = ST_T / 2 + 2;    // Q1 window (vertices I0/2 - 1 ... I0/2 
 constexpr int ST_CW = ST_T / 2 + 1;    // P0 window (cells I0/2 - 1 ... I0/2 + 31)
 constexpr int ST_THREADS = 256;
 constexpr int ST_ROWS = ST_T / (ST_THREADS / 32);   // 8 tile rows per warp
-constexpr int ST_SMEM = (4 * ST_W * ST_H + ST_PW * ST_PW + ST_CW * ST_CW) * (int)sizeof(double);
+constexpr int ST_SCR = 2 * (ST_T / 2) * (ST_T / 2);   // component-0 partial sums of the tile's pressure rows
+constexpr int ST_SMEM = (4 * ST_W * ST_H + ST_PW * ST_PW + ST_CW * ST_CW + ST_SCR) * (int)sizeof(double);
 static_assert(ST_T == 2 * 32 && ST_ROWS % 2 == 0, "lane = column pair, even strips");
+
+// Structural zeros of the B / B^T class weights (the kernel skips them at compile time; the launch
+// checks that every weight outside these patterns is exactly 0, else the gather kernel runs).  The
+// weights are products of 1D tables; per direction, for a Q2 node of type V (on a Q1 vertex) or
+// M (element midpoint): the Q1 derivative table vanishes on the node's own vertex (V: vertices
+// -1, +1; M: 0, +1), the Q1 mass table on the neighbouring vertices of a V node (V: 0; M: 0, +1);
+// the P0 derivative table vanishes for M nodes (V: cells -1, 0), the P0 mass table is V: -1, 0,
+// M: 0.  Component C takes the derivative table in direction C and the mass table in the other.
+__host__ __device__ constexpr bool st_pat1(int p, bool deriv, int d) {     // d in {-1, 0, 1}
+  return p == 0 ? (deriv ? d != 0 : d == 0) : (d == 0 || d == 1);
+}
+__host__ __device__ constexpr bool st_pat0(int p, bool deriv, int d) {     // d in {-1, 0}
+  return p == 0 ? true : (deriv ? false : d == 0);
+}
+__host__ __device__ constexpr bool st_m_bt1(int cl, int C, int dc, int da) {
+  return st_pat1(cl & 1, C == 0, da) && st_pat1(cl >> 1, C == 1, dc);
+}
+__host__ __device__ constexpr bool st_m_bt0(int cl, int C, int df, int de) {
+  return st_pat0(cl & 1, C == 0, de) && st_pat0(cl >> 1, C == 1, df);
+}
+__host__ __device__ constexpr bool st_m_b1(int C, int dj, int di) {        // di, dj in -2 .. 2
+  return (C == 0 ? di != 0 : (di >= -1 && di <= 1)) && (C == 1 ? dj != 0 : (dj >= -1 && dj <= 1));
+}
+__host__ __device__ constexpr bool st_m_b0(int C, int dj, int di) {        // di, dj in 0 .. 2
+  return C == 0 ? di != 1 : dj != 1;
+}
+static bool saddle_masks_ok(const SaddleSt& w) {
+  for (int cl = 0; cl < 4; ++cl)
+    for (int C = 0; C < 2; ++C) {
+      for (int dc = -1; dc <= 1; ++dc)
+        for (int da = -1; da <= 1; ++da)
+          if (!st_m_bt1(cl, C, dc, da) && w.bt1[cl][C][(dc + 1) * 3 + da + 1] != 0.0) return false;
+      for (int df = -1; df <= 0; ++df)
+        for (int de = -1; de <= 0; ++de)
+          if (!st_m_bt0(cl, C, df, de) && w.bt0[cl][C][(df + 1) * 2 + de + 1] != 0.0) return false;
+    }
+  for (int C = 0; C < 2; ++C) {
+    for (int dj = -2; dj <= 2; ++dj)
+      for (int di = -2; di <= 2; ++di)
+        if (!st_m_b1(C, dj, di) && w.b1[C][(dj + 2) * 5 + di + 2] != 0.0) return false;
+    for (int dj = 0; dj <= 2; ++dj)
+      for (int di = 0; di <= 2; ++di)
+        if (!st_m_b0(C, dj, di) && w.b0[C][dj * 3 + di] != 0.0) return false;
+  }
+  return true;
+}
 
 struct SaddleTileArgs {
   StencilOp so; SaddleSt w;
@@ -2467,7 +2514,7 @@ struct SaddleTileArgs {
 // shared-memory layout (one dynamic array; every offset a compile-time constant): E0, O0, E1, O1
 // (ST_W rows x ST_H), then the Q1 window (ST_PW x ST_PW), then the P0 window (ST_CW x ST_CW)
 extern __shared__ __align__(16) double st_sm[];
-constexpr int ST_OFF_P1 = 4 * ST_W * ST_H, ST_OFF_P0 = ST_OFF_P1 + ST_PW * ST_PW;
+constexpr int ST_OFF_P1 = 4 * ST_W * ST_H, ST_OFF_P0 = ST_OFF_P1 + ST_PW * ST_PW, ST_OFF_SCR = ST_OFF_P0 + ST_CW * ST_CW;
 struct StSmem {
   __device__ __forceinline__ const double* E(int c) const { return st_sm + 2 * c * ST_W * ST_H; }
   __device__ __forceinline__ const double* O(int c) const { return st_sm + (2 * c + 1) * ST_W * ST_H; }
@@ -2543,16 +2590,20 @@ __device__ __forceinline__ void st_vel_row(const SaddleTileArgs& a, const StSmem
 #pragma unroll
       for (int dc = -1; dc <= 1; ++dc)
 #pragma unroll
-        for (int da = -1; da <= 1; ++da)
+        for (int da = -1; da <= 1; ++da) {
+          if (!st_m_bt1(2 * PJ + k, C, dc, da)) continue;         // structural zero (compile time)
           bx = fma(a.w.bt1[cl][C][(dc + 1) * 3 + da + 1], S.P1()[(pr + dc) * ST_PW + L + 1 + da], bx);
+        }
       ax = q[k] + bx;
       if (!a.reduced) {
         double cx = 0.0;
 #pragma unroll
         for (int df = -1; df <= 0; ++df)
 #pragma unroll
-          for (int de = -1; de <= 0; ++de)
+          for (int de = -1; de <= 0; ++de) {
+            if (!st_m_bt0(2 * PJ + k, C, df, de)) continue;
             cx = fma(a.w.bt0[cl][C][(df + 1) * 2 + de + 1], S.P0()[(pr + df) * ST_CW + L + 1 + de], cx);
+          }
         ax += cx;
       }
     }
@@ -2575,7 +2626,41 @@ __device__ __forceinline__ void st_vel_row(const SaddleTileArgs& a, const StSmem
       else yr[1] = out[1];
     }
   }
-  (void)n;
+  // ---- pressure rows of the tile's vertex / cell (L, tj / 2) on even rows: the 5 x 5 (Q1) and
+  //      3 x 3 (P0) node neighbourhoods of node (2 va, 2 vc) are exactly this lane's register
+  //      window (columns 2L .. 2L + 4, rows tj - 2 .. tj + 2), so B u needs no further loads.
+  //      Component 0's sum waits in the thread's own scratch entry for component 1's.
+  if constexpr ((t & 1) == 0) {
+    const int cr = tj >> 1;
+    double q1 = 0.0, q0 = 0.0;
+#pragma unroll
+    for (int dj = -2; dj <= 2; ++dj)
+#pragma unroll
+      for (int di = -2; di <= 2; ++di)
+        if (st_m_b1(C, dj, di)) q1 = fma(a.w.b1[C][(dj + 2) * 5 + di + 2], win[(RS + dj + 5) % 5][2 + di], q1);
+#pragma unroll
+    for (int dj = 0; dj <= 2; ++dj)
+#pragma unroll
+      for (int di = 0; di <= 2; ++di)
+        if (st_m_b0(C, dj, di)) q0 = fma(a.w.b0[C][dj * 3 + di], win[(RS + dj) % 5][2 + di], q0);
+    double* scr = st_sm + ST_OFF_SCR + cr * (ST_T / 2) + L;
+    if (C == 0) {
+      scr[0] = q1; scr[ST_SCR / 2] = q0;
+    } else {
+      const int va = (I0 >> 1) + L, vc = (J0 >> 1) + cr;
+      if (!EDGE || (va <= n && vc <= n)) {
+        const double acc = (scr[0] + q1) * sc;
+        a.y[a.n_u + va + (int64_t)(n + 1) * vc] = acc;
+        if (a.dot_out) dot += acc * (sc * S.P1()[(cr + 1) * ST_PW + L + 1]);
+      }
+      if (!EDGE || (va < n && vc < n)) {
+        double acc = (scr[ST_SCR / 2] + q0) * sc;
+        if (a.reduced) acc = 0.0;
+        a.y[a.n_u + a.nk + va + (int64_t)n * vc] = acc;
+        if (a.dot_out) dot += acc * (sc * S.P0()[(cr + 1) * ST_CW + L + 1]);
+      }
+    }
+  }
 }
 
 template <int C, bool EDGE, int... Ts>
@@ -2608,45 +2693,6 @@ __device__ __forceinline__ void st_body(const SaddleTileArgs& a, const StSmem& S
   double dot = 0.0;
   st_vel<0, EDGE>(a, S, I0, J0, sc, dot);
   st_vel<1, EDGE>(a, S, I0, J0, sc, dot);
-  // pressure rows: Q1 vertices (a, c) and P0 cells (e, f) of the tile, lane = column
-  const int L = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int m = a.m, n = a.n, n1 = n + 1;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int cr = w + 8 * r;                      // tile vertex / cell row
-    const int va = (I0 >> 1) + L, vc = (J0 >> 1) + cr;
-    if (!EDGE || (va <= n && vc <= n)) {
-      double acc = 0.0;
-#pragma unroll
-      for (int dj = -2; dj <= 2; ++dj)
-#pragma unroll
-        for (int di = -2; di <= 2; ++di) {
-          const int wi = 2 * L + 2 + di, wj = 2 * cr + 2 + dj;
-          acc = fma(a.w.b1[0][(dj + 2) * 5 + di + 2], st_pnode<EDGE>(S, 0, wi, wj, I0, J0, m), acc);
-          acc = fma(a.w.b1[1][(dj + 2) * 5 + di + 2], st_pnode<EDGE>(S, 1, wi, wj, I0, J0, m), acc);
-        }
-      acc *= sc;
-      const int64_t row = va + (int64_t)n1 * vc;
-      a.y[a.n_u + row] = acc;
-      if (a.dot_out) dot += acc * (sc * S.P1()[(cr + 1) * ST_PW + L + 1]);
-    }
-    if (!EDGE || (va < n && vc < n)) {
-      double acc = 0.0;
-#pragma unroll
-      for (int dj = 0; dj <= 2; ++dj)
-#pragma unroll
-        for (int di = 0; di <= 2; ++di) {
-          const int wi = 2 * L + 2 + di, wj = 2 * cr + 2 + dj;
-          acc = fma(a.w.b0[0][dj * 3 + di], st_pnode<EDGE>(S, 0, wi, wj, I0, J0, m), acc);
-          acc = fma(a.w.b0[1][dj * 3 + di], st_pnode<EDGE>(S, 1, wi, wj, I0, J0, m), acc);
-        }
-      acc *= sc;
-      if (a.reduced) acc = 0.0;
-      const int64_t row = a.nk + va + (int64_t)n * vc;
-      a.y[a.n_u + row] = acc;
-      if (a.dot_out) dot += acc * (sc * S.P0()[(cr + 1) * ST_CW + L + 1]);
-    }
-  }
   if (a.dot_out) { double v[1] = {dot}; reduce_finish<1>(v, a.site, a.slot, a.dot_out); }
 }
 
@@ -2713,7 +2759,7 @@ void launch_saddle_ex(const Problem& P, bool reduced, const double* x, double* y
     b.x = x; b.y = y; b.inv_scale = inv_scale; b.site = a.site; b.slot = slot; b.dot_out = dot_out; b.done = done;
     const int tiles_x = (P.g.m + ST_T - 1) / ST_T;
     // a fused <K z, z> reduction keeps one partial per CTA: at most RED_MAXB of them per slot
-    if (g_saddle_tile && (!dot_out || tiles_x * tiles_x <= RED_MAXB)) {
+    if (g_saddle_tile && (!dot_out || tiles_x * tiles_x <= RED_MAXB) && saddle_masks_ok(P.sst)) {
       static bool smem_set = false;
       if (!smem_set) {
         cudaFuncSetAttribute(k_saddle_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM);

@@ -52,7 +52,7 @@ def main():
     vals = list(zs)
     out["bitwise_equal"] = all(torch.equal(zs[vals[0]], zs[v]) for v in vals[1:])
     out["max_abs_diff"] = max(float((zs[vals[0]] - zs[v]).abs().max()) for v in vals[1:])
-    print(json.dumps(out, indent=1))
+    print(json.dumps(out))
 
 
 if __name__ == "__main__":
