@@ -2171,37 +2171,30 @@ struct SgsPlaneArgs {
 constexpr int SGSP_PAD = 128;                                      // zero words before V (edge reads at -33)
 // TMA box origins must be 16-byte aligned in the innermost dimension: the window's first plane
 // column A0 / 2 must be even, so the tile is 48 wide (halo 8 / 8, the right one >= 6 as required)
-// instead of k_sgs_tile's 50; vertically (dimension 1, no alignment rule) it stays 58.
+// instead of k_sgs_tile's 50; vertically (dimension 1, no alignment rule) it is 26 (64 x 32
+// windows, 256 threads, two adjacent plane rows per thread: the geometry and the register-forwarding
+// sweep of k_sgs_tile<32, 2>).
 constexpr int SGSP_TTX = 48;
+constexpr int SGSP_WY = 32, SGSP_TY = SGSP_WY / 4, SGSP_TTY = SGSP_WY - 6;
+constexpr int SGSP_PLW = SGS_P * (SGSP_WY / 2);                    // one plane of the window (32 x 16)
 static_assert(SGS_W - SGS_HX - SGSP_TTX >= 6 && (SGSP_TTX / 2) % 2 == 0 && (SGS_HX / 2) % 2 == 0, "TMA-aligned tile");
-constexpr int SGSP_BYTES = 8 * SGS_PL * (int)sizeof(double);       // one TMA box (8 planes x 32 x 32)
-constexpr int SGSP_SMEM = (SGSP_PAD + 8 * SGS_PL) * (int)sizeof(double) + 1024 + 64;   // + alignment slack, mbarrier
+constexpr int SGSP_BYTES = 8 * SGSP_PLW * (int)sizeof(double);     // one TMA box (8 planes x 16 x 32)
+constexpr int SGSP_TAIL = 64;                                      // zero words after Cc (edge reads at +32)
+constexpr int SGSP_SMEM = (SGSP_PAD + 8 * SGSP_PLW + SGSP_TAIL) * (int)sizeof(double) + 1024 + 64;   // + alignment slack, mbarrier
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 template <bool IN>
 __device__ __forceinline__ void sgsp_body(const SgsPlaneArgs& a, double* V, double* Cc, unsigned bar, bool tma,
                                           int A0, int C0) {
+  constexpr int WY = SGSP_WY;
   const int i = threadIdx.x, ty = threadIdx.y;
   const int n = a.g.n;
-  const int pw = a.pw, ph = a.ph;
+  const int pw = a.pw;
   const int64_t pl = a.pl;
   const int X0 = A0 >> 1, Y0 = C0 >> 1;                      // window origin in plane coordinates
   const double alpha = a.kproj ? (*a.kproj * a.inv_kk) : 0.0;
-  // ---- r (own entries of every plane, coalesced plane rows) while the TMA is in flight
-  double rv[4][2], rc[4][2];
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-#pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      const int j = ty + SGS_TY * m;
-      const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
-      const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
-      const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
-      const int64_t o = (int64_t)(Y0 + j) * pw + (X0 + i);
-      rv[c][m] = inv ? __ldg(a.rp + c * pl + o) - alpha : 0.0;
-      rc[c][m] = inc ? __ldg(a.rp + (4 + c) * pl + o) + alpha : 0.0;
-    }
+  const int64_t o0 = (int64_t)(Y0 + 2 * ty) * pw + (X0 + i);   // the thread's entry (i, 2 ty) of a plane
   if (tma) {
     // wait for the window (phase 0 of the single-use barrier)
     asm volatile(
@@ -2211,19 +2204,53 @@ __device__ __forceinline__ void sgsp_body(const SgsPlaneArgs& a, double* V, doub
   }
   __syncthreads();
   const SgsK& k = a.k;
-#define SGS_V(PX, PY) do { sgs_colour<SGS_W, 2, PX, PY, IN>(V, Cc, rv[PX + 2 * PY], A0, C0, n, k); __syncthreads(); } while (0)
+  double S[4][2];
+  double own[4][2];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int m = 0; m < 2; ++m) own[c][m] = V[c * SGSP_PLW + (2 * ty + m) * SGS_P + i];
+  sgs_cellsums<WY>(Cc, S);                                       // cells of the forward sweep
+  // right-hand side of the thread's entries, one contiguous plane row per warp, read per colour
+  auto rv_of = [&](int c, double (&rr)[2]) {
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * (2 * ty + m) + (c >> 1);
+      const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
+      rr[m] = inv ? __ldg(a.rp + c * pl + o0 + m * pw) - alpha : 0.0;
+    }
+  };
+#define SGS_V(PX, PY) do { double rr_[2]; rv_of(PX + 2 * PY, rr_); \
+    sgs_colour_own<WY, PX, PY, IN>(V, own, S[PX + 2 * PY], rr_, A0, C0, n, k); __syncthreads(); } while (0)
   SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
-  sgs_cells<SGS_W, 2, 0, 0, IN>(V, Cc, rc[0], A0, C0, n, k);             // P0 (once; see k_sgs_tile)
-  sgs_cells<SGS_W, 2, 1, 0, IN>(V, Cc, rc[1], A0, C0, n, k);
-  sgs_cells<SGS_W, 2, 0, 1, IN>(V, Cc, rc[2], A0, C0, n, k);
-  sgs_cells<SGS_W, 2, 1, 1, IN>(V, Cc, rc[3], A0, C0, n, k);
+  {
+    double rc[4][2];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * (2 * ty + m) + (c >> 1);
+        const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
+        rc[c][m] = inc ? __ldg(a.rp + (4 + c) * pl + o0 + m * pw) + alpha : 0.0;
+      }
+    sgs_cells_own<WY, 0, 0, IN>(V, own, Cc, rc[0], A0, C0, n, k);   // P0 (once; see k_sgs_tile)
+    sgs_cells_own<WY, 1, 0, IN>(V, own, Cc, rc[1], A0, C0, n, k);
+    sgs_cells_own<WY, 0, 1, IN>(V, own, Cc, rc[2], A0, C0, n, k);
+    sgs_cells_own<WY, 1, 1, IN>(V, own, Cc, rc[3], A0, C0, n, k);
+  }
   __syncthreads();
+  sgs_cellsums<WY>(Cc, S);                                       // cells after the P0 update
   SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0);
-  sgs_colour<SGS_W, 2, 0, 0, IN>(V, Cc, rv[0], A0, C0, n, k);            // backward colour 0: each thread reads back
-  __syncwarp();                                                 // only its own entries below
+  {                                                              // backward colour 0: the write phase reads the
+    double rr_[2]; rv_of(0, rr_);                                // thread's own entries only (registers / own cells)
+    sgs_colour_own<WY, 0, 0, IN>(V, own, S[0], rr_, A0, C0, n, k);
+  }
 #undef SGS_V
   asm volatile("griddepcontrol.launch_dependents;");
-  // ---- write the own tile entries: out = co_s S(y) + (co_y y + co_p y_prev), as k_sgs_tile
+  // ---- write the own tile entries: out = co_s S(y) + (co_y y + co_p y_prev), as k_sgs_tile; y and
+  //      y_prev at the thread's entries come from L2 (y was just fetched by the TMA, y_prev by the
+  //      prefetch), contiguous plane rows
+  const bool tile_x = i >= SGS_HX / 2 && i < SGS_HX / 2 + SGSP_TTX / 2;
   const double co_s = a.omega * a.gam;
   const double co_y = a.omega * (1.0 - a.gam);
   const double co_p = 1.0 - a.omega;
@@ -2231,49 +2258,57 @@ __device__ __forceinline__ void sgsp_body(const SgsPlaneArgs& a, double* V, doub
   const int n1 = n + 1, nk = a.g.nk;
   double kd = 0.0;
 #pragma unroll
-  for (int q = 0; q < 8; ++q)
+  for (int m = 0; m < 2; ++m) {
+    const int j = 2 * ty + m;
+    if (!tile_x || j < SGS_HY / 2 || j >= SGS_HY / 2 + SGSP_TTY / 2) continue;
 #pragma unroll
-    for (int m = 0; m < 2; ++m) {
-      const int j = ty + SGS_TY * m;
-      if (i < SGS_HX / 2 || i >= SGS_HX / 2 + SGSP_TTX / 2 || j < SGS_HY / 2 || j >= SGS_HY / 2 + SGS_TTY / 2) continue;
+    for (int h = 0; h < 2; ++h) {                      // vertex planes, then cell planes
+    double yv[4], ypv[4];
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const int64_t po = (4 * h + qq) * pl + o0 + m * pw;
+      yv[qq] = a.yg ? __ldg(a.yg + po) : 0.0;
+      ypv[qq] = use_yp ? __ldg(a.ypg + po) : 0.0;
+    }
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const int q = 4 * h + qq;
       const int px = q & 1, py = (q >> 1) & 1;
       const int ga = A0 + 2 * i + px, gc = C0 + 2 * j + py;
       const bool vert = q < 4;
       if (!IN && !(vert ? (ga <= n && gc <= n) : (ga < n && gc < n))) continue;
-      const int64_t po = q * pl + (int64_t)(Y0 + j) * pw + (X0 + i);
-      const double yv = a.yg ? __ldg(a.yg + po) : 0.0;
-      const double Q = fma(co_y, yv, use_yp ? co_p * __ldg(a.ypg + po) : 0.0);
-      const double o = fma(co_s, (vert ? V : Cc)[(q & 3) * SGS_PL + j * SGS_P + i], Q);
+      const double sv = vert ? own[q & 3][m] : Cc[(q & 3) * SGSP_PLW + j * SGS_P + i];
+      const double Q = fma(co_y, yv[qq], use_yp ? co_p * ypv[qq] : 0.0);
+      const double o = fma(co_s, sv, Q);
       if (a.out_abi) {
         if (vert) a.out_abi[ga + (int64_t)n1 * gc] = o;
         else a.out_abi[nk + ga + (int64_t)n * gc] = o;
       } else {
-        a.outp[po] = o;
+        a.outp[q * pl + o0 + m * pw] = o;
       }
       kd += vert ? o : -o;
     }
-  (void)ph;
+    }
+  }
   if (a.kout) { double v[1] = {kd}; reduce_finish<1>(v, a.site, a.slot, a.kout); }
 }
 
-#ifndef SGSP_MINB
-#define SGSP_MINB SGS_MINB
-#endif
-__global__ void __launch_bounds__(SGS_TX * SGS_TY, SGSP_MINB) k_sgs_plane(const __grid_constant__ SgsPlaneArgs a,
-                                                                        const __grid_constant__ CUtensorMap tm_y,
-                                                                        const __grid_constant__ CUtensorMap tm_yp) {
+__global__ void __launch_bounds__(SGS_TX * SGSP_TY, 4) k_sgs_plane(const __grid_constant__ SgsPlaneArgs a,
+                                                                  const __grid_constant__ CUtensorMap tm_y,
+                                                                  const __grid_constant__ CUtensorMap tm_yp) {
   extern __shared__ unsigned char sgsp_raw[];
-  // 1024-byte aligned window: [pad | V (4 planes) | Cc (4 planes)], mbarrier after it
+  // 1024-byte aligned window: [pad | V (4 planes) | Cc (4 planes) | tail], mbarrier after it
   const unsigned base = smem_u32(sgsp_raw);
   const unsigned off = ((base + SGSP_PAD * 8 + 1023u) & ~1023u) - base;
   double* V = reinterpret_cast<double*>(sgsp_raw + off);
-  double* Cc = V + 4 * SGS_PL;
+  double* Cc = V + 4 * SGSP_PLW;
   double* pad = V - SGSP_PAD;
-  unsigned long long* barp = reinterpret_cast<unsigned long long*>(Cc + 4 * SGS_PL);
+  double* tail = Cc + 4 * SGSP_PLW;
+  unsigned long long* barp = reinterpret_cast<unsigned long long*>(tail + SGSP_TAIL);
   const unsigned bar = smem_u32(barp);
   const int tid = threadIdx.x + SGS_TX * threadIdx.y;
   const int n = a.g.n;
-  const int A0 = (blockIdx.x % a.tiles_x) * SGSP_TTX - SGS_HX, C0 = (blockIdx.x / a.tiles_x) * SGS_TTY - SGS_HY;
+  const int A0 = (blockIdx.x % a.tiles_x) * SGSP_TTX - SGS_HX, C0 = (blockIdx.x / a.tiles_x) * SGSP_TTY - SGS_HY;
   const bool tma = a.yg != nullptr;
   if (tid == 0) {
     if (a.ypg) {   // y_prev is only read at write time: start pulling its window into L2 now
@@ -2289,28 +2324,8 @@ __global__ void __launch_bounds__(SGS_TX * SGS_TY, SGSP_MINB) k_sgs_plane(const 
   if (a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");   // previous step complete and visible
   if (is_done(a.done)) return;
   if (tid < SGSP_PAD) pad[tid] = 0.0;
+  if (tid < SGSP_TAIL) tail[tid] = 0.0;
   if (tma) {
-#if defined(SGSP_NOTMA)
-    {
-      const int X0 = A0 >> 1, Y0 = C0 >> 1;
-      for (int t = tid; t < 8 * SGS_PL; t += SGS_TX * SGS_TY) {
-        const int q = t >> 10, jj = (t >> 5) & 31, ii = t & 31;
-        const int x = X0 + ii, y = Y0 + jj;
-        V[t] = (x >= 0 && y >= 0 && x < a.pw && y < a.ph) ? a.yg[q * a.pl + (int64_t)y * a.pw + x] : 0.0;
-      }
-      __syncthreads();
-      if (tid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-    }
-#elif defined(SGSP_SPLIT)
-    if (tid == 0) {
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(SGSP_BYTES) : "memory");
-      for (int q = 0; q < 8; ++q)
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-            ::"r"(smem_u32(V + q * SGS_PL)), "l"(&tm_y), "r"(A0 >> 1), "r"(C0 >> 1), "r"(q), "r"(bar)
-            : "memory");
-    }
-#else
     if (tid == 0) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(SGSP_BYTES) : "memory");
       asm volatile(
@@ -2318,11 +2333,10 @@ __global__ void __launch_bounds__(SGS_TX * SGS_TY, SGSP_MINB) k_sgs_plane(const 
           ::"r"(smem_u32(V)), "l"(&tm_y), "r"(A0 >> 1), "r"(C0 >> 1), "r"(0), "r"(bar)
           : "memory");
     }
-#endif
   } else {   // first step: y = 0
-    for (int t = tid; t < 8 * SGS_PL; t += SGS_TX * SGS_TY) V[t] = 0.0;
+    for (int t = tid; t < 8 * SGSP_PLW; t += SGS_TX * SGSP_TY) V[t] = 0.0;
   }
-  const bool interior = A0 >= 1 && A0 + SGS_W - 1 <= n - 1 && C0 >= 1 && C0 + SGS_W - 1 <= n - 1;
+  const bool interior = A0 >= 1 && A0 + SGS_W - 1 <= n - 1 && C0 >= 1 && C0 + SGSP_WY - 1 <= n - 1;
   if (interior) sgsp_body<true>(a, V, Cc, bar, tma, A0, C0);
   else sgsp_body<false>(a, V, Cc, bar, tma, A0, C0);
 }
@@ -3892,7 +3906,7 @@ static etq_status mass_pc_apply_planar(const Problem& P, const double* r_p, doub
   a.rp = M.rp; a.kproj = P.dscal + S_KR; a.inv_kk = inv_kk;
   a.gam = gam;
   a.tiles_x = (g.n + 1 + SGSP_TTX - 1) / SGSP_TTX;
-  const int tiles = a.tiles_x * ((g.n + 1 + SGS_TTY - 1) / SGS_TTY);
+  const int tiles = a.tiles_x * ((g.n + 1 + SGSP_TTY - 1) / SGSP_TTY);
   a.site = rs; a.slot = 4; a.done = done;
   for (int k = 0; k < M.m; ++k) {
     if (k == 1) omega = 1.0 / (1.0 - 0.5 * rh * rh);
@@ -3909,7 +3923,7 @@ static etq_status mass_pc_apply_planar(const Problem& P, const double* r_p, doub
     const void* tm_y = M.tmap[cur >= 0 ? cur : 0];
     const void* tm_yp = M.tmap[prev >= 0 ? prev : 0];
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(tiles); cfg.blockDim = dim3(SGS_TX, SGS_TY); cfg.dynamicSmemBytes = SGSP_SMEM; cfg.stream = st;
+    cfg.gridDim = dim3(tiles); cfg.blockDim = dim3(SGS_TX, SGSP_TY); cfg.dynamicSmemBytes = SGSP_SMEM; cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributePriority;
     attr[0].val.priority = g_sgs_high_prio ? hi_prio : lo_prio;
@@ -3990,7 +4004,7 @@ etq_status cheb_tile_bench(const Problem& P, bool post, const double* in_b, cons
   return ETQ_OK;
 }
 
-// TMA descriptor of a planar pressure vector: 3D tensor {pw, ph, 8 planes}, box {32, 32, 8} (one SGS
+// TMA descriptor of a planar pressure vector: 3D tensor {pw, ph, 8 planes}, box {32, 16, 8} (one SGS
 // window), zero fill outside (the domain edges of every window)
 static etq_status encode_planar_map(void* tmap, double* base, int pw, int ph) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -4004,11 +4018,7 @@ static etq_status encode_planar_map(void* tmap, double* base, int pw, int ph) {
   }
   const cuuint64_t dims[3] = {(cuuint64_t)pw, (cuuint64_t)ph, 8};
   const cuuint64_t strides[2] = {(cuuint64_t)pw * sizeof(double), (cuuint64_t)pw * ph * sizeof(double)};
-#if defined(SGSP_SPLIT)
-  const cuuint32_t box[3] = {SGS_P, SGS_P, 1};
-#else
-  const cuuint32_t box[3] = {SGS_P, SGS_P, 8};
-#endif
+  const cuuint32_t box[3] = {SGS_P, SGSP_WY / 2, 8};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides,
                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
