@@ -2722,29 +2722,82 @@ __global__ void __launch_bounds__(ST_THREADS, ST_MINB) k_saddle_tile(SaddleTileA
   const double* xu = a.x;
   const double* p1 = a.x + a.n_u;
   const double* p0 = p1 + a.nk;
-  // ---- stage (cp.async, zero-fill outside the domain)
-  for (int idx = threadIdx.x; idx < ST_W * ST_W; idx += ST_THREADS) {
-    const int wi = idx % ST_W, wj = idx / ST_W;
-    const int gi = I0 - 2 + wi, gj = J0 - 2 + wj;
-    const bool in = gi >= 0 && gj >= 0 && gi < m && gj < m;
-    const int64_t g = in ? gi + (int64_t)m * gj : 0;
-    const int s = wj * ST_H + (wi >> 1);
-    cp_async8(st_sm + ((wi & 1) ? ST_W * ST_H : 0) + s, xu + g, in);
-    cp_async8(st_sm + ((wi & 1) ? 3 : 2) * ST_W * ST_H + s, xu + a.nq + g, in);
-  }
-  for (int idx = threadIdx.x; idx < ST_PW * ST_PW; idx += ST_THREADS) {
-    const int pa = (I0 >> 1) - 1 + idx % ST_PW, pc = (J0 >> 1) - 1 + idx / ST_PW;
-    const bool in = pa >= 0 && pc >= 0 && pa <= n && pc <= n;
-    cp_async8(st_sm + ST_OFF_P1 + idx, p1 + (in ? pa + (int64_t)n1 * pc : 0), in);
-  }
-  for (int idx = threadIdx.x; idx < ST_CW * ST_CW; idx += ST_THREADS) {
-    const int ce = (I0 >> 1) - 1 + idx % ST_CW, cf = (J0 >> 1) - 1 + idx / ST_CW;
-    const bool in = !a.reduced && ce >= 0 && cf >= 0 && ce < n && cf < n;
-    cp_async8(st_sm + ST_OFF_P0 + idx, p0 + (in ? ce + (int64_t)n * cf : 0), in);
+  // ---- stage (cp.async).  Interior tiles: every window entry is inside the domain, and element
+  //      idx = tid + 256 k of a window of width W is walked incrementally (row += 256 / W, column +=
+  //      256 % W with a wrap) from one running source pointer; the shared destinations are linear in
+  //      idx (node planes: idx / 2 within the thread's fixed parity plane).  Edge tiles: zero fill
+  //      outside the domain.
+  const bool edge = I0 - 2 < 1 || J0 - 2 < 1 || I0 + ST_T + 1 > m - 2 || J0 + ST_T + 1 > m - 2;
+  if (!edge) {
+    const int tid = threadIdx.x;
+    {
+      constexpr int TOT = ST_W * ST_W, NF = TOT / ST_THREADS, DJ = ST_THREADS / ST_W, DI = ST_THREADS % ST_W;
+      static_assert(ST_W == 2 * ST_H && DI % 2 == 0 && ST_THREADS % 2 == 0, "fixed parity plane, linear destination");
+      int wj = tid / ST_W, wi = tid - ST_W * wj;
+      const double* src = xu + ((int64_t)m * (J0 - 2 + wj) + (I0 - 2 + wi));
+      double* dst = st_sm + ((wi & 1) ? ST_W * ST_H : 0) + (tid >> 1);
+      const int64_t step = (int64_t)DJ * m + DI, wrap = (int64_t)m - ST_W;
+#pragma unroll 6
+      for (int k = 0; k < NF; ++k) {
+        cp_async8(dst, src, true);
+        cp_async8(dst + 2 * ST_W * ST_H, src + a.nq, true);
+        dst += ST_THREADS / 2; src += step; wi += DI;
+        if (wi >= ST_W) { wi -= ST_W; src += wrap; }
+      }
+      if (tid < TOT - NF * ST_THREADS) {
+        const int idx = NF * ST_THREADS + tid, wj2 = idx / ST_W, wi2 = idx - ST_W * wj2;
+        const double* s2 = xu + ((int64_t)m * (J0 - 2 + wj2) + (I0 - 2 + wi2));
+        double* d2 = st_sm + ((wi2 & 1) ? ST_W * ST_H : 0) + (idx >> 1);
+        cp_async8(d2, s2, true);
+        cp_async8(d2 + 2 * ST_W * ST_H, s2 + a.nq, true);
+      }
+    }
+    {
+      constexpr int TOT = ST_PW * ST_PW, DJ = ST_THREADS / ST_PW, DI = ST_THREADS % ST_PW;
+      int pj = tid / ST_PW, pi = tid - ST_PW * pj;
+      const double* src = p1 + ((int64_t)n1 * ((J0 >> 1) - 1 + pj) + ((I0 >> 1) - 1 + pi));
+      const int64_t step = (int64_t)DJ * n1 + DI, wrap = (int64_t)n1 - ST_PW;
+      for (int idx = tid; idx < TOT; idx += ST_THREADS) {
+        cp_async8(st_sm + ST_OFF_P1 + idx, src, true);
+        src += step; pi += DI;
+        if (pi >= ST_PW) { pi -= ST_PW; src += wrap; }
+      }
+    }
+    {
+      constexpr int TOT = ST_CW * ST_CW, DJ = ST_THREADS / ST_CW, DI = ST_THREADS % ST_CW;
+      int cj = tid / ST_CW, ci = tid - ST_CW * cj;
+      const double* src = p0 + ((int64_t)n * ((J0 >> 1) - 1 + cj) + ((I0 >> 1) - 1 + ci));
+      const int64_t step = (int64_t)DJ * n + DI, wrap = (int64_t)n - ST_CW;
+      const bool on = !a.reduced;
+      for (int idx = tid; idx < TOT; idx += ST_THREADS) {
+        cp_async8(st_sm + ST_OFF_P0 + idx, on ? src : p0, on);
+        src += step; ci += DI;
+        if (ci >= ST_CW) { ci -= ST_CW; src += wrap; }
+      }
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < ST_W * ST_W; idx += ST_THREADS) {
+      const int wi = idx % ST_W, wj = idx / ST_W;
+      const int gi = I0 - 2 + wi, gj = J0 - 2 + wj;
+      const bool in = gi >= 0 && gj >= 0 && gi < m && gj < m;
+      const int64_t g = in ? gi + (int64_t)m * gj : 0;
+      const int s = wj * ST_H + (wi >> 1);
+      cp_async8(st_sm + ((wi & 1) ? ST_W * ST_H : 0) + s, xu + g, in);
+      cp_async8(st_sm + ((wi & 1) ? 3 : 2) * ST_W * ST_H + s, xu + a.nq + g, in);
+    }
+    for (int idx = threadIdx.x; idx < ST_PW * ST_PW; idx += ST_THREADS) {
+      const int pa = (I0 >> 1) - 1 + idx % ST_PW, pc = (J0 >> 1) - 1 + idx / ST_PW;
+      const bool in = pa >= 0 && pc >= 0 && pa <= n && pc <= n;
+      cp_async8(st_sm + ST_OFF_P1 + idx, p1 + (in ? pa + (int64_t)n1 * pc : 0), in);
+    }
+    for (int idx = threadIdx.x; idx < ST_CW * ST_CW; idx += ST_THREADS) {
+      const int ce = (I0 >> 1) - 1 + idx % ST_CW, cf = (J0 >> 1) - 1 + idx / ST_CW;
+      const bool in = !a.reduced && ce >= 0 && cf >= 0 && ce < n && cf < n;
+      cp_async8(st_sm + ST_OFF_P0 + idx, p0 + (in ? ce + (int64_t)n * cf : 0), in);
+    }
   }
   cp_async_wait_all();
   __syncthreads();
-  const bool edge = I0 - 2 < 1 || J0 - 2 < 1 || I0 + ST_T + 1 > m - 2 || J0 + ST_T + 1 > m - 2;
   if (edge) st_body<true>(a, S, I0, J0, sc);
   else st_body<false>(a, S, I0, J0, sc);
 }
