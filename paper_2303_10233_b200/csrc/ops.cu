@@ -766,7 +766,7 @@ __device__ __forceinline__ void ct2_body(const ChebTileArgs& a, double* D0, doub
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // ---- staging: column pairs in window order, pair p = tid + 256 k (row p / 34); all loads of a
   //      group are issued before its stores; interior tiles need no bounds tests
-  constexpr int PR = CT_R / 2, NP = PR * CT_R, NK = (NP + CT_THREADS - 1) / CT_THREADS, G = 5;
+  constexpr int PR = CT_R / 2, NP = PR * CT_R, NK = (NP + CT_THREADS - 1) / CT_THREADS, G = NK;   // one group: every load of the window in flight together
 #pragma unroll
   for (int k0 = 0; k0 < NK; k0 += G) {
     double lb[G][2], lx[G][2];
@@ -1046,7 +1046,7 @@ __device__ __forceinline__ void ct3_body(const ChebTileArgs& a, double* A0, doub
   }
   // ---- staging of the first step's window: pre d0 = D^-1 b / theta (k_cheb_init) into A0; post x
   //      into A0.  Column pairs in window order, all loads of a group before its stores
-  constexpr int PR = CT_R / 2, NP = PR * CT_R, NK = (NP + CT_THREADS - 1) / CT_THREADS, G = 5;
+  constexpr int PR = CT_R / 2, NP = PR * CT_R, NK = (NP + CT_THREADS - 1) / CT_THREADS, G = NK;   // one group: every load of the window in flight together
 #pragma unroll
   for (int k0 = 0; k0 < NK; k0 += G) {
     double lv[G][2];
@@ -1965,6 +1965,26 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
       const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
       (void)inc; (void)inv; (void)rv; (void)rc;
     }
+  // the vertices' right-hand side read per colour (L1 / L2) instead of held in registers; colour 0's
+  // is requested here, behind the staging
+  auto rv_of = [&](int c, double (&rr)[2]) {
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int j = 2 * ty + m;
+      const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
+      const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
+      rr[m] = inv ? __ldg(r1 + ga + (int64_t)n1 * gc) - alpha : 0.0;
+    }
+  };
+  auto rv1 = [&](int c) {
+    const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * ty + (c >> 1);
+    const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
+    return inv ? __ldg(r1 + ga + (int64_t)n1 * gc) - alpha : 0.0;
+  };
+  double ra_[2] = {0.0, 0.0}, rb_[2];
+  double r1a = 0.0;
+  if constexpr (MR == 2) rv_of(0, ra_);
+  else r1a = rv1(0);
   cp_async_wait_all();
   __syncthreads();
   // ---- the y / y_prev part of this thread's outputs (tile row-major), before the sweep
@@ -2022,19 +2042,11 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
         for (int m = 0; m < 2; ++m) own[c][m] = V[c * PL_ + (j0 + m) * SGS_P + i];
     }
     sgs_cellsums<WY>(Cc, S);                                       // cells of the forward sweep
-    // the vertices' right-hand side read per colour (L1 / L2) instead of held in registers
-    auto rv_of = [&](int c, double (&rr)[2]) {
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const int j = 2 * ty + m;
-        const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * j + (c >> 1);
-        const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
-        rr[m] = inv ? __ldg(r1 + ga + (int64_t)n1 * gc) - alpha : 0.0;
-      }
-    };
-#define SGS_V(PX, PY) do { double rr_[2]; rv_of(PX + 2 * PY, rr_); \
-      sgs_colour_own<WY, PX, PY, IN>(V, own, S[PX + 2 * PY], rr_, A0, C0, n, k); __syncthreads(); } while (0)
-    SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
+    // the right-hand side of colour c + 1 is requested before colour c is computed: its L2 latency
+    // passes behind that colour's arithmetic and barrier instead of in front of the next one's
+#define SGS_V(PX, PY, NX, NY, RA, RB) do { rv_of(NX + 2 * NY, RB); \
+      sgs_colour_own<WY, PX, PY, IN>(V, own, S[PX + 2 * PY], RA, A0, C0, n, k); __syncthreads(); } while (0)
+    SGS_V(0, 0, 1, 0, ra_, rb_); SGS_V(1, 0, 0, 1, rb_, ra_); SGS_V(0, 1, 1, 1, ra_, rb_);   // forward: 0, 1, 2
     // the cells' right-hand side read only now (L1 / L2): not held in registers through the
     // forward sweep, where the cell sums S are live
 #pragma unroll
@@ -2046,13 +2058,16 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
         const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
         rc[c][m] = inc ? __ldg(r0 + ga + (int64_t)n * gc) + alpha : 0.0;
       }
+    sgs_colour_own<WY, 1, 1, IN>(V, own, S[3], rb_, A0, C0, n, k); __syncthreads();          // colour 3
     sgs_cells_own<WY, 0, 0, IN>(V, own, Cc, rc[0], A0, C0, n, k);   // P0 (once: the backward sweep's
     sgs_cells_own<WY, 1, 0, IN>(V, own, Cc, rc[1], A0, C0, n, k);   // P0 update would repeat it exactly)
     sgs_cells_own<WY, 0, 1, IN>(V, own, Cc, rc[2], A0, C0, n, k);
     sgs_cells_own<WY, 1, 1, IN>(V, own, Cc, rc[3], A0, C0, n, k);
     __syncthreads();
     sgs_cellsums<WY>(Cc, S);                                       // cells after the P0 update
-    SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
+    // backward: colours 3, 2, 1, 0 (colour 3's right-hand side is still in rb_)
+    SGS_V(1, 1, 0, 1, rb_, ra_); SGS_V(0, 1, 1, 0, ra_, rb_); SGS_V(1, 0, 0, 0, rb_, ra_);
+    sgs_colour_own<WY, 0, 0, IN>(V, own, S[0], ra_, A0, C0, n, k); __syncthreads();
 #undef SGS_V
   } else {
     static_assert(MR == 1, "one or two rows per thread");
@@ -2061,14 +2076,12 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
 #pragma unroll
     for (int c = 0; c < 4; ++c) own[c] = V[c * PL_ + ty * SGS_P + i];
     sgs_cellsums1<WY>(Cc, S);
-    auto rv1 = [&](int c) {
-      const int ga = A0 + 2 * i + (c & 1), gc = C0 + 2 * ty + (c >> 1);
-      const bool inv = IN || (ga >= 0 && ga <= n && gc >= 0 && gc <= n);
-      return inv ? __ldg(r1 + ga + (int64_t)n1 * gc) - alpha : 0.0;
-    };
-#define SGS_V(PX, PY) do { const double rr_ = rv1(PX + 2 * PY); \
-      sgs_colour_own1<WY, PX, PY, IN>(V, own, S[PX + 2 * PY], rr_, A0, C0, n, k); __syncthreads(); } while (0)
-    SGS_V(0, 0); SGS_V(1, 0); SGS_V(0, 1); SGS_V(1, 1);          // forward: colours 0, 1, 2, 3
+    // one row per thread: the same request-ahead of the next colour's right-hand side (rv1 below the
+    // staging wait would add its L2 latency to every colour of a one-wave, latency-bound step)
+#define SGS_V(PX, PY, NX, NY, RA, RB) do { RB = rv1(NX + 2 * NY); \
+      sgs_colour_own1<WY, PX, PY, IN>(V, own, S[PX + 2 * PY], RA, A0, C0, n, k); __syncthreads(); } while (0)
+    double qa = r1a, qb;
+    SGS_V(0, 0, 1, 0, qa, qb); SGS_V(1, 0, 0, 1, qb, qa); SGS_V(0, 1, 1, 1, qa, qb);   // forward: 0, 1, 2
     double rc1[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -2076,13 +2089,15 @@ __device__ __forceinline__ void sgs_tile_body(const SgsTileArgs& a, double* V, d
       const bool inc = IN || (ga >= 0 && ga < n && gc >= 0 && gc < n);
       rc1[c] = inc ? __ldg(r0 + ga + (int64_t)n * gc) + alpha : 0.0;
     }
+    sgs_colour_own1<WY, 1, 1, IN>(V, own, S[3], qb, A0, C0, n, k); __syncthreads();      // colour 3
     sgs_cells_own1<WY, 0, 0, IN>(V, own, Cc, rc1[0], A0, C0, n, k);
     sgs_cells_own1<WY, 1, 0, IN>(V, own, Cc, rc1[1], A0, C0, n, k);
     sgs_cells_own1<WY, 0, 1, IN>(V, own, Cc, rc1[2], A0, C0, n, k);
     sgs_cells_own1<WY, 1, 1, IN>(V, own, Cc, rc1[3], A0, C0, n, k);
     __syncthreads();
     sgs_cellsums1<WY>(Cc, S);
-    SGS_V(1, 1); SGS_V(0, 1); SGS_V(1, 0); SGS_V(0, 0);          // backward: colours 3, 2, 1, 0
+    SGS_V(1, 1, 0, 1, qb, qa); SGS_V(0, 1, 1, 0, qa, qb); SGS_V(1, 0, 0, 0, qb, qa);   // backward: 3, 2, 1
+    sgs_colour_own1<WY, 0, 0, IN>(V, own, S[0], qa, A0, C0, n, k); __syncthreads();      // and 0
 #undef SGS_V
   }
   // the next step's CTAs may launch once every CTA of this grid is writing its tile (they wait in
