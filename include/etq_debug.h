@@ -39,7 +39,9 @@ extern "C" {
  *   option 14 = matrix-free interior rows of the cavity-wind F levels (1 [default]) or stored SELL rows (0);
  *   option 15 = Chebyshev-SGS y_prev read in the Q pass (1 [default]) or staged by cp.async (0) - bitwise;
  *   option 16 = Chebyshev-SGS window: 0 = automatic [default: 64 x 32, with 512 threads when the tiles
- *               fit one wave], 1 = 64 x 64, 2 = 64 x 32 / 256 threads, 3 = 64 x 32 / 512 threads - bitwise sweeps.
+ *               fit one wave], 1 = 64 x 64, 2 = 64 x 32 / 256 threads, 3 = 64 x 32 / 512 threads - bitwise sweeps;
+ *   option 17 = programmatic dependent launches between the kernels of the F V-cycle inside the Oseen
+ *               preconditioners (1 [default]) or plain launches (0) - bitwise the same.
  * Applies to solves whose CUDA graphs are captured afterwards (re-run etq_precond_setup). */
 etq_status etq_debug_set_option(int32_t option, int32_t value);
 

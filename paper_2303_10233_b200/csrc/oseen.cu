@@ -622,7 +622,9 @@ etq_status oseen_precond_apply(const Problem& P, etq_pc_kind kind, const double*
   a.r_u = r; a.z_p = z + nu; a.t_u = P.tu; a.done = done;
   k_bt_sub<<<grid_for(P.BxT1.nslices * 32, BS, 4096), BS, 0, st>>>(a); etq_count_launch();
   }
-  return vcycle_apply_ex(P, P.mg, P.tu, z, nullptr, 0, nullptr, nullptr, done, st);
+  // nothing runs beside the F V-cycle of a block-triangular preconditioner: programmatic dependent
+  // launches between its kernels (as for P3) shorten the latency-bound cycle
+  return vcycle_apply_ex(P, P.mg, P.tu, z, nullptr, 0, nullptr, nullptr, done, st, g_oseen_vc_pdl);
 }
 
 etq_status oseen_setup(Problem& P, etq_pc_kind kind) {
