@@ -41,7 +41,9 @@ extern "C" {
  *   option 16 = Chebyshev-SGS window: 0 = automatic [default: 64 x 32, with 512 threads when the tiles
  *               fit one wave], 1 = 64 x 64, 2 = 64 x 32 / 256 threads, 3 = 64 x 32 / 512 threads - bitwise sweeps;
  *   option 17 = programmatic dependent launches between the kernels of the F V-cycle inside the Oseen
- *               preconditioners (1 [default]) or plain launches (0) - bitwise the same.
+ *               preconditioners (1 [default]) or plain launches (0) - bitwise the same;
+ *   option 18 = the tiled smoother prefetches into L2 the window of the tile that follows it on its SM
+ *               (1 [default]) or not (0) - bitwise the same.
  * Applies to solves whose CUDA graphs are captured afterwards (re-run etq_precond_setup). */
 etq_status etq_debug_set_option(int32_t option, int32_t value);
 

@@ -28,6 +28,7 @@ bool g_cheb_tile2 = true;           // etq_set_option(11): leaner temporally blo
 bool g_sgs_planar = false;          // etq_set_option(10): Chebyshev-SGS on parity planes with TMA windows
 bool g_vc_pdl = true;               // etq_set_option(8): programmatic dependent launches in the V-cycle
 bool g_prolong_tile = true;         // etq_set_option(9): tiled nested-Q2 prolongation
+bool g_ct_prefetch = true;          // etq_debug_set_option(18): L2 prefetch of a later tile's window in the tiled smoother
 bool g_oseen_vc_pdl = true;         // etq_debug_set_option(17): programmatic dependent launches in the F V-cycle of the Oseen preconditioners
 void etq_count_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 int64_t etq_launch_total() { return g_launches.load(std::memory_order_relaxed); }
@@ -741,6 +742,7 @@ etq_status etq_debug_set_option(int32_t option, int32_t value) {
   if (option == 13) { g_p2_vc_pdl = value != 0; return ETQ_OK; }
   if (option == 14) { g_oseen_mf = value != 0; return ETQ_OK; }
   if (option == 15) { g_sgs_yp_ldg = value != 0; return ETQ_OK; }
+  if (option == 18) { g_ct_prefetch = value != 0; return ETQ_OK; }
   if (option == 17) { g_oseen_vc_pdl = value != 0; return ETQ_OK; }
   if (option == 16) { if (value < 0 || value > 3) return ETQ_EINVAL; g_sgs_window = value; return ETQ_OK; }
   return ETQ_EINVAL;

@@ -61,6 +61,7 @@ extern bool g_p2_vc_pdl;                  // api.cu; etq_debug_set_option(13)
 extern bool g_cheb_tile3;                 // api.cu; etq_debug_set_option(12)
 extern bool g_cheb_tile2;                 // api.cu; etq_set_option(11)
 extern bool g_vc_pdl;                     // api.cu; etq_set_option(8)
+extern bool g_ct_prefetch;                // api.cu; etq_debug_set_option(18)
 extern bool g_oseen_vc_pdl;               // api.cu; etq_debug_set_option(17)
 extern bool g_prolong_tile;               // api.cu; etq_set_option(9)
 

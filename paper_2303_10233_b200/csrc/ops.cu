@@ -438,6 +438,7 @@ struct ChebTileArgs {
   const double* done;
   // finest post pass only: z = x + d2 written here (instead of d_out) and <z, dot_with>
   double* z_out; const double* dot_with; RedSite site; int slot; double* dot_out;
+  int prefetch;   // L2 prefetch of a later CTA's window (k_cheb_tile3)
 };
 
 // class stencil of one output from the register window: win[slot][col], rows jj-2..jj+2 in
@@ -1113,12 +1114,38 @@ __device__ __forceinline__ void ct3_body(const ChebTileArgs& a, double* A0, doub
   }
 }
 
+// L2 prefetch of the window a later CTA will stage: the CTA that takes this one's place on the SM
+// is about CT_PF_DIST blocks ahead in launch order (2 resident CTAs on each of 148 SMs), and the
+// staging of a tile is one exposed DRAM latency at 16 warps per SM; with its lines already in L2
+// that wait is an L2 hit.  One 128-byte line per prefetch, rows clamped to the grid.
+constexpr int CT_PF_DIST = 2 * 148 + 32;
+__device__ __forceinline__ void ct_prefetch_window(const double* __restrict__ v, int m, int i0, int j0, int tid) {
+  if (tid >= CT_R) return;
+  const int j = j0 + tid;
+  if (j < 0 || j >= m) return;
+  const int ia = max(i0, 0), ib = min(i0 + CT_R, m);        // [ia, ib)
+  const char* p = reinterpret_cast<const char*>(v + (int64_t)m * j + ia);
+  const char* e = reinterpret_cast<const char*>(v + (int64_t)m * j + ib);
+  p = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)127);
+  for (; p < e; p += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <int POST>
 __global__ void __launch_bounds__(CT_THREADS, 2) k_cheb_tile3(ChebTileArgs a) {
   pdl_wait();
   if (is_done(a.done)) return;
   extern __shared__ __align__(16) double ct_sm[];
   const int m = a.so.m;
+  if (a.prefetch) {
+    const int lin = blockIdx.x + gridDim.x * blockIdx.y + CT_PF_DIST;
+    if (lin < (int)(gridDim.x * gridDim.y)) {
+      const int bx = lin % gridDim.x, by = lin / gridDim.x;
+      const int pi0 = (bx % a.tiles_x) * CT_T - CT_H, pj0 = (bx / a.tiles_x) * CT_T - CT_H;
+      const int64_t poff = (int64_t)by * a.nq;
+      ct_prefetch_window(a.b + poff, m, pi0, pj0, threadIdx.x);
+      if (POST) ct_prefetch_window(a.x_in + poff, m, pi0, pj0, (int)threadIdx.x - 128);
+    }
+  }
   const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
   const int i0 = tx * CT_T - CT_H, j0 = ty * CT_T - CT_H;
   const int64_t off = (int64_t)blockIdx.y * a.nq;
@@ -3629,6 +3656,7 @@ static void launch_cheb_tile(const Level& lv, bool post, const double* b, const 
   for (int k = 0; k < 3; ++k) { a.c1[k] = c1[k]; a.c2[k] = c2[k]; }
   a.done = done;
   a.z_out = z_out; a.dot_with = dot_with; a.site = site ? *site : RedSite{}; a.slot = slot; a.dot_out = dot_out;
+  a.prefetch = g_ct_prefetch ? 1 : 0;
   dim3 grid(a.tiles_x * a.tiles_x, 2);
   if (lv.ct2 && g_cheb_tile3) {
     static bool smem3 = false;
