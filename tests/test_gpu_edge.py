@@ -216,3 +216,30 @@ def test_nan_input_reports_enan():
     with pytest.raises(etq.EtqError) as e:
         Q.gmres_solve(etq.PC_OSEEN_M1, bq, xq, rtol=1e-6, restart=20, maxit=40)
     assert e.value.status == -7
+
+
+@pytest.mark.parametrize("devloop", [1, 0])
+def test_minres_iterate_after_every_small_iteration_count(devloop):
+    """Algorithm 1 lines 16-17: x^{(j)} after exactly j = 1 ... 7 iterations equals the oracle's
+    (the x update of an odd iteration is deferred to the next call or to the tail; the loop may
+    stop inside the two-iteration graph body), in the device loop and in the host loop."""
+    n, a = 16, 0.005
+    s = fem.assemble_system(n)
+    Pr = precond.StokesP2(s, a)
+    P = etq.Problem(n)
+    etq.set_option(3, devloop)
+    try:
+        P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=a))
+        b = zeros(P.N); P.build_rhs(b)
+        scale = None
+        for j in range(1, 8):
+            xo, ro = krylov.minres(lambda v: s.K @ v, s.b, Pr, rtol=0.0, maxit=j)
+            x = zeros(P.N)
+            rep = P.minres_solve(etq.PC_P2_GMG, b, x, rtol=1e-30, maxit=j)
+            assert rep["iterations"] == j == ro.iterations
+            xg = host(x)
+            scale = np.abs(xo).max()
+            assert np.abs(xg - xo).max() <= 1e-10 * scale, (j, np.abs(xg - xo).max() / scale)
+    finally:
+        etq.set_option(3, 1)
+        P.close()
