@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--maxit", type=int, default=5000)
     ap.add_argument("--cpu-baseline-iters", type=int, default=1,
                     help="oracle MINRES iterations timed for cpu_baseline (0 = skip)")
-    ap.add_argument("--kernel-reps", type=int, default=20)
+    ap.add_argument("--kernel-reps", type=int, default=100)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-p3", action="store_true", help="skip the P3 (exact M_Q) time-to-solution block")
     ap.add_argument("--clock-ms", type=int, default=1000, help="nvidia-smi sampling period during the timed region")
@@ -298,9 +298,10 @@ def run_ours(args):
                           "frac_of_peak": (k_bytes / (k_ms * 1e-3) / 1e9 / peak) if k_bytes > 0 else None}
     # one whole MINRES iteration (the step / its iteration count): saddle apply (16 N), P2 apply (both
     # branches), the <z, v> dot inputs read by the P2 epilogues (8 N), lines 8 and 16-17 of Algorithm 1
-    # (k_minres_v: q, v, v_prev in, v_prev out = 32 N; k_minres_wx: z, w, w_prev, x in, w_prev, x out
-    # = 48 N).  Algorithmic bytes (each kernel's vectors once); the pressure vectors are L2-sized
-    it_bytes = 16.0 * P.N + kern[names[4]]["algorithmic_bytes"] + 8.0 * P.N + 80.0 * P.N
+    # (k_minres_v: q, v, v_prev in, v_prev out = 32 N; k_minres_wx: z, w, w_prev in, w_prev out = 32 N,
+    # plus x in and out every other iteration = 8 N on average).  Algorithmic bytes (each kernel's
+    # vectors once); the pressure vectors are L2-sized
+    it_bytes = 16.0 * P.N + kern[names[4]]["algorithmic_bytes"] + 8.0 * P.N + 72.0 * P.N
     it_ms = ms / its if its else float("nan")
     kern["whole MINRES iteration (solve time / iterations)"] = {
         "ms": it_ms, "algorithmic_bytes": it_bytes, "GB_per_s": it_bytes / (it_ms * 1e-3) / 1e9,
@@ -312,7 +313,7 @@ def run_ours(args):
     s0 = kern[names[0]]
     s0["csr_model_bytes"] = stored
     s0["csr_equivalent_GB_per_s"] = stored / (s0["ms"] * 1e-3) / 1e9
-    # dominant kernel of the step by the committed ncu launch-list share (profiles/r01_launches_summary.txt)
+    # dominant kernel of the step by the committed ncu launch-list share (profiles/r02_launches_summary.txt)
     dom_name = names[10]
     dom = kern[dom_name]
     traffic = None

@@ -36,17 +36,17 @@ def pick(d):
 
 def main():
     nd = os.path.join(ROOT, 'profiles', 'ncu')
-    s = pick(raw(os.path.join(nd, 'r01_sgs_tile_n1024.ncu-rep')))
-    c = pick(raw(os.path.join(nd, 'r01_cheb_tile_pre_n1024.ncu-rep')))
-    t = pick(raw(os.path.join(nd, 'r01_saddle_tile_n1024.ncu-rep')))
-    d = {"kernel": "k_sgs_tile (one Chebyshev-SGS step, n = 1024, 64 x 64 windows, 50 x 58 tiles, 378 CTAs)",
+    s = pick(raw(os.path.join(nd, 'r02b_k_sgs_tile.ncu-rep')))
+    c = pick(raw(os.path.join(nd, 'r02b_k_cheb_tile3_pre.ncu-rep')))
+    t = pick(raw(os.path.join(nd, 'r02b_k_saddle_tile.ncu-rep')))
+    d = {"kernel": "k_sgs_tile<32, 2> (one Chebyshev-SGS step, n = 1024, 64 x 32 windows, 50 x 26 tiles, 840 CTAs; end of round 2)",
          "command": "ncu --set full --clock-control none --import-source on -k regex:k_sgs_tile -s 2 -c 1 "
                     "python scripts/profile_kernel.py --n 1024 --which 10 --reps 2",
          "dram_bytes_per_launch": s["dram_read_bytes"] + s["dram_write_bytes"],
          "algorithmic_bytes_per_launch": 67174432, **s,
          "note": "ncu replays with flushed caches: DRAM bytes are cold-cache; inside the solve the 4 pressure "
                  "vectors (67 MB) are partly L2-resident",
-         "other": {"k_cheb_tile<0> (finest pre pass)": {**c, "algorithmic_bytes_per_launch": 201523248},
+         "other": {"k_cheb_tile3<0> (finest pre pass)": {**c, "algorithmic_bytes_per_launch": 201523248},
                    "k_saddle_tile (matrix-free saddle apply)": {**t, "algorithmic_bytes_per_launch": 167936048}}}
     json.dump(d, open(os.path.join(ROOT, 'profiles', 'ncu_traffic.json'), 'w'), indent=1)
     print(json.dumps(d, indent=1))
