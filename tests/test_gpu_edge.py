@@ -243,3 +243,18 @@ def test_minres_iterate_after_every_small_iteration_count(devloop):
     finally:
         etq.set_option(3, 1)
         P.close()
+
+
+def test_indefinite_preconditioner_is_reported():
+    """Algorithm 1 needs <z, v> >= 0 (lines 3 / 10): a V-cycle whose Chebyshev interval ends far
+    below lambda_max(D^-1 A) amplifies the rough modes and is indefinite; MINRES stops with
+    ETQ_EINDEFINITE (-4) instead of taking the square root of a negative number."""
+    P = etq.Problem(32)
+    P.precond_setup(etq.PC_P2_GMG, etq.make_params(cheb_sgs_lo=0.005, smooth_lo=0.05, smooth_hi=0.3))
+    b = zeros(P.N); P.build_rhs(b)
+    x = zeros(P.N)
+    with pytest.raises(etq.EtqError) as e:
+        P.minres_solve(etq.PC_P2_GMG, b, x, rtol=1e-8, maxit=200)
+    assert e.value.status == -4
+    assert np.isfinite(host(x)).all()
+    P.close()
