@@ -1408,6 +1408,19 @@ __global__ void __launch_bounds__(PT_THREADS) k_prolong_tile(int mf, int mc, int
   const int tilesx = (mf + PT_X - 1) / PT_X;
   const int K0 = (blockIdx.x % tilesx) * PT_X, L0 = (blockIdx.x / tilesx) * PT_Y;
   const int I0 = K0 / 2 - 1, J0 = L0 / 2 - 1;
+  // the fine values this thread will update, requested first: their DRAM latency passes behind the
+  // staging and the x pass instead of in front of the final read-modify-write
+  constexpr int PT_NF = PT_Y * PT_X / PT_THREADS;
+  double xf0[PT_NF], xf1[PT_NF];
+#pragma unroll
+  for (int q = 0; q < PT_NF; ++q) {
+    const int idx = threadIdx.x + q * PT_THREADS;
+    const int k = K0 + idx % PT_X, l = L0 + idx / PT_X;
+    const bool on = k < mf && l < mf && k > 0 && l > 0 && k < mf - 1 && l < mf - 1;
+    const int64_t t = on ? k + (int64_t)mf * l : 0;
+    xf0[q] = on ? xf[t] : 0.0;
+    xf1[q] = on ? xf[nqf + t] : 0.0;
+  }
   for (int idx = threadIdx.x; idx < PT_CY * PT_CX; idx += PT_THREADS) {
     const int ci = I0 + idx % PT_CX, cj = J0 + idx / PT_CX;
     const bool in = ci >= 0 && cj >= 0 && ci < mc && cj < mc;
@@ -1434,7 +1447,9 @@ __global__ void __launch_bounds__(PT_THREADS) k_prolong_tile(int mf, int mc, int
   }
   __syncthreads();
   // y pass
-  for (int idx = threadIdx.x; idx < PT_Y * PT_X; idx += PT_THREADS) {
+#pragma unroll
+  for (int qq = 0; qq < PT_NF; ++qq) {
+    const int idx = threadIdx.x + qq * PT_THREADS;
     const int kk = idx % PT_X, k = K0 + kk, l = L0 + idx / PT_X;
     if (k >= mf || l >= mf || k == 0 || l == 0 || k == mf - 1 || l == mf - 1) continue;
     int iy[3]; double wy[3];
@@ -1445,7 +1460,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_prolong_tile(int mf, int mc, int
       s1 = fma(wy[q], tx[1][iy[q] - J0][kk], s1);
     }
     const int64_t t = k + (int64_t)mf * l;
-    xf[t] += s0; xf[nqf + t] += s1;
+    xf[t] = xf0[qq] + s0; xf[nqf + t] = xf1[qq] + s1;
   }
 }
 

@@ -51,7 +51,7 @@ def main():
     etq.set_option(args.option, DEFAULTS[args.option])
     vals = list(zs)
     out["bitwise_equal"] = all(torch.equal(zs[vals[0]], zs[v]) for v in vals[1:])
-    out["max_abs_diff"] = max(float((zs[vals[0]] - zs[v]).abs().max()) for v in vals[1:])
+    out["max_abs_diff"] = max([float((zs[vals[0]] - zs[v]).abs().max()) for v in vals[1:]] + [0.0])
     print(json.dumps(out))
 
 
