@@ -386,7 +386,10 @@ __device__ __forceinline__ void oseen_row2(const StencilOp& so, const double* __
   }
 }
 
-__global__ void __launch_bounds__(BS, 3) k_cheb_step_os(ChebStArgs a, const double* __restrict__ tab) {
+#ifndef OS_MINB
+#define OS_MINB 4
+#endif
+__global__ void __launch_bounds__(BS, OS_MINB) k_cheb_step_os(ChebStArgs a, const double* __restrict__ tab) {
   pdl_wait();
   if (is_done(a.done)) return;
   const int lane = threadIdx.x & 31;
