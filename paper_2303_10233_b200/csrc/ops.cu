@@ -1338,6 +1338,7 @@ __global__ void k_restrict(int mf, int mc, int nqf, int nqc, const double* rf, d
     }
     int ox[5], oy[5]; double wx[5], wy[5];
     const int nx = restrict_taps(I, ox, wx), ny = restrict_taps(J, oy, wy);
+    const double di = dinvc[t];            // requested with the gathers, not after them
     double s0 = 0.0, s1 = 0.0;
     for (int q = 0; q < ny; ++q) {
       const int64_t rowf = (int64_t)(2 * J + oy[q]) * mf;
@@ -1351,7 +1352,6 @@ __global__ void k_restrict(int mf, int mc, int nqf, int nqc, const double* rf, d
       s1 = fma(wy[q], t1, s1);
     }
     bc[t] = s0; bc[nqc + t] = s1;
-    const double di = dinvc[t];
     d0c[t] = di * s0 * itheta; d0c[nqc + t] = di * s1 * itheta;
   }
 }
