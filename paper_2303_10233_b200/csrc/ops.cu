@@ -1336,17 +1336,35 @@ __global__ void k_restrict(int mf, int mc, int nqf, int nqc, const double* rf, d
       bc[t] = 0.0; bc[nqc + t] = 0.0; d0c[t] = 0.0; d0c[nqc + t] = 0.0;
       continue;
     }
-    int ox[5], oy[5]; double wx[5], wy[5];
-    const int nx = restrict_taps(I, ox, wx), ny = restrict_taps(J, oy, wy);
+    // fixed 5 x 5 tap frame (offsets -3, -1, 0, 1, 3): odd (element-midpoint) coarse indices take the
+    // two outer taps with weight 0 and skip their loads, so the loops unroll and every load of a
+    // row is in flight together; the sums start from 0, so the zero taps leave them bitwise unchanged
+    const bool ei = (I & 1) == 0, ej = (J & 1) == 0;
+    const double wo_i = ei ? -0.125 : 0.0, wn_i = ei ? 0.375 : 0.75;
+    const double wo_j = ej ? -0.125 : 0.0, wn_j = ej ? 0.375 : 0.75;
+    const double wx[5] = {wo_i, wn_i, 1.0, wn_i, wo_i}, wy[5] = {wo_j, wn_j, 1.0, wn_j, wo_j};
+    constexpr int off[5] = {-3, -1, 0, 1, 3};
     const double di = dinvc[t];            // requested with the gathers, not after them
+    const double* __restrict__ r0 = rf + (int64_t)(2 * J) * mf + 2 * I;
+    const double* __restrict__ r1 = r0 + nqf;
     double s0 = 0.0, s1 = 0.0;
-    for (int q = 0; q < ny; ++q) {
-      const int64_t rowf = (int64_t)(2 * J + oy[q]) * mf;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      if ((q == 0 || q == 4) && !ej) continue;
+      const int64_t ro = (int64_t)off[q] * mf;
+      double v0[5], v1[5];
+#pragma unroll
+      for (int p = 0; p < 5; ++p) {
+        const bool on = ei || (p != 0 && p != 4);
+        v0[p] = on ? r0[ro + off[p]] : 0.0;
+        v1[p] = on ? r1[ro + off[p]] : 0.0;
+      }
       double t0 = 0.0, t1 = 0.0;
-      for (int p = 0; p < nx; ++p) {
-        const int64_t f = rowf + 2 * I + ox[p];
-        t0 = fma(wx[p], rf[f], t0);
-        t1 = fma(wx[p], rf[nqf + f], t1);
+#pragma unroll
+      for (int p = 0; p < 5; ++p) {
+        if ((p == 0 || p == 4) && !ei) continue;
+        t0 = fma(wx[p], v0[p], t0);
+        t1 = fma(wx[p], v1[p], t1);
       }
       s0 = fma(wy[q], t0, s0);
       s1 = fma(wy[q], t1, s1);
