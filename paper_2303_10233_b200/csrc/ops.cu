@@ -2815,10 +2815,11 @@ __global__ void __launch_bounds__(ST_THREADS, ST_MINB) k_saddle_tile(SaddleTileA
       const double* src = xu + ((int64_t)m * (J0 - 2 + wj) + (I0 - 2 + wi));
       double* dst = st_sm + ((wi & 1) ? ST_W * ST_H : 0) + (tid >> 1);
       const int64_t step = (int64_t)DJ * m + DI, wrap = (int64_t)m - ST_W;
+      // component 0 now, component 1 after the pressure windows, in a second cp.async group:
+      // its latency passes behind component 0's velocity walk
 #pragma unroll 6
       for (int k = 0; k < NF; ++k) {
         cp_async8(dst, src, true);
-        cp_async8(dst + 2 * ST_W * ST_H, src + a.nq, true);
         dst += ST_THREADS / 2; src += step; wi += DI;
         if (wi >= ST_W) { wi -= ST_W; src += wrap; }
       }
@@ -2827,8 +2828,8 @@ __global__ void __launch_bounds__(ST_THREADS, ST_MINB) k_saddle_tile(SaddleTileA
         const double* s2 = xu + ((int64_t)m * (J0 - 2 + wj2) + (I0 - 2 + wi2));
         double* d2 = st_sm + ((wi2 & 1) ? ST_W * ST_H : 0) + (idx >> 1);
         cp_async8(d2, s2, true);
-        cp_async8(d2 + 2 * ST_W * ST_H, s2 + a.nq, true);
       }
+      (void)wj;
     }
     {
       constexpr int TOT = ST_PW * ST_PW, DJ = ST_THREADS / ST_PW, DI = ST_THREADS % ST_PW;
@@ -2853,6 +2854,37 @@ __global__ void __launch_bounds__(ST_THREADS, ST_MINB) k_saddle_tile(SaddleTileA
         if (ci >= ST_CW) { ci -= ST_CW; src += wrap; }
       }
     }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    {
+      constexpr int TOT = ST_W * ST_W, NF = TOT / ST_THREADS, DJ = ST_THREADS / ST_W, DI = ST_THREADS % ST_W;
+      int wj = tid / ST_W, wi = tid - ST_W * wj;
+      const double* src = xu + a.nq + ((int64_t)m * (J0 - 2 + wj) + (I0 - 2 + wi));
+      double* dst = st_sm + 2 * ST_W * ST_H + ((wi & 1) ? ST_W * ST_H : 0) + (tid >> 1);
+      const int64_t step = (int64_t)DJ * m + DI, wrap = (int64_t)m - ST_W;
+#pragma unroll 6
+      for (int k = 0; k < NF; ++k) {
+        cp_async8(dst, src, true);
+        dst += ST_THREADS / 2; src += step; wi += DI;
+        if (wi >= ST_W) { wi -= ST_W; src += wrap; }
+      }
+      if (tid < TOT - NF * ST_THREADS) {
+        const int idx = NF * ST_THREADS + tid, wj2 = idx / ST_W, wi2 = idx - ST_W * wj2;
+        const double* s2 = xu + a.nq + ((int64_t)m * (J0 - 2 + wj2) + (I0 - 2 + wi2));
+        cp_async8(st_sm + 2 * ST_W * ST_H + ((wi2 & 1) ? ST_W * ST_H : 0) + (idx >> 1), s2, true);
+      }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;\n" ::: "memory");
+    __syncthreads();
+    {
+      const double sc0 = sc;
+      double dot = 0.0;
+      st_vel<0, false>(a, S, I0, J0, sc0, dot);
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncthreads();
+      st_vel<1, false>(a, S, I0, J0, sc0, dot);
+      if (a.dot_out) { double v[1] = {dot}; reduce_finish<1>(v, a.site, a.slot, a.dot_out); }
+    }
+    return;
   } else {
     for (int idx = threadIdx.x; idx < ST_W * ST_W; idx += ST_THREADS) {
       const int wi = idx % ST_W, wj = idx / ST_W;
