@@ -35,7 +35,7 @@ extern "C" {
  *               stencil sums: agrees to rounding) or k_cheb_tile (0, bitwise the per-step path);
  *   option 12 = k_cheb_tile3, the smoother with the residual in registers (1 [default], bitwise the
  *               k_cheb_tile2 V-cycle) or k_cheb_tile2 (0);
- *   option 13 = programmatic dependent launches inside the V-cycle of P2 (0 [default]) - bitwise the same;
+ *   option 13 = programmatic dependent launches inside the V-cycle of P2 (1 [default]) - bitwise the same;
  *   option 14 = matrix-free interior rows of the cavity-wind F levels (1 [default]) or stored SELL rows (0);
  *   option 15 = Chebyshev-SGS y_prev read in the Q pass (1 [default]) or staged by cp.async (0) - bitwise;
  *   option 16 = Chebyshev-SGS window: 0 = automatic [default: 64 x 32, with 512 threads when the tiles

@@ -20,7 +20,7 @@ bool g_tail_sm = true;              // etq_set_option(5): shared-memory matrix-f
 bool g_saddle_tile = true;          // etq_set_option(6): shared-memory tiled matrix-free saddle apply
 bool g_sgs_pdl = true;              // etq_set_option(7): programmatic dependent launches in the SGS chain
 bool g_cheb_tile3 = true;
-bool g_p2_vc_pdl = false;
+bool g_p2_vc_pdl = true;
 bool g_oseen_mf = true;
 bool g_sgs_yp_ldg = true; 
 int g_sgs_window = 0;               // etq_debug_set_option(16): Chebyshev-SGS window 0 auto, 1 64x64, 2 64x32, 3 64x32 / 512 threads          // etq_debug_set_option(15): Chebyshev-SGS y_prev loaded in the Q pass             // etq_debug_set_option(14): matrix-free interior rows of the cavity-wind F levels           // etq_debug_set_option(13): programmatic dependent launches inside P2's V-cycle           // etq_debug_set_option(12): smoother with the residual in registers (k_cheb_tile3)
