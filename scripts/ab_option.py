@@ -16,7 +16,7 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 from paper_2303_10233_b200 import etq  # noqa: E402
 
-DEFAULTS = {0: 1, 1: 64, 2: 1, 3: 1, 10: 0, 13: 1, 16: 0, 18: 1}
+DEFAULTS = {0: 1, 1: 64, 2: 1, 3: 1, 4: 0, 10: 0, 13: 1, 16: 0, 18: 1}
 
 
 def main():
